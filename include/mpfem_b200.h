@@ -1,0 +1,158 @@
+/*
+ * mpfem_b200.h -- C-ABI drop-in boundary of the B200-native hot path.
+ *
+ * Plain pointers, sizes and status codes; no torch or C++ types cross this boundary.
+ * Each entry point names the reference interface it replaces (file:line into
+ * /root/reference/proj). A reference-side binding (the mpfem C++ API re-implemented on
+ * top of this ABI) is shown in INTEGRATION.md.
+ *
+ * Status codes mirror the reference CLI (mpfem_cli.cpp:517-527):
+ *   0 ok, 2 ConfigError (bad name/shape/format/mode), 3 CheckError (singular cell,
+ *   dof out of range, dof collision), 4 CUDA/runtime failure (no device, launch error).
+ * FP exception flags (softfloat.hpp:22-36) are a bitmask: 1 overflow, 2 underflow,
+ * 4 invalid, 8 divzero. On the GPU they are detected on rounding of the geometry and
+ * scaled-weight stages and on non-finite outputs; this is coarser than the reference's
+ * per-operation flags (documented in DESIGN.md).
+ *
+ * Formats (softfloat.hpp:17): 0 bf16, 1 fp16, 2 fp32, 3 fp64.
+ * Forms (geometry.hpp:107): 0 mass, 1 poisson.  Engines (mm_units.hpp:31): 0 scalar,
+ * 1 vector, 2 matrix (kept for validate_config parity; dispatch is on the formats).
+ */
+#ifndef MPFEM_B200_H
+#define MPFEM_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpfem_b200_setup_s* mpfem_b200_setup_t;
+
+enum {
+  MPFEM_B200_OK = 0,
+  MPFEM_B200_CONFIG_ERROR = 2,
+  MPFEM_B200_CHECK_ERROR = 3,
+  MPFEM_B200_RUNTIME_ERROR = 4
+};
+
+/* Coefficient kinds for cell_matrices:
+ *   0 ONE            constant one (reference: empty z, multiplication skipped)
+ *   1 SINCOSEXP      c(x) = 1 + 0.5 sin(2 pi x) cos(2 pi y) e^z at x_q = v0 + J xi_q (fp64),
+ *                    rounded once to u_g  (BASELINE configs 0,1,2,4)
+ *   2 EXP10_AFFINE   c = 10^(6 u(x_q)), u affine per cell from 4 vertex values
+ *                    (coef: n_cells x 4 doubles)  (BASELINE config 3)
+ *   3 NODAL          nodal FE coefficient z, n_phi doubles per cell, evaluated exactly as
+ *                    eval_z_at_ug (kernels.cpp:114-136) */
+enum { MPFEM_COEF_ONE = 0, MPFEM_COEF_SINCOSEXP = 1, MPFEM_COEF_EXP10_AFFINE = 2,
+       MPFEM_COEF_NODAL = 3 };
+
+/* Thread-local description of the last failure (empty when none). */
+const char* mpfem_b200_last_error(void);
+
+/* Library version and the compiled device architecture string ("sm_100a"). */
+const char* mpfem_b200_version(void);
+
+/* Replaces make_setup (kernels.hpp:60-62, kernels.cpp:78-108) + validate_config
+ * (kernels.cpp:29-40). cell_kind must be 0 (simplex), dim 3, 1 <= p <= 8.
+ * The handle owns device copies of the rule, the fp64 tabulations and the shared
+ * basis-product operand T; it is immutable and may be shared by streams. */
+int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, int u_g,
+                            int u_q, int u_s, int engine, int n_batch,
+                            mpfem_b200_setup_t* out);
+int mpfem_b200_setup_destroy(mpfem_b200_setup_t setup);
+
+/* Sizes: n_phi, n_q, n_d (1 mass, 3 poisson), K (GEMM depth = blocks x n_q), K_pad,
+ * path (0 tcgen05, 1 fp32 FFMA, 2 fp64, 3 fused small-degree). */
+int mpfem_b200_setup_info(mpfem_b200_setup_t setup, int* n_phi, int* n_q, int* n_d,
+                          int64_t* k, int64_t* k_pad, int* path);
+
+/* Host copies of the rule (n_q x 3 points, n_q weights) the setup uses; bitwise equal to
+ * rule_for(simplex, p) (quadrature.cpp:171-224). */
+int mpfem_b200_setup_rule(mpfem_b200_setup_t setup, double* points, double* weights);
+
+/* Batched replacement for the per-cell loop cell_geometry (geometry.cpp:226-245) ->
+ * bilinear_kernel (kernels.cpp:242-267) over n_cells affine tets, on DEVICE buffers.
+ *   verts:  if cells == NULL, n_cells x 4 x 3 fp64 private vertices;
+ *           else the mesh vertex table (n_verts x 3 fp64) indexed by cells (n_cells x 4 int32)
+ *   coef:   per coefficient kind above (device, may be NULL for ONE/SINCOSEXP), row stride
+ *           coef_stride doubles
+ *   out:    n_cells rows of n_phi x n_phi row-major cell matrices with row pitch
+ *           out_pitch elements (>= n_phi^2); fp32 for u_q in {fp16, fp32}, fp64 for fp64
+ *   stream: cudaStream_t (NULL = legacy default)
+ *   flags:  optional host pointer; OR-ed with the FP flag bitmask (forces a sync) */
+int mpfem_b200_cell_matrices(mpfem_b200_setup_t setup, const double* verts,
+                             const int32_t* cells, int64_t n_cells, int coef_kind,
+                             const double* coef, int64_t coef_stride, void* out,
+                             int64_t out_pitch, void* stream, uint32_t* flags);
+
+/* Same contract on HOST buffers: copies inputs in, runs, copies the matrices out (the
+ * drop-in call a reference user makes). Host buffers should be pinned for full speed. */
+int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t setup, const double* verts,
+                                  int64_t n_verts, const int32_t* cells, int64_t n_cells,
+                                  int coef_kind, const double* coef, int64_t coef_stride,
+                                  void* out, int64_t out_pitch, void* stream,
+                                  uint32_t* flags);
+
+/* Pre-size the scratch (scaled-weight operand W) for n_cells so that later calls on
+ * this setup allocate nothing (CUDA-graph capture safe). */
+int mpfem_b200_reserve(mpfem_b200_setup_t setup, int64_t n_cells);
+
+/* Debug/parity entry: the scaled weights W (kernels.cpp:177-197 build_C, GEMM-packed
+ * order (block, q), blocks (s<=t)) as fp64 carriers for n_cells cells (device out,
+ * n_cells x K doubles). */
+int mpfem_b200_scaled_weights(mpfem_b200_setup_t setup, const double* verts,
+                              const int32_t* cells, int64_t n_cells, int coef_kind,
+                              const double* coef, int64_t coef_stride, double* out,
+                              void* stream, uint32_t* flags);
+
+/* Number of kernel launches the last cell_matrices call on this setup issued. */
+int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
+
+/* ---------------------------------------------------------------- mesh & assembly */
+
+/* Replaces structured_tet_mesh (mesh.cpp:125-163) for the assembly config: host
+ * arrays (n_verts = (nx+1)(ny+1)(nz+1) x 3, n_cells = 6 nx ny nz x 4). */
+int mpfem_b200_structured_tet_mesh(int nx, int ny, int nz, double extent, double jitter,
+                                   uint64_t seed, double* verts, int32_t* cells);
+
+/* Replaces build_dofmap(mesh, basis, continuous) (mesh.cpp:204-298) on DEVICE buffers.
+ * Nodes are identified topologically (sub-simplex vertex ids + lattice position), which
+ * equals the reference's geometric identification on conforming meshes; dof ids are
+ * assigned in first-encounter order over (cell asc, local k asc). cell_dofs: n_cells x
+ * n_phi int32 (device). n_dofs / max_multiplicity written to host pointers. */
+int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_verts,
+                      int32_t* cell_dofs, int32_t* n_dofs, int32_t* max_multiplicity,
+                      void* stream);
+
+/* Sparsity pattern = the reference COO key set sorted by (row, col) (assembly.cpp:67-86)
+ * as CSR. Two-phase: call with col_idx == NULL to get nnz into *nnz and row_ptr
+ * (n_dofs + 1 int64, device) filled; then again with col_idx (nnz int32, device). */
+int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
+                           int32_t n_dofs, int64_t* row_ptr, int32_t* col_idx, int64_t* nnz,
+                           void* stream);
+
+/* Incidence (dof -> (cell, local) pairs in ascending cell order) used by the
+ * deterministic assembly; inc_ptr: n_dofs + 1 int64, inc: n_cells x n_loc int64
+ * (packed cell * n_loc + local). */
+int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
+                         int32_t n_dofs, int64_t* inc_ptr, int64_t* inc, void* stream);
+
+/* Replaces assemble_matrix (assembly.cpp:41-88): scatter-add of local matrices into
+ * CSR values. mode 0 = atomic (red.global, order-free), 1 = deterministic (each entry
+ * summed in ascending cell order, bitwise equal to the reference at fmt).
+ * locals: n_cells x n_loc x n_loc, fp32 (locals_fmt 2) or fp64 (3); values fp32 (fmt 2)
+ * or fp64 (fmt 3). inc_ptr/inc needed for mode 1 (may be NULL for mode 0).
+ * cell_begin/cell_end restrict the contributing cells (multi-GPU slabs); values are
+ * accumulated onto their current contents when accumulate != 0 (else overwritten). */
+int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
+                        int64_t cell_end, int n_loc, const int32_t* cell_dofs,
+                        int32_t n_dofs, const int64_t* row_ptr, const int32_t* col_idx,
+                        const int64_t* inc_ptr, const int64_t* inc, void* values, int fmt,
+                        int mode, int accumulate, int32_t row_begin, int32_t row_end,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,456 @@
+// capi.cu -- the extern "C" boundary (include/mpfem_b200.h): setup handles, the
+// batched cell-matrix driver (K1 geom_w -> K2 GEMM), host-buffer wrapper.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mpfem_b200.h"
+#include "cellmat_simt.cuh"
+#include "cellmat_tc.cuh"
+#include "geom_w.cuh"
+#include "host_setup.hpp"
+
+using namespace mpfem_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw Error(MPFEM_B200_RUNTIME_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    f();
+    return MPFEM_B200_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MPFEM_B200_RUNTIME_ERROR;
+  }
+}
+
+// Device dispatch of a setup: which K2 runs and in which element types.
+enum Path : int { kPathTC = 0, kPathF32 = 1, kPathF64 = 2 };
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    CUDA_OK(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn tensor_map_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  if (!fn) throw Error(MPFEM_B200_RUNTIME_ERROR, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                        uint32_t box_inner, uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(MPFEM_B200_RUNTIME_ERROR, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+int device_sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+}  // namespace
+
+struct mpfem_b200_setup_s {
+  int p = 0, form = 0, up = 3, ug = 3, uq = 3, us = 3, engine = 0;
+  int n_phi = 0, n_q = 0, n_d = 1, n_blocks = 1;
+  int64_t k = 0, k_pad = 0, n_out = 0, n_out_pad = 0;
+  int path = kPathF64;
+  int acc_f16 = 0;
+  int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
+  Rule rule;
+  DevBuf d_rule_w, d_rule_x, d_tab_up, d_B, d_T;
+  DevBuf d_W, d_flags, d_error;
+  // host-API staging
+  DevBuf h_verts, h_cells, h_coef, h_out;
+  int last_launches = 0;
+  int device = 0;
+};
+
+namespace {
+
+size_t elem_size(int w_type) { return w_type <= 1 ? 2 : (w_type == 2 ? 4 : 8); }
+
+void validate(int cell_kind, int dim, int p, int form, const int* fmts, int engine, int n_batch) {
+  if (cell_kind != 0 || dim != 3)
+    throw Error(MPFEM_B200_CONFIG_ERROR, "the B200 path supports affine tetrahedra (simplex, dim 3)");
+  if (p < 1 || p > 8) throw Error(MPFEM_B200_CONFIG_ERROR, "element degree must be in [1, 8]");
+  if (form != 0 && form != 1) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown form");
+  for (int i = 0; i < 4; ++i)
+    if (fmts[i] < 0 || fmts[i] > 3) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown float format");
+  if (engine < 0 || engine > 2) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown engine");
+  // validate_config (kernels.cpp:29-40)
+  if (n_batch < 1) throw Error(MPFEM_B200_CONFIG_ERROR, "batch size must be positive");
+  if (engine == 2 && (fmts[3] != 0 || fmts[2] != 2))
+    throw Error(MPFEM_B200_CONFIG_ERROR,
+                "matrix engine requires the unit's native formats: u_s = bf16, u_q = fp32");
+}
+
+void choose_path(mpfem_b200_setup_s& S) {
+  const int us = S.us, uq = S.uq;
+  if ((us == 0 || us == 1) && uq == 2) {
+    S.path = kPathTC;
+    S.w_type = us == 1 ? 0 : 1;
+  } else if (us == 1 && uq == 1) {
+    S.path = kPathTC;
+    S.w_type = 0;
+    S.acc_f16 = 1;
+  } else if (uq == 3) {
+    S.path = kPathF64;  // any storage, fp64 accumulation; operands rounded to u_s
+    S.w_type = 3;
+  } else if (us == 2 && uq == 2) {
+    S.path = kPathF32;
+    S.w_type = 2;
+  } else {
+    throw Error(MPFEM_B200_CONFIG_ERROR,
+                "unsupported accumulation: u_q must be fp32 or fp64, or fp16 with fp16 storage");
+  }
+}
+
+void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
+                 int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
+                 int w_type, cudaStream_t st) {
+  GeomWParams P;
+  P.verts = verts;
+  P.cells = cells;
+  P.n_cells = n;
+  P.coef_kind = coef_kind;
+  P.coef = coef;
+  P.coef_stride = coef_stride;
+  P.rule_w = static_cast<const double*>(S.d_rule_w.p);
+  P.rule_x = static_cast<const double*>(S.d_rule_x.p);
+  P.tab_up = static_cast<const double*>(S.d_tab_up.p);
+  P.n_phi = S.n_phi;
+  P.n_q = S.n_q;
+  P.up = S.up;
+  P.ug = S.ug;
+  P.us = S.us;
+  P.poisson = S.form;
+  P.k_pad = k_pad;
+  P.w_type = w_type;
+  P.W = W;
+  P.flags = static_cast<uint32_t*>(S.d_flags.p);
+  P.error = static_cast<int*>(S.d_error.p);
+  const int64_t threads = n * 32;
+  const unsigned grid = unsigned((threads + 255) / 256);
+  switch (w_type) {
+    case 0: geom_w_kernel<__half><<<grid, 256, 0, st>>>(P); break;
+    case 1: geom_w_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(P); break;
+    case 2: geom_w_kernel<float><<<grid, 256, 0, st>>>(P); break;
+    default: geom_w_kernel<double><<<grid, 256, 0, st>>>(P); break;
+  }
+  CUDA_OK(cudaGetLastError());
+}
+
+void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, int64_t stride) {
+  if (coef_kind < 0 || coef_kind > 3) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown coefficient kind");
+  if (coef_kind == 2 && (!coef || stride < 4))
+    throw Error(MPFEM_B200_CONFIG_ERROR, "affine coefficient needs 4 values per cell");
+  if (coef_kind == 3 && (!coef || stride < S.n_phi))
+    throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
+}
+
+void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells,
+                       int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* out,
+                       int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+  check_coef(S, coef_kind, coef, coef_stride);
+  if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
+  if (out_pitch < S.n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
+  S.last_launches = 0;
+  if (flags) {
+    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
+    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
+  }
+  if (n == 0) return;
+  S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
+  launch_geom(S, verts, cells, n, coef_kind, coef, coef_stride, S.d_W.p, S.k_pad, S.w_type, st);
+  ++S.last_launches;
+  if (S.path == kPathTC) {
+    const CUtensorMapDataType dt =
+        S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc::BM);
+    CUtensorMap tb = make_map_2d(S.d_W.p, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc::BN);
+    tc::Params P;
+    P.n_cells = n;
+    P.n_out = int(S.n_out);
+    P.n_out_tiles = int(S.n_out_pad / tc::BM);
+    P.n_cell_tiles = int((n + tc::BN - 1) / tc::BN);
+    P.num_k_blocks = int(S.k_pad / tc::BK);
+    P.out = static_cast<float*>(out);
+    P.out_pitch = out_pitch;
+    P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc::BM, tc::BN);
+    P.acc_f16 = S.acc_f16;
+    P.flags = static_cast<uint32_t*>(S.d_flags.p);
+    const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
+    const int grid = int(std::min<int64_t>(tiles, device_sm_count()));
+    static bool attr_set = false;
+    if (!attr_set) {
+      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   tc::SMEM_BYTES));
+      attr_set = true;
+    }
+    tc::cellmat_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
+  } else if (S.path == kPathF32) {
+    constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
+    dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
+    cellmat_simt_kernel<float, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
+        static_cast<const float*>(S.d_W.p), static_cast<const float*>(S.d_T.p),
+        static_cast<float*>(out), n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch,
+        static_cast<uint32_t*>(S.d_flags.p));
+  } else {
+    constexpr int BM = 64, BN = 128, BK = 16, TM = 4, TN = 8;
+    dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
+    cellmat_simt_kernel<double, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
+        static_cast<const double*>(S.d_W.p), static_cast<const double*>(S.d_T.p),
+        static_cast<double*>(out), n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch,
+        static_cast<uint32_t*>(S.d_flags.p));
+  }
+  CUDA_OK(cudaGetLastError());
+  ++S.last_launches;
+  if (flags) {
+    uint32_t h[2] = {0, 0};
+    CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(&h[1], S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    *flags |= h[0];
+    if (h[1] == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpfem_b200_last_error(void) { return g_last_error.c_str(); }
+const char* mpfem_b200_version(void) { return "mpfem_b200 0.1 sm_100a"; }
+
+int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, int u_g, int u_q,
+                            int u_s, int engine, int n_batch, mpfem_b200_setup_t* out) {
+  return guarded([&] {
+    if (!out) throw Error(MPFEM_B200_CONFIG_ERROR, "null output handle");
+    int fmts[4] = {u_p, u_g, u_q, u_s};
+    validate(cell_kind, dim, p, form, fmts, engine, n_batch);
+    auto S = std::make_unique<mpfem_b200_setup_s>();
+    S->p = p;
+    S->form = form;
+    S->up = u_p;
+    S->ug = u_g;
+    S->uq = u_q;
+    S->us = u_s;
+    S->engine = engine;
+    choose_path(*S);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(MPFEM_B200_RUNTIME_ERROR, "no CUDA device: the B200 path has no CPU fallback");
+    CUDA_OK(cudaGetDevice(&S->device));
+    S->rule = simplex_rule(p);
+    Basis basis = simplex_basis(p);
+    S->n_phi = basis.n_phi;
+    S->n_q = S->rule.n_q;
+    S->n_d = form ? 3 : 1;
+    S->n_blocks = form ? 6 : 1;
+    S->k = int64_t(S->n_blocks) * S->n_q;
+    const int64_t kal = S->path == kPathTC ? tc::BK : 16;
+    S->k_pad = (S->k + kal - 1) / kal * kal;
+    S->n_out = int64_t(S->n_phi) * S->n_phi;
+    S->n_out_pad = (S->n_out + 127) / 128 * 128;
+    uint32_t fl = 0;
+    std::vector<double> tab_up = tabulate(basis, S->rule, u_p, u_p, false, fl);
+    std::vector<double> B = tabulate(basis, S->rule, 3, 3, form == 1, fl);
+    S->d_rule_w.ensure(sizeof(double) * S->n_q);
+    S->d_rule_x.ensure(sizeof(double) * 3 * S->n_q);
+    S->d_tab_up.ensure(sizeof(double) * tab_up.size());
+    S->d_B.ensure(sizeof(double) * B.size());
+    CUDA_OK(cudaMemcpy(S->d_rule_w.p, S->rule.weights.data(), sizeof(double) * S->n_q, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(S->d_rule_x.p, S->rule.points.data(), sizeof(double) * 3 * S->n_q, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(S->d_tab_up.p, tab_up.data(), sizeof(double) * tab_up.size(), cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(S->d_B.p, B.data(), sizeof(double) * B.size(), cudaMemcpyHostToDevice));
+    S->d_flags.ensure(16);
+    S->d_error.ensure(16);
+    CUDA_OK(cudaMemset(S->d_flags.p, 0, 16));
+    CUDA_OK(cudaMemset(S->d_error.p, 0, 16));
+    const size_t tbytes = size_t(S->k_pad) * size_t(S->n_out_pad) * elem_size(S->w_type);
+    S->d_T.ensure(tbytes);
+    const int transposed = S->path == kPathTC;
+    const int64_t total = S->k_pad * S->n_out_pad;
+    const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
+    const double* dB = static_cast<const double*>(S->d_B.p);
+    switch (S->w_type) {
+      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+    }
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaDeviceSynchronize());
+    *out = S.release();
+  });
+}
+
+int mpfem_b200_setup_destroy(mpfem_b200_setup_t setup) {
+  return guarded([&] { delete setup; });
+}
+
+int mpfem_b200_setup_info(mpfem_b200_setup_t S, int* n_phi, int* n_q, int* n_d, int64_t* k,
+                          int64_t* k_pad, int* path) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (n_phi) *n_phi = S->n_phi;
+    if (n_q) *n_q = S->n_q;
+    if (n_d) *n_d = S->n_d;
+    if (k) *k = S->k;
+    if (k_pad) *k_pad = S->k_pad;
+    if (path) *path = S->path;
+  });
+}
+
+int mpfem_b200_setup_rule(mpfem_b200_setup_t S, double* points, double* weights) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (points) std::memcpy(points, S->rule.points.data(), sizeof(double) * 3 * S->n_q);
+    if (weights) std::memcpy(weights, S->rule.weights.data(), sizeof(double) * S->n_q);
+  });
+}
+
+int mpfem_b200_reserve(mpfem_b200_setup_t S, int64_t n_cells) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    S->d_W.ensure(size_t(n_cells) * size_t(S->k_pad) * elem_size(S->w_type));
+  });
+}
+
+int mpfem_b200_cell_matrices(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
+                             int64_t n_cells, int coef_kind, const double* coef,
+                             int64_t coef_stride, void* out, int64_t out_pitch, void* stream,
+                             uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, out, out_pitch,
+                      static_cast<cudaStream_t>(stream), flags);
+  });
+}
+
+int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t S, const double* verts, int64_t n_verts,
+                                  const int32_t* cells, int64_t n_cells, int coef_kind,
+                                  const double* coef, int64_t coef_stride, void* out,
+                                  int64_t out_pitch, void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    check_coef(*S, coef_kind, coef, coef_stride);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 12);
+    S->h_verts.ensure(vbytes);
+    CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
+    const int32_t* dcells = nullptr;
+    if (cells) {
+      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * 4);
+      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * 4,
+                              cudaMemcpyHostToDevice, st));
+      dcells = static_cast<const int32_t*>(S->h_cells.p);
+    }
+    const double* dcoef = nullptr;
+    if (coef && (coef_kind == 2 || coef_kind == 3)) {
+      const size_t cb = sizeof(double) * size_t(n_cells) * size_t(coef_stride);
+      S->h_coef.ensure(cb);
+      CUDA_OK(cudaMemcpyAsync(S->h_coef.p, coef, cb, cudaMemcpyHostToDevice, st));
+      dcoef = static_cast<const double*>(S->h_coef.p);
+    }
+    const size_t esz = S->path == kPathF64 ? 8 : 4;
+    const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
+    S->h_out.ensure(obytes);
+    run_cell_matrices(*S, static_cast<const double*>(S->h_verts.p), dcells, n_cells, coef_kind, dcoef,
+                      coef_stride, S->h_out.p, out_pitch, st, flags);
+    CUDA_OK(cudaMemcpyAsync(out, S->h_out.p, obytes, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int mpfem_b200_scaled_weights(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
+                              int64_t n_cells, int coef_kind, const double* coef,
+                              int64_t coef_stride, double* out, void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    check_coef(*S, coef_kind, coef, coef_stride);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_OK(cudaMemsetAsync(S->d_flags.p, 0, 4, st));
+    if (n_cells > 0)
+      launch_geom(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, out, S->k, 3, st);
+    if (flags) {
+      uint32_t h = 0;
+      CUDA_OK(cudaMemcpyAsync(&h, S->d_flags.p, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+      *flags |= h;
+    }
+  });
+}
+
+int mpfem_b200_last_launch_count(mpfem_b200_setup_t S) { return S ? S->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+// device_fp.cuh -- reduced-precision arithmetic on the device, bit-identical to the
+// reference's emulation (softfloat.hpp:72-216): every op is computed once in binary64
+// (explicit _rn intrinsics, so nvcc cannot contract into FMA) and rounded once to the
+// target format. For t <= 25 significand bits the binary64 intermediate cannot cause a
+// double-rounding error (2t + 2 <= 53), which is the reference's own argument.
+#pragma once
+#include <cstdint>
+
+namespace mpfem_b200 {
+
+enum Fmt : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
+enum FlagBits : uint32_t { kOverflow = 1u, kUnderflow = 2u, kInvalid = 4u, kDivzero = 8u };
+
+struct FmtParams {
+  int drop;           // 53 - t
+  double min_normal;  // 2^e_min
+  double inv_min_sub; // 1 / (2^(e_min + 1 - t)), a power of two
+  double min_sub;
+  double max_finite;
+};
+
+__host__ __device__ inline FmtParams fmt_params(int f) {
+  switch (f) {
+    case kBF16: return {45, 0x1.0p-126, 0x1.0p133, 0x1.0p-133, 0x1.fep127};
+    case kFP16: return {42, 0x1.0p-14, 0x1.0p24, 0x1.0p-24, 65504.0};
+    default:    return {29, 0x1.0p-126, 0x1.0p149, 0x1.0p-149, 0x1.fffffep127};
+  }
+}
+
+__device__ __forceinline__ double canonical_nan_d() {
+  return __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// round_to(x, f) with SubnormalPolicy::supported (softfloat.hpp:147-157).
+__device__ __forceinline__ double dround(double x, int f, uint32_t& fl) {
+  if (f == kFP64) {
+    if (isnan(x)) { fl |= kInvalid; return canonical_nan_d(); }
+    return x;
+  }
+  if (f == kFP32) {
+    float g = __double2float_rn(x);
+    if (isnan(g)) { fl |= kInvalid; return canonical_nan_d(); }
+    if (isinf(g)) { if (!isinf(x)) fl |= kOverflow; return (double)g; }
+    if (x != 0.0 && fabs(x) < 0x1.0p-126 && (double)g != x) fl |= kUnderflow;
+    return (double)g;
+  }
+  const FmtParams fp = fmt_params(f);
+  unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+  unsigned long long mag = bits & 0x7fffffffffffffffull;
+  if (mag >= 0x7ff0000000000000ull) {
+    if (mag > 0x7ff0000000000000ull) { fl |= kInvalid; return canonical_nan_d(); }
+    return x;
+  }
+  if (mag == 0) return x;
+  double ax = __longlong_as_double((long long)mag);
+  if (ax < fp.min_normal) {
+    double q = __dmul_rn(rint(__dmul_rn(ax, fp.inv_min_sub)), fp.min_sub);
+    double r = copysign(q, x);
+    if (r != x) fl |= kUnderflow;
+    return r;
+  }
+  unsigned long long mask = (1ull << fp.drop) - 1ull;
+  unsigned long long rem = bits & mask;
+  unsigned long long half = 1ull << (fp.drop - 1);
+  bits &= ~mask;
+  if (rem > half || (rem == half && (bits & (1ull << fp.drop)))) bits += 1ull << fp.drop;
+  double r = __longlong_as_double((long long)bits);
+  if (fabs(r) > fp.max_finite) { fl |= kOverflow; return copysign(__longlong_as_double(0x7ff0000000000000ll), x); }
+  return r;
+}
+
+// fp_op at format f (softfloat.hpp:170-186): exact binary64 op, one rounding.
+__device__ __forceinline__ double dadd(double a, double b, int f, uint32_t& fl) {
+  double r = __dadd_rn(a, b);
+  if (f == kFP64 && isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  return dround(r, f, fl);
+}
+__device__ __forceinline__ double dsub(double a, double b, int f, uint32_t& fl) {
+  double r = __dsub_rn(a, b);
+  if (f == kFP64 && isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  return dround(r, f, fl);
+}
+__device__ __forceinline__ double dmul(double a, double b, int f, uint32_t& fl) {
+  double r = __dmul_rn(a, b);
+  if (f == kFP64 && isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  return dround(r, f, fl);
+}
+__device__ __forceinline__ double ddiv(double a, double b, int f, uint32_t& fl) {
+  if (b == 0.0 && a != 0.0 && !isnan(a) && !isinf(a)) fl |= kDivzero;
+  double r = __ddiv_rn(a, b);
+  if (f == kFP64 && isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  return dround(r, f, fl);
+}
+
+// Affine-tet geometry at format f, the exact op sequence of cell_geometry's reduced-
+// precision fields (geometry.cpp:12-118): J through the P1 basis gradients at the
+// centroid (-1,-1,-1 / e_s, exact), LU with partial pivoting, det, inverse by three
+// solves, geometry tensor upper triangle mirrored. Returns false on an exact zero pivot.
+struct TetGeometry {
+  double det, abs_det;
+  double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson); g[0] = |det| (mass)
+};
+
+__device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool poisson,
+                                             TetGeometry& out, uint32_t& fl) {
+  // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
+  double jac[3][3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+  #pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double x = dround(v[k][i], f, fl);
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
+        jac[i][s] = dadd(jac[i][s], dmul(x, g, f, fl), f, fl);
+      }
+    }
+  }
+  // lu_decompose (geometry.cpp:33-57)
+  double lu[3][3];
+  int perm[3] = {0, 1, 2};
+  int sign = 1;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) lu[i][s] = jac[i][s];
+  #pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    int pivot = col;
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (fabs(lu[r][col]) > fabs(lu[pivot][col])) pivot = r;
+    if (lu[pivot][col] == 0.0) return false;
+    if (pivot != col) {
+      #pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double t = lu[pivot][c];
+        lu[pivot][c] = lu[col][c];
+        lu[col][c] = t;
+      }
+      int t = perm[pivot];
+      perm[pivot] = perm[col];
+      perm[col] = t;
+      sign = -sign;
+    }
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      double m = ddiv(lu[r][col], lu[col][col], f, fl);
+      lu[r][col] = m;
+      #pragma unroll
+      for (int c = col + 1; c < 3; ++c) lu[r][c] = dsub(lu[r][c], dmul(m, lu[col][c], f, fl), f, fl);
+    }
+  }
+  double det = (double)sign;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) det = dmul(det, lu[i][i], f, fl);
+  out.det = det;
+  out.abs_det = fabs(det);
+  if (!poisson) {
+    out.g[0] = out.abs_det;
+    return true;
+  }
+  // inverse_lu (geometry.cpp:70-95); the LU is recomputed there but is identical.
+  double inv[3][3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double y[3];
+    #pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double s = perm[r] == k ? 1.0 : 0.0;
+      #pragma unroll
+      for (int c = 0; c < r; ++c) s = dsub(s, dmul(lu[r][c], y[c], f, fl), f, fl);
+      y[r] = s;
+    }
+    #pragma unroll
+    for (int r = 2; r >= 0; --r) {
+      double s = y[r];
+      #pragma unroll
+      for (int c = r + 1; c < 3; ++c) s = dsub(s, dmul(lu[r][c], inv[c][k], f, fl), f, fl);
+      inv[r][k] = ddiv(s, lu[r][r], f, fl);
+    }
+  }
+  // geometry_tensor (geometry.cpp:97-118)
+  int idx = 0;
+  #pragma unroll
+  for (int s = 0; s < 3; ++s)
+    #pragma unroll
+    for (int t = s; t < 3; ++t) {
+      double dot = 0.0;
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) dot = dadd(dot, dmul(inv[s][k], inv[t][k], f, fl), f, fl);
+      out.g[idx++] = dmul(out.abs_det, dot, f, fl);
+    }
+  return true;
+}
+
+// Analytic coefficient at a quadrature point (BASELINE configs 0-2,4): x_q = v0 + J xi
+// in binary64, left to right, then c = 1 + 0.5 sin(2 pi x) cos(2 pi y) e^z.
+__device__ __forceinline__ double coef_sincosexp(const double v[4][3], const double* xi) {
+  double x[3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = v[0][i];
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) acc = __dadd_rn(acc, __dmul_rn(__dsub_rn(v[s + 1][i], v[0][i]), xi[s]));
+    x[i] = acc;
+  }
+  const double two_pi = 6.283185307179586476925286766559;
+  double s = sin(__dmul_rn(two_pi, x[0]));
+  double c = cos(__dmul_rn(two_pi, x[1]));
+  double e = exp(x[2]);
+  return __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(0.5, s), c), e));
+}
+
+// Config-3 coefficient: c = 10^(6 u(x_q)), u affine with vertex values u4.
+__device__ __forceinline__ double coef_exp10_affine(const double* u4, const double* xi) {
+  double l0 = __dsub_rn(__dsub_rn(__dsub_rn(1.0, xi[0]), xi[1]), xi[2]);
+  double u = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(u4[0], l0), __dmul_rn(u4[1], xi[0])),
+                                 __dmul_rn(u4[2], xi[1])),
+                       __dmul_rn(u4[3], xi[2]));
+  return pow(10.0, __dmul_rn(6.0, u));
+}
+
+}  // namespace mpfem_b200

@@ -1,0 +1,153 @@
+// geom_w.cuh -- K1: per-cell geometry + coefficient + scaled-weight pass.
+//
+// One warp per cell. Every lane evaluates the cell geometry at u_g (identical op
+// sequence, so no broadcast is needed), then lanes stride over quadrature points and
+// write the cell's row of the GEMM operand W:
+//   W[c, b*n_q + q] = round_us(round_ug(round_ug(omega_q * G_b) * zhat_q))
+// which is build_C (kernels.cpp:177-197) with the (s,t) pairs packed to the upper
+// triangle b = (s<=t): (0,0),(0,1),(0,2),(1,1),(1,2),(2,2) (C is symmetric bitwise, so
+// the packed GEMM operand T carries B_s B_t + B_t B_s for s<t).
+// zhat_q is c(x_q) rounded to u_g for analytic coefficients, or eval_z_at_ug
+// (kernels.cpp:114-136) for nodal coefficients. Entries K..K_pad are zero.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "device_fp.cuh"
+
+namespace mpfem_b200 {
+
+struct GeomWParams {
+  const double* verts;     // private: n_cells x 12 ; mesh: vertex table n_verts x 3
+  const int32_t* cells;    // NULL or n_cells x 4
+  int64_t n_cells;
+  int coef_kind;
+  const double* coef;
+  int64_t coef_stride;
+  const double* rule_w;    // n_q
+  const double* rule_x;    // n_q x 3
+  const double* tab_up;    // n_phi x n_q basis values at u_p (nodal path)
+  int n_phi, n_q, up, ug, us;
+  int poisson;
+  int64_t k_pad;
+  int w_type;              // 0 fp16 bits, 1 bf16 bits, 2 fp32, 3 fp64
+  void* W;
+  uint32_t* flags;
+  int* error;              // set to 3 on a singular cell
+};
+
+template <typename T>
+__device__ __forceinline__ void store_w(void* W, int64_t idx, double v);
+template <>
+__device__ __forceinline__ void store_w<__half>(void* W, int64_t idx, double v) {
+  static_cast<__half*>(W)[idx] = __float2half_rn(__double2float_rn(v));  // exact: v is fp16
+}
+template <>
+__device__ __forceinline__ void store_w<__nv_bfloat16>(void* W, int64_t idx, double v) {
+  static_cast<__nv_bfloat16*>(W)[idx] = __float2bfloat16_rn(__double2float_rn(v));  // exact
+}
+template <>
+__device__ __forceinline__ void store_w<float>(void* W, int64_t idx, double v) {
+  static_cast<float*>(W)[idx] = __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) {
+  static_cast<double*>(W)[idx] = v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) geom_w_kernel(GeomWParams P) {
+  const int lane = threadIdx.x & 31;
+  const int64_t cell = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (cell >= P.n_cells) return;
+  uint32_t fl = 0;
+  double v[4][3];
+  if (P.cells) {
+    #pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int64_t vid = P.cells[cell * 4 + k];
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
+    }
+  } else {
+    #pragma unroll
+    for (int k = 0; k < 4; ++k)
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
+  }
+  TetGeometry g;
+  bool ok = tet_geometry(v, P.ug, P.poisson != 0, g, fl);
+  if (!ok) {
+    if (lane == 0) atomicExch(P.error, 3);
+    return;
+  }
+  const int nb = P.poisson ? 6 : 1;
+  const int64_t row = cell * P.k_pad;
+  const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
+  for (int q = lane; q < P.n_q; q += 32) {
+    double zq = 1.0;
+    bool have_z = true;
+    switch (P.coef_kind) {
+      case 1: zq = dround(coef_sincosexp(v, P.rule_x + 3 * q), P.ug, fl); break;
+      case 2: zq = dround(coef_exp10_affine(coef, P.rule_x + 3 * q), P.ug, fl); break;
+      case 3: {
+        double acc = 0.0;
+        for (int k = 0; k < P.n_phi; ++k)
+          acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * P.n_q + q], P.up, fl),
+                     P.up, fl);
+        zq = dround(acc, P.ug, fl);
+        break;
+      }
+      default: have_z = false;
+    }
+    double omega = dround(P.rule_w[q], P.ug, fl);
+    for (int b = 0; b < nb; ++b) {
+      double val = dmul(omega, g.g[b], P.ug, fl);
+      if (have_z) val = dmul(val, zq, P.ug, fl);
+      store_w<T>(P.W, row + int64_t(b) * P.n_q + q, dround(val, P.us, fl));
+    }
+  }
+  for (int64_t k = int64_t(nb) * P.n_q + lane; k < P.k_pad; k += 32) store_w<T>(P.W, row + k, 0.0);
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (lane == 0 && fl) atomicOr(P.flags, fl);
+}
+
+// Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
+//   T[(b,q), (i,j)] = round_us(B_s[i,q] B_t[j,q] (+ B_t[i,q] B_s[j,q] if s<t)).
+// transposed != 0 stores Tt[o][k] (K contiguous; the tcgen05 A operand), else T[k][o].
+template <typename T>
+__global__ void build_t_kernel(const double* B, int n_phi, int n_q, int poisson, int us,
+                               int64_t k_len, int64_t k_pad, int64_t n_out, int64_t n_out_pad,
+                               int transposed, void* out) {
+  const int64_t total = k_pad * n_out_pad;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    int64_t k, o;
+    if (transposed) { o = idx / k_pad; k = idx % k_pad; }
+    else { k = idx / n_out_pad; o = idx % n_out_pad; }
+    double val = 0.0;
+    if (k < k_len && o < n_out) {
+      int b = int(k / n_q), q = int(k % n_q);
+      int i = int(o / n_phi), j = int(o % n_phi);
+      int s = 0, t = 0;
+      if (poisson) {
+        const int ss[6] = {0, 0, 0, 1, 1, 2}, tt[6] = {0, 1, 2, 1, 2, 2};
+        s = ss[b];
+        t = tt[b];
+      }
+      const double bsi = B[(int64_t(s) * n_phi + i) * n_q + q];
+      const double btj = B[(int64_t(t) * n_phi + j) * n_q + q];
+      val = __dmul_rn(bsi, btj);
+      if (s != t) {
+        const double bti = B[(int64_t(t) * n_phi + i) * n_q + q];
+        const double bsj = B[(int64_t(s) * n_phi + j) * n_q + q];
+        val = __dadd_rn(val, __dmul_rn(bti, bsj));
+      }
+      uint32_t fl = 0;
+      val = dround(val, us, fl);
+    }
+    store_w<T>(out, idx, val);
+  }
+}
+
+}  // namespace mpfem_b200
