@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark of the B200 hot path (driver contract in DESIGN.md §6).
+
+Workload (BASELINE.json configs[1]): Poisson stiffness cell matrices, Lagrange P4 on 65,536
+seeded affine tetrahedra (reference tet + U(-0.15, 0.15) noise, seed 1 + rank), the
+125-point collapsed Gauss-Jacobi rule, c(x) = 1 + 0.5 sin(2 pi x) cos(2 pi y) e^z, mixed
+precision (u_p = fp32, G_K at u_g = fp64, u_q = fp32 TMEM accumulation, u_s = fp16
+storage), 35 x 35 fp32 outputs. One step = vertices in HBM -> geometry/scaled weights (K1)
+-> tcgen05 cell-matrix GEMM (K2) -> matrices in HBM.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--sweep]
+
+N > 1 runs under torchrun: every rank processes its own 65,536 cells (weak scaling, no
+collective on the data path); time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P_DEG = 4
+N_CELLS = 65536
+METRIC = "cell matrices/s"
+UNIT = "cells/s"
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def nphi(p):
+    return (p + 1) * (p + 2) * (p + 3) // 6
+
+
+def work_per_cell(p, form, out_bytes=4):
+    n = nphi(p)
+    nq = (p + 1) ** 3
+    nd = 3 if form == 1 else 1
+    flops = 2.0 * n * n * nq * nd * nd          # SURVEY 8d F_cell (dense, reference Alg. 1 depth)
+    bytes_ = 96.0 + out_bytes * n * n           # fp64 vertices in + full matrix out
+    return flops, bytes_
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sms:
+            return None
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": float(max(maxs)),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_baseline(p, form, cfg_tuple, verts, coef_kind, target_s=10.0):
+    """The reference's own CPU path (oracle/_ref, compiled from the unmodified sources) on
+    this host's cores, on a bounded prefix sample of the same cells; the C restatement
+    (oracle/) stands in where _ref was not built. Returns (cells/s, kind, cores, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle, Reference, reference_available
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    v = verts.reshape(-1, 12)
+    if reference_available():
+        R = Reference()
+        n0 = min(v.shape[0], 2 * cores)
+        secs, _ = R.cpu_baseline(p, form, cfg_tuple, v[:n0], coef_kind, None, cores)
+        rate = n0 / max(secs, 1e-9)
+        n = int(min(v.shape[0], max(n0, rate * target_s)))
+        secs, _ = R.cpu_baseline(p, form, cfg_tuple, v[:n], coef_kind, None, cores)
+        return n / secs, "reference", cores, f"first {n} of the {v.shape[0]} cells, MPFEM_THREADS={cores}"
+    O = Oracle()
+    n = 2
+    t = time.perf_counter()
+    O.bilinear(p, form, cfg_tuple, v[:n], coef_kind, None)
+    dt = time.perf_counter() - t
+    n2 = int(max(2, min(v.shape[0], (target_s / max(dt, 1e-9)) * n)))
+    t = time.perf_counter()
+    O.bilinear(p, form, cfg_tuple, v[:n2], coef_kind, None)
+    dt = time.perf_counter() - t
+    return n2 / dt, "port", 1, f"first {n2} of the {v.shape[0]} cells, 1 thread (C restatement)"
+
+
+MIXED_CFG = dict(u_p=2, u_g=3, u_q=2, u_s=1, engine=0)  # config 1: G_K at fp64
+
+
+def workload_config():
+    return {"workload": "config1: poisson P4 stiffness, 65536 seeded affine tets, mixed "
+                        "(u_s=fp16, fp32 TMEM accumulation, G_K fp64), c(x)=1+0.5sin(2pi x)cos(2pi y)e^z",
+            "p": P_DEG, "cells_per_gpu": N_CELLS, "form": "poisson", "mode": "mixed",
+            "u_p": "fp32", "u_g": "fp64", "u_q": "fp32", "u_s": "fp16",
+            "l2": "flushed before every timed step (256 MiB write)",
+            "output": "fp32, 35x35 row-major per cell"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import paper_2410_12614_b200 as mp  # host-only generator (no GPU needed)
+    verts, _ = mp.gen_tets(0, 1, N_CELLS)
+    cfg = (MIXED_CFG["u_p"], MIXED_CFG["u_g"], MIXED_CFG["u_q"], MIXED_CFG["u_s"], MIXED_CFG["engine"])
+    rates = []
+    info = None
+    for _ in range(args.warmup):
+        cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=2.0)
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        r, kind, cores, sample = cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=args.ref_seconds)
+        rates.append(r)
+        info = (kind, cores, sample)
+    wall = time.perf_counter() - t_all
+    value = float(np.mean(rates))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * N_CELLS / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (seeded)", "config": workload_config(),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[1], "kind": info[0],
+                             "sample": info[2]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+def run_sweep(mp, torch, dev):
+    """BASELINE config 2: p = 1..8, mass and Poisson, mixed (bf16 storage) and fp64; cell
+    count per p chosen so the outputs total 4 GiB (fp32: 2^32 / (4 n_phi^2))."""
+    hbm, tc_peak, _, _ = peaks()
+    res = []
+    for p in range(1, 9):
+        for form in (0, 1):
+            for mode in ("mixed", "fp64"):
+                if mode == "mixed":
+                    cfg = mp.KernelConfig(form=form, u_p=2, u_g=2, u_q=2, u_s=0, engine=2)
+                    ob = 4
+                else:
+                    cfg = mp.KernelConfig(form=form)
+                    ob = 8
+                n = (1 << 32) // (ob * nphi(p) ** 2)
+                if mode == "fp64":
+                    n = min(n, 1 << 20)  # bounded: fp64 is compute-bound, fewer cells suffice
+                verts, _ = mp.gen_tets(0, 7 + p, n)
+                vd = torch.from_numpy(verts).to(dev)
+                s = mp.make_setup(p, cfg)
+                s.reserve(n)
+                out = torch.empty((n, nphi(p) ** 2), dtype=torch.float32 if ob == 4 else torch.float64, device=dev)
+                for _ in range(2):
+                    s.cell_matrices(vd, None, 1, out=out)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 3
+                e0.record()
+                for _ in range(reps):
+                    s.cell_matrices(vd, None, 1, out=out)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                f, b = work_per_cell(p, form, ob)
+                t_roof = max(n * f / (tc_peak * 1e12) if mode == "mixed" else 0.0, n * b / (hbm * 1e9))
+                res.append({"p": p, "form": "poisson" if form else "mass", "mode": mode, "cells": n,
+                            "ms": ms, "cells_per_s": n / (ms * 1e-3),
+                            "tflops_dense_equiv": n * f / (ms * 1e-3) / 1e12,
+                            "hbm_gbs_algorithmic": n * b / (ms * 1e-3) / 1e9,
+                            "roofline_frac": (t_roof / (ms * 1e-3)) if mode == "mixed" else None})
+                del s, out, vd
+                torch.cuda.empty_cache()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--sweep", action="store_true", help="add the config-2 p=1..8 sweep")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_2410_12614_b200 as mp
+
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    hbm, tc_peak, tc_sus, peak_src = peaks()
+
+    verts_np, _ = mp.gen_tets(0, 1 + rank, N_CELLS)
+    verts_pinned = torch.from_numpy(verts_np).pin_memory()
+    vd = verts_pinned.to(dev)
+    cfg = mp.KernelConfig(form=mp.FormKind.poisson, **{k: v for k, v in MIXED_CFG.items()})
+    setup = mp.make_setup(P_DEG, cfg)
+    setup.reserve(N_CELLS)
+    n2 = setup.n_phi ** 2
+    out = torch.empty((N_CELLS, n2), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        setup.cell_matrices(vd, None, mp.CoefKind.sincosexp, out=out)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each, CUDA events on the launch stream
+    setup.set_timing(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k_ms = []
+    sampler = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.05)
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        k_ms.append(None)
+        if i % 16 == 15 or i == args.steps - 1:
+            pass
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    launches = setup.last_launch_count() * args.steps
+    setup.set_timing(False)
+
+    # per-kernel durations (same stream, CUDA events recorded by the library) on a short
+    # re-run of identical steps; the dominant kernel is K2
+    setup.set_timing(True)
+    k1, k2 = [], []
+    for _ in range(20):
+        flush.zero_()
+        step()
+        t = setup.last_timings()
+        k1.append(t[0])
+        k2.append(t[1])
+    setup.set_timing(False)
+    k1_ms, k2_ms = float(np.median(k1)), float(np.median(k2))
+
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * N_CELLS / (ms_per_step * 1e-3)
+
+    # ---- end to end through the public host-buffer API (pinned host memory)
+    out_host = torch.empty((N_CELLS, setup.n_phi, setup.n_phi), dtype=torch.float32).pin_memory()
+    out_host_np = out_host.numpy()
+    verts_host_np = verts_pinned.numpy()
+    e2e_steps = max(3, min(args.steps, 20))
+    setup.cell_matrices_host(verts_host_np, None, mp.CoefKind.sincosexp, out=out_host_np)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        setup.cell_matrices_host(verts_host_np, None, mp.CoefKind.sincosexp, out=out_host_np)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * N_CELLS / (e2e_ms * 1e-3)
+
+    f_cell, b_cell = work_per_cell(P_DEG, 1, 4)
+    flops_launch = N_CELLS * f_cell
+    achieved_tflops = flops_launch / (k2_ms * 1e-3) / 1e12
+    executed = 2.0 * N_CELLS * setup.k * n2  # packed (s<=t) depth actually run
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp16 storage / fp32 accumulate",
+        "data": "synthetic (seeded tets, gen kind 0, seed 1+rank)",
+        "config": workload_config(),
+        "tflops_dense_equiv": N_CELLS * world * f_cell / (ms_per_step * 1e-3) / 1e12,
+        "kernels_ms": {"geom_w": k1_ms, "cellmat_tc": k2_ms},
+        "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tc_peak,
+                     "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak, "traffic": None,
+                     "kernel": "cellmat_tc_kernel",
+                     "note": (f"achieved = dense-equivalent F_cell {f_cell:.0f} flop x {N_CELLS} cells / "
+                              f"K2 duration; peak = {peak_src} bf16 burst; the kernel executes the "
+                              f"(s<=t)-packed depth, {executed / flops_launch:.3f} of F_cell"),
+                     "executed_flop_fraction": executed / flops_launch,
+                     "step_hbm_frac": (N_CELLS * b_cell / (ms_per_step * 1e-3) / 1e9) / hbm},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(verts_np.nbytes),
+                "d2h_bytes_per_step": int(out_host_np.nbytes), "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if args.sweep and rank == 0:
+        line["sweep"] = run_sweep(mp, torch, dev)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cfg_t = (MIXED_CFG["u_p"], MIXED_CFG["u_g"], MIXED_CFG["u_q"], MIXED_CFG["u_s"], MIXED_CFG["engine"])
+        r, kind, cores, sample = cpu_baseline(P_DEG, 1, cfg_t, verts_np, 1, target_s=args.ref_seconds)
+        line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -109,7 +109,18 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t setup, const double* verts,
 /* Number of kernel launches the last cell_matrices call on this setup issued. */
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 
+/* Per-kernel timing: when enabled, cell_matrices records CUDA events on its stream
+ * around K1 (geometry/W) and K2 (GEMM); last_timings returns their durations in ms
+ * (synchronizing on the events), count as return value (negative status on error). */
+int mpfem_b200_set_timing(mpfem_b200_setup_t setup, int enable);
+int mpfem_b200_last_timings(mpfem_b200_setup_t setup, float* ms, int max_n);
+
 /* ---------------------------------------------------------------- mesh & assembly */
+
+/* Seeded synthetic cells on the host (std::mt19937_64 = the reference Rng, common.hpp:21-35).
+ * kind 0: BASELINE configs 0-2 tets (n x 4 x 3 doubles); kind 1: config-3 anisotropic
+ * rotated tets plus 4 affine-field vertex values per cell in coef (n x 4). */
+int mpfem_b200_gen_tets(int kind, uint64_t seed, int64_t n, double* verts, double* coef);
 
 /* Replaces structured_tet_mesh (mesh.cpp:125-163) for the assembly config: host
  * arrays (n_verts = (nx+1)(ny+1)(nz+1) x 3, n_cells = 6 nx ny nz x 4). */

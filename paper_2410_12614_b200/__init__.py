@@ -130,6 +130,9 @@ def lib():
         "mpfem_b200_scaled_weights": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
                                                 vp, u32p]),
         "mpfem_b200_last_launch_count": (C.c_int, [vp]),
+        "mpfem_b200_set_timing": (C.c_int, [vp, C.c_int]),
+        "mpfem_b200_last_timings": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
+        "mpfem_b200_gen_tets": (C.c_int, [C.c_int, C.c_uint64, C.c_int64, vp, vp]),
         "mpfem_b200_structured_tet_mesh": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
                                                      C.c_double, C.c_uint64, vp, vp]),
         "mpfem_b200_dofmap": (C.c_int, [C.c_int, vp, C.c_int64, C.c_int64, vp, i32p, i32p, vp]),
@@ -289,6 +292,17 @@ class KernelSetup:
     def last_launch_count(self) -> int:
         return lib().mpfem_b200_last_launch_count(self._h)
 
+    def set_timing(self, enable: bool) -> None:
+        check(lib().mpfem_b200_set_timing(self._h, int(enable)))
+
+    def last_timings(self) -> list[float]:
+        """Durations (ms) of K1 and K2 of the last call, from CUDA events on its stream."""
+        buf = (C.c_float * 8)()
+        n = lib().mpfem_b200_last_timings(self._h, buf, 8)
+        if n < 0:
+            check(-n)
+        return [buf[i] for i in range(n)]
+
 
 def make_setup(p: int, config: KernelConfig, cell_kind: int = 0, dim: int = 3) -> KernelSetup:
     """make_setup (kernels.hpp:60-62) for affine tetrahedra."""
@@ -303,3 +317,21 @@ def bilinear_kernel(setup: KernelSetup, verts, cells=None, coef_kind: int = Coef
     if setup.config.mode != ModeKind.bilinear:
         raise ConfigError("configuration is not a bilinear-mode config")
     return setup.cell_matrices(verts, cells, coef_kind, coef, **kw)
+
+
+def gen_tets(kind: int, seed: int, n: int):
+    """Seeded synthetic tets (BASELINE configs 0-3) on the host: (verts (n,4,3), coef (n,4))."""
+    verts = np.zeros((n, 4, 3))
+    coef = np.zeros((n, 4))
+    check(lib().mpfem_b200_gen_tets(int(kind), int(seed), int(n), _ptr(verts), _ptr(coef)))
+    return verts, coef
+
+
+def structured_tet_mesh(nx: int, ny: int, nz: int, extent: float = 1.0, jitter: float = 0.15,
+                        seed: int = 1):
+    """structured_tet_mesh (mesh.hpp:38-39 defaults): (vertices (nv,3), cells (nc,4) int32)."""
+    verts = np.zeros(((nx + 1) * (ny + 1) * (nz + 1), 3))
+    cells = np.zeros((6 * nx * ny * nz, 4), dtype=np.int32)
+    check(lib().mpfem_b200_structured_tet_mesh(nx, ny, nz, float(extent), float(jitter), int(seed),
+                                               _ptr(verts), _ptr(cells)))
+    return verts, cells

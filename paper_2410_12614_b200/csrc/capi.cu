@@ -132,6 +132,19 @@ struct mpfem_b200_setup_s {
   DevBuf h_verts, h_cells, h_coef, h_out;
   int last_launches = 0;
   int device = 0;
+  // optional per-kernel timing of the last cell_matrices call (CUDA events on its stream)
+  int timing = 0;
+  cudaEvent_t ev[8] = {};
+  int n_ev = 0;
+  ~mpfem_b200_setup_s() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void mark(cudaStream_t st) {
+    if (!timing || n_ev >= 8) return;
+    if (!ev[n_ev]) CUDA_OK(cudaEventCreate(&ev[n_ev]));
+    CUDA_OK(cudaEventRecord(ev[n_ev++], st));
+  }
 };
 
 namespace {
@@ -228,10 +241,13 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
     CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
   }
+  S.n_ev = 0;
   if (n == 0) return;
   S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
+  S.mark(st);
   launch_geom(S, verts, cells, n, coef_kind, coef, coef_stride, S.d_W.p, S.k_pad, S.w_type, st);
   ++S.last_launches;
+  S.mark(st);
   if (S.path == kPathTC) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -274,6 +290,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   }
   CUDA_OK(cudaGetLastError());
   ++S.last_launches;
+  S.mark(st);
   if (flags) {
     uint32_t h[2] = {0, 0};
     CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
@@ -452,5 +469,25 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t S, const double* verts, const i
 }
 
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t S) { return S ? S->last_launches : 0; }
+
+int mpfem_b200_set_timing(mpfem_b200_setup_t S, int enable) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    S->timing = enable != 0;
+    S->n_ev = 0;
+  });
+}
+
+int mpfem_b200_last_timings(mpfem_b200_setup_t S, float* ms, int max_n) {
+  int n = 0;
+  int st = guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    for (int i = 0; i + 1 < S->n_ev && n < max_n; ++i) {
+      CUDA_OK(cudaEventSynchronize(S->ev[i + 1]));
+      CUDA_OK(cudaEventElapsedTime(&ms[n++], S->ev[i], S->ev[i + 1]));
+    }
+  });
+  return st ? -st : n;
+}
 
 }  // extern "C"
