@@ -126,7 +126,7 @@ struct mpfem_b200_setup_s {
   int acc_f16 = 0;
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
   Rule rule;
-  DevBuf d_rule_w, d_rule_x, d_tab_up, d_B, d_T;
+  DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T;
   DevBuf d_W, d_flags, d_error;
   // host-API staging
   DevBuf h_verts, h_cells, h_coef, h_out;
@@ -187,6 +187,33 @@ void choose_path(mpfem_b200_setup_s& S) {
   }
 }
 
+template <typename T, int US>
+void launch_geom_ug(int ug, unsigned grid, cudaStream_t st, const GeomWParams& P) {
+  switch (ug) {
+    case 0: geom_w_kernel<T, 0, US><<<grid, kGeomCells, 0, st>>>(P); break;
+    case 1: geom_w_kernel<T, 1, US><<<grid, kGeomCells, 0, st>>>(P); break;
+    case 2: geom_w_kernel<T, 2, US><<<grid, kGeomCells, 0, st>>>(P); break;
+    default: geom_w_kernel<T, 3, US><<<grid, kGeomCells, 0, st>>>(P); break;
+  }
+}
+
+// W element type follows u_s except on the fp64 path, where any u_s is carried in fp64.
+void launch_geom_typed(int w_type, int ug, int us, unsigned grid, cudaStream_t st,
+                       const GeomWParams& P) {
+  switch (w_type) {
+    case 0: launch_geom_ug<__half, 1>(ug, grid, st, P); break;
+    case 1: launch_geom_ug<__nv_bfloat16, 0>(ug, grid, st, P); break;
+    case 2: launch_geom_ug<float, 2>(ug, grid, st, P); break;
+    default:
+      switch (us) {
+        case 0: launch_geom_ug<double, 0>(ug, grid, st, P); break;
+        case 1: launch_geom_ug<double, 1>(ug, grid, st, P); break;
+        case 2: launch_geom_ug<double, 2>(ug, grid, st, P); break;
+        default: launch_geom_ug<double, 3>(ug, grid, st, P); break;
+      }
+  }
+}
+
 void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
                  int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
                  int w_type, cudaStream_t st) {
@@ -197,7 +224,7 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.coef_kind = coef_kind;
   P.coef = coef;
   P.coef_stride = coef_stride;
-  P.rule_w = static_cast<const double*>(S.d_rule_w.p);
+  P.rule_w = static_cast<const double*>(S.d_rule_w_ug.p);
   P.rule_x = static_cast<const double*>(S.d_rule_x.p);
   P.tab_up = static_cast<const double*>(S.d_tab_up.p);
   P.n_phi = S.n_phi;
@@ -211,14 +238,8 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.W = W;
   P.flags = static_cast<uint32_t*>(S.d_flags.p);
   P.error = static_cast<int*>(S.d_error.p);
-  const int64_t threads = n * 32;
-  const unsigned grid = unsigned((threads + 255) / 256);
-  switch (w_type) {
-    case 0: geom_w_kernel<__half><<<grid, 256, 0, st>>>(P); break;
-    case 1: geom_w_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(P); break;
-    case 2: geom_w_kernel<float><<<grid, 256, 0, st>>>(P); break;
-    default: geom_w_kernel<double><<<grid, 256, 0, st>>>(P); break;
-  }
+  const unsigned grid = unsigned((n + kGeomCells - 1) / kGeomCells);
+  launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -342,10 +363,14 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     std::vector<double> tab_up = tabulate(basis, S->rule, u_p, u_p, false, fl);
     std::vector<double> B = tabulate(basis, S->rule, 3, 3, form == 1, fl);
     S->d_rule_w.ensure(sizeof(double) * S->n_q);
+    std::vector<double> w_ug(S->n_q);  // fp_cast(omega_q, fp64, u_g) (kernels.cpp:185)
+    for (int q = 0; q < S->n_q; ++q) w_ug[q] = host_round(S->rule.weights[q], u_g, fl);
+    S->d_rule_w_ug.ensure(sizeof(double) * S->n_q);
     S->d_rule_x.ensure(sizeof(double) * 3 * S->n_q);
     S->d_tab_up.ensure(sizeof(double) * tab_up.size());
     S->d_B.ensure(sizeof(double) * B.size());
     CUDA_OK(cudaMemcpy(S->d_rule_w.p, S->rule.weights.data(), sizeof(double) * S->n_q, cudaMemcpyHostToDevice));
+    CUDA_OK(cudaMemcpy(S->d_rule_w_ug.p, w_ug.data(), sizeof(double) * S->n_q, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(S->d_rule_x.p, S->rule.points.data(), sizeof(double) * 3 * S->n_q, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(S->d_tab_up.p, tab_up.data(), sizeof(double) * tab_up.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(S->d_B.p, B.data(), sizeof(double) * B.size(), cudaMemcpyHostToDevice));

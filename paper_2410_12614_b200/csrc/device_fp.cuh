@@ -69,6 +69,26 @@ __device__ __forceinline__ double dround(double x, int f, uint32_t& fl) {
   return r;
 }
 
+// Compile-time-format rounding: identical results to dround(x, F, fl), but the format
+// dispatch folds away (fp64 is the identity, fp32 a single conversion).
+template <int F>
+__device__ __forceinline__ double droundT(double x, uint32_t& fl) {
+  if constexpr (F == kFP64) {
+    if (isnan(x)) { fl |= kInvalid; return canonical_nan_d(); }
+    return x;
+  } else {
+    return dround(x, F, fl);
+  }
+}
+template <int F>
+__device__ __forceinline__ double dmulT(double a, double b, uint32_t& fl) {
+  double r = __dmul_rn(a, b);
+  if constexpr (F == kFP64) {
+    if (isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  }
+  return droundT<F>(r, fl);
+}
+
 // fp_op at format f (softfloat.hpp:170-186): exact binary64 op, one rounding.
 __device__ __forceinline__ double dadd(double a, double b, int f, uint32_t& fl) {
   double r = __dadd_rn(a, b);
@@ -132,21 +152,33 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool p
   #pragma unroll
   for (int col = 0; col < 3; ++col) {
     int pivot = col;
+    double best = fabs(lu[col][col]);
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const double a = fabs(lu[r][col]);
+      if (a > best) { best = a; pivot = r; }
+    }
+    // first max wins (strict >), as lu_decompose; swaps with static indices only so the
+    // 3x3 factors stay in registers
+    double pv = lu[col][col];
     #pragma unroll
     for (int r = col + 1; r < 3; ++r)
-      if (fabs(lu[r][col]) > fabs(lu[pivot][col])) pivot = r;
-    if (lu[pivot][col] == 0.0) return false;
-    if (pivot != col) {
-      #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double t = lu[pivot][c];
-        lu[pivot][c] = lu[col][c];
-        lu[col][c] = t;
+      if (pivot == r) pv = lu[r][col];
+    if (pv == 0.0) return false;
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      if (pivot == r) {
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double t = lu[r][c];
+          lu[r][c] = lu[col][c];
+          lu[col][c] = t;
+        }
+        int t = perm[r];
+        perm[r] = perm[col];
+        perm[col] = t;
+        sign = -sign;
       }
-      int t = perm[pivot];
-      perm[pivot] = perm[col];
-      perm[col] = t;
-      sign = -sign;
     }
     #pragma unroll
     for (int r = col + 1; r < 3; ++r) {
@@ -210,11 +242,28 @@ __device__ __forceinline__ double coef_sincosexp(const double v[4][3], const dou
     for (int s = 0; s < 3; ++s) acc = __dadd_rn(acc, __dmul_rn(__dsub_rn(v[s + 1][i], v[0][i]), xi[s]));
     x[i] = acc;
   }
-  const double two_pi = 6.283185307179586476925286766559;
-  double s = sin(__dmul_rn(two_pi, x[0]));
-  double c = cos(__dmul_rn(two_pi, x[1]));
+  // sin(2 pi x) as sinpi(2x): exact argument reduction (2x is exact in binary64)
+  double s = sinpi(__dmul_rn(2.0, x[0]));
+  double c = cospi(__dmul_rn(2.0, x[1]));
   double e = exp(x[2]);
   return __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(0.5, s), c), e));
+}
+
+// Same, from the cell's origin v0 and edge vectors E[s] = v_{s+1} - v0 (precomputed).
+__device__ __forceinline__ double coef_sincosexp_e(const double* v0, const double* E,
+                                                   const double* xi) {
+  double x[3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = v0[i];
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) acc = __dadd_rn(acc, __dmul_rn(E[s * 3 + i], xi[s]));
+    x[i] = acc;
+  }
+  double sn = sinpi(__dmul_rn(2.0, x[0]));
+  double cs = cospi(__dmul_rn(2.0, x[1]));
+  double e = exp(x[2]);
+  return __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(0.5, sn), cs), e));
 }
 
 // Config-3 coefficient: c = 10^(6 u(x_q)), u affine with vertex values u4.

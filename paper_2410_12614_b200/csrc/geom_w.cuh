@@ -1,8 +1,7 @@
 // geom_w.cuh -- K1: per-cell geometry + coefficient + scaled-weight pass.
 //
-// One warp per cell. Every lane evaluates the cell geometry at u_g (identical op
-// sequence, so no broadcast is needed), then lanes stride over quadrature points and
-// write the cell's row of the GEMM operand W:
+// Geometry once per cell (one thread), then one warp per cell whose lanes stride over
+// quadrature points and write the cell's row of the GEMM operand W:
 //   W[c, b*n_q + q] = round_us(round_ug(round_ug(omega_q * G_b) * zhat_q))
 // which is build_C (kernels.cpp:177-197) with the (s,t) pairs packed to the upper
 // triangle b = (s<=t): (0,0),(0,1),(0,2),(1,1),(1,2),(2,2) (C is symmetric bitwise, so
@@ -55,59 +54,94 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
   static_cast<double*>(W)[idx] = v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(256) geom_w_kernel(GeomWParams P) {
-  const int lane = threadIdx.x & 31;
-  const int64_t cell = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (cell >= P.n_cells) return;
+// Two phases per CTA of kGeomCells cells:
+//  (1) one thread per cell: geometry at u_g into shared memory (G, origin, edges);
+//  (2) one warp per cell, lanes over quadrature points: coefficient + W row.
+// UG / US are compile-time so the emulated rounding folds to the plain op for fp64 and a
+// single conversion for fp32.
+constexpr int kGeomCells = 128;
+
+template <typename T, int UG, int US>
+__global__ void __launch_bounds__(kGeomCells) geom_w_kernel(GeomWParams P) {
+  __shared__ double sG[kGeomCells][6];
+  __shared__ double sV0[kGeomCells][3];
+  __shared__ double sE[kGeomCells][9];
+  __shared__ int sBad[kGeomCells];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int64_t cell0 = int64_t(blockIdx.x) * kGeomCells;
   uint32_t fl = 0;
-  double v[4][3];
-  if (P.cells) {
-    #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int64_t vid = P.cells[cell * 4 + k];
-      #pragma unroll
-      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
-    }
-  } else {
-    #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      #pragma unroll
-      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
-  }
-  TetGeometry g;
-  bool ok = tet_geometry(v, P.ug, P.poisson != 0, g, fl);
-  if (!ok) {
-    if (lane == 0) atomicExch(P.error, 3);
-    return;
-  }
-  const int nb = P.poisson ? 6 : 1;
-  const int64_t row = cell * P.k_pad;
-  const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
-  for (int q = lane; q < P.n_q; q += 32) {
-    double zq = 1.0;
-    bool have_z = true;
-    switch (P.coef_kind) {
-      case 1: zq = dround(coef_sincosexp(v, P.rule_x + 3 * q), P.ug, fl); break;
-      case 2: zq = dround(coef_exp10_affine(coef, P.rule_x + 3 * q), P.ug, fl); break;
-      case 3: {
-        double acc = 0.0;
-        for (int k = 0; k < P.n_phi; ++k)
-          acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * P.n_q + q], P.up, fl),
-                     P.up, fl);
-        zq = dround(acc, P.ug, fl);
-        break;
+  {
+    const int64_t cell = cell0 + tid;
+    sBad[tid] = 1;
+    if (cell < P.n_cells) {
+      double v[4][3];
+      if (P.cells) {
+        #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t vid = P.cells[cell * 4 + k];
+          #pragma unroll
+          for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
+        }
+      } else {
+        #pragma unroll
+        for (int k = 0; k < 4; ++k)
+          #pragma unroll
+          for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
       }
-      default: have_z = false;
-    }
-    double omega = dround(P.rule_w[q], P.ug, fl);
-    for (int b = 0; b < nb; ++b) {
-      double val = dmul(omega, g.g[b], P.ug, fl);
-      if (have_z) val = dmul(val, zq, P.ug, fl);
-      store_w<T>(P.W, row + int64_t(b) * P.n_q + q, dround(val, P.us, fl));
+      TetGeometry g;
+      const bool ok = tet_geometry(v, UG, P.poisson != 0, g, fl);
+      sBad[tid] = ok ? 0 : 2;
+      if (!ok) atomicExch(P.error, 3);
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) sG[tid][b] = g.g[b];
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        sV0[tid][a] = v[0][a];
+        #pragma unroll
+        for (int s = 0; s < 3; ++s) sE[tid][s * 3 + a] = __dsub_rn(v[s + 1][a], v[0][a]);
+      }
     }
   }
-  for (int64_t k = int64_t(nb) * P.n_q + lane; k < P.k_pad; k += 32) store_w<T>(P.W, row + k, 0.0);
+  __syncthreads();
+  const int nb = P.poisson ? 6 : 1;
+  for (int j = warp; j < kGeomCells; j += kGeomCells / 32) {
+    const int64_t cell = cell0 + j;
+    if (cell >= P.n_cells || sBad[j]) continue;
+    const int64_t row = cell * P.k_pad;
+    const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
+    double G[6];
+    #pragma unroll
+    for (int b = 0; b < 6; ++b) G[b] = sG[j][b];
+    for (int q = lane; q < P.n_q; q += 32) {
+      const double* xi = P.rule_x + 3 * q;
+      double zq = 1.0;
+      bool have_z = true;
+      switch (P.coef_kind) {
+        case 1: zq = droundT<UG>(coef_sincosexp_e(sV0[j], sE[j], xi), fl); break;
+        case 2: zq = droundT<UG>(coef_exp10_affine(coef, xi), fl); break;
+        case 3: {
+          double acc = 0.0;
+          for (int k = 0; k < P.n_phi; ++k)
+            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * P.n_q + q], P.up, fl),
+                       P.up, fl);
+          zq = droundT<UG>(acc, fl);
+          break;
+        }
+        default: have_z = false;
+      }
+      const double omega = P.rule_w[q];  // already rounded to u_g on the host
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        if (b < nb) {
+          double val = dmulT<UG>(omega, G[b], fl);
+          if (have_z) val = dmulT<UG>(val, zq, fl);
+          store_w<T>(P.W, row + int64_t(b) * P.n_q + q, droundT<US>(val, fl));
+        }
+      }
+    }
+    for (int64_t k = int64_t(nb) * P.n_q + lane; k < P.k_pad; k += 32) store_w<T>(P.W, row + k, 0.0);
+  }
   fl = __reduce_or_sync(0xffffffffu, fl);
   if (lane == 0 && fl) atomicOr(P.flags, fl);
 }
