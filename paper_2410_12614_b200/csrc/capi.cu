@@ -190,10 +190,10 @@ void choose_path(mpfem_b200_setup_s& S) {
 template <typename T, int US>
 void launch_geom_ug(int ug, unsigned grid, cudaStream_t st, const GeomWParams& P) {
   switch (ug) {
-    case 0: geom_w_kernel<T, 0, US><<<grid, kGeomCells, 0, st>>>(P); break;
-    case 1: geom_w_kernel<T, 1, US><<<grid, kGeomCells, 0, st>>>(P); break;
-    case 2: geom_w_kernel<T, 2, US><<<grid, kGeomCells, 0, st>>>(P); break;
-    default: geom_w_kernel<T, 3, US><<<grid, kGeomCells, 0, st>>>(P); break;
+    case 0: geom_w_kernel<T, 0, US><<<grid, kGeomThreads, 0, st>>>(P); break;
+    case 1: geom_w_kernel<T, 1, US><<<grid, kGeomThreads, 0, st>>>(P); break;
+    case 2: geom_w_kernel<T, 2, US><<<grid, kGeomThreads, 0, st>>>(P); break;
+    default: geom_w_kernel<T, 3, US><<<grid, kGeomThreads, 0, st>>>(P); break;
   }
 }
 
@@ -283,17 +283,21 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     P.out = static_cast<float*>(out);
     P.out_pitch = out_pitch;
     P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc::BM, tc::BN);
-    P.acc_f16 = S.acc_f16;
     P.flags = static_cast<uint32_t*>(S.d_flags.p);
     const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
     const int grid = int(std::min<int64_t>(tiles, device_sm_count()));
     static bool attr_set = false;
     if (!attr_set) {
-      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   tc::SMEM_BYTES));
+      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel<false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
+      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel<true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
       attr_set = true;
     }
-    tc::cellmat_tc_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
+    if (S.acc_f16)
+      tc::cellmat_tc_kernel<true><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
+    else
+      tc::cellmat_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
   } else if (S.path == kPathF32) {
     constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
     dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));

@@ -11,7 +11,8 @@
 //   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16,
 //               fp32 (or f16) accumulators in TMEM, two 256-column buffers
 //   warp 2      TMEM allocator (512 columns)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b.x32 -> registers -> global. TMEM lane =
+//   warps 4-11  epilogue (two per TMEM lane quarter, half the columns each):
+//               tcgen05.ld 32x32b.x32 -> registers -> global. TMEM lane =
 //               output entry, column = cell, so one warp store writes 32 consecutive
 //               entries (128 B) of one cell's row-major matrix: coalesced, no staging.
 // Tiles are ordered cell-block-major so the W block of a cell block is reused from L2
@@ -32,7 +33,8 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int THREADS = 256;
+constexpr int EPI_WARPS = 8;      // two warps per TMEM lane quarter, each half the columns
+constexpr int THREADS = 128 + EPI_WARPS * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -45,7 +47,6 @@ struct Params {
   float* out;
   int64_t out_pitch;
   uint32_t idesc;
-  int acc_f16;
   uint32_t* flags;
 };
 
@@ -141,6 +142,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int ab_bf16, int d_f32, int m,
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
 
+template <bool ACC_F16>
 __global__ void __launch_bounds__(THREADS, 1)
     cellmat_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const Params P) {
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -222,10 +224,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    // TMEM lane quarter = warp % 4 (hardware rule); the two warps of a quarter split the
+    // accumulator's 256 columns (cells) in halves.
     const int quarter = warp & 3;
+    const int half = (warp - 4) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t bad = 0;
+    uint32_t expo_or = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
       mbar_wait(&tfull[acc], acc_phase);
@@ -233,19 +238,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int o = ot * BM + quarter * 32 + lane;
       const bool o_ok = o < P.n_out;
       #pragma unroll 1
-      for (int chunk = 0; chunk < BN / 32; ++chunk) {
+      for (int chunk = half * (BN / 64); chunk < (half + 1) * (BN / 64); ++chunk) {
         uint32_t r[32];
         tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
         const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
         if (o_ok) {
           float* dst = P.out + cell0 * P.out_pitch + o;
-          #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (cell0 + j < P.n_cells) {
-              float v = P.acc_f16 ? __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)))
-                                  : __uint_as_float(r[j]);
-              bad |= isfinite(v) ? 0u : 1u;
-              __stcs(dst + int64_t(j) * P.out_pitch, v);
+          const int64_t left = P.n_cells - cell0;
+          if (left >= 32) {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float v;
+              if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
+              else v = __uint_as_float(r[j]);
+              expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+              __stcs(dst, v);
+              dst += P.out_pitch;
+            }
+          } else {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < left) {
+                float v;
+                if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
+                else v = __uint_as_float(r[j]);
+                expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+                __stcs(dst, v);
+              }
+              dst += P.out_pitch;
             }
           }
         }
@@ -255,8 +275,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (lane == 0 && bad) atomicOr(P.flags, 4u);
+    expo_or = __reduce_or_sync(0xffffffffu, expo_or);
+    if (lane == 0 && expo_or) atomicOr(P.flags, 4u);
   }
   tc_fence_before();
   __syncthreads();

@@ -59,10 +59,11 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
 //  (2) one warp per cell, lanes over quadrature points: coefficient + W row.
 // UG / US are compile-time so the emulated rounding folds to the plain op for fp64 and a
 // single conversion for fp32.
-constexpr int kGeomCells = 128;
+constexpr int kGeomCells = 64;     // cells per CTA
+constexpr int kGeomThreads = 256;  // 8 warps share the (cell, q) expansion
 
 template <typename T, int UG, int US>
-__global__ void __launch_bounds__(kGeomCells) geom_w_kernel(GeomWParams P) {
+__global__ void __launch_bounds__(kGeomThreads) geom_w_kernel(GeomWParams P) {
   __shared__ double sG[kGeomCells][6];
   __shared__ double sV0[kGeomCells][3];
   __shared__ double sE[kGeomCells][9];
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kGeomCells) geom_w_kernel(GeomWParams P) {
   const int lane = tid & 31, warp = tid >> 5;
   const int64_t cell0 = int64_t(blockIdx.x) * kGeomCells;
   uint32_t fl = 0;
-  {
+  if (tid < kGeomCells) {
     const int64_t cell = cell0 + tid;
     sBad[tid] = 1;
     if (cell < P.n_cells) {
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kGeomCells) geom_w_kernel(GeomWParams P) {
   }
   __syncthreads();
   const int nb = P.poisson ? 6 : 1;
-  for (int j = warp; j < kGeomCells; j += kGeomCells / 32) {
+  for (int j = warp; j < kGeomCells; j += kGeomThreads / 32) {
     const int64_t cell = cell0 + j;
     if (cell >= P.n_cells || sBad[j]) continue;
     const int64_t row = cell * P.k_pad;
