@@ -274,7 +274,6 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each, CUDA events on the launch stream
-    setup.set_timing(True)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     k_ms = []
     sampler = ClockSampler(local)
@@ -298,10 +297,9 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(np.sum(step_ms))
     launches = setup.last_launch_count() * args.steps
-    setup.set_timing(False)
 
-    # per-kernel durations (same stream, CUDA events recorded by the library) on a short
-    # re-run of identical steps; the dominant kernel is K2
+    # per-kernel durations (CUDA events recorded by the library on the launch stream) on a
+    # short re-run of identical steps with K1/K2 unoverlapped; the dominant kernel is K2
     setup.set_timing(True)
     k1, k2 = [], []
     for _ in range(20):

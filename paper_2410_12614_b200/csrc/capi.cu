@@ -132,6 +132,11 @@ struct mpfem_b200_setup_s {
   DevBuf h_verts, h_cells, h_coef, h_out;
   int last_launches = 0;
   int device = 0;
+  // K1/K2 overlap: K2 of chunk i runs on `side` while K1 of chunk i+1 runs on the caller's
+  // stream; fork/join through events keeps the call stream-ordered (and graph-capturable).
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t chunk_ready[8] = {};
   // optional per-kernel timing of the last cell_matrices call (CUDA events on its stream)
   int timing = 0;
   cudaEvent_t ev[8] = {};
@@ -139,6 +144,11 @@ struct mpfem_b200_setup_s {
   ~mpfem_b200_setup_s() {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : chunk_ready)
+      if (e) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
   }
   void mark(cudaStream_t st) {
     if (!timing || n_ev >= 8) return;
@@ -251,29 +261,13 @@ void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, 
     throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
 }
 
-void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells,
-                       int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* out,
-                       int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
-  check_coef(S, coef_kind, coef, coef_stride);
-  if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
-  if (out_pitch < S.n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
-  S.last_launches = 0;
-  if (flags) {
-    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
-    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
-  }
-  S.n_ev = 0;
-  if (n == 0) return;
-  S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
-  S.mark(st);
-  launch_geom(S, verts, cells, n, coef_kind, coef, coef_stride, S.d_W.p, S.k_pad, S.w_type, st);
-  ++S.last_launches;
-  S.mark(st);
+void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t out_pitch,
+                 cudaStream_t st) {
   if (S.path == kPathTC) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc::BM);
-    CUtensorMap tb = make_map_2d(S.d_W.p, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc::BN);
+    CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc::BN);
     tc::Params P;
     P.n_cells = n;
     P.n_out = int(S.n_out);
@@ -302,20 +296,77 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
     dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
     cellmat_simt_kernel<float, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
-        static_cast<const float*>(S.d_W.p), static_cast<const float*>(S.d_T.p),
-        static_cast<float*>(out), n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch,
-        static_cast<uint32_t*>(S.d_flags.p));
+        static_cast<const float*>(W), static_cast<const float*>(S.d_T.p), static_cast<float*>(out),
+        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(S.d_flags.p));
   } else {
     constexpr int BM = 64, BN = 128, BK = 16, TM = 4, TN = 8;
     dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
     cellmat_simt_kernel<double, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
-        static_cast<const double*>(S.d_W.p), static_cast<const double*>(S.d_T.p),
-        static_cast<double*>(out), n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch,
-        static_cast<uint32_t*>(S.d_flags.p));
+        static_cast<const double*>(W), static_cast<const double*>(S.d_T.p), static_cast<double*>(out),
+        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(S.d_flags.p));
   }
   CUDA_OK(cudaGetLastError());
-  ++S.last_launches;
-  S.mark(st);
+}
+
+void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells,
+                       int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* out,
+                       int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+  check_coef(S, coef_kind, coef, coef_stride);
+  if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
+  if (out_pitch < S.n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
+  S.last_launches = 0;
+  if (flags) {
+    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
+    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
+  }
+  S.n_ev = 0;
+  if (n == 0) return;
+  S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
+  // Chunking: enough K2 tiles per chunk to fill the GPU about three times over.
+  const int64_t cell_tiles = (n + tc::BN - 1) / tc::BN;
+  const int64_t out_tiles = S.n_out_pad / tc::BM;
+  int n_chunks = int(std::min<int64_t>(4, std::max<int64_t>(1, cell_tiles * out_tiles / (3 * device_sm_count()))));
+  if (S.timing) n_chunks = 1;  // per-kernel timing measures K1 and K2 unoverlapped
+  const int64_t tiles_per_chunk = (cell_tiles + n_chunks - 1) / n_chunks;
+  if (n_chunks > 1) {
+    if (!S.side) {
+      CUDA_OK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+      CUDA_OK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&S.join, cudaEventDisableTiming));
+      for (auto& e : S.chunk_ready) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CUDA_OK(cudaEventRecord(S.fork, st));
+    CUDA_OK(cudaStreamWaitEvent(S.side, S.fork, 0));
+  }
+  for (int ch = 0; ch < n_chunks; ++ch) {
+    const int64_t c0 = ch * tiles_per_chunk * tc::BN;
+    const int64_t c1 = std::min<int64_t>(n, (ch + 1) * tiles_per_chunk * tc::BN);
+    if (c0 >= c1) break;
+    const int64_t m = c1 - c0;
+    const size_t wb = size_t(S.k_pad) * elem_size(S.w_type);
+    void* Wc = static_cast<char*>(S.d_W.p) + size_t(c0) * wb;
+    const double* vc = cells ? verts : verts + c0 * 12;
+    const int32_t* cc = cells ? cells + c0 * 4 : nullptr;
+    const double* coefc = coef ? coef + c0 * coef_stride : nullptr;
+    S.mark(st);
+    launch_geom(S, vc, cc, m, coef_kind, coefc, coef_stride, Wc, S.k_pad, S.w_type, st);
+    ++S.last_launches;
+    S.mark(st);
+    cudaStream_t gs = st;
+    if (n_chunks > 1) {
+      CUDA_OK(cudaEventRecord(S.chunk_ready[ch], st));
+      CUDA_OK(cudaStreamWaitEvent(S.side, S.chunk_ready[ch], 0));
+      gs = S.side;
+    }
+    char* outc = static_cast<char*>(out) + size_t(c0) * size_t(out_pitch) * (S.path == kPathF64 ? 8 : 4);
+    launch_gemm(S, Wc, m, outc, out_pitch, gs);
+    ++S.last_launches;
+    S.mark(gs);
+  }
+  if (n_chunks > 1) {
+    CUDA_OK(cudaEventRecord(S.join, S.side));
+    CUDA_OK(cudaStreamWaitEvent(st, S.join, 0));
+  }
   if (flags) {
     uint32_t h[2] = {0, 0};
     CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));

@@ -76,9 +76,50 @@ __device__ __forceinline__ double droundT(double x, uint32_t& fl) {
   if constexpr (F == kFP64) {
     if (isnan(x)) { fl |= kInvalid; return canonical_nan_d(); }
     return x;
+  } else if constexpr (F == kFP32) {
+    return dround(x, F, fl);
   } else {
+    // Fast path: binary64 exponents whose RNE result is a normal finite value of the
+    // format (no underflow, no overflow, no special): round-half-even by bias-and-truncate
+    // on the bit pattern (the carry into the exponent is the binade promotion). Everything
+    // else takes the general path.
+    constexpr int kDrop = F == kBF16 ? 45 : 42;
+    constexpr unsigned long long kELo = F == kBF16 ? 1023 - 126 : 1023 - 14;
+    constexpr unsigned long long kEHi = F == kBF16 ? 1023 + 126 : 1023 + 14;
+    unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+    const unsigned long long e = (bits >> 52) & 0x7ffull;
+    if (e >= kELo && e <= kEHi) {
+      bits += ((1ull << (kDrop - 1)) - 1ull) + ((bits >> kDrop) & 1ull);
+      bits &= ~((1ull << kDrop) - 1ull);
+      return __longlong_as_double((long long)bits);
+    }
     return dround(x, F, fl);
   }
+}
+template <int F>
+__device__ __forceinline__ double daddT(double a, double b, uint32_t& fl) {
+  double r = __dadd_rn(a, b);
+  if constexpr (F == kFP64) {
+    if (isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  }
+  return droundT<F>(r, fl);
+}
+template <int F>
+__device__ __forceinline__ double dsubT(double a, double b, uint32_t& fl) {
+  double r = __dsub_rn(a, b);
+  if constexpr (F == kFP64) {
+    if (isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  }
+  return droundT<F>(r, fl);
+}
+template <int F>
+__device__ __forceinline__ double ddivT(double a, double b, uint32_t& fl) {
+  if (b == 0.0 && a != 0.0 && !isnan(a) && !isinf(a)) fl |= kDivzero;
+  double r = __ddiv_rn(a, b);
+  if constexpr (F == kFP64) {
+    if (isinf(r) && !isinf(a) && !isinf(b)) fl |= kOverflow;
+  }
+  return droundT<F>(r, fl);
 }
 template <int F>
 __device__ __forceinline__ double dmulT(double a, double b, uint32_t& fl) {
@@ -121,8 +162,9 @@ struct TetGeometry {
   double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson); g[0] = |det| (mass)
 };
 
-__device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool poisson,
-                                             TetGeometry& out, uint32_t& fl) {
+template <int F>
+__device__ __forceinline__ bool tet_geometry(const double v[4][3], bool poisson, TetGeometry& out,
+                                             uint32_t& fl) {
   // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
   double jac[3][3];
   #pragma unroll
@@ -133,11 +175,11 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool p
   for (int k = 0; k < 4; ++k) {
     #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      double x = dround(v[k][i], f, fl);
+      double x = droundT<F>(v[k][i], fl);
       #pragma unroll
       for (int s = 0; s < 3; ++s) {
         double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
-        jac[i][s] = dadd(jac[i][s], dmul(x, g, f, fl), f, fl);
+        jac[i][s] = daddT<F>(jac[i][s], dmulT<F>(x, g, fl), fl);
       }
     }
   }
@@ -182,15 +224,15 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool p
     }
     #pragma unroll
     for (int r = col + 1; r < 3; ++r) {
-      double m = ddiv(lu[r][col], lu[col][col], f, fl);
+      double m = ddivT<F>(lu[r][col], lu[col][col], fl);
       lu[r][col] = m;
       #pragma unroll
-      for (int c = col + 1; c < 3; ++c) lu[r][c] = dsub(lu[r][c], dmul(m, lu[col][c], f, fl), f, fl);
+      for (int c = col + 1; c < 3; ++c) lu[r][c] = dsubT<F>(lu[r][c], dmulT<F>(m, lu[col][c], fl), fl);
     }
   }
   double det = (double)sign;
   #pragma unroll
-  for (int i = 0; i < 3; ++i) det = dmul(det, lu[i][i], f, fl);
+  for (int i = 0; i < 3; ++i) det = dmulT<F>(det, lu[i][i], fl);
   out.det = det;
   out.abs_det = fabs(det);
   if (!poisson) {
@@ -206,15 +248,15 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool p
     for (int r = 0; r < 3; ++r) {
       double s = perm[r] == k ? 1.0 : 0.0;
       #pragma unroll
-      for (int c = 0; c < r; ++c) s = dsub(s, dmul(lu[r][c], y[c], f, fl), f, fl);
+      for (int c = 0; c < r; ++c) s = dsubT<F>(s, dmulT<F>(lu[r][c], y[c], fl), fl);
       y[r] = s;
     }
     #pragma unroll
     for (int r = 2; r >= 0; --r) {
       double s = y[r];
       #pragma unroll
-      for (int c = r + 1; c < 3; ++c) s = dsub(s, dmul(lu[r][c], inv[c][k], f, fl), f, fl);
-      inv[r][k] = ddiv(s, lu[r][r], f, fl);
+      for (int c = r + 1; c < 3; ++c) s = dsubT<F>(s, dmulT<F>(lu[r][c], inv[c][k], fl), fl);
+      inv[r][k] = ddivT<F>(s, lu[r][r], fl);
     }
   }
   // geometry_tensor (geometry.cpp:97-118)
@@ -225,8 +267,8 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], int f, bool p
     for (int t = s; t < 3; ++t) {
       double dot = 0.0;
       #pragma unroll
-      for (int k = 0; k < 3; ++k) dot = dadd(dot, dmul(inv[s][k], inv[t][k], f, fl), f, fl);
-      out.g[idx++] = dmul(out.abs_det, dot, f, fl);
+      for (int k = 0; k < 3; ++k) dot = daddT<F>(dot, dmulT<F>(inv[s][k], inv[t][k], fl), fl);
+      out.g[idx++] = dmulT<F>(out.abs_det, dot, fl);
     }
   return true;
 }

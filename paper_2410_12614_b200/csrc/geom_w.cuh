@@ -63,7 +63,7 @@ constexpr int kGeomCells = 64;     // cells per CTA
 constexpr int kGeomThreads = 256;  // 8 warps share the (cell, q) expansion
 
 template <typename T, int UG, int US>
-__global__ void __launch_bounds__(kGeomThreads) geom_w_kernel(GeomWParams P) {
+__global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) {
   __shared__ double sG[kGeomCells][6];
   __shared__ double sV0[kGeomCells][3];
   __shared__ double sE[kGeomCells][9];
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kGeomThreads) geom_w_kernel(GeomWParams P) {
           for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
       }
       TetGeometry g;
-      const bool ok = tet_geometry(v, UG, P.poisson != 0, g, fl);
+      const bool ok = tet_geometry<UG>(v, P.poisson != 0, g, fl);
       sBad[tid] = ok ? 0 : 2;
       if (!ok) atomicExch(P.error, 3);
       #pragma unroll
