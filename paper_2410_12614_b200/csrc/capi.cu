@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -325,7 +326,12 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   // Chunking: enough K2 tiles per chunk to fill the GPU about three times over.
   const int64_t cell_tiles = (n + tc::BN - 1) / tc::BN;
   const int64_t out_tiles = S.n_out_pad / tc::BM;
-  int n_chunks = int(std::min<int64_t>(4, std::max<int64_t>(1, cell_tiles * out_tiles / (3 * device_sm_count()))));
+  // Overlapping K1 of chunk i+1 with K2 of chunk i measured slower than back-to-back on B200
+  // (the K1 CTAs contend with the persistent K2 CTAs), so one chunk is the default.
+  int n_chunks = 1;
+  (void)cell_tiles;
+  (void)out_tiles;
+  if (const char* env = std::getenv("MPFEM_B200_CHUNKS")) n_chunks = std::max(1, std::min(8, std::atoi(env)));
   if (S.timing) n_chunks = 1;  // per-kernel timing measures K1 and K2 unoverlapped
   const int64_t tiles_per_chunk = (cell_tiles + n_chunks - 1) / n_chunks;
   if (n_chunks > 1) {

@@ -4,6 +4,9 @@
 // target format. For t <= 25 significand bits the binary64 intermediate cannot cause a
 // double-rounding error (2t + 2 <= 53), which is the reference's own argument.
 #pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
 #include <cstdint>
 
 namespace mpfem_b200 {
@@ -78,22 +81,20 @@ __device__ __forceinline__ double droundT(double x, uint32_t& fl) {
     return x;
   } else if constexpr (F == kFP32) {
     return dround(x, F, fl);
+  } else if constexpr (F == kFP16) {
+    // cvt.rn.f16.f64: one RNE rounding, subnormals included (== round_narrow)
+    if (isnan(x)) { fl |= kInvalid; return canonical_nan_d(); }
+    const double r = __half2float(__double2half(x));
+    if (isinf(r) && !isinf(x)) fl |= kOverflow;
+    if (fabs(r) < 0x1.0p-14 && r != x) fl |= kUnderflow;
+    return r;
   } else {
-    // Fast path: binary64 exponents whose RNE result is a normal finite value of the
-    // format (no underflow, no overflow, no special): round-half-even by bias-and-truncate
-    // on the bit pattern (the carry into the exponent is the binade promotion). Everything
-    // else takes the general path.
-    constexpr int kDrop = F == kBF16 ? 45 : 42;
-    constexpr unsigned long long kELo = F == kBF16 ? 1023 - 126 : 1023 - 14;
-    constexpr unsigned long long kEHi = F == kBF16 ? 1023 + 126 : 1023 + 14;
-    unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-    const unsigned long long e = (bits >> 52) & 0x7ffull;
-    if (e >= kELo && e <= kEHi) {
-      bits += ((1ull << (kDrop - 1)) - 1ull) + ((bits >> kDrop) & 1ull);
-      bits &= ~((1ull << kDrop) - 1ull);
-      return __longlong_as_double((long long)bits);
-    }
-    return dround(x, F, fl);
+    // cvt.rn.bf16.f64 (sm_90+): one RNE rounding
+    if (isnan(x)) { fl |= kInvalid; return canonical_nan_d(); }
+    const double r = __bfloat162float(__double2bfloat16(x));
+    if (isinf(r) && !isinf(x)) fl |= kOverflow;
+    if (fabs(r) < 0x1.0p-126 && r != x) fl |= kUnderflow;
+    return r;
   }
 }
 template <int F>

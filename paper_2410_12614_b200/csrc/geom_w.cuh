@@ -12,6 +12,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "device_fp.cuh"
 
 namespace mpfem_b200 {
@@ -34,6 +36,50 @@ struct GeomWParams {
   uint32_t* flags;
   int* error;              // set to 3 on a singular cell
 };
+
+// Storage rounding round_us(v) (one RNE conversion, subnormals kept) of a u_g value held
+// in double or float, returned in the element type T. FP events are accumulated cheaply
+// from the stored bits: `amax` tracks the largest |bits| (>= inf pattern means an
+// overflow or a NaN reached storage) and `tiny` a nonzero value stored as subnormal/zero
+// (underflow). For T = double (the fp64 GEMM path) any US is carried exactly.
+struct StoreFlags {
+  uint32_t amax = 0;  // max |bits| in units of the storage format's inf pattern
+  uint32_t tiny = 0;
+};
+
+template <typename T, int US, typename V>
+__device__ __forceinline__ T to_storage(V v, StoreFlags& sf) {
+  if constexpr (std::is_same_v<T, __half>) {
+    const __half h = std::is_same_v<V, float> ? __float2half_rn(float(v)) : __double2half(double(v));
+    const uint32_t a = __half_as_ushort(h) & 0x7fffu;
+    sf.amax = max(sf.amax, a >= 0x7c00u ? (a == 0x7c00u ? 1u : 2u) : 0u);
+    sf.tiny |= (a < 0x0400u) & (v != V(0));
+    return h;
+  } else if constexpr (std::is_same_v<T, __nv_bfloat16>) {
+    const __nv_bfloat16 h = std::is_same_v<V, float> ? __float2bfloat16_rn(float(v)) : __double2bfloat16(double(v));
+    const uint32_t a = __bfloat16_as_ushort(h) & 0x7fffu;
+    sf.amax = max(sf.amax, a >= 0x7f80u ? (a == 0x7f80u ? 1u : 2u) : 0u);
+    sf.tiny |= (a < 0x0080u) & (v != V(0));
+    return h;
+  } else if constexpr (std::is_same_v<T, float>) {
+    const float f = float(v);  // v is float already, or a double rounded once here
+    const uint32_t a = __float_as_uint(f) & 0x7fffffffu;
+    sf.amax = max(sf.amax, a >= 0x7f800000u ? (a == 0x7f800000u ? 1u : 2u) : 0u);
+    sf.tiny |= (a < 0x00800000u) & (double(f) != double(v) || false) & (v != V(0));
+    return f;
+  } else {
+    uint32_t dummy = 0;
+    const double d = droundT<US>(double(v), dummy);
+    const bool fin = isfinite(d);
+    sf.amax = max(sf.amax, fin ? 0u : (isnan(d) ? 2u : 1u));
+    sf.tiny |= (dummy & kUnderflow) ? 1u : 0u;
+    return d;
+  }
+}
+
+__device__ __forceinline__ uint32_t store_flags_bits(const StoreFlags& sf) {
+  return (sf.amax == 1u ? kOverflow : 0u) | (sf.amax >= 2u ? kInvalid : 0u) | (sf.tiny ? kUnderflow : 0u);
+}
 
 template <typename T>
 __device__ __forceinline__ void store_w(void* W, int64_t idx, double v);
@@ -106,6 +152,7 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
   }
   __syncthreads();
   const int nb = P.poisson ? 6 : 1;
+  StoreFlags sf;
   for (int j = warp; j < kGeomCells; j += kGeomThreads / 32) {
     const int64_t cell = cell0 + j;
     if (cell >= P.n_cells || sBad[j]) continue;
@@ -114,6 +161,7 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
     double G[6];
     #pragma unroll
     for (int b = 0; b < 6; ++b) G[b] = sG[j][b];
+    const int nq = P.n_q;
     for (int q = lane; q < P.n_q; q += 32) {
       const double* xi = P.rule_x + 3 * q;
       double zq = 1.0;
@@ -132,17 +180,42 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
         default: have_z = false;
       }
       const double omega = P.rule_w[q];  // already rounded to u_g on the host
-      #pragma unroll
-      for (int b = 0; b < 6; ++b) {
-        if (b < nb) {
-          double val = dmulT<UG>(omega, G[b], fl);
-          if (have_z) val = dmulT<UG>(val, zq, fl);
-          store_w<T>(P.W, row + int64_t(b) * P.n_q + q, droundT<US>(val, fl));
+      T* wrow = static_cast<T*>(P.W) + row + q;
+      // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192).
+      if constexpr (UG == kFP32) {
+        // fp32 operands: the hardware fp32 product is the correctly rounded binary64 one
+        const float om = float(omega), zf = float(zq);
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            float val = __fmul_rn(om, float(G[b]));
+            if (have_z) val = __fmul_rn(val, zf);
+            wrow[b * nq] = to_storage<T, US>(val, sf);
+          }
+        }
+      } else if constexpr (UG == kFP64) {
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            double val = __dmul_rn(omega, G[b]);
+            if (have_z) val = __dmul_rn(val, zq);
+            wrow[b * nq] = to_storage<T, US>(val, sf);
+          }
+        }
+      } else {
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            double val = droundT<UG>(__dmul_rn(omega, G[b]), fl);
+            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
+            wrow[b * nq] = to_storage<T, US>(val, sf);
+          }
         }
       }
     }
     for (int64_t k = int64_t(nb) * P.n_q + lane; k < P.k_pad; k += 32) store_w<T>(P.W, row + k, 0.0);
   }
+  fl |= store_flags_bits(sf);
   fl = __reduce_or_sync(0xffffffffu, fl);
   if (lane == 0 && fl) atomicOr(P.flags, fl);
 }
