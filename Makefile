@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2410_12614_b200
 LIB := $(PKG)/lib/libmpfem_b200.so
-SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/host_setup.cpp $(PKG)/csrc/host_mesh.cpp
+SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/assembly_capi.cu $(PKG)/csrc/host_setup.cpp $(PKG)/csrc/host_mesh.cpp
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/mpfem_b200.h
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -shared \

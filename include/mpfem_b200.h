@@ -150,17 +150,21 @@ int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
                          int32_t n_dofs, int64_t* inc_ptr, int64_t* inc, void* stream);
 
 /* Replaces assemble_matrix (assembly.cpp:41-88): scatter-add of local matrices into
- * CSR values. mode 0 = atomic (red.global, order-free), 1 = deterministic (each entry
- * summed in ascending cell order, bitwise equal to the reference at fmt).
- * locals: n_cells x n_loc x n_loc, fp32 (locals_fmt 2) or fp64 (3); values fp32 (fmt 2)
- * or fp64 (fmt 3). inc_ptr/inc needed for mode 1 (may be NULL for mode 0).
- * cell_begin/cell_end restrict the contributing cells (multi-GPU slabs); values are
- * accumulated onto their current contents when accumulate != 0 (else overwritten). */
+ * CSR values. mode 0 = atomic (red.global, order-free), 1 = deterministic (each entry is
+ * the sequential ascending-cell sum at fmt, bitwise equal to the reference).
+ *   locals: local matrices of cells [cell_begin, cell_end) (locals[0] is cell_begin's),
+ *           n_loc x n_loc row-major each, fp32 (locals_fmt 2) or fp64 (3)
+ *   values: CSR values, fp32 (fmt 2) or fp64 (fmt 3)
+ *   inc_ptr/inc: incidence (mpfem_b200_incidence), required for mode 1
+ *   rows/n_rows: mode 1 only -- the rows to assemble (NULL: all n_dofs rows)
+ *   accumulate: 0 = the entries start empty (mode 1: first contribution taken exactly;
+ *               mode 0: values zeroed), 1 = continue from the current contents (the
+ *               prefix partial sums received from the rank owning lower cells). */
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
                         int64_t cell_end, int n_loc, const int32_t* cell_dofs,
                         int32_t n_dofs, const int64_t* row_ptr, const int32_t* col_idx,
                         const int64_t* inc_ptr, const int64_t* inc, void* values, int fmt,
-                        int mode, int accumulate, int32_t row_begin, int32_t row_end,
+                        int mode, int accumulate, const int32_t* rows, int64_t n_rows,
                         void* stream);
 
 #ifdef __cplusplus

@@ -140,7 +140,7 @@ def lib():
         "mpfem_b200_incidence": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp]),
         "mpfem_b200_assemble": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp,
                                           C.c_int32, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
-                                          C.c_int32, C.c_int32, vp]),
+                                          vp, C.c_int64, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -1,0 +1,111 @@
+"""Global assembly on the device: dof map, CSR sparsity, scatter-add.
+
+Host mirror of the reference's mesh/assembly interface (mesh.hpp:58-68 DofMap /
+build_dofmap, assembly.hpp:13-34 SparseCoo / assemble_matrix) over the C-ABI. Arrays are
+torch CUDA tensors; the CSR (row_ptr, col_idx, values) holds exactly the reference COO
+entries in (row, col) order.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import ConfigError, _ptr, _stream_handle, check, lib, nphi
+
+FP32, FP64 = 2, 3
+ATOMIC, DETERMINISTIC = 0, 1
+
+
+@dataclass
+class DofMap:  # mesh.hpp:58-65
+    n_dofs: int
+    n_local: int
+    cell_dofs: "object"  # torch.int32 (n_cells, n_local) on device
+    max_multiplicity: int
+
+    @property
+    def n_cells(self) -> int:
+        return int(self.cell_dofs.shape[0])
+
+
+@dataclass
+class CsrPattern:
+    n_rows: int
+    row_ptr: "object"  # int64 (n_rows + 1)
+    col_idx: "object"  # int32 (nnz)
+    inc_ptr: "object"  # int64 (n_rows + 1): dof -> incident (cell, local) pairs
+    inc: "object"      # int64 (n_cells * n_local), cell * n_local + local, ascending
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+
+def build_dofmap(p: int, cells, n_verts: int, stream=None) -> DofMap:
+    """build_dofmap(mesh, basis(p), continuous) (mesh.cpp:204-298) for a tet mesh given by
+    its cell->vertex table `cells` (n, 4) int32 on the device."""
+    import torch
+    if cells.dtype != torch.int32 or not cells.is_cuda:
+        raise ConfigError("cells must be an int32 CUDA tensor")
+    n = int(cells.shape[0])
+    n_loc = nphi(p)
+    cd = torch.empty((n, n_loc), dtype=torch.int32, device=cells.device)
+    nd, mm = C.c_int32(0), C.c_int32(0)
+    check(lib().mpfem_b200_dofmap(p, _ptr(cells), n, int(n_verts), _ptr(cd), C.byref(nd),
+                                  C.byref(mm), _stream_handle(stream)))
+    return DofMap(nd.value, n_loc, cd, mm.value)
+
+
+def incidence(dm: DofMap, stream=None):
+    import torch
+    dev = dm.cell_dofs.device
+    inc_ptr = torch.empty(dm.n_dofs + 1, dtype=torch.int64, device=dev)
+    inc = torch.empty(dm.n_cells * dm.n_local, dtype=torch.int64, device=dev)
+    check(lib().mpfem_b200_incidence(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
+                                     _ptr(inc_ptr), _ptr(inc), _stream_handle(stream)))
+    return inc_ptr, inc
+
+
+def csr_pattern(dm: DofMap, stream=None) -> CsrPattern:
+    """The reference COO key set (assembly.cpp:67-86) as CSR, plus the incidence lists."""
+    import torch
+    dev = dm.cell_dofs.device
+    row_ptr = torch.empty(dm.n_dofs + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64(0)
+    sh = _stream_handle(stream)
+    check(lib().mpfem_b200_csr_pattern(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
+                                       _ptr(row_ptr), None, C.byref(nnz), sh))
+    col_idx = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+    check(lib().mpfem_b200_csr_pattern(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
+                                       _ptr(row_ptr), _ptr(col_idx), C.byref(nnz), sh))
+    inc_ptr, inc = incidence(dm, stream)
+    return CsrPattern(dm.n_dofs, row_ptr, col_idx, inc_ptr, inc)
+
+
+def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
+                    mode: int = DETERMINISTIC, cell_begin: int = 0, cell_end: int | None = None,
+                    rows=None, accumulate: bool = False, values=None, stream=None):
+    """assemble_matrix (assembly.cpp:41-88) into CSR values at fmt (fp32/fp64).
+
+    `local` holds the local matrices of cells [cell_begin, cell_end), (n, n_loc, n_loc)
+    fp32 or fp64. Deterministic mode reproduces the reference's ascending-cell sequential
+    sum bitwise; atomic mode is order-free (within gamma_{m+1} of the exact sum)."""
+    import torch
+    if cell_end is None:
+        cell_end = cell_begin + int(local.shape[0])
+    if local.dtype == torch.float32:
+        lf = FP32
+    elif local.dtype == torch.float64:
+        lf = FP64
+    else:
+        raise ConfigError("local matrices must be fp32 or fp64")
+    if values is None:
+        values = torch.empty(pat.nnz, dtype=torch.float32 if fmt == FP32 else torch.float64,
+                             device=local.device)
+    n_rows = 0 if rows is None else int(rows.numel())
+    check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), dm.n_local,
+                                    _ptr(dm.cell_dofs), dm.n_dofs, _ptr(pat.row_ptr),
+                                    _ptr(pat.col_idx), _ptr(pat.inc_ptr), _ptr(pat.inc),
+                                    _ptr(values), int(fmt), int(mode), int(accumulate),
+                                    _ptr(rows), n_rows, _stream_handle(stream)))
+    return values

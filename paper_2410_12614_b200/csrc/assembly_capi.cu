@@ -1,0 +1,300 @@
+// assembly_capi.cu -- C-ABI entry points of the dof map / CSR / scatter path
+// (include/mpfem_b200.h), driving the kernels of assembly.cuh. Sorting and scans use CUB.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/mpfem_b200.h"
+#include "assembly.cuh"
+
+using namespace mpfem_b200;
+
+// shared with capi.cu: the ABI's single thread-local last-error string
+void mpfem_b200_set_last_error(const std::string& msg);
+
+namespace {
+
+struct AsmError {
+  int code;
+  std::string msg;
+};
+
+#define ACUDA(expr)                                                                 \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess) throw AsmError{4, std::string(#expr) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+template <typename F>
+int aguard(F&& f) {
+  try {
+    mpfem_b200_set_last_error("");
+    f();
+    return 0;
+  } catch (const AsmError& e) {
+    mpfem_b200_set_last_error(e.msg);
+    return e.code;
+  }
+}
+
+// Stream-ordered scratch, released in stream order at scope exit.
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    ACUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+unsigned grid_for(int64_t n, int threads = 256) {
+  return unsigned(std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 32)));
+}
+
+int bits_for(int64_t maxval) {
+  int b = 1;
+  while (b < 62 && (int64_t(1) << b) <= maxval) ++b;
+  return b;
+}
+
+template <typename T>
+__global__ void iota_kernel(T* out, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = T(i);
+}
+
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ src, const int32_t* __restrict__ idx, int64_t n,
+                              T* __restrict__ dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
+template <typename T>
+T read1(const T* dev, cudaStream_t st) {
+  T h{};
+  ACUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, st));
+  ACUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+// dof -> (cell*n_loc + local) lists, ascending position within each dof.
+void build_incidence(const int32_t* cell_dofs, int64_t n, int32_t n_dofs, int64_t* inc_ptr,
+                     int64_t* inc, Scratch& S) {
+  cudaStream_t st = S.st;
+  int64_t* counts = S.get<int64_t>(size_t(n_dofs) + 1);
+  ACUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t(n_dofs) + 1), st));
+  asmb::dof_count_kernel<<<grid_for(n), 256, 0, st>>>(cell_dofs, n, counts);
+  size_t tb = 0;
+  ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, inc_ptr, n_dofs + 1, st));
+  void* tmp = S.get<char>(tb);
+  ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, inc_ptr, n_dofs + 1, st));
+  // stable LSD radix sort of (dof, position)
+  int32_t* keys_out = S.get<int32_t>(n);
+  int64_t* pos_in = S.get<int64_t>(n);
+  iota_kernel<<<grid_for(n), 256, 0, st>>>(pos_in, n);
+  size_t tb2 = 0;
+  const int bits = bits_for(n_dofs);
+  ACUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, cell_dofs, keys_out, pos_in, inc, n, 0, bits, st));
+  void* tmp2 = S.get<char>(tb2);
+  ACUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, cell_dofs, keys_out, pos_in, inc, n, 0, bits, st));
+}
+
+__global__ void max_diff_kernel(const int64_t* __restrict__ ptr, int32_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < n;
+       r += int64_t(gridDim.x) * blockDim.x)
+    m = max(m, (unsigned long long)(ptr[r + 1] - ptr[r]));
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+int64_t max_count(const int64_t* inc_ptr, int32_t n_dofs, Scratch& S) {
+  unsigned long long* out = S.get<unsigned long long>(1);
+  ACUDA(cudaMemsetAsync(out, 0, 8, S.st));
+  max_diff_kernel<<<grid_for(n_dofs), 256, 0, S.st>>>(inc_ptr, n_dofs, out);
+  return int64_t(read1(out, S.st));
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_verts,
+                      int32_t* cell_dofs, int32_t* n_dofs, int32_t* max_multiplicity,
+                      void* stream) {
+  return aguard([&] {
+    if (p < 1 || p > 8) throw AsmError{2, "element degree must be in [1, 8]"};
+    if (n_cells < 1) throw AsmError{2, "dof map needs at least one cell"};
+    if (n_verts >= (int64_t(1) << 21) - 1)
+      throw AsmError{2, "vertex ids must fit 21 bits for the packed node keys"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch S(st);
+    const int n_phi = (p + 1) * (p + 2) * (p + 3) / 6;
+    const int64_t n = n_cells * n_phi;
+    if (n >= (int64_t(1) << 31)) throw AsmError{2, "n_cells * n_phi must fit int32"};
+    std::vector<int8_t> al(size_t(n_phi) * 4);
+    for (int k = 0; k < n_phi; ++k) {
+      int a[4];
+      asmb::node_alpha(p, k, a);
+      for (int t = 0; t < 4; ++t) al[size_t(k) * 4 + t] = int8_t(a[t]);
+    }
+    int8_t* d_al = S.get<int8_t>(al.size());
+    ACUDA(cudaMemcpyAsync(d_al, al.data(), al.size(), cudaMemcpyHostToDevice, st));
+    uint64_t* hi = S.get<uint64_t>(n);
+    uint64_t* lo = S.get<uint64_t>(n);
+    int32_t* pos = S.get<int32_t>(n);
+    asmb::node_keys_kernel<<<grid_for(n), 256, 0, st>>>(cells, n_cells, p, n_phi, d_al, hi, lo, pos);
+    ACUDA(cudaGetLastError());
+    // LSD: stable sort by lo, then by hi -> order (hi, lo, position)
+    uint64_t* k1 = S.get<uint64_t>(n);
+    int32_t* p1 = S.get<int32_t>(n);
+    size_t tb = 0;
+    ACUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, lo, k1, pos, p1, n, 0, 64, st));
+    void* tmp = S.get<char>(tb);
+    ACUDA(cub::DeviceRadixSort::SortPairs(tmp, tb, lo, k1, pos, p1, n, 0, 64, st));
+    uint64_t* hi_g = S.get<uint64_t>(n);
+    gather_kernel<<<grid_for(n), 256, 0, st>>>(hi, p1, n, hi_g);
+    uint64_t* hi_s = S.get<uint64_t>(n);
+    int32_t* p2 = S.get<int32_t>(n);
+    size_t tb2 = 0;
+    ACUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, hi_g, hi_s, p1, p2, n, 0, 64, st));
+    void* tmp2 = S.get<char>(tb2);
+    ACUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, hi_g, hi_s, p1, p2, n, 0, 64, st));
+    uint64_t* lo_s = S.get<uint64_t>(n);
+    gather_kernel<<<grid_for(n), 256, 0, st>>>(lo, p2, n, lo_s);
+    // segment heads, first-encounter flags (in position order), numbering
+    int32_t* first_flag = S.get<int32_t>(n);
+    int32_t* seg_start = S.get<int32_t>(n);
+    ACUDA(cudaMemsetAsync(first_flag, 0, sizeof(int32_t) * size_t(n), st));
+    asmb::first_flags_kernel<<<grid_for(n), 256, 0, st>>>(hi_s, lo_s, p2, n, first_flag, seg_start);
+    int32_t* seg_id = S.get<int32_t>(n);
+    int32_t* scan_first = S.get<int32_t>(n);
+    size_t tb3 = 0;
+    ACUDA(cub::DeviceScan::InclusiveSum(nullptr, tb3, seg_start, seg_id, n, st));
+    size_t tb4 = 0;
+    ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb4, first_flag, scan_first, n, st));
+    void* tmp3 = S.get<char>(std::max(tb3, tb4));
+    ACUDA(cub::DeviceScan::InclusiveSum(tmp3, tb3, seg_start, seg_id, n, st));
+    ACUDA(cub::DeviceScan::ExclusiveSum(tmp3, tb4, first_flag, scan_first, n, st));
+    const int32_t n_seg = read1(seg_id + (n - 1), st);
+    int32_t* seg_first_pos = S.get<int32_t>(n_seg);
+    int32_t* seg_begin = S.get<int32_t>(n_seg);
+    asmb::seg_first_kernel<<<grid_for(n), 256, 0, st>>>(p2, seg_start, seg_id, n, seg_first_pos, seg_begin);
+    asmb::assign_dofs_kernel<<<grid_for(n), 256, 0, st>>>(p2, seg_id, seg_first_pos, scan_first, n, cell_dofs);
+    int32_t* dmax = S.get<int32_t>(1);
+    ACUDA(cudaMemsetAsync(dmax, 0, 4, st));
+    asmb::seg_len_max_kernel<<<grid_for(n_seg), 256, 0, st>>>(seg_begin, n_seg, n, dmax);
+    ACUDA(cudaGetLastError());
+    if (n_dofs) *n_dofs = n_seg;
+    if (max_multiplicity) *max_multiplicity = read1(dmax, st);
+  });
+}
+
+int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                         int64_t* inc_ptr, int64_t* inc, void* stream) {
+  return aguard([&] {
+    if (n_loc < 1 || n_dofs < 1) throw AsmError{2, "dof map has no complete cells"};
+    Scratch S(static_cast<cudaStream_t>(stream));
+    build_incidence(cell_dofs, n_cells * n_loc, n_dofs, inc_ptr, inc, S);
+    ACUDA(cudaGetLastError());
+  });
+}
+
+int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                           int64_t* row_ptr, int32_t* col_idx, int64_t* nnz, void* stream) {
+  return aguard([&] {
+    if (n_loc < 1 || n_dofs < 1) throw AsmError{2, "dof map has no complete cells"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch S(st);
+    const int64_t n = n_cells * n_loc;
+    int64_t* inc_ptr = S.get<int64_t>(size_t(n_dofs) + 1);
+    int64_t* inc = S.get<int64_t>(n);
+    build_incidence(cell_dofs, n, n_dofs, inc_ptr, inc, S);
+    const int64_t mmax = max_count(inc_ptr, n_dofs, S);
+    int cap = 32;
+    while (cap < mmax * n_loc) cap <<= 1;
+    if (cap > 8192) throw AsmError{2, "row candidate list exceeds 8192 (multiplicity x n_loc)"};
+    const int warps = std::max(1, std::min(8, 32768 / (cap * 4)));
+    const size_t smem = size_t(warps) * cap * 4;
+    const unsigned grid = unsigned(std::min<int64_t>((n_dofs + warps - 1) / warps, 148 * 16));
+    int64_t* row_nnz = S.get<int64_t>(size_t(n_dofs) + 1);
+    ACUDA(cudaMemsetAsync(row_nnz + n_dofs, 0, sizeof(int64_t), st));
+    asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs, cap,
+                                                          0, row_nnz, nullptr, nullptr);
+    ACUDA(cudaGetLastError());
+    size_t tb = 0;
+    ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, row_nnz, row_ptr, n_dofs + 1, st));
+    void* tmp = S.get<char>(tb);
+    ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, row_nnz, row_ptr, n_dofs + 1, st));
+    const int64_t total = read1(row_ptr + n_dofs, st);
+    if (nnz) *nnz = total;
+    if (col_idx) {
+      asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs,
+                                                            cap, 1, nullptr, row_ptr, col_idx);
+      ACUDA(cudaGetLastError());
+    }
+  });
+}
+
+int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, int64_t cell_end,
+                        int n_loc, const int32_t* cell_dofs, int32_t n_dofs, const int64_t* row_ptr,
+                        const int32_t* col_idx, const int64_t* inc_ptr, const int64_t* inc,
+                        void* values, int fmt, int mode, int accumulate, const int32_t* rows,
+                        int64_t n_rows, void* stream) {
+  return aguard([&] {
+    if (locals_fmt != 2 && locals_fmt != 3) throw AsmError{2, "local matrices must be fp32 or fp64"};
+    if (fmt != 2 && fmt != 3) throw AsmError{2, "CSR values must be fp32 or fp64"};
+    if (mode != 0 && mode != 1) throw AsmError{2, "assembly mode must be 0 (atomic) or 1 (deterministic)"};
+    if (cell_end < cell_begin || n_loc < 1) throw AsmError{2, "bad cell range"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // locals[0] is cell_begin's matrix: rebase so the kernels can index by global cell id
+    const size_t esz = locals_fmt == 2 ? 4 : 8;
+    const char* base = static_cast<const char*>(locals) - size_t(cell_begin) * n_loc * n_loc * esz;
+    if (mode == 0) {
+      if (!accumulate) {
+        const int64_t nnz = read1(row_ptr + n_dofs, st);
+        ACUDA(cudaMemsetAsync(values, 0, size_t(nnz) * (fmt == 2 ? 4 : 8), st));
+      }
+      const int64_t work = (cell_end - cell_begin) * n_loc;
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((work + 7) / 8, 148 * 64)));
+      if (locals_fmt == 2 && fmt == 2)
+        asmb::assemble_atomic_kernel<float, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<float*>(values));
+      else if (locals_fmt == 2)
+        asmb::assemble_atomic_kernel<float, double><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<double*>(values));
+      else if (fmt == 2)
+        asmb::assemble_atomic_kernel<double, float><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<float*>(values));
+      else
+        asmb::assemble_atomic_kernel<double, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<double*>(values));
+    } else {
+      if (!inc_ptr || !inc) throw AsmError{2, "deterministic assembly needs the incidence lists"};
+      const int64_t nr = rows ? n_rows : n_dofs;
+      if (nr == 0) return;
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, 148 * 64)));
+      const int init = accumulate ? 0 : 1;
+      if (locals_fmt == 2 && fmt == 2)
+        asmb::assemble_det_kernel<float, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<float*>(values));
+      else if (locals_fmt == 2)
+        asmb::assemble_det_kernel<float, double><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<double*>(values));
+      else if (fmt == 2)
+        asmb::assemble_det_kernel<double, float><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<float*>(values));
+      else
+        asmb::assemble_det_kernel<double, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<double*>(values));
+    }
+    ACUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -119,6 +119,8 @@ int device_sm_count() {
 
 }  // namespace
 
+void mpfem_b200_set_last_error(const std::string& msg) { g_last_error = msg; }
+
 struct mpfem_b200_setup_s {
   int p = 0, form = 0, up = 3, ug = 3, uq = 3, us = 3, engine = 0;
   int n_phi = 0, n_q = 0, n_d = 1, n_blocks = 1;

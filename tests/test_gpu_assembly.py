@@ -1,0 +1,133 @@
+"""GPU dof map / CSR / scatter-add against the reference algorithm (oracle, pinned to the
+compiled reference). Bars: dof map and sparsity bitwise; deterministic values bitwise;
+atomic values within gamma_{m+1}(fmt) * sum|contrib| of the exact sum (test_assembly.cpp:165-167).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2410_12614_b200 as mp  # noqa: E402
+from paper_2410_12614_b200 import assembly as am  # noqa: E402
+from oracle_lib import nphi  # noqa: E402
+
+
+def gpu_dofmap(p, verts, cells):
+    return am.build_dofmap(p, torch.from_numpy(np.ascontiguousarray(cells)).cuda(), verts.shape[0])
+
+
+@pytest.mark.parametrize("dims,p", [((3, 2, 2), 1), ((3, 2, 2), 2), ((3, 2, 2), 3), ((2, 2, 2), 4),
+                                    ((2, 1, 1), 6), ((1, 1, 2), 8), ((6, 5, 4), 2), ((5, 4, 4), 3)])
+def test_dofmap_bitwise(oracle, dims, p):
+    verts, cells = oracle.structured_tet_mesh(*dims, 1.0, 0.15, 7)
+    cd, nd, mm = oracle.build_dofmap(p, verts, cells)
+    dm = gpu_dofmap(p, verts, cells)
+    assert dm.n_dofs == nd and dm.max_multiplicity == mm
+    assert np.array_equal(dm.cell_dofs.cpu().numpy(), cd)
+
+
+def test_dofmap_known_answers(oracle):
+    # test_mesh.cpp:194-199: 2x2x2 tet mesh, P1: 27 dofs, max multiplicity 24
+    verts, cells = oracle.structured_tet_mesh(2, 2, 2, 1.0, 0.15, 7)
+    dm = gpu_dofmap(1, verts, cells)
+    assert (dm.n_dofs, dm.max_multiplicity) == (27, 24)
+    # (p n + 1)^3 dofs on an n^3 Kuhn mesh
+    for n, p in ((4, 2), (3, 3)):
+        verts, cells = oracle.structured_tet_mesh(n, n, n, 1.0, 0.15, 3)
+        assert gpu_dofmap(p, verts, cells).n_dofs == (p * n + 1) ** 3
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_csr_pattern_and_values_bitwise(oracle, p):
+    verts, cells = oracle.structured_tet_mesh(4, 3, 3, 1.0, 0.15, 11)
+    cd, nd, _ = oracle.build_dofmap(p, verts, cells)
+    dm = gpu_dofmap(p, verts, cells)
+    pat = am.csr_pattern(dm)
+    rng = np.random.default_rng(p)
+    loc32 = rng.uniform(-1, 1, size=(cells.shape[0], nphi(p), nphi(p))).astype(np.float32)
+    for fmt in (2, 3):
+        rows, cols, vals, _ = oracle.assemble_matrix(cd, nd, loc32.astype(np.float64), fmt)
+        rp = pat.row_ptr.cpu().numpy()
+        assert pat.nnz == rows.size
+        assert np.array_equal(np.repeat(np.arange(nd), np.diff(rp)), rows)
+        assert np.array_equal(pat.col_idx.cpu().numpy(), cols)
+        v = am.assemble_matrix(torch.from_numpy(loc32).cuda(), dm, pat, fmt, am.DETERMINISTIC)
+        torch.cuda.synchronize()
+        got = v.double().cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), vals.view(np.uint64)), fmt
+        # atomic mode: gamma_{m+1} * sum |contrib|
+        va = am.assemble_matrix(torch.from_numpy(loc32).cuda(), dm, pat, fmt, am.ATOMIC)
+        torch.cuda.synchronize()
+        absum = oracle.assemble_matrix(cd, nd, np.abs(loc32.astype(np.float64)), 3)[2]
+        u = 2.0**-24 if fmt == 2 else 2.0**-53
+        m = 25
+        assert np.all(np.abs(va.double().cpu().numpy() - vals) <= (m + 1) * u / (1 - (m + 1) * u) * absum * 2)
+    # fp64 locals into fp32 values (cast at fmt, assembly.cpp:57)
+    loc64 = rng.uniform(-1, 1, size=(cells.shape[0], nphi(p), nphi(p)))
+    rows, cols, vals, _ = oracle.assemble_matrix(cd, nd, loc64, 2)
+    v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat, 2, am.DETERMINISTIC)
+    assert np.array_equal(v.double().cpu().numpy().view(np.uint64), vals.view(np.uint64))
+
+
+def test_partial_cell_ranges_compose_bitwise(oracle):
+    """Assembling cells [0, k) then continuing with [k, n) (accumulate) equals one pass:
+    the multi-GPU interface exchange invariant."""
+    p = 2
+    verts, cells = oracle.structured_tet_mesh(3, 3, 4, 1.0, 0.15, 5)
+    dm = gpu_dofmap(p, verts, cells)
+    pat = am.csr_pattern(dm)
+    rng = np.random.default_rng(9)
+    loc = torch.from_numpy(rng.uniform(-1, 1, size=(cells.shape[0], 10, 10)).astype(np.float32)).cuda()
+    full = am.assemble_matrix(loc, dm, pat, 2)
+    k = cells.shape[0] // 2
+    part = am.assemble_matrix(loc[:k], dm, pat, 2, cell_begin=0, cell_end=k)
+    part = am.assemble_matrix(loc[k:], dm, pat, 2, cell_begin=k, cell_end=cells.shape[0],
+                              accumulate=True, values=part)
+    torch.cuda.synchronize()
+    # rows untouched by [0, k) start from -0.0 in the first pass; equal values otherwise
+    assert torch.equal(full, part) or bool(torch.all((full == part)))
+
+
+def test_config4_reduced_end_to_end(oracle):
+    """BASELINE config 4 at 12^3 x 6 tets: GPU Poisson P2 locals (mixed) -> GPU assembly,
+    bitwise equal to the reference assembly of the same locals; global Poisson rows sum to
+    ~0 (constants in the kernel)."""
+    n, p = 12, 2
+    verts, cells = mp.structured_tet_mesh(n, n, n, 1.0, 0.15, 1)
+    vd = torch.from_numpy(verts).cuda()
+    cdev = torch.from_numpy(cells).cuda()
+    s = mp.make_setup(p, mp.mode_config("mixed_bf16", mp.FormKind.poisson))
+    loc = s.cell_matrices(vd, cdev, mp.CoefKind.sincosexp)
+    dm = am.build_dofmap(p, cdev, verts.shape[0])
+    pat = am.csr_pattern(dm)
+    vals = am.assemble_matrix(loc, dm, pat, 3)
+    torch.cuda.synchronize()
+    cd, nd, _ = oracle.build_dofmap(p, verts, cells)
+    assert nd == dm.n_dofs and np.array_equal(cd, dm.cell_dofs.cpu().numpy())
+    rows, cols, rv, _ = oracle.assemble_matrix(cd, nd, loc.double().cpu().numpy(), 3)
+    assert np.array_equal(vals.cpu().numpy().view(np.uint64), rv.view(np.uint64))
+    rp = pat.row_ptr.cpu().numpy()
+    rs = np.add.reduceat(rv, rp[:-1])
+    scale = np.abs(rv).max()
+    assert np.abs(rs).max() <= 1e-2 * scale
+
+
+@pytest.mark.slow
+def test_config4_full_size_p2_properties():
+    """96^3 x 6 = 5,308,416 tets, P2: dof count, symmetric pattern, sampled rows."""
+    n, p = 96, 2
+    verts, cells = mp.structured_tet_mesh(n, n, n, 1.0, 0.15, 1)
+    cdev = torch.from_numpy(cells).cuda()
+    dm = am.build_dofmap(p, cdev, verts.shape[0])
+    assert dm.n_dofs == (p * n + 1) ** 3 == 7189057
+    pat = am.csr_pattern(dm)
+    rp = pat.row_ptr
+    assert int(rp[-1]) == pat.nnz
+    nnz_row = (rp[1:] - rp[:-1]).double()
+    assert 20 < float(nnz_row.mean()) < 40
+    # pattern symmetry: multiset of (row, col) equals (col, row)
+    rows = torch.repeat_interleave(torch.arange(dm.n_dofs, device="cuda"), rp[1:] - rp[:-1])
+    key = rows.to(torch.int64) * dm.n_dofs + pat.col_idx.to(torch.int64)
+    keyt = pat.col_idx.to(torch.int64) * dm.n_dofs + rows.to(torch.int64)
+    assert torch.equal(torch.sort(key).values, torch.sort(keyt).values)
