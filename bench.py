@@ -225,6 +225,73 @@ def run_sweep(mp, torch, dev):
     return res
 
 
+def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
+    """BASELINE config 4: 96^3 hexes x 6 tets, Poisson with c(x), mixed (bf16 storage)
+    cell kernels, deterministic CSR assembly in fp32 and fp64; z-slabs over the ranks with
+    the interface partial-sum exchange. Times are CUDA-event times, max over ranks."""
+    from paper_2410_12614_b200 import assembly as am
+    from paper_2410_12614_b200 import distributed as D
+    hbm = peaks()[0]
+    verts, cells = mp.structured_tet_mesh(n, n, n, 1.0, 0.15, 1)
+    vd = torch.from_numpy(verts).to(dev)
+    cdev = torch.from_numpy(cells).to(dev)
+    cpl = 6 * n * n
+    cb, ce = D.slab_cell_range(rank, world, n, cpl)
+    out = []
+
+    class Backend:
+        assemble_matrix = staticmethod(am.assemble_matrix)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            r = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, r
+
+    for p in degrees:
+        t_dof, dm = timed(lambda: am.build_dofmap(p, cdev, verts.shape[0]), 1)
+        t_pat, pat = timed(lambda: am.csr_pattern(dm), 1)
+        plan = D.plan_slabs(dm, pat, rank, world, cb, ce)
+        s = mp.make_setup(p, mp.mode_config("mixed_bf16", mp.FormKind.poisson))
+        s.reserve(ce - cb)
+        local = torch.empty((ce - cb, nphi(p), nphi(p)), dtype=torch.float32, device=dev)
+        t_cell, _ = timed(lambda: s.cell_matrices(vd, cdev[cb:ce], mp.CoefKind.sincosexp, out=local.view(ce - cb, -1)))
+        res = {"p": p, "n_dofs": dm.n_dofs, "nnz": pat.nnz, "cells_per_rank": ce - cb,
+               "dofmap_ms": t_dof, "csr_pattern_ms": t_pat, "cell_kernels_ms": t_cell}
+        for fmt in (2, 3):
+            sv = 4 if fmt == 2 else 8
+            if world > 1:
+                t_asm, _ = timed(lambda: D.assemble_slab(Backend, local, dm, pat, plan, fmt))
+            else:
+                vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
+                t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
+            nb = (ce - cb) * (nphi(p) ** 2 * 4 + 4 * nphi(p)) + pat.nnz / world * (sv + 4) + 8 * (dm.n_dofs + 1) / world
+            key = "fp32" if fmt == 2 else "fp64"
+            res[f"assemble_{key}_ms"] = t_asm
+            res[f"assemble_{key}_hbm_frac"] = nb / (t_asm * 1e-3) / 1e9 / hbm
+        if world == 1:
+            vals = torch.empty(pat.nnz, dtype=torch.float32, device=dev)
+            t_at, _ = timed(lambda: am.assemble_matrix(local, dm, pat, 2, am.ATOMIC, values=vals))
+            res["assemble_atomic_fp32_ms"] = t_at
+        res["kernels_plus_assembly_fp32_ms"] = t_cell + res["assemble_fp32_ms"]
+        out.append(res)
+        del local, pat, dm, s
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -233,6 +300,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--sweep", action="store_true", help="add the config-2 p=1..8 sweep")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-assembly", action="store_true", help="skip the config-4 assembly key")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -363,6 +431,10 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if not args.no_assembly:
+        line["assembly"] = {"workload": "config4: 96^3 x 6 tets, poisson P2/P3, mixed-bf16 kernels, "
+                                        "deterministic CSR, z-slabs over ranks",
+                            "results": run_assembly(mp, torch, dev, rank, world)}
     if args.sweep and rank == 0:
         line["sweep"] = run_sweep(mp, torch, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
