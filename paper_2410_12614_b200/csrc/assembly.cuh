@@ -226,10 +226,13 @@ __device__ __forceinline__ int64_t find_col(const int32_t* __restrict__ cols, in
   return lo;
 }
 
-// Deterministic: one warp per row (rows list or all rows). Accumulators live in the
-// values array itself (this warp owns the row). init != 0 starts from -0.0 (so the first
-// contribution is taken exactly, as the reference's cast), else continues from the
-// current contents (multi-GPU partial sums).
+// Deterministic: one warp per row (rows list or all rows). The row's columns and its
+// accumulators live in shared memory; the incident local rows are fetched in bulk
+// (all lanes, independent loads, positions binary-searched in shared memory) and then
+// added strictly in ascending incidence order, so each CSR entry is the reference's
+// sequential ascending-cell sum. init != 0 starts every entry at -0.0 (the first
+// contribution is then taken exactly, as the reference's cast); otherwise the sum
+// continues from the current values (multi-GPU prefix partial sums).
 template <typename TL, typename TV>
 __global__ void assemble_det_kernel(const TL* __restrict__ locals, int n_loc,
                                     const int32_t* __restrict__ cell_dofs,
@@ -238,29 +241,64 @@ __global__ void assemble_det_kernel(const TL* __restrict__ locals, int n_loc,
                                     const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
                                     const int32_t* __restrict__ rows, int64_t n_rows,
                                     int64_t cell_begin, int64_t cell_end, int init,
-                                    TV* __restrict__ values) {
+                                    TV* __restrict__ values, int cap_cols, int cap_buf) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t per_warp = size_t(cap_cols) * (sizeof(int32_t) + sizeof(TV)) +
+                          size_t(cap_buf) * (sizeof(int32_t) + sizeof(TV));
+  unsigned char* base = smem_raw + w * per_warp;
+  TV* acc = reinterpret_cast<TV*>(base);
+  TV* bv = reinterpret_cast<TV*>(base + size_t(cap_cols) * sizeof(TV));
+  int32_t* scol = reinterpret_cast<int32_t*>(base + size_t(cap_cols + cap_buf) * sizeof(TV));
+  int32_t* bx = scol + cap_cols;
+  const int chunk = cap_buf / n_loc;  // incidences per bulk fetch
   for (int64_t ri = int64_t(blockIdx.x) * warps + w; ri < n_rows; ri += int64_t(gridDim.x) * warps) {
     const int64_t r = rows ? rows[ri] : ri;
-    const int64_t cb = row_ptr[r], ce = row_ptr[r + 1];
-    if (init)
-      for (int64_t x = cb + lane; x < ce; x += 32) values[x] = TV(-0.0);
+    const int64_t cb = row_ptr[r];
+    const int nr = int(row_ptr[r + 1] - cb);
+    for (int x = lane; x < nr; x += 32) {
+      scol[x] = col_idx[cb + x];
+      acc[x] = init ? TV(-0.0) : values[cb + x];
+    }
     __syncwarp();
     const int64_t ib = inc_ptr[r], ie = inc_ptr[r + 1];
-    for (int64_t t = ib; t < ie; ++t) {
-      const int64_t pk = inc[t];
-      const int64_t cell = pk / n_loc;
-      if (cell < cell_begin || cell >= cell_end) continue;
-      const int i = int(pk % n_loc);
-      const TL* lrow = locals + (cell * n_loc + i) * n_loc;
-      for (int j = lane; j < n_loc; j += 32) {
-        const int32_t col = cell_dofs[cell * n_loc + j];
-        const int64_t x = find_col(col_idx, cb, ce, col);
-        values[x] = values[x] + cast_value<TL, TV>(lrow[j]);
+    for (int64_t t0 = ib; t0 < ie; t0 += chunk) {
+      const int nt = int((ie - t0) < int64_t(chunk) ? (ie - t0) : int64_t(chunk));
+      const int nf = nt * n_loc;
+      for (int f = lane; f < nf; f += 32) {
+        const int t = f / n_loc, j = f - t * n_loc;
+        const int64_t pk = inc[t0 + t];
+        const int64_t cell = pk / n_loc;
+        int32_t x = -1;
+        TV v = TV(0);
+        if (cell >= cell_begin && cell < cell_end) {
+          const int i = int(pk - cell * n_loc);
+          const int32_t col = cell_dofs[cell * n_loc + j];
+          v = cast_value<TL, TV>(locals[(cell * n_loc + i) * n_loc + j]);
+          int lo = 0, hi = nr;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (scol[mid] < col) lo = mid + 1;
+            else hi = mid;
+          }
+          x = lo;
+        }
+        bx[f] = x;
+        bv[f] = v;
       }
       __syncwarp();
+      for (int t = 0; t < nt; ++t) {
+        for (int j = lane; j < n_loc; j += 32) {
+          const int f = t * n_loc + j;
+          const int32_t x = bx[f];
+          if (x >= 0) acc[x] = acc[x] + bv[f];
+        }
+        __syncwarp();
+      }
     }
+    for (int x = lane; x < nr; x += 32) values[cb + x] = acc[x];
+    __syncwarp();
   }
 }
 

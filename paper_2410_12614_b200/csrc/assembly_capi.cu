@@ -128,6 +128,32 @@ int64_t max_count(const int64_t* inc_ptr, int32_t n_dofs, Scratch& S) {
   return int64_t(read1(out, S.st));
 }
 
+struct DetLaunch {
+  unsigned grid;
+  int threads;
+  size_t smem;
+  cudaStream_t st;
+  int n_loc;
+  const int32_t* cell_dofs;
+  const int64_t* row_ptr;
+  const int32_t* col_idx;
+  const int64_t* inc_ptr;
+  const int64_t* inc;
+  const int32_t* rows;
+  int64_t n_rows, cell_begin, cell_end;
+  int init, cap_cols, cap_buf;
+};
+
+template <typename TL, typename TV>
+void launch_det(const DetLaunch& L, const char* locals, void* values) {
+  auto kern = asmb::assemble_det_kernel<TL, TV>;
+  ACUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem)));
+  kern<<<L.grid, L.threads, L.smem, L.st>>>(reinterpret_cast<const TL*>(locals), L.n_loc, L.cell_dofs,
+                                             L.row_ptr, L.col_idx, L.inc_ptr, L.inc, L.rows, L.n_rows,
+                                             L.cell_begin, L.cell_end, L.init, static_cast<TV*>(values),
+                                             L.cap_cols, L.cap_buf);
+}
+
 }  // namespace
 
 extern "C" {
@@ -282,16 +308,25 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, 
       if (!inc_ptr || !inc) throw AsmError{2, "deterministic assembly needs the incidence lists"};
       const int64_t nr = rows ? n_rows : n_dofs;
       if (nr == 0) return;
-      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, 148 * 64)));
+      // shared-memory plan: row columns + accumulators, and a bulk buffer of incident rows
+      Scratch S(st);
+      const int64_t max_nnz_row = max_count(row_ptr, n_dofs, S);
+      int cap_cols = 32;
+      while (cap_cols < max_nnz_row) cap_cols <<= 1;
+      const int cap_buf = std::max(n_loc, (1024 / n_loc) * n_loc);
+      const size_t vsz = fmt == 2 ? 4 : 8;
+      const size_t per_warp = size_t(cap_cols) * (4 + vsz) + size_t(cap_buf) * (4 + vsz);
+      const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp)));
+      const size_t smem = per_warp * warps;
+      if (smem > 200 * 1024) throw AsmError{2, "row too long for the shared-memory assembly plan"};
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nr + warps - 1) / warps, 148 * 64)));
       const int init = accumulate ? 0 : 1;
-      if (locals_fmt == 2 && fmt == 2)
-        asmb::assemble_det_kernel<float, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<float*>(values));
-      else if (locals_fmt == 2)
-        asmb::assemble_det_kernel<float, double><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<double*>(values));
-      else if (fmt == 2)
-        asmb::assemble_det_kernel<double, float><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<float*>(values));
-      else
-        asmb::assemble_det_kernel<double, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc, rows, nr, cell_begin, cell_end, init, static_cast<double*>(values));
+      const DetLaunch L{grid, warps * 32, smem, st, n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc,
+                        rows, nr, cell_begin, cell_end, init, cap_cols, cap_buf};
+      if (locals_fmt == 2 && fmt == 2) launch_det<float, float>(L, base, values);
+      else if (locals_fmt == 2) launch_det<float, double>(L, base, values);
+      else if (fmt == 2) launch_det<double, float>(L, base, values);
+      else launch_det<double, double>(L, base, values);
     }
     ACUDA(cudaGetLastError());
   });
