@@ -149,23 +149,30 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
 int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
                          int32_t n_dofs, int64_t* inc_ptr, int64_t* inc, void* stream);
 
+/* Scatter plan for a mesh (computed once, like the pattern):
+ *   pos_map (n_cells x n_loc x n_loc int32): CSR position of every local entry;
+ *   seg_ptr (nnz + 1 int64) and perm (n_cells x n_loc^2 uint32): local-entry indices sorted
+ *   stably by position -- each CSR entry's contributions in the reference's order
+ *   (cell asc, i asc, j asc; assembly.cpp:50-67). seg_ptr/perm may be NULL (atomic only). */
+int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
+                            int32_t n_dofs, const int64_t* row_ptr, const int32_t* col_idx,
+                            int32_t* pos_map, int64_t* seg_ptr, uint32_t* perm, void* stream);
+
 /* Replaces assemble_matrix (assembly.cpp:41-88): scatter-add of local matrices into
- * CSR values. mode 0 = atomic (red.global, order-free), 1 = deterministic (each entry is
- * the sequential ascending-cell sum at fmt, bitwise equal to the reference).
+ * CSR values. mode 0 = atomic (red.global at pos_map, order-free), 1 = deterministic
+ * (each entry summed sequentially in the reference's order at fmt: bitwise equal).
  *   locals: local matrices of cells [cell_begin, cell_end) (locals[0] is cell_begin's),
  *           n_loc x n_loc row-major each, fp32 (locals_fmt 2) or fp64 (3)
  *   values: CSR values, fp32 (fmt 2) or fp64 (fmt 3)
- *   inc_ptr/inc: incidence (mpfem_b200_incidence), required for mode 1
- *   rows/n_rows: mode 1 only -- the rows to assemble (NULL: all n_dofs rows)
- *   accumulate: 0 = the entries start empty (mode 1: first contribution taken exactly;
+ *   rows/n_rows: mode 1 only -- restrict to these rows (NULL: every entry)
+ *   accumulate: 0 = entries start empty (mode 1: first contribution taken exactly;
  *               mode 0: values zeroed), 1 = continue from the current contents (the
  *               prefix partial sums received from the rank owning lower cells). */
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
-                        int64_t cell_end, int n_loc, const int32_t* cell_dofs,
-                        int32_t n_dofs, const int64_t* row_ptr, const int32_t* col_idx,
-                        const int64_t* inc_ptr, const int64_t* inc, void* values, int fmt,
-                        int mode, int accumulate, const int32_t* rows, int64_t n_rows,
-                        void* stream);
+                        int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
+                        const int32_t* pos_map, const int64_t* seg_ptr, const uint32_t* perm,
+                        void* values, int fmt, int mode, int accumulate, const int32_t* rows,
+                        int64_t n_rows, void* stream);
 
 #ifdef __cplusplus
 }

@@ -138,8 +138,10 @@ def lib():
         "mpfem_b200_dofmap": (C.c_int, [C.c_int, vp, C.c_int64, C.c_int64, vp, i32p, i32p, vp]),
         "mpfem_b200_csr_pattern": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int32, vp, vp, i64p, vp]),
         "mpfem_b200_incidence": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp]),
+        "mpfem_b200_scatter_plan": (C.c_int, [vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp, vp,
+                                              vp, vp]),
         "mpfem_b200_assemble": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp,
-                                          C.c_int32, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
+                                          C.c_int32, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                           vp, C.c_int64, vp]),
     }
     for name, (res, args) in sig.items():

@@ -35,6 +35,9 @@ class CsrPattern:
     col_idx: "object"  # int32 (nnz)
     inc_ptr: "object"  # int64 (n_rows + 1): dof -> incident (cell, local) pairs
     inc: "object"      # int64 (n_cells * n_local), cell * n_local + local, ascending
+    pos_map: "object" = None  # int32 (n_cells * n_local^2): CSR position of each local entry
+    seg_ptr: "object" = None  # int64 (nnz + 1): contribution segments per CSR entry
+    perm: "object" = None     # int32 view of uint32 (n_cells * n_local^2): reference order
 
     @property
     def nnz(self) -> int:
@@ -66,8 +69,9 @@ def incidence(dm: DofMap, stream=None):
     return inc_ptr, inc
 
 
-def csr_pattern(dm: DofMap, stream=None) -> CsrPattern:
-    """The reference COO key set (assembly.cpp:67-86) as CSR, plus the incidence lists."""
+def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: bool = True) -> CsrPattern:
+    """The reference COO key set (assembly.cpp:67-86) as CSR, plus the incidence lists and
+    (plan=True) the scatter plan used by assemble_matrix."""
     import torch
     dev = dm.cell_dofs.device
     row_ptr = torch.empty(dm.n_dofs + 1, dtype=torch.int64, device=dev)
@@ -79,7 +83,17 @@ def csr_pattern(dm: DofMap, stream=None) -> CsrPattern:
     check(lib().mpfem_b200_csr_pattern(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
                                        _ptr(row_ptr), _ptr(col_idx), C.byref(nnz), sh))
     inc_ptr, inc = incidence(dm, stream)
-    return CsrPattern(dm.n_dofs, row_ptr, col_idx, inc_ptr, inc)
+    pat = CsrPattern(dm.n_dofs, row_ptr, col_idx, inc_ptr, inc)
+    if plan:
+        nk = dm.n_cells * dm.n_local * dm.n_local
+        pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
+        if deterministic_plan:
+            pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int64, device=dev)
+            pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
+        check(lib().mpfem_b200_scatter_plan(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
+                                            _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
+                                            _ptr(pat.seg_ptr), _ptr(pat.perm), sh))
+    return pat
 
 
 def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
@@ -103,9 +117,11 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
         values = torch.empty(pat.nnz, dtype=torch.float32 if fmt == FP32 else torch.float64,
                              device=local.device)
     n_rows = 0 if rows is None else int(rows.numel())
+    if pat.pos_map is None:
+        raise ConfigError("assemble_matrix needs a pattern built with plan=True")
     check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), dm.n_local,
-                                    _ptr(dm.cell_dofs), dm.n_dofs, _ptr(pat.row_ptr),
-                                    _ptr(pat.col_idx), _ptr(pat.inc_ptr), _ptr(pat.inc),
-                                    _ptr(values), int(fmt), int(mode), int(accumulate),
-                                    _ptr(rows), n_rows, _stream_handle(stream)))
+                                    _ptr(pat.row_ptr), dm.n_dofs, _ptr(pat.pos_map),
+                                    _ptr(pat.seg_ptr), _ptr(pat.perm), _ptr(values), int(fmt),
+                                    int(mode), int(accumulate), _ptr(rows), n_rows,
+                                    _stream_handle(stream)))
     return values

@@ -14,11 +14,11 @@
 // incidence lists), sorted and deduplicated per row by one warp in shared memory; the
 // result is the reference COO key set in (row, col) order.
 //
-// Scatter. Deterministic mode is row-centric: one warp per row walks the row's incident
-// (cell, local i) pairs in ascending cell order and adds local row i into the row's
-// accumulators (lane j handles column dof(c, j)), so every CSR entry is the sequential
-// ascending-cell sum of the reference, bit for bit. Atomic mode issues one red.global.add
-// per local entry at the binary-searched CSR position.
+// Scatter plan (precomputed once per mesh, like the pattern): pos_map gives the CSR
+// position of every local entry; perm lists the local entries sorted stably by that
+// position, so within an entry's segment they appear in the reference's order (cell asc,
+// i asc, j asc). Deterministic mode sums each segment sequentially at the value format --
+// the reference's sum bit for bit; atomic mode issues one red.global.add per local entry.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -216,114 +216,88 @@ __device__ __forceinline__ TV cast_value(TL x) {
   else return TV(x);
 }
 
-__device__ __forceinline__ int64_t find_col(const int32_t* __restrict__ cols, int64_t lo, int64_t hi,
-                                            int32_t col) {
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (cols[mid] < col) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// Deterministic: one warp per row (rows list or all rows). The row's columns and its
-// accumulators live in shared memory; the incident local rows are fetched in bulk
-// (all lanes, independent loads, positions binary-searched in shared memory) and then
-// added strictly in ascending incidence order, so each CSR entry is the reference's
-// sequential ascending-cell sum. init != 0 starts every entry at -0.0 (the first
-// contribution is then taken exactly, as the reference's cast); otherwise the sum
-// continues from the current values (multi-GPU prefix partial sums).
-template <typename TL, typename TV>
-__global__ void assemble_det_kernel(const TL* __restrict__ locals, int n_loc,
-                                    const int32_t* __restrict__ cell_dofs,
-                                    const int64_t* __restrict__ row_ptr,
-                                    const int32_t* __restrict__ col_idx,
-                                    const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
-                                    const int32_t* __restrict__ rows, int64_t n_rows,
-                                    int64_t cell_begin, int64_t cell_end, int init,
-                                    TV* __restrict__ values, int cap_cols, int cap_buf) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// Scatter plan, part 1: CSR position of every local entry (c, i, j), found once by binary
+// search in row dof(c, i). One warp per local row (c, i), lanes over j.
+__global__ void pos_map_kernel(const int32_t* __restrict__ cell_dofs, int64_t n_cells, int n_loc,
+                               const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                               int32_t* __restrict__ pos_map) {
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t per_warp = size_t(cap_cols) * (sizeof(int32_t) + sizeof(TV)) +
-                          size_t(cap_buf) * (sizeof(int32_t) + sizeof(TV));
-  unsigned char* base = smem_raw + w * per_warp;
-  TV* acc = reinterpret_cast<TV*>(base);
-  TV* bv = reinterpret_cast<TV*>(base + size_t(cap_cols) * sizeof(TV));
-  int32_t* scol = reinterpret_cast<int32_t*>(base + size_t(cap_cols + cap_buf) * sizeof(TV));
-  int32_t* bx = scol + cap_cols;
-  const int chunk = cap_buf / n_loc;  // incidences per bulk fetch
-  for (int64_t ri = int64_t(blockIdx.x) * warps + w; ri < n_rows; ri += int64_t(gridDim.x) * warps) {
-    const int64_t r = rows ? rows[ri] : ri;
-    const int64_t cb = row_ptr[r];
-    const int nr = int(row_ptr[r + 1] - cb);
-    for (int x = lane; x < nr; x += 32) {
-      scol[x] = col_idx[cb + x];
-      acc[x] = init ? TV(-0.0) : values[cb + x];
-    }
-    __syncwarp();
-    const int64_t ib = inc_ptr[r], ie = inc_ptr[r + 1];
-    for (int64_t t0 = ib; t0 < ie; t0 += chunk) {
-      const int nt = int((ie - t0) < int64_t(chunk) ? (ie - t0) : int64_t(chunk));
-      const int nf = nt * n_loc;
-      for (int f = lane; f < nf; f += 32) {
-        const int t = f / n_loc, j = f - t * n_loc;
-        const int64_t pk = inc[t0 + t];
-        const int64_t cell = pk / n_loc;
-        int32_t x = -1;
-        TV v = TV(0);
-        if (cell >= cell_begin && cell < cell_end) {
-          const int i = int(pk - cell * n_loc);
-          const int32_t col = cell_dofs[cell * n_loc + j];
-          v = cast_value<TL, TV>(locals[(cell * n_loc + i) * n_loc + j]);
-          int lo = 0, hi = nr;
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (scol[mid] < col) lo = mid + 1;
-            else hi = mid;
-          }
-          x = lo;
-        }
-        bx[f] = x;
-        bv[f] = v;
-      }
-      __syncwarp();
-      for (int t = 0; t < nt; ++t) {
-        for (int j = lane; j < n_loc; j += 32) {
-          const int f = t * n_loc + j;
-          const int32_t x = bx[f];
-          if (x >= 0) acc[x] = acc[x] + bv[f];
-        }
-        __syncwarp();
-      }
-    }
-    for (int x = lane; x < nr; x += 32) values[cb + x] = acc[x];
-    __syncwarp();
-  }
-}
-
-// Atomic: one warp per (cell, local row i); lanes over j.
-template <typename TL, typename TV>
-__global__ void assemble_atomic_kernel(const TL* __restrict__ locals, int n_loc,
-                                       const int32_t* __restrict__ cell_dofs,
-                                       const int64_t* __restrict__ row_ptr,
-                                       const int32_t* __restrict__ col_idx, int64_t cell_begin,
-                                       int64_t cell_end, TV* __restrict__ values) {
-  const int warps = blockDim.x >> 5;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t total = (cell_end - cell_begin) * n_loc;
+  const int64_t total = n_cells * n_loc;
   for (int64_t t = int64_t(blockIdx.x) * warps + w; t < total; t += int64_t(gridDim.x) * warps) {
-    const int64_t cell = cell_begin + t / n_loc;
-    const int i = int(t % n_loc);
-    const int32_t r = cell_dofs[cell * n_loc + i];
-    const int64_t cb = row_ptr[r], ce = row_ptr[r + 1];
-    const TL* lrow = locals + (cell * n_loc + i) * n_loc;
+    const int64_t cell = t / n_loc;
+    const int32_t r = cell_dofs[t];
+    int64_t lo0 = row_ptr[r], hi0 = row_ptr[r + 1];
     for (int j = lane; j < n_loc; j += 32) {
       const int32_t col = cell_dofs[cell * n_loc + j];
-      const int64_t x = find_col(col_idx, cb, ce, col);
-      atomicAdd(&values[x], cast_value<TL, TV>(lrow[j]));
+      int64_t lo = lo0, hi = hi0;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (col_idx[mid] < col) lo = mid + 1;
+        else hi = mid;
+      }
+      pos_map[t * n_loc + j] = int32_t(lo);
     }
   }
+}
+
+// Deterministic scatter: thread per CSR entry (all rows) walks its contributions in the
+// reference order (perm is sorted by (entry, local index), local index ascending = cell
+// asc, i asc, j asc) and sums them sequentially at the value format. Contributions of
+// cells outside [cell_begin, cell_end) are skipped (multi-GPU slabs). init: first
+// contribution taken exactly (start from -0.0); else continue from values[e].
+template <typename TL, typename TV>
+__device__ __forceinline__ void entry_sum(const TL* __restrict__ locals, int64_t per_cell,
+                                          const int64_t* __restrict__ seg_ptr,
+                                          const uint32_t* __restrict__ perm, int64_t e,
+                                          int64_t cell_begin, int64_t cell_end, int init,
+                                          TV* __restrict__ values) {
+  TV acc = init ? TV(-0.0) : values[e];
+  const int64_t b = seg_ptr[e], en = seg_ptr[e + 1];
+  for (int64_t t = b; t < en; ++t) {
+    const int64_t k = perm[t];
+    const int64_t cell = k / per_cell;
+    if (cell < cell_begin || cell >= cell_end) continue;
+    acc = acc + cast_value<TL, TV>(locals[k]);
+  }
+  values[e] = acc;
+}
+
+template <typename TL, typename TV>
+__global__ void assemble_seg_kernel(const TL* __restrict__ locals, int64_t per_cell,
+                                    const int64_t* __restrict__ seg_ptr, const uint32_t* __restrict__ perm,
+                                    int64_t nnz, int64_t cell_begin, int64_t cell_end, int init,
+                                    TV* __restrict__ values) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += int64_t(gridDim.x) * blockDim.x)
+    entry_sum(locals, per_cell, seg_ptr, perm, e, cell_begin, cell_end, init, values);
+}
+
+// Same for a list of rows: one warp per row, lanes over the row's entries.
+template <typename TL, typename TV>
+__global__ void assemble_seg_rows_kernel(const TL* __restrict__ locals, int64_t per_cell,
+                                         const int64_t* __restrict__ row_ptr,
+                                         const int64_t* __restrict__ seg_ptr,
+                                         const uint32_t* __restrict__ perm,
+                                         const int32_t* __restrict__ rows, int64_t n_rows,
+                                         int64_t cell_begin, int64_t cell_end, int init,
+                                         TV* __restrict__ values) {
+  const int warps = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t ri = int64_t(blockIdx.x) * warps + w; ri < n_rows; ri += int64_t(gridDim.x) * warps) {
+    const int64_t r = rows[ri];
+    for (int64_t e = row_ptr[r] + lane; e < row_ptr[r + 1]; e += 32)
+      entry_sum(locals, per_cell, seg_ptr, perm, e, cell_begin, cell_end, init, values);
+  }
+}
+
+// Atomic scatter: thread per local entry, red.global.add at its precomputed position.
+template <typename TL, typename TV>
+__global__ void assemble_atomic_kernel(const TL* __restrict__ locals, const int32_t* __restrict__ pos_map,
+                                       int64_t k_begin, int64_t k_end, TV* __restrict__ values) {
+  for (int64_t k = k_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < k_end;
+       k += int64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&values[pos_map[k]], cast_value<TL, TV>(locals[k]));
 }
 
 }  // namespace asmb

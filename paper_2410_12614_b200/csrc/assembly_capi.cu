@@ -44,7 +44,18 @@ int aguard(F&& f) {
 struct Scratch {
   cudaStream_t st;
   std::vector<void*> ptrs;
-  explicit Scratch(cudaStream_t s) : st(s) {}
+  explicit Scratch(cudaStream_t s) : st(s) {
+    static bool pool_set = false;  // keep freed blocks cached: setup calls reuse GBs of scratch
+    if (!pool_set) {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set = true;
+    }
+  }
   template <typename T>
   T* get(size_t n) {
     void* p = nullptr;
@@ -126,32 +137,6 @@ int64_t max_count(const int64_t* inc_ptr, int32_t n_dofs, Scratch& S) {
   ACUDA(cudaMemsetAsync(out, 0, 8, S.st));
   max_diff_kernel<<<grid_for(n_dofs), 256, 0, S.st>>>(inc_ptr, n_dofs, out);
   return int64_t(read1(out, S.st));
-}
-
-struct DetLaunch {
-  unsigned grid;
-  int threads;
-  size_t smem;
-  cudaStream_t st;
-  int n_loc;
-  const int32_t* cell_dofs;
-  const int64_t* row_ptr;
-  const int32_t* col_idx;
-  const int64_t* inc_ptr;
-  const int64_t* inc;
-  const int32_t* rows;
-  int64_t n_rows, cell_begin, cell_end;
-  int init, cap_cols, cap_buf;
-};
-
-template <typename TL, typename TV>
-void launch_det(const DetLaunch& L, const char* locals, void* values) {
-  auto kern = asmb::assemble_det_kernel<TL, TV>;
-  ACUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem)));
-  kern<<<L.grid, L.threads, L.smem, L.st>>>(reinterpret_cast<const TL*>(locals), L.n_loc, L.cell_dofs,
-                                             L.row_ptr, L.col_idx, L.inc_ptr, L.inc, L.rows, L.n_rows,
-                                             L.cell_begin, L.cell_end, L.init, static_cast<TV*>(values),
-                                             L.cap_cols, L.cap_buf);
 }
 
 }  // namespace
@@ -275,58 +260,96 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
   });
 }
 
+int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                            const int64_t* row_ptr, const int32_t* col_idx, int32_t* pos_map,
+                            int64_t* seg_ptr, uint32_t* perm, void* stream) {
+  return aguard([&] {
+    if (n_loc < 1 || n_dofs < 1 || !pos_map) throw AsmError{2, "scatter plan needs a dof map and pos_map"};
+    const int64_t nk = n_cells * n_loc * n_loc;
+    if (nk > int64_t(UINT32_MAX)) throw AsmError{2, "n_cells * n_loc^2 must fit 32 bits"};
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch S(st);
+    const int64_t rows_total = n_cells * n_loc;
+    asmb::pos_map_kernel<<<unsigned(std::min<int64_t>((rows_total + 7) / 8, 148 * 64)), 256, 0, st>>>(
+        cell_dofs, n_cells, n_loc, row_ptr, col_idx, pos_map);
+    ACUDA(cudaGetLastError());
+    if (!seg_ptr && !perm) return;
+    if (!seg_ptr || !perm) throw AsmError{2, "deterministic plan needs both seg_ptr and perm"};
+    const int64_t nnz = read1(row_ptr + n_dofs, st);
+    // segment offsets: every entry has >= 1 contribution; counts by position, then scan
+    int64_t* counts = S.get<int64_t>(size_t(nnz) + 1);
+    ACUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t(nnz) + 1), st));
+    asmb::dof_count_kernel<<<grid_for(nk), 256, 0, st>>>(pos_map, nk, counts);
+    size_t tb = 0;
+    ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, seg_ptr, nnz + 1, st));
+    void* tmp = S.get<char>(tb);
+    ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, seg_ptr, nnz + 1, st));
+    // perm = local indices sorted stably by CSR position
+    uint32_t* idx = S.get<uint32_t>(nk);
+    int32_t* keys_out = S.get<int32_t>(nk);
+    iota_kernel<<<grid_for(nk), 256, 0, st>>>(idx, nk);
+    size_t tb2 = 0;
+    const int bits = bits_for(nnz);
+    ACUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, pos_map, keys_out, idx, perm, nk, 0, bits, st));
+    void* tmp2 = S.get<char>(tb2);
+    ACUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, pos_map, keys_out, idx, perm, nk, 0, bits, st));
+    ACUDA(cudaGetLastError());
+  });
+}
+
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, int64_t cell_end,
-                        int n_loc, const int32_t* cell_dofs, int32_t n_dofs, const int64_t* row_ptr,
-                        const int32_t* col_idx, const int64_t* inc_ptr, const int64_t* inc,
-                        void* values, int fmt, int mode, int accumulate, const int32_t* rows,
-                        int64_t n_rows, void* stream) {
+                        int n_loc, const int64_t* row_ptr, int32_t n_dofs, const int32_t* pos_map,
+                        const int64_t* seg_ptr, const uint32_t* perm, void* values, int fmt,
+                        int mode, int accumulate, const int32_t* rows, int64_t n_rows,
+                        void* stream) {
   return aguard([&] {
     if (locals_fmt != 2 && locals_fmt != 3) throw AsmError{2, "local matrices must be fp32 or fp64"};
     if (fmt != 2 && fmt != 3) throw AsmError{2, "CSR values must be fp32 or fp64"};
     if (mode != 0 && mode != 1) throw AsmError{2, "assembly mode must be 0 (atomic) or 1 (deterministic)"};
     if (cell_end < cell_begin || n_loc < 1) throw AsmError{2, "bad cell range"};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // locals[0] is cell_begin's matrix: rebase so the kernels can index by global cell id
+    const int64_t per_cell = int64_t(n_loc) * n_loc;
+    // locals[0] is cell_begin's matrix: rebase so kernels index by global local-entry id
     const size_t esz = locals_fmt == 2 ? 4 : 8;
-    const char* base = static_cast<const char*>(locals) - size_t(cell_begin) * n_loc * n_loc * esz;
+    const char* base = static_cast<const char*>(locals) - size_t(cell_begin) * size_t(per_cell) * esz;
     if (mode == 0) {
+      if (!pos_map) throw AsmError{2, "atomic assembly needs the scatter plan's pos_map"};
       if (!accumulate) {
         const int64_t nnz = read1(row_ptr + n_dofs, st);
         ACUDA(cudaMemsetAsync(values, 0, size_t(nnz) * (fmt == 2 ? 4 : 8), st));
       }
-      const int64_t work = (cell_end - cell_begin) * n_loc;
-      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((work + 7) / 8, 148 * 64)));
+      const int64_t kb = cell_begin * per_cell, ke = cell_end * per_cell;
+      const unsigned grid = grid_for(ke - kb);
       if (locals_fmt == 2 && fmt == 2)
-        asmb::assemble_atomic_kernel<float, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<float*>(values));
+        asmb::assemble_atomic_kernel<float, float><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), pos_map, kb, ke, static_cast<float*>(values));
       else if (locals_fmt == 2)
-        asmb::assemble_atomic_kernel<float, double><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<double*>(values));
+        asmb::assemble_atomic_kernel<float, double><<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(base), pos_map, kb, ke, static_cast<double*>(values));
       else if (fmt == 2)
-        asmb::assemble_atomic_kernel<double, float><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<float*>(values));
+        asmb::assemble_atomic_kernel<double, float><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), pos_map, kb, ke, static_cast<float*>(values));
       else
-        asmb::assemble_atomic_kernel<double, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), n_loc, cell_dofs, row_ptr, col_idx, cell_begin, cell_end, static_cast<double*>(values));
+        asmb::assemble_atomic_kernel<double, double><<<grid, 256, 0, st>>>(reinterpret_cast<const double*>(base), pos_map, kb, ke, static_cast<double*>(values));
     } else {
-      if (!inc_ptr || !inc) throw AsmError{2, "deterministic assembly needs the incidence lists"};
-      const int64_t nr = rows ? n_rows : n_dofs;
-      if (nr == 0) return;
-      // shared-memory plan: row columns + accumulators, and a bulk buffer of incident rows
-      Scratch S(st);
-      const int64_t max_nnz_row = max_count(row_ptr, n_dofs, S);
-      int cap_cols = 32;
-      while (cap_cols < max_nnz_row) cap_cols <<= 1;
-      const int cap_buf = std::max(n_loc, (1024 / n_loc) * n_loc);
-      const size_t vsz = fmt == 2 ? 4 : 8;
-      const size_t per_warp = size_t(cap_cols) * (4 + vsz) + size_t(cap_buf) * (4 + vsz);
-      const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / per_warp)));
-      const size_t smem = per_warp * warps;
-      if (smem > 200 * 1024) throw AsmError{2, "row too long for the shared-memory assembly plan"};
-      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((nr + warps - 1) / warps, 148 * 64)));
+      if (!seg_ptr || !perm) throw AsmError{2, "deterministic assembly needs the scatter plan (seg_ptr, perm)"};
       const int init = accumulate ? 0 : 1;
-      const DetLaunch L{grid, warps * 32, smem, st, n_loc, cell_dofs, row_ptr, col_idx, inc_ptr, inc,
-                        rows, nr, cell_begin, cell_end, init, cap_cols, cap_buf};
-      if (locals_fmt == 2 && fmt == 2) launch_det<float, float>(L, base, values);
-      else if (locals_fmt == 2) launch_det<float, double>(L, base, values);
-      else if (fmt == 2) launch_det<double, float>(L, base, values);
-      else launch_det<double, double>(L, base, values);
+      if (rows) {
+        if (n_rows == 0) return;
+        const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((n_rows + 7) / 8, 148 * 64)));
+#define MPFEM_SEG_ROWS(TL, TV) asmb::assemble_seg_rows_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base), per_cell, row_ptr, seg_ptr, perm, rows, n_rows, cell_begin, cell_end, init, static_cast<TV*>(values))
+        if (locals_fmt == 2 && fmt == 2) MPFEM_SEG_ROWS(float, float);
+        else if (locals_fmt == 2) MPFEM_SEG_ROWS(float, double);
+        else if (fmt == 2) MPFEM_SEG_ROWS(double, float);
+        else MPFEM_SEG_ROWS(double, double);
+#undef MPFEM_SEG_ROWS
+      } else {
+        const int64_t nnz = read1(row_ptr + n_dofs, st);
+        const unsigned grid = grid_for(nnz);
+#define MPFEM_SEG(TL, TV) asmb::assemble_seg_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, static_cast<TV*>(values))
+        if (locals_fmt == 2 && fmt == 2) MPFEM_SEG(float, float);
+        else if (locals_fmt == 2) MPFEM_SEG(float, double);
+        else if (fmt == 2) MPFEM_SEG(double, float);
+        else MPFEM_SEG(double, double);
+#undef MPFEM_SEG
+      }
     }
     ACUDA(cudaGetLastError());
   });
