@@ -130,7 +130,7 @@ struct mpfem_b200_setup_s {
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
   Rule rule;
   DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T;
-  DevBuf d_W, d_flags, d_error;
+  DevBuf d_W, d_flags, d_error, d_geo;
   // host-API staging
   DevBuf h_verts, h_cells, h_coef, h_out;
   int last_launches = 0;
@@ -201,28 +201,34 @@ void choose_path(mpfem_b200_setup_s& S) {
 }
 
 template <typename T, int US>
-void launch_geom_ug(int ug, unsigned grid, cudaStream_t st, const GeomWParams& P) {
+void launch_geom_ug(int ug, unsigned grid_cells, unsigned grid_w, cudaStream_t st, const GeomWParams& P,
+                    CellGeo* geo) {
   switch (ug) {
-    case 0: geom_w_kernel<T, 0, US><<<grid, kGeomThreads, 0, st>>>(P); break;
-    case 1: geom_w_kernel<T, 1, US><<<grid, kGeomThreads, 0, st>>>(P); break;
-    case 2: geom_w_kernel<T, 2, US><<<grid, kGeomThreads, 0, st>>>(P); break;
-    default: geom_w_kernel<T, 3, US><<<grid, kGeomThreads, 0, st>>>(P); break;
+#define MPFEM_K1(UGV)                                                                       \
+  cell_geometry_kernel<UGV><<<grid_cells, 256, 0, st>>>(P, geo);                            \
+  scaled_weights_kernel<T, UGV, US><<<grid_w, 256, 0, st>>>(P, geo);                        \
+  break;
+    case 0: MPFEM_K1(0)
+    case 1: MPFEM_K1(1)
+    case 2: MPFEM_K1(2)
+    default: MPFEM_K1(3)
+#undef MPFEM_K1
   }
 }
 
 // W element type follows u_s except on the fp64 path, where any u_s is carried in fp64.
-void launch_geom_typed(int w_type, int ug, int us, unsigned grid, cudaStream_t st,
-                       const GeomWParams& P) {
+void launch_geom_typed(int w_type, int ug, int us, unsigned gc, unsigned gw, cudaStream_t st,
+                       const GeomWParams& P, CellGeo* geo) {
   switch (w_type) {
-    case 0: launch_geom_ug<__half, 1>(ug, grid, st, P); break;
-    case 1: launch_geom_ug<__nv_bfloat16, 0>(ug, grid, st, P); break;
-    case 2: launch_geom_ug<float, 2>(ug, grid, st, P); break;
+    case 0: launch_geom_ug<__half, 1>(ug, gc, gw, st, P, geo); break;
+    case 1: launch_geom_ug<__nv_bfloat16, 0>(ug, gc, gw, st, P, geo); break;
+    case 2: launch_geom_ug<float, 2>(ug, gc, gw, st, P, geo); break;
     default:
       switch (us) {
-        case 0: launch_geom_ug<double, 0>(ug, grid, st, P); break;
-        case 1: launch_geom_ug<double, 1>(ug, grid, st, P); break;
-        case 2: launch_geom_ug<double, 2>(ug, grid, st, P); break;
-        default: launch_geom_ug<double, 3>(ug, grid, st, P); break;
+        case 0: launch_geom_ug<double, 0>(ug, gc, gw, st, P, geo); break;
+        case 1: launch_geom_ug<double, 1>(ug, gc, gw, st, P, geo); break;
+        case 2: launch_geom_ug<double, 2>(ug, gc, gw, st, P, geo); break;
+        default: launch_geom_ug<double, 3>(ug, gc, gw, st, P, geo); break;
       }
   }
 }
@@ -251,8 +257,10 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.W = W;
   P.flags = static_cast<uint32_t*>(S.d_flags.p);
   P.error = static_cast<int*>(S.d_error.p);
-  const unsigned grid = unsigned((n + kGeomCells - 1) / kGeomCells);
-  launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
+  S.d_geo.ensure(sizeof(CellGeo) * size_t(n));
+  const unsigned gc = unsigned((n + 255) / 256);
+  const unsigned gw = unsigned(std::min<int64_t>((n * S.n_q + 255) / 256, int64_t(device_sm_count()) * 64));
+  launch_geom_typed(w_type, S.ug, S.us, gc, gw, st, P, static_cast<CellGeo*>(S.d_geo.p));
   CUDA_OK(cudaGetLastError());
 }
 
@@ -358,7 +366,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     const double* coefc = coef ? coef + c0 * coef_stride : nullptr;
     S.mark(st);
     launch_geom(S, vc, cc, m, coef_kind, coefc, coef_stride, Wc, S.k_pad, S.w_type, st);
-    ++S.last_launches;
+    S.last_launches += 2;
     S.mark(st);
     cudaStream_t gs = st;
     if (n_chunks > 1) {

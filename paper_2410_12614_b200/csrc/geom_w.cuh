@@ -100,124 +100,125 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
   static_cast<double*>(W)[idx] = v;
 }
 
-// Two phases per CTA of kGeomCells cells:
-//  (1) one thread per cell: geometry at u_g into shared memory (G, origin, edges);
-//  (2) one warp per cell, lanes over quadrature points: coefficient + W row.
-// UG / US are compile-time so the emulated rounding folds to the plain op for fp64 and a
+// K1 runs as two launches:
+//  (a) cell_geometry_kernel: one thread per cell, the reference's LU/inverse/tensor
+//      sequence at u_g (geometry.cpp:12-118) -> CellGeo (G, origin, edges) in a scratch array;
+//  (b) scaled_weights_kernel: one thread per (cell, q): coefficient z_q and the cell's
+//      W entries at q for every (s<=t) block.
+// UG / US are compile-time, so the emulated rounding folds to the plain op for fp64 and a
 // single conversion for fp32.
-constexpr int kGeomCells = 64;     // cells per CTA
-constexpr int kGeomThreads = 256;  // 8 warps share the (cell, q) expansion
+struct CellGeo {
+  double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson) or |det| (mass)
+  double v0[3];
+  double e[9];  // e[s*3 + i] = v_{s+1}[i] - v0[i]
+};
 
-template <typename T, int UG, int US>
-__global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) {
-  __shared__ double sG[kGeomCells][6];
-  __shared__ double sV0[kGeomCells][3];
-  __shared__ double sE[kGeomCells][9];
-  __shared__ int sBad[kGeomCells];
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int64_t cell0 = int64_t(blockIdx.x) * kGeomCells;
+template <int UG>
+__global__ void __launch_bounds__(256) cell_geometry_kernel(GeomWParams P, CellGeo* __restrict__ geo) {
+  const int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   uint32_t fl = 0;
-  if (tid < kGeomCells) {
-    const int64_t cell = cell0 + tid;
-    sBad[tid] = 1;
-    if (cell < P.n_cells) {
-      double v[4][3];
-      if (P.cells) {
-        #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int64_t vid = P.cells[cell * 4 + k];
-          #pragma unroll
-          for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
-        }
-      } else {
-        #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          #pragma unroll
-          for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
-      }
-      TetGeometry g;
-      const bool ok = tet_geometry<UG>(v, P.poisson != 0, g, fl);
-      sBad[tid] = ok ? 0 : 2;
-      if (!ok) atomicExch(P.error, 3);
+  if (cell < P.n_cells) {
+    double v[4][3];
+    if (P.cells) {
       #pragma unroll
-      for (int b = 0; b < 6; ++b) sG[tid][b] = g.g[b];
-      #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        sV0[tid][a] = v[0][a];
+      for (int k = 0; k < 4; ++k) {
+        const int64_t vid = P.cells[cell * 4 + k];
         #pragma unroll
-        for (int s = 0; s < 3; ++s) sE[tid][s * 3 + a] = __dsub_rn(v[s + 1][a], v[0][a]);
+        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
       }
+    } else {
+      #pragma unroll
+      for (int k = 0; k < 4; ++k)
+        #pragma unroll
+        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
+    }
+    TetGeometry g;
+    if (!tet_geometry<UG>(v, P.poisson != 0, g, fl)) {
+      atomicExch(P.error, 3);
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+    }
+    CellGeo& o = geo[cell];
+    #pragma unroll
+    for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
+    #pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o.v0[a] = v[0][a];
+      #pragma unroll
+      for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = __dsub_rn(v[s2 + 1][a], v[0][a]);
     }
   }
-  __syncthreads();
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if ((threadIdx.x & 31) == 0 && fl) atomicOr(P.flags, fl);
+}
+
+template <typename T, int UG, int US>
+__global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
+                                                             const CellGeo* __restrict__ geo) {
+  const int64_t total = P.n_cells * P.n_q;
+  const int nq = P.n_q;
   const int nb = P.poisson ? 6 : 1;
+  const int64_t pad = P.k_pad - int64_t(nb) * nq;
+  uint32_t fl = 0;
   StoreFlags sf;
-  for (int j = warp; j < kGeomCells; j += kGeomThreads / 32) {
-    const int64_t cell = cell0 + j;
-    if (cell >= P.n_cells || sBad[j]) continue;
-    const int64_t row = cell * P.k_pad;
-    const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
-    double G[6];
-    #pragma unroll
-    for (int b = 0; b < 6; ++b) G[b] = sG[j][b];
-    const int nq = P.n_q;
-    for (int q = lane; q < P.n_q; q += 32) {
-      const double* xi = P.rule_x + 3 * q;
-      double zq = 1.0;
-      bool have_z = true;
-      switch (P.coef_kind) {
-        case 1: zq = droundT<UG>(coef_sincosexp_e(sV0[j], sE[j], xi), fl); break;
-        case 2: zq = droundT<UG>(coef_exp10_affine(coef, xi), fl); break;
-        case 3: {
-          double acc = 0.0;
-          for (int k = 0; k < P.n_phi; ++k)
-            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * P.n_q + q], P.up, fl),
-                       P.up, fl);
-          zq = droundT<UG>(acc, fl);
-          break;
-        }
-        default: have_z = false;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = idx / nq;
+    const int q = int(idx - cell * nq);
+    const CellGeo& cg = geo[cell];
+    const double* xi = P.rule_x + 3 * q;
+    double zq = 1.0;
+    bool have_z = true;
+    switch (P.coef_kind) {
+      case 1: zq = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl); break;
+      case 2: zq = droundT<UG>(coef_exp10_affine(P.coef + cell * P.coef_stride, xi), fl); break;
+      case 3: {
+        const double* z = P.coef + cell * P.coef_stride;
+        double acc = 0.0;
+        for (int k = 0; k < P.n_phi; ++k)
+          acc = dadd(acc, dmul(dround(z[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
+        zq = droundT<UG>(acc, fl);
+        break;
       }
-      const double omega = P.rule_w[q];  // already rounded to u_g on the host
-      T* wrow = static_cast<T*>(P.W) + row + q;
-      // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192).
-      if constexpr (UG == kFP32) {
-        // fp32 operands: the hardware fp32 product is the correctly rounded binary64 one
-        const float om = float(omega), zf = float(zq);
-        #pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            float val = __fmul_rn(om, float(G[b]));
-            if (have_z) val = __fmul_rn(val, zf);
-            wrow[b * nq] = to_storage<T, US>(val, sf);
-          }
+      default: have_z = false;
+    }
+    const double omega = P.rule_w[q];  // already rounded to u_g on the host
+    T* wrow = static_cast<T*>(P.W) + cell * P.k_pad;
+    // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
+    if constexpr (UG == kFP32) {
+      const float om = float(omega), zf = float(zq);  // fp32 values: the fp32 product is
+      #pragma unroll                                   // the correctly rounded exact one
+      for (int b = 0; b < 6; ++b) {
+        if (b < nb) {
+          float val = __fmul_rn(om, float(cg.g[b]));
+          if (have_z) val = __fmul_rn(val, zf);
+          wrow[b * nq + q] = to_storage<T, US>(val, sf);
         }
-      } else if constexpr (UG == kFP64) {
-        #pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            double val = __dmul_rn(omega, G[b]);
-            if (have_z) val = __dmul_rn(val, zq);
-            wrow[b * nq] = to_storage<T, US>(val, sf);
-          }
+      }
+    } else if constexpr (UG == kFP64) {
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        if (b < nb) {
+          double val = __dmul_rn(omega, cg.g[b]);
+          if (have_z) val = __dmul_rn(val, zq);
+          wrow[b * nq + q] = to_storage<T, US>(val, sf);
         }
-      } else {
-        #pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            double val = droundT<UG>(__dmul_rn(omega, G[b]), fl);
-            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
-            wrow[b * nq] = to_storage<T, US>(val, sf);
-          }
+      }
+    } else {
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        if (b < nb) {
+          double val = droundT<UG>(__dmul_rn(omega, cg.g[b]), fl);
+          if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
+          wrow[b * nq + q] = to_storage<T, US>(val, sf);
         }
       }
     }
-    for (int64_t k = int64_t(nb) * P.n_q + lane; k < P.k_pad; k += 32) store_w<T>(P.W, row + k, 0.0);
+    for (int64_t z = q; z < pad; z += nq) wrow[int64_t(nb) * nq + z] = T(0.0f);
   }
   fl |= store_flags_bits(sf);
   fl = __reduce_or_sync(0xffffffffu, fl);
-  if (lane == 0 && fl) atomicOr(P.flags, fl);
+  if ((threadIdx.x & 31) == 0 && fl) atomicOr(P.flags, fl);
 }
 
 // Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
