@@ -253,6 +253,9 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.us = S.us;
   P.poisson = S.form;
   P.k_pad = k_pad;
+  P.div_nq = FastDiv::make(uint32_t(S.n_q));
+  if (n * int64_t(S.n_q) >= (int64_t(1) << 31))
+    throw Error(MPFEM_B200_CONFIG_ERROR, "n_cells * n_q must be < 2^31 per call (split the batch)");
   P.w_type = w_type;
   P.W = W;
   P.flags = static_cast<uint32_t*>(S.d_flags.p);

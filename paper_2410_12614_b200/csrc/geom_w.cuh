@@ -18,6 +18,32 @@
 
 namespace mpfem_b200 {
 
+// x / d for 32-bit x by multiply-high with a precomputed magic (Granlund-Montgomery):
+// m = ceil(2^(32+s) / d), s = ceil(log2 d); exact for all x < 2^31.
+struct FastDiv {
+  uint32_t d = 1, m = 0, s = 0;
+  __host__ __device__ uint32_t div(uint32_t x) const {
+    return s == 0 && m == 0 ? x : (__umulhi_compat(x, m) + ((x - __umulhi_compat(x, m)) >> 1)) >> (s - 1);
+  }
+  __host__ __device__ static uint32_t __umulhi_compat(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    return __umulhi(a, b);
+#else
+    return uint32_t((uint64_t(a) * uint64_t(b)) >> 32);
+#endif
+  }
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    if (d == 1) return f;
+    uint32_t s = 0;
+    while ((uint64_t(1) << s) < d) ++s;
+    f.s = s;
+    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1);
+    return f;
+  }
+};
+
 struct GeomWParams {
   const double* verts;     // private: n_cells x 12 ; mesh: vertex table n_verts x 3
   const int32_t* cells;    // NULL or n_cells x 4
@@ -31,6 +57,7 @@ struct GeomWParams {
   int n_phi, n_q, up, ug, us;
   int poisson;
   int64_t k_pad;
+  FastDiv div_nq;          // idx / n_q for the (cell, q) expansion
   int w_type;              // 0 fp16 bits, 1 bf16 bits, 2 fp32, 3 fp64
   void* W;
   uint32_t* flags;
@@ -163,8 +190,9 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
   StoreFlags sf;
   for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t cell = idx / nq;
-    const int q = int(idx - cell * nq);
+    const uint32_t cell32 = P.div_nq.div(uint32_t(idx));
+    const int64_t cell = cell32;
+    const int q = int(uint32_t(idx) - cell32 * uint32_t(nq));
     const CellGeo& cg = geo[cell];
     const double* xi = P.rule_x + 3 * q;
     double zq = 1.0;
