@@ -298,21 +298,24 @@ __device__ __forceinline__ double coef_sincosexp(const double v[4][3], const dou
 // configs' coordinate range: sinpi/cospi <= 1.6 ulp, exp <= 1 ulp (the glibc/CUDA libm
 // functions are within 1-2 ulp of the same values; analytic-coefficient parity with the
 // oracle is tolerance-based for that reason).
+// Coefficients live in constant memory so DFMA reads them as constant-bank operands
+// (fp64 immediates would otherwise be materialised with two UMOVs each).
+__constant__ double kSinPiC[13] = {3.141592653589793, -5.16771278004997, 2.5501640398773455,
+                                   -0.5992645293207921, 0.08214588661112823, -0.0073704309457143504,
+                                   0.00046630280576761255, -2.1915353447830217e-05, 7.952054001475513e-07,
+                                   -2.2948428997269873e-08, 5.392664662608129e-10,
+                                   -1.0518471716932065e-11, 1.7302192458361107e-13};
+__constant__ double kExpC[15] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,
+                                 0.008333333333333333, 0.001388888888888889, 0.0001984126984126984,
+                                 2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07,
+                                 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
+                                 1.1470745597729725e-11};
+
 __device__ __forceinline__ double sinpi_poly(double r) {  // sin(pi r), |r| <= 0.5
   const double s = r * r;
-  double p = 1.7302192458361107e-13;
-  p = fma(p, s, -1.0518471716932065e-11);
-  p = fma(p, s, 5.392664662608129e-10);
-  p = fma(p, s, -2.2948428997269873e-08);
-  p = fma(p, s, 7.952054001475513e-07);
-  p = fma(p, s, -2.1915353447830217e-05);
-  p = fma(p, s, 0.00046630280576761255);
-  p = fma(p, s, -0.0073704309457143504);
-  p = fma(p, s, 0.08214588661112823);
-  p = fma(p, s, -0.5992645293207921);
-  p = fma(p, s, 2.5501640398773455);
-  p = fma(p, s, -5.16771278004997);
-  p = fma(p, s, 3.141592653589793);
+  double p = kSinPiC[12];
+  #pragma unroll
+  for (int k = 11; k >= 0; --k) p = fma(p, s, kSinPiC[k]);
   return r * p;
 }
 __device__ __forceinline__ double flip_if_odd(double v, double n) {
@@ -331,21 +334,9 @@ __device__ __forceinline__ double fast_exp(double z) {
   const double n = rint(z * 1.4426950408889634);
   double r = fma(-n, 6.93147180369123816490e-01, z);  // ln2 hi: n * hi is exact
   r = fma(-n, 1.90821492927058770002e-10, r);
-  double p = 1.1470745597729725e-11;
-  p = fma(p, r, 1.6059043836821613e-10);
-  p = fma(p, r, 2.08767569878681e-09);
-  p = fma(p, r, 2.505210838544172e-08);
-  p = fma(p, r, 2.755731922398589e-07);
-  p = fma(p, r, 2.7557319223985893e-06);
-  p = fma(p, r, 2.48015873015873e-05);
-  p = fma(p, r, 0.0001984126984126984);
-  p = fma(p, r, 0.001388888888888889);
-  p = fma(p, r, 0.008333333333333333);
-  p = fma(p, r, 0.041666666666666664);
-  p = fma(p, r, 0.16666666666666666);
-  p = fma(p, r, 0.5);
-  p = fma(p, r, 1.0);
-  p = fma(p, r, 1.0);
+  double p = kExpC[14];
+  #pragma unroll
+  for (int k = 13; k >= 0; --k) p = fma(p, r, kExpC[k]);
   return p * __longlong_as_double((static_cast<long long>(n) + 1023ll) << 52);
 }
 
@@ -357,7 +348,7 @@ __device__ __forceinline__ double coef_sincosexp_e(const double* v0, const doubl
   for (int i = 0; i < 3; ++i) {
     double acc = v0[i];
     #pragma unroll
-    for (int s = 0; s < 3; ++s) acc = __dadd_rn(acc, __dmul_rn(E[s * 3 + i], xi[s]));
+    for (int s = 0; s < 3; ++s) acc = fma(E[s * 3 + i], xi[s], acc);
     x[i] = acc;
   }
   double sn = fast_sinpi(__dmul_rn(2.0, x[0]));

@@ -134,7 +134,7 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
 //      W entries at q for every (s<=t) block.
 // UG / US are compile-time, so the emulated rounding folds to the plain op for fp64 and a
 // single conversion for fp32.
-struct CellGeo {
+struct __align__(16) CellGeo {
   double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson) or |det| (mass)
   double v0[3];
   double e[9];  // e[s*3 + i] = v_{s+1}[i] - v0[i]
@@ -193,7 +193,13 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
     const uint32_t cell32 = P.div_nq.div(uint32_t(idx));
     const int64_t cell = cell32;
     const int q = int(uint32_t(idx) - cell32 * uint32_t(nq));
-    const CellGeo& cg = geo[cell];
+    CellGeo cg;  // 9 x 16-byte loads (L1-resident: ~n_q consecutive threads share a cell)
+    {
+      const double2* src = reinterpret_cast<const double2*>(geo + cell);
+      double2* dst = reinterpret_cast<double2*>(&cg);
+      #pragma unroll
+      for (int k = 0; k < 9; ++k) dst[k] = __ldg(src + k);
+    }
     const double* xi = P.rule_x + 3 * q;
     double zq = 1.0;
     bool have_z = true;
