@@ -69,7 +69,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
       }
     }
   }
-  if (bad) atomicOr(flags, 4u);
+  if (bad && !(*reinterpret_cast<volatile uint32_t*>(flags) & 4u)) atomicOr(flags, 4u);
 }
 
 }  // namespace mpfem_b200

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
     expo_or = __reduce_or_sync(0xffffffffu, expo_or);
-    if (lane == 0 && expo_or) atomicOr(P.flags, 4u);
+    if (lane == 0 && expo_or && !(*reinterpret_cast<volatile uint32_t*>(P.flags) & 4u)) atomicOr(P.flags, 4u);
   }
   tc_fence_before();
   __syncthreads();

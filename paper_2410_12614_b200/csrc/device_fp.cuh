@@ -72,6 +72,16 @@ __device__ __forceinline__ double dround(double x, int f, uint32_t& fl) {
   return r;
 }
 
+// Publishes a warp's FP flags: one lane, and only the bits not yet visible, so that
+// thousands of warps raising the same flag do not serialise on one L2 address.
+__device__ __forceinline__ void publish_flags(uint32_t* flags, uint32_t fl) {
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if ((threadIdx.x & 31) == 0 && fl) {
+    const uint32_t seen = *reinterpret_cast<volatile uint32_t*>(flags);
+    if (fl & ~seen) atomicOr(flags, fl);
+  }
+}
+
 // Compile-time-format rounding: identical results to dround(x, F, fl), but the format
 // dispatch folds away (fp64 is the identity, fp32 a single conversion).
 template <int F>

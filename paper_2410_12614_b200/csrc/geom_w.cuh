@@ -175,8 +175,7 @@ __global__ void __launch_bounds__(256) cell_geometry_kernel(GeomWParams P, CellG
       for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = __dsub_rn(v[s2 + 1][a], v[0][a]);
     }
   }
-  fl = __reduce_or_sync(0xffffffffu, fl);
-  if ((threadIdx.x & 31) == 0 && fl) atomicOr(P.flags, fl);
+  publish_flags(P.flags, fl);
 }
 
 template <typename T, int UG, int US>
@@ -250,9 +249,7 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
     }
     for (int64_t z = q; z < pad; z += nq) wrow[int64_t(nb) * nq + z] = T(0.0f);
   }
-  fl |= store_flags_bits(sf);
-  fl = __reduce_or_sync(0xffffffffu, fl);
-  if ((threadIdx.x & 31) == 0 && fl) atomicOr(P.flags, fl);
+  publish_flags(P.flags, fl | store_flags_bits(sf));
 }
 
 // Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
