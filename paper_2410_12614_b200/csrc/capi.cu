@@ -253,7 +253,7 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.us = S.us;
   P.poisson = S.form;
   P.k_pad = k_pad;
-  P.div_nq = FastDiv::make(uint32_t(S.n_q));
+  P.div_nq = FastDiv::make(uint32_t((S.n_q + kQPT - 1) / kQPT));
   if (n * int64_t(S.n_q) >= (int64_t(1) << 31))
     throw Error(MPFEM_B200_CONFIG_ERROR, "n_cells * n_q must be < 2^31 per call (split the batch)");
   P.w_type = w_type;
@@ -262,7 +262,7 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.error = static_cast<int*>(S.d_error.p);
   S.d_geo.ensure(sizeof(CellGeo) * size_t(n));
   const unsigned gc = unsigned((n + 255) / 256);
-  const unsigned gw = unsigned(std::min<int64_t>((n * S.n_q + 255) / 256, int64_t(device_sm_count()) * 64));
+  const unsigned gw = unsigned(std::min<int64_t>((n * ((S.n_q + kQPT - 1) / kQPT) + 255) / 256, int64_t(device_sm_count()) * 64));
   launch_geom_typed(w_type, S.ug, S.us, gc, gw, st, P, static_cast<CellGeo*>(S.d_geo.p));
   CUDA_OK(cudaGetLastError());
 }

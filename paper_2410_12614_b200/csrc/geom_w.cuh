@@ -178,11 +178,16 @@ __global__ void __launch_bounds__(256) cell_geometry_kernel(GeomWParams P, CellG
   publish_flags(P.flags, fl);
 }
 
+// One thread per (cell, group of kQPT consecutive quadrature points): the per-cell state
+// is loaded once per kQPT points and consecutive threads still write consecutive q.
+constexpr int kQPT = 4;
+
 template <typename T, int UG, int US>
 __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
                                                              const CellGeo* __restrict__ geo) {
-  const int64_t total = P.n_cells * P.n_q;
   const int nq = P.n_q;
+  const int ngroups = (nq + kQPT - 1) / kQPT;  // P.div_nq divides by ngroups here
+  const int64_t total = P.n_cells * ngroups;
   const int nb = P.poisson ? 6 : 1;
   const int64_t pad = P.k_pad - int64_t(nb) * nq;
   uint32_t fl = 0;
@@ -191,63 +196,68 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
        idx += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t cell32 = P.div_nq.div(uint32_t(idx));
     const int64_t cell = cell32;
-    const int q = int(uint32_t(idx) - cell32 * uint32_t(nq));
-    CellGeo cg;  // 9 x 16-byte loads (L1-resident: ~n_q consecutive threads share a cell)
+    const int g = int(uint32_t(idx) - cell32 * uint32_t(ngroups));
+    CellGeo cg;  // 9 x 16-byte loads, once per kQPT points
     {
       const double2* src = reinterpret_cast<const double2*>(geo + cell);
       double2* dst = reinterpret_cast<double2*>(&cg);
       #pragma unroll
       for (int k = 0; k < 9; ++k) dst[k] = __ldg(src + k);
     }
-    const double* xi = P.rule_x + 3 * q;
-    double zq = 1.0;
-    bool have_z = true;
-    switch (P.coef_kind) {
-      case 1: zq = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl); break;
-      case 2: zq = droundT<UG>(coef_exp10_affine(P.coef + cell * P.coef_stride, xi), fl); break;
-      case 3: {
-        const double* z = P.coef + cell * P.coef_stride;
-        double acc = 0.0;
-        for (int k = 0; k < P.n_phi; ++k)
-          acc = dadd(acc, dmul(dround(z[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
-        zq = droundT<UG>(acc, fl);
-        break;
-      }
-      default: have_z = false;
-    }
-    const double omega = P.rule_w[q];  // already rounded to u_g on the host
     T* wrow = static_cast<T*>(P.W) + cell * P.k_pad;
-    // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
-    if constexpr (UG == kFP32) {
-      const float om = float(omega), zf = float(zq);  // fp32 values: the fp32 product is
-      #pragma unroll                                   // the correctly rounded exact one
-      for (int b = 0; b < 6; ++b) {
-        if (b < nb) {
-          float val = __fmul_rn(om, float(cg.g[b]));
-          if (have_z) val = __fmul_rn(val, zf);
-          wrow[b * nq + q] = to_storage<T, US>(val, sf);
+    const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
+    #pragma unroll 1
+    for (int qq = 0; qq < kQPT; ++qq) {
+      const int q = g + qq * ngroups;  // strided so a warp's stores stay contiguous in q
+      if (q >= nq) break;
+      const double* xi = P.rule_x + 3 * q;
+      double zq = 1.0;
+      bool have_z = true;
+      switch (P.coef_kind) {
+        case 1: zq = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl); break;
+        case 2: zq = droundT<UG>(coef_exp10_affine(coef, xi), fl); break;
+        case 3: {
+          double acc = 0.0;
+          for (int k = 0; k < P.n_phi; ++k)
+            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
+          zq = droundT<UG>(acc, fl);
+          break;
         }
+        default: have_z = false;
       }
-    } else if constexpr (UG == kFP64) {
-      #pragma unroll
-      for (int b = 0; b < 6; ++b) {
-        if (b < nb) {
-          double val = __dmul_rn(omega, cg.g[b]);
-          if (have_z) val = __dmul_rn(val, zq);
-          wrow[b * nq + q] = to_storage<T, US>(val, sf);
+      const double omega = P.rule_w[q];  // already rounded to u_g on the host
+      // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
+      if constexpr (UG == kFP32) {
+        const float om = float(omega), zf = float(zq);  // fp32 values: the fp32 product is
+        #pragma unroll                                   // the correctly rounded exact one
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            float val = __fmul_rn(om, float(cg.g[b]));
+            if (have_z) val = __fmul_rn(val, zf);
+            wrow[b * nq + q] = to_storage<T, US>(val, sf);
+          }
         }
-      }
-    } else {
-      #pragma unroll
-      for (int b = 0; b < 6; ++b) {
-        if (b < nb) {
-          double val = droundT<UG>(__dmul_rn(omega, cg.g[b]), fl);
-          if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
-          wrow[b * nq + q] = to_storage<T, US>(val, sf);
+      } else if constexpr (UG == kFP64) {
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            double val = __dmul_rn(omega, cg.g[b]);
+            if (have_z) val = __dmul_rn(val, zq);
+            wrow[b * nq + q] = to_storage<T, US>(val, sf);
+          }
+        }
+      } else {
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            double val = droundT<UG>(__dmul_rn(omega, cg.g[b]), fl);
+            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
+            wrow[b * nq + q] = to_storage<T, US>(val, sf);
+          }
         }
       }
     }
-    for (int64_t z = q; z < pad; z += nq) wrow[int64_t(nb) * nq + z] = T(0.0f);
+    for (int64_t z = g; z < pad; z += ngroups) wrow[int64_t(nb) * nq + z] = T(0.0f);
   }
   publish_flags(P.flags, fl | store_flags_bits(sf));
 }
