@@ -62,7 +62,7 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
                             mpfem_b200_setup_t* out);
 int mpfem_b200_setup_destroy(mpfem_b200_setup_t setup);
 
-/* Sizes: n_phi, n_q, n_d (1 mass, 3 poisson), K (GEMM depth = blocks x n_q), K_pad,
+/* Sizes: n_phi, n_q, n_d (1 mass, 3 poisson), K (GEMM depth = blocks x nq_pad), K_pad,
  * path (0 tcgen05, 1 fp32 FFMA, 2 fp64, 3 fused small-degree). */
 int mpfem_b200_setup_info(mpfem_b200_setup_t setup, int* n_phi, int* n_q, int* n_d,
                           int64_t* k, int64_t* k_pad, int* path);
@@ -98,9 +98,9 @@ int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t setup, const double* verts,
  * this setup allocate nothing (CUDA-graph capture safe). */
 int mpfem_b200_reserve(mpfem_b200_setup_t setup, int64_t n_cells);
 
-/* Debug/parity entry: the scaled weights W (kernels.cpp:177-197 build_C, GEMM-packed
- * order (block, q), blocks (s<=t)) as fp64 carriers for n_cells cells (device out,
- * n_cells x K doubles). */
+/* Debug/parity entry: the scaled weights W (kernels.cpp:177-197 build_C) in the GEMM
+ * layout -- blocks (s<=t) of nq_pad = round_up(n_q, 8) entries, zero for q >= n_q -- as
+ * fp64 carriers for n_cells cells (device out, n_cells x K doubles, K = blocks x nq_pad). */
 int mpfem_b200_scaled_weights(mpfem_b200_setup_t setup, const double* verts,
                               const int32_t* cells, int64_t n_cells, int coef_kind,
                               const double* coef, int64_t coef_stride, double* out,

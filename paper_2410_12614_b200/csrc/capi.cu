@@ -123,7 +123,7 @@ void mpfem_b200_set_last_error(const std::string& msg) { g_last_error = msg; }
 
 struct mpfem_b200_setup_s {
   int p = 0, form = 0, up = 3, ug = 3, uq = 3, us = 3, engine = 0;
-  int n_phi = 0, n_q = 0, n_d = 1, n_blocks = 1;
+  int n_phi = 0, n_q = 0, n_d = 1, n_blocks = 1, nq_pad = 0;
   int64_t k = 0, k_pad = 0, n_out = 0, n_out_pad = 0;
   int path = kPathF64;
   int acc_f16 = 0;
@@ -253,7 +253,8 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.us = S.us;
   P.poisson = S.form;
   P.k_pad = k_pad;
-  P.div_nq = FastDiv::make(uint32_t((S.n_q + kQPT - 1) / kQPT));
+  P.div_nq = FastDiv::make(uint32_t(S.nq_pad / kQPT));
+  P.nq_pad = S.nq_pad;
   if (n * int64_t(S.n_q) >= (int64_t(1) << 31))
     throw Error(MPFEM_B200_CONFIG_ERROR, "n_cells * n_q must be < 2^31 per call (split the batch)");
   P.w_type = w_type;
@@ -262,7 +263,7 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.error = static_cast<int*>(S.d_error.p);
   S.d_geo.ensure(sizeof(CellGeo) * size_t(n));
   const unsigned gc = unsigned((n + 255) / 256);
-  const unsigned gw = unsigned(std::min<int64_t>((n * ((S.n_q + kQPT - 1) / kQPT) + 255) / 256, int64_t(device_sm_count()) * 64));
+  const unsigned gw = unsigned(std::min<int64_t>((n * (S.nq_pad / kQPT) + 255) / 256, int64_t(device_sm_count()) * 64));
   launch_geom_typed(w_type, S.ug, S.us, gc, gw, st, P, static_cast<CellGeo*>(S.d_geo.p));
   CUDA_OK(cudaGetLastError());
 }
@@ -428,7 +429,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->n_q = S->rule.n_q;
     S->n_d = form ? 3 : 1;
     S->n_blocks = form ? 6 : 1;
-    S->k = int64_t(S->n_blocks) * S->n_q;
+    S->nq_pad = (S->n_q + kQPT - 1) / kQPT * kQPT;
+    S->k = int64_t(S->n_blocks) * S->nq_pad;
     const int64_t kal = S->path == kPathTC ? tc::BK : 16;
     S->k_pad = (S->k + kal - 1) / kal * kal;
     S->n_out = int64_t(S->n_phi) * S->n_phi;
@@ -459,10 +461,10 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
     const double* dB = static_cast<const double*>(S->d_B.p);
     switch (S->w_type) {
-      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-      case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-      default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
     }
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaDeviceSynchronize());

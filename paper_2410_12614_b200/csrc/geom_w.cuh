@@ -57,7 +57,8 @@ struct GeomWParams {
   int n_phi, n_q, up, ug, us;
   int poisson;
   int64_t k_pad;
-  FastDiv div_nq;          // idx / n_q for the (cell, q) expansion
+  FastDiv div_nq;          // idx / groups-per-cell for the (cell, q-group) expansion
+  int nq_pad;              // block stride of W and T along K: round_up(n_q, 8)
   int w_type;              // 0 fp16 bits, 1 bf16 bits, 2 fp32, 3 fp64
   void* W;
   uint32_t* flags;
@@ -178,86 +179,96 @@ __global__ void __launch_bounds__(256) cell_geometry_kernel(GeomWParams P, CellG
   publish_flags(P.flags, fl);
 }
 
-// One thread per (cell, group of kQPT consecutive quadrature points): the per-cell state
-// is loaded once per kQPT points and consecutive threads still write consecutive q.
-constexpr int kQPT = 4;
+// One thread per (cell, group of kQPT = 8 consecutive quadrature points). The W row is
+// laid out in blocks of nq_pad = round_up(n_q, 8) entries (entries q >= n_q are zero, as
+// are the matching rows of T), so each thread writes each block with one 16-byte store
+// and the per-cell state is loaded once per 8 points.
+constexpr int kQPT = 8;
+
+template <typename T>
+struct Pack8 {
+  T v[8];
+};
 
 template <typename T, int UG, int US>
 __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
                                                              const CellGeo* __restrict__ geo) {
   const int nq = P.n_q;
-  const int ngroups = (nq + kQPT - 1) / kQPT;  // P.div_nq divides by ngroups here
+  const int nqp = P.nq_pad;
+  const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
   const int64_t total = P.n_cells * ngroups;
   const int nb = P.poisson ? 6 : 1;
-  const int64_t pad = P.k_pad - int64_t(nb) * nq;
   uint32_t fl = 0;
   StoreFlags sf;
   for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t cell32 = P.div_nq.div(uint32_t(idx));
     const int64_t cell = cell32;
-    const int g = int(uint32_t(idx) - cell32 * uint32_t(ngroups));
-    CellGeo cg;  // 9 x 16-byte loads, once per kQPT points
+    const int q0 = int(uint32_t(idx) - cell32 * uint32_t(ngroups)) * kQPT;
+    CellGeo cg;  // 9 x 16-byte loads, once per 8 points
     {
       const double2* src = reinterpret_cast<const double2*>(geo + cell);
       double2* dst = reinterpret_cast<double2*>(&cg);
       #pragma unroll
       for (int k = 0; k < 9; ++k) dst[k] = __ldg(src + k);
     }
-    T* wrow = static_cast<T*>(P.W) + cell * P.k_pad;
     const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
-    #pragma unroll 1
-    for (int qq = 0; qq < kQPT; ++qq) {
-      const int q = g + qq * ngroups;  // strided so a warp's stores stay contiguous in q
-      if (q >= nq) break;
-      const double* xi = P.rule_x + 3 * q;
-      double zq = 1.0;
-      bool have_z = true;
-      switch (P.coef_kind) {
-        case 1: zq = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl); break;
-        case 2: zq = droundT<UG>(coef_exp10_affine(coef, xi), fl); break;
-        case 3: {
+    double zq[kQPT], om[kQPT];
+    #pragma unroll
+    for (int j = 0; j < kQPT; ++j) {
+      const int q = q0 + j;
+      zq[j] = 1.0;
+      om[j] = 0.0;  // padding points (q >= n_q) produce exact zeros
+      if (q < nq) {
+        om[j] = P.rule_w[q];  // already rounded to u_g on the host
+        const double* xi = P.rule_x + 3 * q;
+        if (P.coef_kind == 1) {
+          zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
+        } else if (P.coef_kind == 2) {
+          zq[j] = droundT<UG>(coef_exp10_affine(coef, xi), fl);
+        } else if (P.coef_kind == 3) {
           double acc = 0.0;
           for (int k = 0; k < P.n_phi; ++k)
             acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
-          zq = droundT<UG>(acc, fl);
-          break;
-        }
-        default: have_z = false;
-      }
-      const double omega = P.rule_w[q];  // already rounded to u_g on the host
-      // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
-      if constexpr (UG == kFP32) {
-        const float om = float(omega), zf = float(zq);  // fp32 values: the fp32 product is
-        #pragma unroll                                   // the correctly rounded exact one
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            float val = __fmul_rn(om, float(cg.g[b]));
-            if (have_z) val = __fmul_rn(val, zf);
-            wrow[b * nq + q] = to_storage<T, US>(val, sf);
-          }
-        }
-      } else if constexpr (UG == kFP64) {
-        #pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            double val = __dmul_rn(omega, cg.g[b]);
-            if (have_z) val = __dmul_rn(val, zq);
-            wrow[b * nq + q] = to_storage<T, US>(val, sf);
-          }
-        }
-      } else {
-        #pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          if (b < nb) {
-            double val = droundT<UG>(__dmul_rn(omega, cg.g[b]), fl);
-            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
-            wrow[b * nq + q] = to_storage<T, US>(val, sf);
-          }
+          zq[j] = droundT<UG>(acc, fl);
         }
       }
     }
-    for (int64_t z = g; z < pad; z += ngroups) wrow[int64_t(nb) * nq + z] = T(0.0f);
+    const bool have_z = P.coef_kind != 0;
+    T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
+    // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
+    #pragma unroll
+    for (int b = 0; b < 6; ++b) {
+      if (b < nb) {
+        Pack8<T> pk;
+        #pragma unroll
+        for (int j = 0; j < kQPT; ++j) {
+          if constexpr (UG == kFP32) {
+            float val = __fmul_rn(float(om[j]), float(cg.g[b]));  // fp32 values: exact-then-round
+            if (have_z) val = __fmul_rn(val, float(zq[j]));
+            pk.v[j] = to_storage<T, US>(val, sf);
+          } else if constexpr (UG == kFP64) {
+            double val = __dmul_rn(om[j], cg.g[b]);
+            if (have_z) val = __dmul_rn(val, zq[j]);
+            pk.v[j] = to_storage<T, US>(val, sf);
+          } else {
+            double val = droundT<UG>(__dmul_rn(om[j], cg.g[b]), fl);
+            if (have_z) val = droundT<UG>(__dmul_rn(val, zq[j]), fl);
+            pk.v[j] = to_storage<T, US>(val, sf);
+          }
+        }
+        // one 16-byte store per block for 16-bit storage (2 / 4 for fp32 / fp64)
+        const uint4* srcv = reinterpret_cast<const uint4*>(&pk);
+        uint4* dstv = reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp);
+        #pragma unroll
+        for (int k = 0; k < int(sizeof(Pack8<T>) / 16); ++k) dstv[k] = srcv[k];
+      }
+    }
+    // tail K..K_pad of the row: zeros (the group that owns the last block's start writes it)
+    if (q0 == 0) {
+      T* tail = static_cast<T*>(P.W) + cell * P.k_pad;
+      for (int64_t k = int64_t(nb) * nqp; k < P.k_pad; ++k) tail[k] = T(0.0f);
+    }
   }
   publish_flags(P.flags, fl | store_flags_bits(sf));
 }
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
 //   T[(b,q), (i,j)] = round_us(B_s[i,q] B_t[j,q] (+ B_t[i,q] B_s[j,q] if s<t)).
 // transposed != 0 stores Tt[o][k] (K contiguous; the tcgen05 A operand), else T[k][o].
 template <typename T>
-__global__ void build_t_kernel(const double* B, int n_phi, int n_q, int poisson, int us,
+__global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, int poisson, int us,
                                int64_t k_len, int64_t k_pad, int64_t n_out, int64_t n_out_pad,
                                int transposed, void* out) {
   const int64_t total = k_pad * n_out_pad;
@@ -276,8 +287,8 @@ __global__ void build_t_kernel(const double* B, int n_phi, int n_q, int poisson,
     if (transposed) { o = idx / k_pad; k = idx % k_pad; }
     else { k = idx / n_out_pad; o = idx % n_out_pad; }
     double val = 0.0;
-    if (k < k_len && o < n_out) {
-      int b = int(k / n_q), q = int(k % n_q);
+    const int b = int(k / nq_pad), q = int(k % nq_pad);
+    if (k < k_len && o < n_out && q < n_q) {
       int i = int(o / n_phi), j = int(o % n_phi);
       int s = 0, t = 0;
       if (poisson) {

@@ -81,9 +81,13 @@ def test_scaled_weights_match_build_C(oracle, tets, mode, form, kind):
         n = 6
         coef = coef_for(kind, p, n, rng)
         w, _ = s.scaled_weights(dev(tets[:n]), None, kind, None if coef is None else dev(coef))
-        w = w.cpu().numpy()
         nd = 3 if form == POISSON else 1
         blocks = PACK if form == POISSON else [(0, 0)]
+        # W layout: blocks of nq_pad = round_up(n_q, 8) entries, zero beyond n_q
+        nqp = s.k // len(blocks)
+        w = w.cpu().numpy().reshape(n, len(blocks), nqp)
+        assert np.all(w[:, :, nq(p):] == 0.0)
+        w = np.ascontiguousarray(w[:, :, :nq(p)]).reshape(n, -1)
         us = UNIT_ROUNDOFF[int(cfg.u_s)]
         for c in range(n):
             ref, _ = oracle.build_C(p, form, cfg_tuple(cfg), tets[c], kind,
