@@ -206,7 +206,12 @@ void launch_geom_ug(int ug, unsigned grid_cells, unsigned grid_w, cudaStream_t s
   switch (ug) {
 #define MPFEM_K1(UGV)                                                                       \
   cell_geometry_kernel<UGV><<<grid_cells, 256, 0, st>>>(P, geo);                            \
-  scaled_weights_kernel<T, UGV, US><<<grid_w, 256, 0, st>>>(P, geo);                        \
+  switch (P.coef_kind) {                                                                    \
+    case 0: scaled_weights_kernel<T, UGV, US, 0><<<grid_w, 256, 0, st>>>(P, geo); break;    \
+    case 1: scaled_weights_kernel<T, UGV, US, 1><<<grid_w, 256, 0, st>>>(P, geo); break;    \
+    case 2: scaled_weights_kernel<T, UGV, US, 2><<<grid_w, 256, 0, st>>>(P, geo); break;    \
+    default: scaled_weights_kernel<T, UGV, US, 3><<<grid_w, 256, 0, st>>>(P, geo); break;   \
+  }                                                                                         \
   break;
     case 0: MPFEM_K1(0)
     case 1: MPFEM_K1(1)

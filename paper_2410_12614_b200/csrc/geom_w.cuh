@@ -190,9 +190,9 @@ struct Pack8 {
   T v[8];
 };
 
-template <typename T, int UG, int US>
-__global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
-                                                             const CellGeo* __restrict__ geo) {
+template <typename T, int UG, int US, int COEF>
+__global__ void __launch_bounds__(256, 3) scaled_weights_kernel(GeomWParams P,
+                                                                const CellGeo* __restrict__ geo) {
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
@@ -222,11 +222,11 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
       if (q < nq) {
         om[j] = P.rule_w[q];  // already rounded to u_g on the host
         const double* xi = P.rule_x + 3 * q;
-        if (P.coef_kind == 1) {
+        if constexpr (COEF == 1) {
           zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
-        } else if (P.coef_kind == 2) {
+        } else if constexpr (COEF == 2) {
           zq[j] = droundT<UG>(coef_exp10_affine(coef, xi), fl);
-        } else if (P.coef_kind == 3) {
+        } else if constexpr (COEF == 3) {
           double acc = 0.0;
           for (int k = 0; k < P.n_phi; ++k)
             acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256) scaled_weights_kernel(GeomWParams P,
         }
       }
     }
-    const bool have_z = P.coef_kind != 0;
+    constexpr bool have_z = COEF != 0;
     T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
     // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
     #pragma unroll
