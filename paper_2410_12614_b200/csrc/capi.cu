@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/mpfem_b200.h"
+#include "cellmat_fused.cuh"
 #include "cellmat_simt.cuh"
 #include "cellmat_tc.cuh"
 #include "geom_w.cuh"
@@ -54,7 +55,7 @@ int guarded(F&& f) {
 }
 
 // Device dispatch of a setup: which K2 runs and in which element types.
-enum Path : int { kPathTC = 0, kPathF32 = 1, kPathF64 = 2 };
+enum Path : int { kPathTC = 0, kPathF32 = 1, kPathF64 = 2, kPathFused = 3 };
 
 struct DevBuf {
   void* p = nullptr;
@@ -181,6 +182,13 @@ void validate(int cell_kind, int dim, int p, int form, const int* fmts, int engi
 
 void choose_path(mpfem_b200_setup_s& S) {
   const int us = S.us, uq = S.uq;
+  // Tiny GEMM depth (K <= 48) and small matrices: one thread per cell runs the whole
+  // path in registers (cellmat_fused.cuh); fp32 accumulation of u_s-rounded operands.
+  if (uq == 2 && us <= 2 && (S.ug == 2 || S.ug == 3) && (S.p == 1 || (S.p == 2 && S.form == 0))) {
+    S.path = kPathFused;
+    S.w_type = us == 2 ? 2 : (us == 1 ? 0 : 1);
+    return;
+  }
   if ((us == 0 || us == 1) && uq == 2) {
     S.path = kPathTC;
     S.w_type = us == 1 ? 0 : 1;
@@ -328,6 +336,49 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
   CUDA_OK(cudaGetLastError());
 }
 
+template <int P, int FORM, int UG>
+void launch_fused_us(int us, unsigned grid, cudaStream_t st, const FusedParams& F) {
+  switch (us) {
+    case 0: cellmat_fused_kernel<P, FORM, UG, 0><<<grid, 128, 0, st>>>(F); break;
+    case 1: cellmat_fused_kernel<P, FORM, UG, 1><<<grid, 128, 0, st>>>(F); break;
+    default: cellmat_fused_kernel<P, FORM, UG, 2><<<grid, 128, 0, st>>>(F); break;
+  }
+}
+
+void launch_fused(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
+                  int coef_kind, const double* coef, int64_t coef_stride, float* out,
+                  int64_t out_pitch, cudaStream_t st) {
+  FusedParams F;
+  F.verts = verts;
+  F.cells = cells;
+  F.n_cells = n;
+  F.coef_kind = coef_kind;
+  F.coef = coef;
+  F.coef_stride = coef_stride;
+  F.rule_w_ug = static_cast<const double*>(S.d_rule_w_ug.p);
+  F.rule_x = static_cast<const double*>(S.d_rule_x.p);
+  F.tab_up = static_cast<const double*>(S.d_tab_up.p);
+  F.T = static_cast<const float*>(S.d_T.p);
+  F.us = S.us;
+  F.up = S.up;
+  F.out = out;
+  F.out_pitch = out_pitch;
+  F.flags = static_cast<uint32_t*>(S.d_flags.p);
+  F.error = static_cast<int*>(S.d_error.p);
+  const unsigned grid = unsigned((n + 127) / 128);
+  const int key = S.p * 100 + S.form * 10 + S.ug;
+  switch (key) {
+    case 102: launch_fused_us<1, 0, 2>(S.us, grid, st, F); break;
+    case 103: launch_fused_us<1, 0, 3>(S.us, grid, st, F); break;
+    case 112: launch_fused_us<1, 1, 2>(S.us, grid, st, F); break;
+    case 113: launch_fused_us<1, 1, 3>(S.us, grid, st, F); break;
+    case 202: launch_fused_us<2, 0, 2>(S.us, grid, st, F); break;
+    case 203: launch_fused_us<2, 0, 3>(S.us, grid, st, F); break;
+    default: throw Error(MPFEM_B200_CONFIG_ERROR, "no fused kernel for this degree/form");
+  }
+  CUDA_OK(cudaGetLastError());
+}
+
 void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells,
                        int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* out,
                        int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
@@ -341,6 +392,14 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   }
   S.n_ev = 0;
   if (n == 0) return;
+  if (S.path == kPathFused) {
+    if (n * int64_t(S.n_q) >= (int64_t(1) << 40)) throw Error(MPFEM_B200_CONFIG_ERROR, "batch too large");
+    S.mark(st);
+    launch_fused(S, verts, cells, n, coef_kind, coef, coef_stride, static_cast<float*>(out), out_pitch, st);
+    ++S.last_launches;
+    S.mark(st);
+    S.mark(st);
+  } else {
   S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
   // Chunking: enough K2 tiles per chunk to fill the GPU about three times over.
   const int64_t cell_tiles = (n + tc::BN - 1) / tc::BN;
@@ -392,6 +451,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     CUDA_OK(cudaEventRecord(S.join, S.side));
     CUDA_OK(cudaStreamWaitEvent(st, S.join, 0));
   }
+  }  // non-fused paths
   if (flags) {
     uint32_t h[2] = {0, 0};
     CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
@@ -459,13 +519,22 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->d_error.ensure(16);
     CUDA_OK(cudaMemset(S->d_flags.p, 0, 16));
     CUDA_OK(cudaMemset(S->d_error.p, 0, 16));
-    const size_t tbytes = size_t(S->k_pad) * size_t(S->n_out_pad) * elem_size(S->w_type);
-    S->d_T.ensure(tbytes);
+    size_t tbytes = size_t(S->k_pad) * size_t(S->n_out_pad) * elem_size(S->w_type);
+    if (S->path == kPathFused) {
+      // fp32 T[k][o] with k = block * n_q + q (no padding), values rounded to u_s
+      const int64_t kf = int64_t(S->n_blocks) * S->n_q;
+      S->d_T.ensure(sizeof(float) * size_t(kf) * size_t(S->n_out));
+      const int64_t tot = kf * S->n_out;
+      build_t_kernel<float><<<unsigned((tot + 255) / 256), 256>>>(static_cast<const double*>(S->d_B.p), S->n_phi, S->n_q, S->n_q, form, u_s, kf, kf, S->n_out, S->n_out, 0, S->d_T.p);
+      CUDA_OK(cudaGetLastError());
+      tbytes = 0;
+    }
+    if (tbytes) S->d_T.ensure(tbytes);
     const int transposed = S->path == kPathTC;
-    const int64_t total = S->k_pad * S->n_out_pad;
+    const int64_t total = tbytes ? S->k_pad * S->n_out_pad : 0;
     const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
     const double* dB = static_cast<const double*>(S->d_B.p);
-    switch (S->w_type) {
+    if (total) switch (S->w_type) {
       case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
       case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
       case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;

@@ -1,0 +1,165 @@
+// cellmat_fused.cuh -- small-degree fused path (p = 1 mass/Poisson, p = 2 mass).
+//
+// For these degrees the GEMM depth K = n_blocks * n_q is 8..48 and a cell matrix has
+// 16..100 entries: a cell's whole computation fits one thread's registers, and
+// materialising W (and padding its rows to a 64-wide TMA box) would move several times
+// more bytes than the output. One thread per cell therefore runs the complete hot path:
+//   geometry at u_g (tet_geometry, bit-identical to cell_geometry) ->
+//   coefficient at the quadrature points -> W_k = round_us(round_ug(round_ug(omega G) z))
+//   (bit-identical to build_C) -> A_o = sum_k W_k T[k, o] with FFMA in fp32 (u_q = fp32)
+//   -> 16-byte stores of the cell's row-major matrix.
+// T (the shared basis products, rounded to u_s) lives in shared memory and is read as a
+// broadcast (every thread reads the same T[k, o]). HBM traffic is 96 B in + 4 n_phi^2 B
+// out per cell: the path's algorithmic bytes.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "device_fp.cuh"
+#include "geom_w.cuh"
+
+namespace mpfem_b200 {
+
+struct FusedParams {
+  const double* verts;
+  const int32_t* cells;
+  int64_t n_cells;
+  int coef_kind;
+  const double* coef;
+  int64_t coef_stride;
+  const double* rule_w_ug;  // n_q, rounded to u_g
+  const double* rule_x;     // n_q x 3
+  const double* tab_up;     // n_phi x n_q (nodal coefficient path)
+  const float* T;           // K x n_out (fp32 carriers of u_s values)
+  int us, up;
+  float* out;
+  int64_t out_pitch;
+  uint32_t* flags;
+  int* error;
+};
+
+template <int US>
+__device__ __forceinline__ float round_storage_f(double v, StoreFlags& sf) {
+  if constexpr (US == kFP16) return __half2float(to_storage<__half, kFP16>(v, sf));
+  else if constexpr (US == kBF16) return __bfloat162float(to_storage<__nv_bfloat16, kBF16>(v, sf));
+  else return to_storage<float, kFP32>(v, sf);
+}
+
+template <int P, int FORM, int UG, int US>
+__global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
+  constexpr int NPHI = (P + 1) * (P + 2) * (P + 3) / 6;
+  constexpr int NQ = (P + 1) * (P + 1) * (P + 1);
+  constexpr int NB = FORM ? 6 : 1;
+  constexpr int K = NB * NQ;
+  constexpr int NOUT = NPHI * NPHI;
+  __shared__ float sT[K * NOUT];
+  __shared__ double sW[NQ], sX[NQ * 3];
+  for (int i = threadIdx.x; i < K * NOUT; i += blockDim.x) sT[i] = F.T[i];
+  for (int i = threadIdx.x; i < NQ; i += blockDim.x) sW[i] = F.rule_w_ug[i];
+  for (int i = threadIdx.x; i < NQ * 3; i += blockDim.x) sX[i] = F.rule_x[i];
+  __syncthreads();
+  const int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint32_t fl = 0;
+  StoreFlags sf;
+  if (cell < F.n_cells) {
+    double v[4][3];
+    if (F.cells) {
+      #pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t vid = F.cells[cell * 4 + k];
+        #pragma unroll
+        for (int a = 0; a < 3; ++a) v[k][a] = F.verts[vid * 3 + a];
+      }
+    } else {
+      const double2* src = reinterpret_cast<const double2*>(F.verts + cell * 12);
+      double flat[12];
+      #pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const double2 t = __ldg(src + k);
+        flat[2 * k] = t.x;
+        flat[2 * k + 1] = t.y;
+      }
+      #pragma unroll
+      for (int k = 0; k < 4; ++k)
+        #pragma unroll
+        for (int a = 0; a < 3; ++a) v[k][a] = flat[k * 3 + a];
+    }
+    TetGeometry g;
+    if (!tet_geometry<UG>(v, FORM != 0, g, fl)) {
+      atomicExch(F.error, 3);
+    } else {
+      double v0[3], E[9];
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        v0[a] = v[0][a];
+        #pragma unroll
+        for (int s = 0; s < 3; ++s) E[s * 3 + a] = __dsub_rn(v[s + 1][a], v[0][a]);
+      }
+      const double* zc = F.coef ? F.coef + cell * F.coef_stride : nullptr;
+      float w[K];
+      #pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        double zq = 1.0;
+        const double* xi = sX + 3 * q;
+        if (F.coef_kind == 1) {
+          if constexpr (UG == kFP32) zq = double(coef_sincosexp_f(v0, E, xi));
+          else zq = droundT<UG>(coef_sincosexp_e(v0, E, xi), fl);
+        } else if (F.coef_kind == 2) {
+          zq = droundT<UG>(coef_exp10_affine(zc, xi), fl);
+        } else if (F.coef_kind == 3) {
+          double acc = 0.0;
+          for (int k = 0; k < NPHI; ++k)
+            acc = dadd(acc, dmul(dround(zc[k], F.up, fl), F.tab_up[k * NQ + q], F.up, fl), F.up, fl);
+          zq = droundT<UG>(acc, fl);
+        }
+        const bool have_z = F.coef_kind != 0;
+        #pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          double val;
+          if constexpr (UG == kFP32) {
+            float t = __fmul_rn(float(sW[q]), float(g.g[b]));
+            if (have_z) t = __fmul_rn(t, float(zq));
+            val = t;
+          } else {
+            val = droundT<UG>(__dmul_rn(sW[q], g.g[b]), fl);
+            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
+          }
+          w[b * NQ + q] = round_storage_f<US>(val, sf);
+        }
+      }
+      float acc[NOUT];
+      #pragma unroll
+      for (int o = 0; o < NOUT; ++o) acc[o] = 0.0f;
+      #pragma unroll 1
+      for (int k = 0; k < K; ++k) {
+        const float wk = w[k];
+        const float4* trow = reinterpret_cast<const float4*>(sT + k * NOUT);
+        #pragma unroll
+        for (int o4 = 0; o4 < NOUT / 4; ++o4) {
+          const float4 t = trow[o4];
+          acc[4 * o4 + 0] = fmaf(wk, t.x, acc[4 * o4 + 0]);
+          acc[4 * o4 + 1] = fmaf(wk, t.y, acc[4 * o4 + 1]);
+          acc[4 * o4 + 2] = fmaf(wk, t.z, acc[4 * o4 + 2]);
+          acc[4 * o4 + 3] = fmaf(wk, t.w, acc[4 * o4 + 3]);
+        }
+      }
+      uint32_t bad = 0;
+      #pragma unroll
+      for (int o = 0; o < NOUT; ++o) bad |= (__float_as_uint(acc[o]) & 0x7f800000u) == 0x7f800000u;
+      if (bad) fl |= kInvalid;
+      float* dst = F.out + cell * F.out_pitch;
+      if ((F.out_pitch & 3) == 0) {
+        #pragma unroll
+        for (int o4 = 0; o4 < NOUT / 4; ++o4)
+          __stcs(reinterpret_cast<float4*>(dst) + o4,
+                 make_float4(acc[4 * o4], acc[4 * o4 + 1], acc[4 * o4 + 2], acc[4 * o4 + 3]));
+      } else {
+        #pragma unroll
+        for (int o = 0; o < NOUT; ++o) __stcs(dst + o, acc[o]);
+      }
+    }
+  }
+  publish_flags(F.flags, fl | store_flags_bits(sf));
+}
+
+}  // namespace mpfem_b200

@@ -350,6 +350,59 @@ __device__ __forceinline__ double fast_exp(double z) {
   return p * __longlong_as_double((static_cast<long long>(n) + 1023ll) << 52);
 }
 
+// fp32 counterparts for u_g = fp32 (the coefficient is rounded to fp32 anyway): same
+// reductions, Taylor series truncated below 2^-27; <= 1.7 ulp(fp32) against 100-bit mpmath.
+__constant__ float kSinPiF[7] = {3.1415927410125732f, -5.167712688446045f, 2.550163984298706f,
+                                 -0.5992645025253296f, 0.08214588463306427f, -0.00737043097615242f,
+                                 0.0004663027939386666f};
+__constant__ float kExpF[9] = {1.0f, 1.0f, 0.5f, 0.1666666716337204f, 0.0416666679084301f,
+                               0.008333333767950535f, 0.0013888889225199819f,
+                               0.00019841270113829523f, 2.4801587642286904e-05f};
+__device__ __forceinline__ float sinpi_poly_f(float r) {
+  const float s = r * r;
+  float p = kSinPiF[6];
+  #pragma unroll
+  for (int k = 5; k >= 0; --k) p = fmaf(p, s, kSinPiF[k]);
+  return r * p;
+}
+__device__ __forceinline__ float flip_if_odd_f(float v, float n) {
+  const int odd = static_cast<int>(n) & 1;
+  return __int_as_float(__float_as_int(v) ^ (odd << 31));
+}
+__device__ __forceinline__ float fast_sinpi_f(float a) {
+  const float n = rintf(a);
+  return flip_if_odd_f(sinpi_poly_f(a - n), n);
+}
+__device__ __forceinline__ float fast_cospi_f(float a) {
+  const float n = rintf(a);
+  return flip_if_odd_f(sinpi_poly_f(0.5f - fabsf(a - n)), n);
+}
+__device__ __forceinline__ float fast_exp_f(float z) {
+  const float n = rintf(z * 1.4426950408889634f);
+  float r = fmaf(-n, 0.693145751953125f, z);
+  r = fmaf(-n, 1.428606765330187e-06f, r);
+  float p = kExpF[8];
+  #pragma unroll
+  for (int k = 7; k >= 0; --k) p = fmaf(p, r, kExpF[k]);
+  return p * __int_as_float((static_cast<int>(n) + 127) << 23);
+}
+
+// c(x_q) with the physical point in binary64 and the transcendentals in fp32, for u_g = fp32.
+__device__ __forceinline__ float coef_sincosexp_f(const double* v0, const double* E, const double* xi) {
+  double x[3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double acc = v0[i];
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) acc = fma(E[s * 3 + i], xi[s], acc);
+    x[i] = acc;
+  }
+  const float sn = fast_sinpi_f(float(2.0 * x[0]));
+  const float cs = fast_cospi_f(float(2.0 * x[1]));
+  const float e = fast_exp_f(float(x[2]));
+  return fmaf(0.5f * sn * cs, e, 1.0f);
+}
+
 // Same, from the cell's origin v0 and edge vectors E[s] = v_{s+1} - v0 (precomputed).
 __device__ __forceinline__ double coef_sincosexp_e(const double* v0, const double* E,
                                                    const double* xi) {

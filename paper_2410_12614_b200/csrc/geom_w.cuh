@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(256, 3) scaled_weights_kernel(GeomWParams P,
       if (q < nq) {
         om[j] = P.rule_w[q];  // already rounded to u_g on the host
         const double* xi = P.rule_x + 3 * q;
-        if constexpr (COEF == 1) {
+        if constexpr (COEF == 1 && UG == kFP32) {
+          zq[j] = double(coef_sincosexp_f(cg.v0, cg.e, xi));
+        } else if constexpr (COEF == 1) {
           zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
         } else if constexpr (COEF == 2) {
           zq[j] = droundT<UG>(coef_exp10_affine(coef, xi), fl);
