@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
       float acc[NOUT];
       #pragma unroll
       for (int o = 0; o < NOUT; ++o) acc[o] = 0.0f;
-      #pragma unroll 1
+      #pragma unroll  // fully: w[] must stay in registers
       for (int k = 0; k < K; ++k) {
         const float wk = w[k];
         const float4* trow = reinterpret_cast<const float4*>(sT + k * NOUT);

@@ -97,11 +97,15 @@ def test_scaled_weights_match_build_C(oracle, tets, mode, form, kind):
             if kind in (COEF_ONE, COEF_NODAL):
                 assert np.array_equal(w[c].view(np.uint64), want.view(np.uint64)), (p, c)
             else:
-                # CUDA and glibc transcendentals may differ by a few fp64 ulps
+                # The analytic coefficient is evaluated on the GPU by polynomial kernels at
+                # u_g (fp32 for u_g = fp32, fp64 otherwise) within ~2 ulp of the correctly
+                # rounded value the oracle uses: W may differ in the last place of u_s.
                 diff = np.abs(w[c] - want)
-                tol = max(2.0 * us, 16 * 2.0**-53)
+                wide = int(cfg.u_s) >= 2
+                tol = 8.0 * us if wide else 2.0 * us
+                tol = max(tol, 16 * 2.0**-53)
                 assert np.all(diff <= tol * np.abs(want) + 1e-300), (p, c)
-                if int(cfg.u_s) != 3:  # a libm ulp rarely survives rounding to u_s
+                if not wide:  # a ~2-ulp(u_g) coefficient difference rarely survives rounding to u_s
                     assert np.mean(diff > 0) <= 0.02, (p, c)
 
 
