@@ -336,12 +336,22 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
   CUDA_OK(cudaGetLastError());
 }
 
+template <int P, int FORM, int UG, int US>
+void launch_fused_coef(int coef, unsigned grid, cudaStream_t st, const FusedParams& F) {
+  switch (coef) {
+    case 0: cellmat_fused_kernel<P, FORM, UG, US, 0><<<grid, 128, 0, st>>>(F); break;
+    case 1: cellmat_fused_kernel<P, FORM, UG, US, 1><<<grid, 128, 0, st>>>(F); break;
+    case 2: cellmat_fused_kernel<P, FORM, UG, US, 2><<<grid, 128, 0, st>>>(F); break;
+    default: cellmat_fused_kernel<P, FORM, UG, US, 3><<<grid, 128, 0, st>>>(F); break;
+  }
+}
+
 template <int P, int FORM, int UG>
 void launch_fused_us(int us, unsigned grid, cudaStream_t st, const FusedParams& F) {
   switch (us) {
-    case 0: cellmat_fused_kernel<P, FORM, UG, 0><<<grid, 128, 0, st>>>(F); break;
-    case 1: cellmat_fused_kernel<P, FORM, UG, 1><<<grid, 128, 0, st>>>(F); break;
-    default: cellmat_fused_kernel<P, FORM, UG, 2><<<grid, 128, 0, st>>>(F); break;
+    case 0: launch_fused_coef<P, FORM, UG, 0>(F.coef_kind, grid, st, F); break;
+    case 1: launch_fused_coef<P, FORM, UG, 1>(F.coef_kind, grid, st, F); break;
+    default: launch_fused_coef<P, FORM, UG, 2>(F.coef_kind, grid, st, F); break;
   }
 }
 

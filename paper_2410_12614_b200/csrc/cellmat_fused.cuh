@@ -5,8 +5,8 @@
 // materialising W (and padding its rows to a 64-wide TMA box) would move several times
 // more bytes than the output. One thread per cell therefore runs the complete hot path:
 //   geometry at u_g (tet_geometry, bit-identical to cell_geometry) ->
-//   coefficient at the quadrature points -> W_k = round_us(round_ug(round_ug(omega G) z))
-//   (bit-identical to build_C) -> A_o = sum_k W_k T[k, o] with FFMA in fp32 (u_q = fp32)
+//   for each quadrature point q: coefficient, W_(b,q) = round_us(round_ug(round_ug(omega G_b) z))
+//   (bit-identical to build_C), A_o += W_(b,q) T[(b,q), o] with FFMA in fp32 (u_q = fp32)
 //   -> 16-byte stores of the cell's row-major matrix.
 // T (the shared basis products, rounded to u_s) lives in shared memory and is read as a
 // broadcast (every thread reads the same T[k, o]). HBM traffic is 96 B in + 4 n_phi^2 B
@@ -45,14 +45,14 @@ __device__ __forceinline__ float round_storage_f(double v, StoreFlags& sf) {
   else return to_storage<float, kFP32>(v, sf);
 }
 
-template <int P, int FORM, int UG, int US>
+template <int P, int FORM, int UG, int US, int COEF>
 __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
   constexpr int NPHI = (P + 1) * (P + 2) * (P + 3) / 6;
   constexpr int NQ = (P + 1) * (P + 1) * (P + 1);
   constexpr int NB = FORM ? 6 : 1;
   constexpr int K = NB * NQ;
   constexpr int NOUT = NPHI * NPHI;
-  __shared__ float sT[K * NOUT];
+  __shared__ __align__(16) float sT[K * NOUT];
   __shared__ double sW[NQ], sX[NQ * 3];
   for (int i = threadIdx.x; i < K * NOUT; i += blockDim.x) sT[i] = F.T[i];
   for (int i = threadIdx.x; i < NQ; i += blockDim.x) sW[i] = F.rule_w_ug[i];
@@ -96,51 +96,46 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
         for (int s = 0; s < 3; ++s) E[s * 3 + a] = __dsub_rn(v[s + 1][a], v[0][a]);
       }
       const double* zc = F.coef ? F.coef + cell * F.coef_stride : nullptr;
-      float w[K];
+      float acc[NOUT];
       #pragma unroll
+      for (int o = 0; o < NOUT; ++o) acc[o] = 0.0f;
+      // depth loop q-outer: W_(b,q) is generated and consumed immediately
+      #pragma unroll 1
       for (int q = 0; q < NQ; ++q) {
         double zq = 1.0;
         const double* xi = sX + 3 * q;
-        if (F.coef_kind == 1) {
+        if constexpr (COEF == 1) {
           if constexpr (UG == kFP32) zq = double(coef_sincosexp_f(v0, E, xi));
           else zq = droundT<UG>(coef_sincosexp_e(v0, E, xi), fl);
-        } else if (F.coef_kind == 2) {
+        } else if constexpr (COEF == 2) {
           zq = droundT<UG>(coef_exp10_affine(zc, xi), fl);
-        } else if (F.coef_kind == 3) {
-          double acc = 0.0;
+        } else if constexpr (COEF == 3) {
+          double a2 = 0.0;
           for (int k = 0; k < NPHI; ++k)
-            acc = dadd(acc, dmul(dround(zc[k], F.up, fl), F.tab_up[k * NQ + q], F.up, fl), F.up, fl);
-          zq = droundT<UG>(acc, fl);
+            a2 = dadd(a2, dmul(dround(zc[k], F.up, fl), F.tab_up[k * NQ + q], F.up, fl), F.up, fl);
+          zq = droundT<UG>(a2, fl);
         }
-        const bool have_z = F.coef_kind != 0;
         #pragma unroll
         for (int b = 0; b < NB; ++b) {
           double val;
           if constexpr (UG == kFP32) {
             float t = __fmul_rn(float(sW[q]), float(g.g[b]));
-            if (have_z) t = __fmul_rn(t, float(zq));
+            if constexpr (COEF != 0) t = __fmul_rn(t, float(zq));
             val = t;
           } else {
             val = droundT<UG>(__dmul_rn(sW[q], g.g[b]), fl);
-            if (have_z) val = droundT<UG>(__dmul_rn(val, zq), fl);
+            if constexpr (COEF != 0) val = droundT<UG>(__dmul_rn(val, zq), fl);
           }
-          w[b * NQ + q] = round_storage_f<US>(val, sf);
-        }
-      }
-      float acc[NOUT];
-      #pragma unroll
-      for (int o = 0; o < NOUT; ++o) acc[o] = 0.0f;
-      #pragma unroll  // fully: w[] must stay in registers
-      for (int k = 0; k < K; ++k) {
-        const float wk = w[k];
-        const float4* trow = reinterpret_cast<const float4*>(sT + k * NOUT);
-        #pragma unroll
-        for (int o4 = 0; o4 < NOUT / 4; ++o4) {
-          const float4 t = trow[o4];
-          acc[4 * o4 + 0] = fmaf(wk, t.x, acc[4 * o4 + 0]);
-          acc[4 * o4 + 1] = fmaf(wk, t.y, acc[4 * o4 + 1]);
-          acc[4 * o4 + 2] = fmaf(wk, t.z, acc[4 * o4 + 2]);
-          acc[4 * o4 + 3] = fmaf(wk, t.w, acc[4 * o4 + 3]);
+          const float wk = round_storage_f<US>(val, sf);
+          const float4* trow = reinterpret_cast<const float4*>(sT + (b * NQ + q) * NOUT);
+          #pragma unroll
+          for (int o4 = 0; o4 < NOUT / 4; ++o4) {
+            const float4 t = trow[o4];
+            acc[4 * o4 + 0] = fmaf(wk, t.x, acc[4 * o4 + 0]);
+            acc[4 * o4 + 1] = fmaf(wk, t.y, acc[4 * o4 + 1]);
+            acc[4 * o4 + 2] = fmaf(wk, t.z, acc[4 * o4 + 2]);
+            acc[4 * o4 + 3] = fmaf(wk, t.w, acc[4 * o4 + 3]);
+          }
         }
       }
       uint32_t bad = 0;

@@ -173,9 +173,13 @@ struct TetGeometry {
   double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson); g[0] = |det| (mass)
 };
 
+__device__ __forceinline__ bool tet_geometry_f32(const double v[4][3], bool poisson, TetGeometry& out,
+                                                 uint32_t& fl);
+
 template <int F>
 __device__ __forceinline__ bool tet_geometry(const double v[4][3], bool poisson, TetGeometry& out,
                                              uint32_t& fl) {
+  if constexpr (F == kFP32) return tet_geometry_f32(v, poisson, out, fl);
   // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
   double jac[3][3];
   #pragma unroll
@@ -281,6 +285,117 @@ __device__ __forceinline__ bool tet_geometry(const double v[4][3], bool poisson,
       for (int k = 0; k < 3; ++k) dot = daddT<F>(dot, dmulT<F>(inv[s][k], inv[t][k], fl), fl);
       out.g[idx++] = dmulT<F>(out.abs_det, dot, fl);
     }
+  return true;
+}
+
+// u_g = fp32: the same op sequence in native fp32 arithmetic. IEEE fp32 +,-,*,/ are the
+// correctly rounded results of the exact operations, i.e. exactly round_fp32 of the exact
+// binary64 op the emulation computes (no double rounding, softfloat.hpp:12-16), so the
+// values are bit-identical to tet_geometry<kFP32>; FP events are detected on the results.
+__device__ __forceinline__ bool tet_geometry_f32(const double v[4][3], bool poisson, TetGeometry& out,
+                                                 uint32_t& fl) {
+  float x[4][3];
+  #pragma unroll
+  for (int k = 0; k < 4; ++k)
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) x[k][i] = __double2float_rn(v[k][i]);
+  float jac[3][3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      // sum over k ascending of x_k * grad_k[s]: 0 + (-x0) then + x_{s+1} (others add +-0)
+      float a = __fadd_rn(0.0f, __fmul_rn(x[0][i], -1.0f));
+      #pragma unroll
+      for (int k = 1; k < 4; ++k) a = __fadd_rn(a, __fmul_rn(x[k][i], (k - 1 == s) ? 1.0f : 0.0f));
+      jac[i][s] = a;
+    }
+  float lu[3][3];
+  int perm[3] = {0, 1, 2};
+  int sign = 1;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) lu[i][s] = jac[i][s];
+  #pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    int pivot = col;
+    float best = fabsf(lu[col][col]);
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const float a = fabsf(lu[r][col]);
+      if (a > best) { best = a; pivot = r; }
+    }
+    float pv = lu[col][col];
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (pivot == r) pv = lu[r][col];
+    if (pv == 0.0f) return false;
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      if (pivot == r) {
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float t = lu[r][c];
+          lu[r][c] = lu[col][c];
+          lu[col][c] = t;
+        }
+        const int t = perm[r];
+        perm[r] = perm[col];
+        perm[col] = t;
+        sign = -sign;
+      }
+    }
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const float m = __fdiv_rn(lu[r][col], lu[col][col]);
+      lu[r][col] = m;
+      #pragma unroll
+      for (int c = col + 1; c < 3; ++c) lu[r][c] = __fsub_rn(lu[r][c], __fmul_rn(m, lu[col][c]));
+    }
+  }
+  float det = float(sign);
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) det = __fmul_rn(det, lu[i][i]);
+  out.det = det;
+  out.abs_det = fabsf(det);
+  if (!poisson) {
+    out.g[0] = out.abs_det;
+  } else {
+    float inv[3][3];
+    #pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float y[3];
+      #pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        float s = perm[r] == k ? 1.0f : 0.0f;
+        #pragma unroll
+        for (int c = 0; c < r; ++c) s = __fsub_rn(s, __fmul_rn(lu[r][c], y[c]));
+        y[r] = s;
+      }
+      #pragma unroll
+      for (int r = 2; r >= 0; --r) {
+        float s = y[r];
+        #pragma unroll
+        for (int c = r + 1; c < 3; ++c) s = __fsub_rn(s, __fmul_rn(lu[r][c], inv[c][k]));
+        inv[r][k] = __fdiv_rn(s, lu[r][r]);
+      }
+    }
+    int idx = 0;
+    #pragma unroll
+    for (int s = 0; s < 3; ++s)
+      #pragma unroll
+      for (int t = s; t < 3; ++t) {
+        float dot = 0.0f;
+        #pragma unroll
+        for (int k = 0; k < 3; ++k) dot = __fadd_rn(dot, __fmul_rn(inv[s][k], inv[t][k]));
+        const float gv = __fmul_rn(float(out.abs_det), dot);
+        out.g[idx++] = gv;
+        if (!isfinite(gv)) fl |= isnan(gv) ? kInvalid : kOverflow;
+        if (gv != 0.0f && fabsf(gv) < 0x1.0p-126f) fl |= kUnderflow;
+      }
+  }
+  if (!isfinite(det)) fl |= isnan(det) ? kInvalid : kOverflow;
   return true;
 }
 
