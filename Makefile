@@ -2,22 +2,33 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2410_12614_b200
 LIB := $(PKG)/lib/libmpfem_b200.so
-SRCS := $(PKG)/csrc/capi.cu $(PKG)/csrc/assembly_capi.cu $(PKG)/csrc/host_setup.cpp $(PKG)/csrc/host_mesh.cpp
+OBJDIR := $(PKG)/lib/obj
+CU_SRCS := capi assembly_capi launch_geom launch_fused
+CPP_SRCS := host_setup host_mesh
+OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU_SRCS) $(CPP_SRCS)))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/mpfem_b200.h
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -shared \
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off \
            --expt-relaxed-constexpr -Xptxas -v
 
 all: $(LIB) oracle
 
-$(LIB): $(SRCS) $(HDRS)
-	mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -o $@ $(SRCS) 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; exit 1)
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	cat $(OBJDIR)/*.ptxas.log > $(PKG)/lib/ptxas.log
 
 oracle:
 	$(MAKE) -s -C oracle all
 
 clean:
-	rm -f $(LIB)
+	rm -rf $(LIB) $(OBJDIR)
 
 .PHONY: all oracle clean

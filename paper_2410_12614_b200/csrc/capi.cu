@@ -23,6 +23,14 @@
 
 using namespace mpfem_b200;
 
+namespace mpfem_b200 {
+// K1 / fused-kernel instantiations live in launch_geom.cu / launch_fused.cu (separate
+// translation units, compiled in parallel).
+void launch_geom_typed(int w_type, int ug, int us, unsigned gc, unsigned gw, cudaStream_t st,
+                       const GeomWParams& P, CellGeo* geo);
+void launch_fused_dispatch(int key, int us, unsigned grid, cudaStream_t st, const FusedParams& F);
+}  // namespace mpfem_b200
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -208,44 +216,6 @@ void choose_path(mpfem_b200_setup_s& S) {
   }
 }
 
-template <typename T, int US>
-void launch_geom_ug(int ug, unsigned grid_cells, unsigned grid_w, cudaStream_t st, const GeomWParams& P,
-                    CellGeo* geo) {
-  switch (ug) {
-#define MPFEM_K1(UGV)                                                                       \
-  cell_geometry_kernel<UGV><<<grid_cells, 256, 0, st>>>(P, geo);                            \
-  switch (P.coef_kind) {                                                                    \
-    case 0: scaled_weights_kernel<T, UGV, US, 0><<<grid_w, 256, 0, st>>>(P, geo); break;    \
-    case 1: scaled_weights_kernel<T, UGV, US, 1><<<grid_w, 256, 0, st>>>(P, geo); break;    \
-    case 2: scaled_weights_kernel<T, UGV, US, 2><<<grid_w, 256, 0, st>>>(P, geo); break;    \
-    default: scaled_weights_kernel<T, UGV, US, 3><<<grid_w, 256, 0, st>>>(P, geo); break;   \
-  }                                                                                         \
-  break;
-    case 0: MPFEM_K1(0)
-    case 1: MPFEM_K1(1)
-    case 2: MPFEM_K1(2)
-    default: MPFEM_K1(3)
-#undef MPFEM_K1
-  }
-}
-
-// W element type follows u_s except on the fp64 path, where any u_s is carried in fp64.
-void launch_geom_typed(int w_type, int ug, int us, unsigned gc, unsigned gw, cudaStream_t st,
-                       const GeomWParams& P, CellGeo* geo) {
-  switch (w_type) {
-    case 0: launch_geom_ug<__half, 1>(ug, gc, gw, st, P, geo); break;
-    case 1: launch_geom_ug<__nv_bfloat16, 0>(ug, gc, gw, st, P, geo); break;
-    case 2: launch_geom_ug<float, 2>(ug, gc, gw, st, P, geo); break;
-    default:
-      switch (us) {
-        case 0: launch_geom_ug<double, 0>(ug, gc, gw, st, P, geo); break;
-        case 1: launch_geom_ug<double, 1>(ug, gc, gw, st, P, geo); break;
-        case 2: launch_geom_ug<double, 2>(ug, gc, gw, st, P, geo); break;
-        default: launch_geom_ug<double, 3>(ug, gc, gw, st, P, geo); break;
-      }
-  }
-}
-
 void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
                  int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
                  int w_type, cudaStream_t st) {
@@ -336,25 +306,6 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
   CUDA_OK(cudaGetLastError());
 }
 
-template <int P, int FORM, int UG, int US>
-void launch_fused_coef(int coef, unsigned grid, cudaStream_t st, const FusedParams& F) {
-  switch (coef) {
-    case 0: cellmat_fused_kernel<P, FORM, UG, US, 0><<<grid, 128, 0, st>>>(F); break;
-    case 1: cellmat_fused_kernel<P, FORM, UG, US, 1><<<grid, 128, 0, st>>>(F); break;
-    case 2: cellmat_fused_kernel<P, FORM, UG, US, 2><<<grid, 128, 0, st>>>(F); break;
-    default: cellmat_fused_kernel<P, FORM, UG, US, 3><<<grid, 128, 0, st>>>(F); break;
-  }
-}
-
-template <int P, int FORM, int UG>
-void launch_fused_us(int us, unsigned grid, cudaStream_t st, const FusedParams& F) {
-  switch (us) {
-    case 0: launch_fused_coef<P, FORM, UG, 0>(F.coef_kind, grid, st, F); break;
-    case 1: launch_fused_coef<P, FORM, UG, 1>(F.coef_kind, grid, st, F); break;
-    default: launch_fused_coef<P, FORM, UG, 2>(F.coef_kind, grid, st, F); break;
-  }
-}
-
 void launch_fused(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
                   int coef_kind, const double* coef, int64_t coef_stride, float* out,
                   int64_t out_pitch, cudaStream_t st) {
@@ -376,16 +327,7 @@ void launch_fused(mpfem_b200_setup_s& S, const double* verts, const int32_t* cel
   F.flags = static_cast<uint32_t*>(S.d_flags.p);
   F.error = static_cast<int*>(S.d_error.p);
   const unsigned grid = unsigned((n + 127) / 128);
-  const int key = S.p * 100 + S.form * 10 + S.ug;
-  switch (key) {
-    case 102: launch_fused_us<1, 0, 2>(S.us, grid, st, F); break;
-    case 103: launch_fused_us<1, 0, 3>(S.us, grid, st, F); break;
-    case 112: launch_fused_us<1, 1, 2>(S.us, grid, st, F); break;
-    case 113: launch_fused_us<1, 1, 3>(S.us, grid, st, F); break;
-    case 202: launch_fused_us<2, 0, 2>(S.us, grid, st, F); break;
-    case 203: launch_fused_us<2, 0, 3>(S.us, grid, st, F); break;
-    default: throw Error(MPFEM_B200_CONFIG_ERROR, "no fused kernel for this degree/form");
-  }
+  launch_fused_dispatch(S.p * 100 + S.form * 10 + S.ug, S.us, grid, st, F);
   CUDA_OK(cudaGetLastError());
 }
 
