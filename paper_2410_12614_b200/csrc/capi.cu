@@ -138,7 +138,8 @@ struct mpfem_b200_setup_s {
   int acc_f16 = 0;
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
   Rule rule;
-  DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T;
+  DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
+  int n_rows = 0;  // tcgen05 path: rows of Tt (upper-triangle 8x4 blocks, padded to 128)
   DevBuf d_W, d_flags, d_error, d_geo;
   // host-API staging
   DevBuf h_verts, h_cells, h_coef, h_out;
@@ -269,6 +270,8 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     tc::Params P;
     P.n_cells = n;
     P.n_out = int(S.n_out);
+    P.n_phi = S.n_phi;
+    P.rows = static_cast<const int32_t*>(S.d_rows.p);
     P.n_out_tiles = int(S.n_out_pad / tc::BM);
     P.n_cell_tiles = int((n + tc::BN - 1) / tc::BN);
     P.num_k_blocks = int(S.k_pad / tc::BK);
@@ -452,6 +455,24 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->k_pad = (S->k + kal - 1) / kal * kal;
     S->n_out = int64_t(S->n_phi) * S->n_phi;
     S->n_out_pad = (S->n_out + 127) / 128 * 128;
+    std::vector<int32_t> rows;
+    if (S->path == kPathTC) {
+      // upper-triangle cover by 8 (rows) x 4 (cols) blocks; lane l -> (8r + l/4, 4c + l%4)
+      const int n = S->n_phi;
+      for (int r = 0; 8 * r < n; ++r)
+        for (int c = 0; 4 * c < n; ++c) {
+          if (4 * c + 3 < 8 * r) continue;  // block entirely below the diagonal
+          for (int l = 0; l < 32; ++l) {
+            const int i = 8 * r + l / 4, j = 4 * c + l % 4;
+            rows.push_back(i < n && j < n ? (i | (j << 16)) : -1);
+          }
+        }
+      while (rows.size() % 128) rows.push_back(-1);
+      S->n_out_pad = int64_t(rows.size());
+      S->n_rows = int(rows.size());
+      S->d_rows.ensure(sizeof(int32_t) * rows.size());
+      CUDA_OK(cudaMemcpy(S->d_rows.p, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice));
+    }
     uint32_t fl = 0;
     std::vector<double> tab_up = tabulate(basis, S->rule, u_p, u_p, false, fl);
     std::vector<double> B = tabulate(basis, S->rule, 3, 3, form == 1, fl);
@@ -487,8 +508,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
     const double* dB = static_cast<const double*>(S->d_B.p);
     if (total) switch (S->w_type) {
-      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
+      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
+      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
       case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
       default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
     }

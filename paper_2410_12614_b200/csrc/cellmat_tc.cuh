@@ -15,6 +15,10 @@
 //               tcgen05.ld 32x32b.x32 -> registers -> global. TMEM lane =
 //               output entry, column = cell, so one warp store writes 32 consecutive
 //               entries (128 B) of one cell's row-major matrix: coalesced, no staging.
+// Symmetry: T is bitwise symmetric in (i, j) (products and the s<t pair sums commute), so
+// A_ij and A_ji are bitwise equal; the A operand's rows cover only 8x4 blocks of the
+// upper triangle (row table P.rows) and the epilogue writes each value to (i, j) and (j, i).
+// An 8x4 block gives one warp 8 rows x 16 B direct and 4 rows x 32 B mirrored stores.
 // Tiles are ordered cell-block-major so the W block of a cell block is reused from L2
 // by the CTAs that work on its output tiles at the same time.
 #pragma once
@@ -40,7 +44,9 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barrier
 
 struct Params {
   int64_t n_cells;
-  int n_out;          // n_phi^2
+  int n_out;          // rows of Tt actually used (valid output rows)
+  int n_phi;
+  const int32_t* rows;  // output-row table: (i | j << 16) or -1; A_ij = A_ji is written twice
   int n_out_tiles;
   int n_cell_tiles;
   int num_k_blocks;
@@ -236,37 +242,31 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int o = ot * BM + quarter * 32 + lane;
-      const bool o_ok = o < P.n_out;
+      const int32_t e = P.rows[o];
+      const bool o_ok = e >= 0;
+      const int ei = e & 0xffff, ej = e >> 16;
+      const int off_d = ei * P.n_phi + ej;                 // entry (i, j)
+      const int off_m = ej * P.n_phi + ei;                 // its mirror (j, i)
+      const bool mirror = o_ok && ei != ej;
       #pragma unroll 1
       for (int chunk = half * (BN / 64); chunk < (half + 1) * (BN / 64); ++chunk) {
         uint32_t r[32];
         tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
         const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
         if (o_ok) {
-          float* dst = P.out + cell0 * P.out_pitch + o;
+          float* base = P.out + cell0 * P.out_pitch;
           const int64_t left = P.n_cells - cell0;
-          if (left >= 32) {
-            #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+          #pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (left >= 32 || j < left) {
               float v;
               if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
               else v = __uint_as_float(r[j]);
               expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-              __stcs(dst, v);
-              dst += P.out_pitch;
+              __stcs(base + off_d, v);
+              if (mirror) __stcs(base + off_m, v);
             }
-          } else {
-            #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < left) {
-                float v;
-                if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
-                else v = __uint_as_float(r[j]);
-                expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-                __stcs(dst, v);
-              }
-              dst += P.out_pitch;
-            }
+            base += P.out_pitch;
           }
         }
       }

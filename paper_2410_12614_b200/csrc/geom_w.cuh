@@ -278,10 +278,12 @@ __global__ void __launch_bounds__(256, 3) scaled_weights_kernel(GeomWParams P,
 // Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
 //   T[(b,q), (i,j)] = round_us(B_s[i,q] B_t[j,q] (+ B_t[i,q] B_s[j,q] if s<t)).
 // transposed != 0 stores Tt[o][k] (K contiguous; the tcgen05 A operand), else T[k][o].
+// rows: optional output-row table (tcgen05 path): row o computes entry (i, j) =
+// (rows[o] & 0xffff, rows[o] >> 16), or nothing when rows[o] < 0; NULL means o = i*n_phi + j.
 template <typename T>
 __global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, int poisson, int us,
                                int64_t k_len, int64_t k_pad, int64_t n_out, int64_t n_out_pad,
-                               int transposed, void* out) {
+                               int transposed, void* out, const int32_t* rows = nullptr) {
   const int64_t total = k_pad * n_out_pad;
   for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += int64_t(gridDim.x) * blockDim.x) {
@@ -290,8 +292,15 @@ __global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, 
     else { k = idx / n_out_pad; o = idx % n_out_pad; }
     double val = 0.0;
     const int b = int(k / nq_pad), q = int(k % nq_pad);
-    if (k < k_len && o < n_out && q < n_q) {
-      int i = int(o / n_phi), j = int(o % n_phi);
+    int i = int(o / n_phi), j = int(o % n_phi);
+    bool valid = o < n_out;
+    if (rows) {
+      const int32_t e = rows[o];
+      valid = e >= 0;
+      i = e & 0xffff;
+      j = e >> 16;
+    }
+    if (k < k_len && valid && q < n_q) {
       int s = 0, t = 0;
       if (poisson) {
         const int ss[6] = {0, 0, 0, 1, 1, 2}, tt[6] = {0, 1, 2, 1, 2, 2};
