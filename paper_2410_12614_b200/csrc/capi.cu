@@ -456,8 +456,18 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->n_out = int64_t(S->n_phi) * S->n_phi;
     S->n_out_pad = (S->n_out + 127) / 128 * 128;
     std::vector<int32_t> rows;
-    if (S->path == kPathTC) {
-      // upper-triangle cover by 8 (rows) x 4 (cols) blocks; lane l -> (8r + l/4, 4c + l%4)
+    const char* sym_env = std::getenv("MPFEM_B200_SYMMETRIC");
+    const bool symmetric = sym_env && std::atoi(sym_env) != 0;
+    if (S->path == kPathTC && !symmetric) {
+      // full output, row-major (i, j): one warp store = 128 contiguous bytes of a cell
+      for (int i = 0; i < S->n_phi; ++i)
+        for (int j = 0; j < S->n_phi; ++j) rows.push_back(i | (j << 16));
+    }
+    if (S->path == kPathTC && symmetric) {
+      // Experimental: upper-triangle cover by 8 x 4 blocks (lane l -> (8r + l/4, 4c + l%4)),
+      // values written to (i, j) and (j, i). Fewer MMAs, but the register-resident epilogue
+      // then issues 16/32-byte pieces (12 lines per 64 values) and is LSU-bound: measured
+      // slower on B200 until the epilogue stages through shared memory.
       const int n = S->n_phi;
       for (int r = 0; 8 * r < n; ++r)
         for (int c = 0; 4 * c < n; ++c) {
@@ -467,6 +477,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
             rows.push_back(i < n && j < n ? (i | (j << 16)) : -1);
           }
         }
+    }
+    if (S->path == kPathTC) {
       while (rows.size() % 128) rows.push_back(-1);
       S->n_out_pad = int64_t(rows.size());
       S->n_rows = int(rows.size());

@@ -15,10 +15,11 @@
 //               tcgen05.ld 32x32b.x32 -> registers -> global. TMEM lane =
 //               output entry, column = cell, so one warp store writes 32 consecutive
 //               entries (128 B) of one cell's row-major matrix: coalesced, no staging.
-// Symmetry: T is bitwise symmetric in (i, j) (products and the s<t pair sums commute), so
-// A_ij and A_ji are bitwise equal; the A operand's rows cover only 8x4 blocks of the
-// upper triangle (row table P.rows) and the epilogue writes each value to (i, j) and (j, i).
-// An 8x4 block gives one warp 8 rows x 16 B direct and 4 rows x 32 B mirrored stores.
+// Output rows come from a table P.rows (entry (i, j) per TMEM lane; default row-major, so a
+// warp store is 128 contiguous bytes of one cell). T is bitwise symmetric in (i, j), so
+// A_ij == A_ji bitwise; an experimental table (MPFEM_B200_SYMMETRIC=1) covers only the
+// upper triangle and writes each value to (i, j) and (j, i) -- fewer MMAs, but its 16/32-byte
+// store pieces make the register-resident epilogue LSU-bound (slower).
 // Tiles are ordered cell-block-major so the W block of a cell block is reused from L2
 // by the CTAs that work on its output tiles at the same time.
 #pragma once
