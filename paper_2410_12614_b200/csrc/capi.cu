@@ -474,7 +474,7 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
           if (4 * c + 3 < 8 * r) continue;  // block entirely below the diagonal
           for (int l = 0; l < 32; ++l) {
             const int i = 8 * r + l / 4, j = 4 * c + l % 4;
-            rows.push_back(i < n && j < n ? (i | (j << 16)) : -1);
+            rows.push_back(i < n && j < n ? (i | (j << 16) | (i != j ? (1 << 30) : 0)) : -1);
           }
         }
     }

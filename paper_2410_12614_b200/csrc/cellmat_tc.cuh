@@ -47,7 +47,7 @@ struct Params {
   int64_t n_cells;
   int n_out;          // rows of Tt actually used (valid output rows)
   int n_phi;
-  const int32_t* rows;  // output-row table: (i | j << 16) or -1; A_ij = A_ji is written twice
+  const int32_t* rows;  // output-row table: i | j << 16 | mirror << 30, or -1 (padding)
   int n_out_tiles;
   int n_cell_tiles;
   int num_k_blocks;
@@ -245,10 +245,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int o = ot * BM + quarter * 32 + lane;
       const int32_t e = P.rows[o];
       const bool o_ok = e >= 0;
-      const int ei = e & 0xffff, ej = e >> 16;
+      const int ei = e & 0xffff, ej = (e >> 16) & 0x3fff;
       const int off_d = ei * P.n_phi + ej;                 // entry (i, j)
       const int off_m = ej * P.n_phi + ei;                 // its mirror (j, i)
-      const bool mirror = o_ok && ei != ej;
+      const bool mirror = o_ok && (e & (1 << 30));         // symmetric table only
       #pragma unroll 1
       for (int chunk = half * (BN / 64); chunk < (half + 1) * (BN / 64); ++chunk) {
         uint32_t r[32];

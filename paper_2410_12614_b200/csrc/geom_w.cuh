@@ -298,7 +298,7 @@ __global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, 
       const int32_t e = rows[o];
       valid = e >= 0;
       i = e & 0xffff;
-      j = e >> 16;
+      j = (e >> 16) & 0x3fff;
     }
     if (k < k_len && valid && q < n_q) {
       int s = 0, t = 0;
