@@ -255,19 +255,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
         const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
         if (o_ok) {
-          float* base = P.out + cell0 * P.out_pitch;
+          float* dst = P.out + cell0 * P.out_pitch + off_d;
           const int64_t left = P.n_cells - cell0;
-          #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (left >= 32 || j < left) {
+          if (left >= 32 && !mirror) {  // common case: full chunk, row-major table
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
               float v;
               if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
               else v = __uint_as_float(r[j]);
               expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-              __stcs(base + off_d, v);
-              if (mirror) __stcs(base + off_m, v);
+              __stcs(dst, v);
+              dst += P.out_pitch;
             }
-            base += P.out_pitch;
+          } else {
+            float* base = P.out + cell0 * P.out_pitch;
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j < left) {
+                float v;
+                if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
+                else v = __uint_as_float(r[j]);
+                expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+                __stcs(base + off_d, v);
+                if (mirror) __stcs(base + off_m, v);
+              }
+              base += P.out_pitch;
+            }
           }
         }
       }
