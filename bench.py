@@ -43,6 +43,25 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def profiled_traffic(kernel_prefix="cellmat_tc_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from
+    the committed `ncu --set full` capture summary (profiles/r*_ncu_summary.json), or None."""
+    import glob
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            for k in d.get("ncu_full", []):
+                if kernel_prefix in k.get("kernel", ""):
+                    rd = float(k["dram__bytes_read.sum"]) * 1e6  # ncu reports Mbyte
+                    wr = float(k["dram__bytes_write.sum"]) * 1e6
+                    best = {"bytes": rd + wr, "source": os.path.relpath(path, ROOT)}
+        except Exception:
+            continue
+    return best
+
+
 def nphi(p):
     return (p + 1) * (p + 2) * (p + 3) // 6
 
@@ -419,7 +438,10 @@ def main():
         "tflops_dense_equiv": N_CELLS * world * f_cell / (ms_per_step * 1e-3) / 1e12,
         "kernels_ms": {"geom_w": k1_ms, "cellmat_tc": k2_ms},
         "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": tc_peak,
-                     "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved_tflops / tc_peak,
+                     "traffic": (lambda t: t["bytes"] if t else None)(profiled_traffic()),
+                     "traffic_source": (lambda t: t["source"] if t else None)(profiled_traffic()),
+                     "algorithmic_bytes": N_CELLS * b_cell,
                      "kernel": "cellmat_tc_kernel",
                      "note": (f"achieved = dense-equivalent F_cell {f_cell:.0f} flop x {N_CELLS} cells / "
                               f"K2 duration; peak = {peak_src} bf16 burst; the kernel executes the "

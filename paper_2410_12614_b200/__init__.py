@@ -22,7 +22,8 @@ __all__ = [
     "bilinear_kernel", "mode_config", "lib", "LIB_PATH",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libmpfem_b200.so")
+LIB_PATH = os.environ.get("MPFEM_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libmpfem_b200.so")
 
 
 class Fmt(enum.IntEnum):  # softfloat.hpp:17

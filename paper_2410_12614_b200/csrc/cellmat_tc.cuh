@@ -32,15 +32,22 @@ namespace mpfem_b200 {
 namespace tc {
 
 constexpr int BM = 128;  // output entries per tile (MMA M, TMEM lanes)
-constexpr int BN = 256;  // cells per tile (MMA N, TMEM columns per accumulator)
+#ifndef MPFEM_TC_BN
+#define MPFEM_TC_BN 256
+#endif
+#ifndef MPFEM_TC_STAGES
+#define MPFEM_TC_STAGES 4
+#endif
+constexpr int BN = MPFEM_TC_BN;  // cells per tile (MMA N, TMEM columns per accumulator)
 constexpr int BK = 64;   // 16-bit elements per K block = one 128-byte swizzle row
-constexpr int STAGES = 4;
+constexpr int STAGES = MPFEM_TC_STAGES;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EPI_WARPS = 8;      // two warps per TMEM lane quarter, each half the columns
+constexpr int EPI_SPLIT = EPI_WARPS / 4;
 constexpr int THREADS = 128 + EPI_WARPS * 32;
-constexpr int TMEM_COLS = 512;
+constexpr int TMEM_COLS = 2 * BN >= 512 ? 512 : (2 * BN >= 256 ? 256 : 128);
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 struct Params {
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     // TMEM lane quarter = warp % 4 (hardware rule); the two warps of a quarter split the
     // accumulator's 256 columns (cells) in halves.
     const int quarter = warp & 3;
-    const int half = (warp - 4) >> 2;
+    const int half = (warp - 4) >> 2;  // which 1/EPI_SPLIT of the columns
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t expo_or = 0;
@@ -250,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int off_m = ej * P.n_phi + ei;                 // its mirror (j, i)
       const bool mirror = o_ok && (e & (1 << 30));         // symmetric table only
       #pragma unroll 1
-      for (int chunk = half * (BN / 64); chunk < (half + 1) * (BN / 64); ++chunk) {
+      for (int chunk = half * (BN / 32 / EPI_SPLIT); chunk < (half + 1) * (BN / 32 / EPI_SPLIT); ++chunk) {
         uint32_t r[32];
         tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
         const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
