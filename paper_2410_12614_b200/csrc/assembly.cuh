@@ -263,55 +263,14 @@ __device__ __forceinline__ void entry_sum(const TL* __restrict__ locals, int64_t
   values[e] = acc;
 }
 
-// All entries: each thread owns kSegEnt consecutive CSR entries, whose contributions are
-// one contiguous perm range; the gathers are issued together (memory-level parallelism),
-// then each entry is summed strictly in order.
-constexpr int kSegEnt = 4;
-constexpr int kSegBuf = 32;  // gathered values held in registers per thread
-
 template <typename TL, typename TV>
-__global__ void __launch_bounds__(256) assemble_seg_kernel(const TL* __restrict__ locals, int64_t per_cell,
+__global__ void assemble_seg_kernel(const TL* __restrict__ locals, int64_t per_cell,
                                     const int64_t* __restrict__ seg_ptr, const uint32_t* __restrict__ perm,
                                     int64_t nnz, int64_t cell_begin, int64_t cell_end, int init,
                                     TV* __restrict__ values) {
-  const int64_t kb = cell_begin * per_cell, ke = cell_end * per_cell;
-  const int64_t n_groups = (nnz + kSegEnt - 1) / kSegEnt;
-  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < n_groups;
-       g += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t e0 = g * kSegEnt;
-    const int ne = int(nnz - e0 < kSegEnt ? nnz - e0 : kSegEnt);
-    int64_t sp[kSegEnt + 1];
-    #pragma unroll
-    for (int x = 0; x <= kSegEnt; ++x) sp[x] = x <= ne ? seg_ptr[e0 + x] : 0;
-    const int64_t b = sp[0], total = sp[ne] - b;
-    if (total <= kSegBuf) {
-      TV buf[kSegBuf];
-      #pragma unroll
-      for (int t = 0; t < kSegBuf; ++t) {
-        buf[t] = TV(0);
-        if (t < total) {
-          const int64_t k = perm[b + t];
-          buf[t] = (k >= kb && k < ke) ? cast_value<TL, TV>(locals[k]) : TV(-0.0);
-        }
-      }
-      int t = 0;
-      #pragma unroll
-      for (int x = 0; x < kSegEnt; ++x) {
-        if (x < ne) {
-          TV acc = init ? TV(-0.0) : values[e0 + x];
-          const int len = int(sp[x + 1] - sp[x]);
-          #pragma unroll
-          for (int u = 0; u < kSegBuf; ++u)
-            if (u >= t && u < t + len) acc = acc + buf[u];  // -0.0 for skipped cells: exact no-op
-          t += len;
-          values[e0 + x] = acc;
-        }
-      }
-    } else {
-      for (int x = 0; x < ne; ++x)
-        entry_sum(locals, per_cell, seg_ptr, perm, e0 + x, cell_begin, cell_end, init, values);
-    }
-  }
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+       e += int64_t(gridDim.x) * blockDim.x)
+    entry_sum(locals, per_cell, seg_ptr, perm, e, cell_begin, cell_end, init, values);
 }
 
 // Same for a list of rows: one warp per row, lanes over the row's entries.

@@ -342,7 +342,7 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, 
 #undef MPFEM_SEG_ROWS
       } else {
         const int64_t nnz = read1(row_ptr + n_dofs, st);
-        const unsigned grid = grid_for((nnz + asmb::kSegEnt - 1) / asmb::kSegEnt);
+        const unsigned grid = grid_for(nnz);
 #define MPFEM_SEG(TL, TV) asmb::assemble_seg_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, static_cast<TV*>(values))
         if (locals_fmt == 2 && fmt == 2) MPFEM_SEG(float, float);
         else if (locals_fmt == 2) MPFEM_SEG(float, double);
