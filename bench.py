@@ -244,6 +244,14 @@ def run_sweep(mp, torch, dev):
     return res
 
 
+def max_over_ranks(torch, value, dev):
+    import torch.distributed as dist
+    on_cpu = dist.get_backend() == "gloo"
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if on_cpu else dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
     """BASELINE config 4: 96^3 hexes x 6 tets, Poisson with c(x), mixed (bf16 storage)
     cell kernels, deterministic CSR assembly in fp32 and fp64; z-slabs over the ranks with
@@ -274,9 +282,7 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         if world > 1:
-            t = torch.tensor([ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = max_over_ranks(torch, ms, dev)
         return ms, r
 
     for p in degrees:
@@ -334,11 +340,12 @@ def main():
     import torch
     import paper_2410_12614_b200 as mp
 
+    backend = os.environ.get("MPFEM_DIST_BACKEND", "nccl")  # gloo: test ranks sharing a GPU
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local)
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dist.init_process_group(backend)
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     hbm, tc_peak, tc_sus, peak_src = peaks()
 
@@ -399,9 +406,7 @@ def main():
     k1_ms, k2_ms = float(np.median(k1)), float(np.median(k2))
 
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(torch, total_ms, dev)
     ms_per_step = total_ms / args.steps
     value = world * N_CELLS / (ms_per_step * 1e-3)
 
@@ -420,9 +425,7 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(torch, e2e_ms, dev)
     e2e_value = world * N_CELLS / (e2e_ms * 1e-3)
 
     f_cell, b_cell = work_per_cell(P_DEG, 1, 4)

@@ -103,16 +103,22 @@ def assemble_slab(backend, local, dm, pat, plan: SlabPlan, fmt: int, group=None)
                                 accumulate=False, values=values)
     send_buf = values[plan.send_index].contiguous()
     recv_buf = torch.empty(int(plan.recv_index.numel()), dtype=dtype, device=local.device)
-    # 2. the single neighbour exchange (r -> r+1), batched
+    # 2. the single neighbour exchange (r -> r+1), batched (NCCL: device buffers over
+    #    NVLink; gloo: staged through host memory)
     if plan.world > 1:
+        host = dist.get_backend(group) == "gloo" and send_buf.is_cuda
+        sb = send_buf.cpu() if host else send_buf
+        rb = torch.empty(recv_buf.shape, dtype=dtype) if host else recv_buf
         ops = []
         if plan.rank + 1 < plan.world:
-            ops.append(dist.P2POp(dist.isend, send_buf, plan.rank + 1, group))
+            ops.append(dist.P2POp(dist.isend, sb, plan.rank + 1, group))
         if plan.rank > 0:
-            ops.append(dist.P2POp(dist.irecv, recv_buf, plan.rank - 1, group))
+            ops.append(dist.P2POp(dist.irecv, rb, plan.rank - 1, group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if host:
+            recv_buf.copy_(rb)
     # 3. continue the received sums, start the fresh rows
     if plan.recv_rows.numel():
         values[plan.recv_index] = recv_buf
