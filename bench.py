@@ -297,11 +297,12 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
                "dofmap_ms": t_dof, "csr_pattern_ms": t_pat, "cell_kernels_ms": t_cell}
         for fmt in (2, 3):
             sv = 4 if fmt == 2 else 8
+            vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
             if world > 1:
-                t_asm, _ = timed(lambda: D.assemble_slab(Backend, local, dm, pat, plan, fmt))
+                t_asm, _ = timed(lambda: D.assemble_slab(Backend, local, dm, pat, plan, fmt, values=vals))
             else:
-                vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
                 t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
+            del vals
             nb = (ce - cb) * (nphi(p) ** 2 * 4 + 4 * nphi(p)) + pat.nnz / world * (sv + 4) + 8 * (dm.n_dofs + 1) / world
             key = "fp32" if fmt == 2 else "fp64"
             res[f"assemble_{key}_ms"] = t_asm

@@ -88,14 +88,15 @@ def check_adjacent(dm, pat, ranges) -> None:
         raise ValueError("slabs thinner than one cell layer: a row spans more than two ranks")
 
 
-def assemble_slab(backend, local, dm, pat, plan: SlabPlan, fmt: int, group=None):
+def assemble_slab(backend, local, dm, pat, plan: SlabPlan, fmt: int, group=None, values=None):
     """Deterministic assembly of this rank's owned rows. `local` holds the local matrices of
-    cells [plan.cell_begin, plan.cell_end). Returns the full-length values tensor, valid on
-    plan.owned_rows' segments."""
+    cells [plan.cell_begin, plan.cell_end). Returns the full-length values tensor (pass
+    `values` to reuse one), valid on plan.owned_rows' segments."""
     import torch
     import torch.distributed as dist
     dtype = torch.float32 if fmt == 2 else torch.float64
-    values = torch.zeros(pat.nnz, dtype=dtype, device=local.device)
+    if values is None:
+        values = torch.empty(pat.nnz, dtype=dtype, device=local.device)
     cb, ce = plan.cell_begin, plan.cell_end
     # 1. prefix partial sums of the rows the next rank finishes (our cells only)
     if plan.send_rows.numel():
