@@ -27,8 +27,8 @@ using namespace mpfem_b200;
 namespace mpfem_b200 {
 // K1 / fused-kernel instantiations live in launch_geom.cu / launch_fused.cu (separate
 // translation units, compiled in parallel).
-void launch_geom_typed(int w_type, int ug, int us, unsigned gc, unsigned gw, cudaStream_t st,
-                       const GeomWParams& P, CellGeo* geo);
+void launch_geom_typed(int w_type, int ug, int us, unsigned grid, cudaStream_t st,
+                       const GeomWParams& P);
 void launch_fused_dispatch(int key, int us, unsigned grid, cudaStream_t st, const FusedParams& F);
 }  // namespace mpfem_b200
 
@@ -142,7 +142,7 @@ struct mpfem_b200_setup_s {
   Rule rule;
   DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
   int n_rows = 0;  // tcgen05 path: rows of Tt (upper-triangle 8x4 blocks, padded to 128)
-  DevBuf d_W, d_flags, d_error, d_geo;
+  DevBuf d_W, d_flags, d_error;
   // host-API staging
   DevBuf h_verts, h_cells, h_coef, h_out;
   int last_launches = 0;
@@ -241,16 +241,13 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.k_pad = k_pad;
   P.div_nq = FastDiv::make(uint32_t(S.nq_pad / kQPT));
   P.nq_pad = S.nq_pad;
-  if (n * int64_t(S.n_q) >= (int64_t(1) << 31))
-    throw Error(MPFEM_B200_CONFIG_ERROR, "n_cells * n_q must be < 2^31 per call (split the batch)");
   P.w_type = w_type;
   P.W = W;
   P.flags = static_cast<uint32_t*>(S.d_flags.p);
   P.error = static_cast<int*>(S.d_error.p);
-  S.d_geo.ensure(sizeof(CellGeo) * size_t(n));
-  const unsigned gc = unsigned((n + 255) / 256);
-  const unsigned gw = unsigned(std::min<int64_t>((n * (S.nq_pad / kQPT) + 255) / 256, int64_t(device_sm_count()) * 64));
-  launch_geom_typed(w_type, S.ug, S.us, gc, gw, st, P, static_cast<CellGeo*>(S.d_geo.p));
+  const int64_t tiles = (n + kTileCells - 1) / kTileCells;
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * 3));
+  launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -436,7 +433,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     const double* coefc = coef ? coef + c0 * coef_stride : nullptr;
     S.mark(st);
     launch_geom(S, vc, cc, m, coef_kind, coefc, coef_stride, Wc, S.k_pad, S.w_type, st);
-    S.last_launches += 2;
+    S.last_launches += 1;
     S.mark(st);
     cudaStream_t gs = st;
     if (n_chunks > 1) {

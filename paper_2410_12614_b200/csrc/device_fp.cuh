@@ -177,9 +177,153 @@ __device__ __forceinline__ bool tet_geometry_f32(const double v[4][3], bool pois
                                                  uint32_t& fl);
 
 template <int F>
+__device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poisson, TetGeometry& out,
+                                                     uint32_t& fl);
+__device__ __forceinline__ bool tet_geometry_f64_fast(const double v[4][3], bool poisson, TetGeometry& out,
+                                                      uint32_t& hmax);
+
+// u_g = fp64 runs the op sequence with plain IEEE binary64 ops (bitwise the same values:
+// every emulated op at fp64 is the hardware op) and only tracks the largest |high word| of
+// the inputs and every intermediate; FP events at fp64 need a non-finite value somewhere
+// (overflow, invalid) or a zero pivot, and in that rare case the flagged sequence reruns
+// to produce the reference's flags exactly.
+template <int F>
 __device__ __forceinline__ bool tet_geometry(const double v[4][3], bool poisson, TetGeometry& out,
                                              uint32_t& fl) {
-  if constexpr (F == kFP32) return tet_geometry_f32(v, poisson, out, fl);
+  if constexpr (F == kFP32) {
+    return tet_geometry_f32(v, poisson, out, fl);
+  } else if constexpr (F == kFP64) {
+    uint32_t hmax = 0;
+    const bool ok = tet_geometry_f64_fast(v, poisson, out, hmax);
+    if (ok && hmax < 0x7ff00000u) return true;
+    return tet_geometry_flagged<F>(v, poisson, out, fl);
+  } else {
+    return tet_geometry_flagged<F>(v, poisson, out, fl);
+  }
+}
+
+__device__ __forceinline__ void track_hi(double r, uint32_t& hmax) {
+  hmax = max(hmax, uint32_t(__double2hiint(r)) & 0x7fffffffu);
+}
+
+__device__ __forceinline__ bool tet_geometry_f64_fast(const double v[4][3], bool poisson, TetGeometry& out,
+                                                      uint32_t& hmax) {
+  double jac[3][3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+  #pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double x = v[k][i];
+      track_hi(x, hmax);
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        const double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
+        jac[i][s] = __dadd_rn(jac[i][s], __dmul_rn(x, g));
+        track_hi(jac[i][s], hmax);
+      }
+    }
+  }
+  double lu[3][3];
+  int perm[3] = {0, 1, 2};
+  int sign = 1;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) lu[i][s] = jac[i][s];
+  #pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    int pivot = col;
+    double best = fabs(lu[col][col]);
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const double a = fabs(lu[r][col]);
+      if (a > best) { best = a; pivot = r; }
+    }
+    double pv = lu[col][col];
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (pivot == r) pv = lu[r][col];
+    if (pv == 0.0) return false;
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      if (pivot == r) {
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double t = lu[r][c];
+          lu[r][c] = lu[col][c];
+          lu[col][c] = t;
+        }
+        int t = perm[r];
+        perm[r] = perm[col];
+        perm[col] = t;
+        sign = -sign;
+      }
+    }
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const double m = __ddiv_rn(lu[r][col], lu[col][col]);
+      track_hi(m, hmax);
+      lu[r][col] = m;
+      #pragma unroll
+      for (int c = col + 1; c < 3; ++c) {
+        lu[r][c] = __dsub_rn(lu[r][c], __dmul_rn(m, lu[col][c]));
+        track_hi(lu[r][c], hmax);
+      }
+    }
+  }
+  double det = (double)sign;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) det = __dmul_rn(det, lu[i][i]);
+  track_hi(det, hmax);
+  out.det = det;
+  out.abs_det = fabs(det);
+  if (!poisson) {
+    out.g[0] = out.abs_det;
+    return true;
+  }
+  double inv[3][3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double y[3];
+    #pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      double s = perm[r] == k ? 1.0 : 0.0;
+      #pragma unroll
+      for (int c = 0; c < r; ++c) s = __dsub_rn(s, __dmul_rn(lu[r][c], y[c]));
+      track_hi(s, hmax);
+      y[r] = s;
+    }
+    #pragma unroll
+    for (int r = 2; r >= 0; --r) {
+      double s = y[r];
+      #pragma unroll
+      for (int c = r + 1; c < 3; ++c) s = __dsub_rn(s, __dmul_rn(lu[r][c], inv[c][k]));
+      inv[r][k] = __ddiv_rn(s, lu[r][r]);
+      track_hi(inv[r][k], hmax);
+    }
+  }
+  int idx = 0;
+  #pragma unroll
+  for (int s = 0; s < 3; ++s)
+    #pragma unroll
+    for (int t = s; t < 3; ++t) {
+      double dot = 0.0;
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) dot = __dadd_rn(dot, __dmul_rn(inv[s][k], inv[t][k]));
+      out.g[idx] = __dmul_rn(out.abs_det, dot);
+      track_hi(out.g[idx], hmax);
+      ++idx;
+    }
+  return true;
+}
+
+template <int F>
+__device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poisson, TetGeometry& out,
+                                                     uint32_t& fl) {
   // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
   double jac[3][3];
   #pragma unroll
@@ -443,26 +587,33 @@ __device__ __forceinline__ double sinpi_poly(double r) {  // sin(pi r), |r| <= 0
   for (int k = 11; k >= 0; --k) p = fma(p, s, kSinPiC[k]);
   return r * p;
 }
-__device__ __forceinline__ double flip_if_odd(double v, double n) {
-  const long long odd = static_cast<long long>(n) & 1ll;
-  return __longlong_as_double(__double_as_longlong(v) ^ (odd << 63));
+// Rounding to an integer without the fp64 conversion pipe (FRND / F2I run at a fraction
+// of DFMA throughput): t = a + 1.5*2^52 rounds a to the nearest integer (ties to even) in
+// the DADD itself for |a| < 2^51; t - 1.5*2^52 is that integer exactly and the low word of
+// t holds it in two's complement.
+constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
+__device__ __forceinline__ double flip_if_odd(double v, uint32_t n_lo) {
+  return __hiloint2double(__double2hiint(v) ^ int((n_lo & 1u) << 31), __double2loint(v));
 }
 __device__ __forceinline__ double fast_sinpi(double a) {
-  const double n = rint(a);
-  return flip_if_odd(sinpi_poly(a - n), n);
+  const double t = __dadd_rn(a, kRoundMagic);
+  const double n = __dsub_rn(t, kRoundMagic);
+  return flip_if_odd(sinpi_poly(__dsub_rn(a, n)), uint32_t(__double2loint(t)));
 }
 __device__ __forceinline__ double fast_cospi(double a) {  // cos(pi r) = sin(pi (1/2 - |r|))
-  const double n = rint(a);
-  return flip_if_odd(sinpi_poly(0.5 - fabs(a - n)), n);
+  const double t = __dadd_rn(a, kRoundMagic);
+  const double n = __dsub_rn(t, kRoundMagic);
+  return flip_if_odd(sinpi_poly(__dsub_rn(0.5, fabs(__dsub_rn(a, n)))), uint32_t(__double2loint(t)));
 }
 __device__ __forceinline__ double fast_exp(double z) {
-  const double n = rint(z * 1.4426950408889634);
+  const double t = __dadd_rn(__dmul_rn(z, 1.4426950408889634), kRoundMagic);
+  const double n = __dsub_rn(t, kRoundMagic);
   double r = fma(-n, 6.93147180369123816490e-01, z);  // ln2 hi: n * hi is exact
   r = fma(-n, 1.90821492927058770002e-10, r);
   double p = kExpC[14];
   #pragma unroll
   for (int k = 13; k >= 0; --k) p = fma(p, r, kExpC[k]);
-  return p * __longlong_as_double((static_cast<long long>(n) + 1023ll) << 52);
+  return p * __hiloint2double((__double2loint(t) + 1023) << 20, 0);
 }
 
 // fp32 counterparts for u_g = fp32 (the coefficient is rounded to fp32 anyway): same

@@ -1,7 +1,7 @@
 // geom_w.cuh -- K1: per-cell geometry + coefficient + scaled-weight pass.
 //
-// Geometry once per cell (one thread), then one warp per cell whose lanes stride over
-// quadrature points and write the cell's row of the GEMM operand W:
+// Geometry once per cell (one lane of a tile's first warp), then all threads of the CTA
+// expand the tile's (cell, quadrature point) pairs into the rows of the GEMM operand W:
 //   W[c, b*n_q + q] = round_us(round_ug(round_ug(omega_q * G_b) * zhat_q))
 // which is build_C (kernels.cpp:177-197) with the (s,t) pairs packed to the upper
 // triangle b = (s<=t): (0,0),(0,1),(0,2),(1,1),(1,2),(2,2) (C is symmetric bitwise, so
@@ -128,11 +128,16 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
   static_cast<double*>(W)[idx] = v;
 }
 
-// K1 runs as two launches:
-//  (a) cell_geometry_kernel: one thread per cell, the reference's LU/inverse/tensor
-//      sequence at u_g (geometry.cpp:12-118) -> CellGeo (G, origin, edges) in a scratch array;
-//  (b) scaled_weights_kernel: one thread per (cell, q): coefficient z_q and the cell's
-//      W entries at q for every (s<=t) block.
+// K1 is one launch, one CTA per tile of kTileCells cells (grid-stride over tiles):
+//  phase 1: warp 0 runs the reference's LU/inverse/tensor sequence at u_g
+//           (geometry.cpp:12-118) for the tile's cells, one lane per cell -> shared memory;
+//  phase 2: all threads expand (cell, group of kQPT = 8 consecutive quadrature points)
+//           items: coefficient z_q and the W entries of every (s<=t) block at those points.
+// The rule (weights rounded to u_g, reference points) is staged in shared memory once per
+// CTA, permuted to [j][group] so that the lanes of a warp (consecutive groups, same j)
+// read consecutive words. Each thread writes each block of its 8 points with one 16-byte
+// store (W rows use blocks of nq_pad = round_up(n_q, 8); entries q >= n_q are zero, as are
+// the matching rows of T).
 // UG / US are compile-time, so the emulated rounding folds to the plain op for fp64 and a
 // single conversion for fp32.
 struct __align__(16) CellGeo {
@@ -141,135 +146,155 @@ struct __align__(16) CellGeo {
   double e[9];  // e[s*3 + i] = v_{s+1}[i] - v0[i]
 };
 
-template <int UG>
-__global__ void __launch_bounds__(256) cell_geometry_kernel(GeomWParams P, CellGeo* __restrict__ geo) {
-  const int64_t cell = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint32_t fl = 0;
-  if (cell < P.n_cells) {
-    double v[4][3];
-    if (P.cells) {
-      #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t vid = P.cells[cell * 4 + k];
-        #pragma unroll
-        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
-      }
-    } else {
-      #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        #pragma unroll
-        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
-    }
-    TetGeometry g;
-    if (!tet_geometry<UG>(v, P.poisson != 0, g, fl)) {
-      atomicExch(P.error, 3);
-      #pragma unroll
-      for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
-    }
-    CellGeo& o = geo[cell];
-    #pragma unroll
-    for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
-    #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      o.v0[a] = v[0][a];
-      #pragma unroll
-      for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = __dsub_rn(v[s2 + 1][a], v[0][a]);
-    }
-  }
-  publish_flags(P.flags, fl);
-}
-
-// One thread per (cell, group of kQPT = 8 consecutive quadrature points). The W row is
-// laid out in blocks of nq_pad = round_up(n_q, 8) entries (entries q >= n_q are zero, as
-// are the matching rows of T), so each thread writes each block with one 16-byte store
-// and the per-cell state is loaded once per 8 points.
 constexpr int kQPT = 8;
+constexpr int kTileCells = 32;
+constexpr int kGeomThreads = 256;
 
 template <typename T>
 struct Pack8 {
   T v[8];
 };
 
+template <int UG>
+__device__ __forceinline__ void cell_geometry(const GeomWParams& P, int64_t cell, CellGeo& o,
+                                              uint32_t& fl) {
+  double v[4][3];
+  if (P.cells) {
+    #pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t vid = P.cells[cell * 4 + k];
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[vid * 3 + a];
+    }
+  } else {
+    #pragma unroll
+    for (int k = 0; k < 4; ++k)
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) v[k][a] = P.verts[cell * 12 + k * 3 + a];
+  }
+  TetGeometry g;
+  if (!tet_geometry<UG>(v, P.poisson != 0, g, fl)) {
+    atomicExch(P.error, 3);
+    #pragma unroll
+    for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+  }
+  #pragma unroll
+  for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
+  #pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    o.v0[a] = v[0][a];
+    #pragma unroll
+    for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = __dsub_rn(v[s2 + 1][a], v[0][a]);
+  }
+}
+
+// dynamic shared memory of geom_w_kernel: weights and the three point coordinates,
+// each nq_pad doubles in [j][group] order
+__host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad) { return size_t(4) * nq_pad * sizeof(double); }
+
 template <typename T, int UG, int US, int COEF>
-__global__ void __launch_bounds__(256, 3) scaled_weights_kernel(GeomWParams P,
-                                                                const CellGeo* __restrict__ geo) {
+__global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) {
+  extern __shared__ double s_rule[];
+  __shared__ CellGeo s_geo[kTileCells];
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
-  const int64_t total = P.n_cells * ngroups;
   const int nb = P.poisson ? 6 : 1;
+  double* sW = s_rule;
+  double* sX = s_rule + nqp;  // sX[a * nqp + perm(q)]
+  for (int q = threadIdx.x; q < nqp; q += blockDim.x) {
+    const int pq = (q % kQPT) * ngroups + q / kQPT;
+    const bool ok = q < nq;
+    sW[pq] = ok ? P.rule_w[q] : 0.0;
+    #pragma unroll
+    for (int a = 0; a < 3; ++a) sX[a * nqp + pq] = ok ? P.rule_x[3 * q + a] : 0.0;
+  }
   uint32_t fl = 0;
   StoreFlags sf;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t cell32 = P.div_nq.div(uint32_t(idx));
-    const int64_t cell = cell32;
-    const int q0 = int(uint32_t(idx) - cell32 * uint32_t(ngroups)) * kQPT;
-    CellGeo cg;  // 9 x 16-byte loads, once per 8 points
-    {
-      const double2* src = reinterpret_cast<const double2*>(geo + cell);
-      double2* dst = reinterpret_cast<double2*>(&cg);
+  const int64_t n_tiles = (P.n_cells + kTileCells - 1) / kTileCells;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t c0 = tile * kTileCells;
+    const int64_t left = P.n_cells - c0;
+    const int nc = left < kTileCells ? int(left) : kTileCells;
+    __syncthreads();  // previous tile's readers of s_geo are done (and s_rule is staged)
+    if (threadIdx.x < nc) cell_geometry<UG>(P, c0 + threadIdx.x, s_geo[threadIdx.x], fl);
+    __syncthreads();
+    const uint32_t items = uint32_t(nc * ngroups);
+    for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+      const uint32_t cl = P.div_nq.div(it);
+      const int grp = int(it - cl * uint32_t(ngroups));
+      const int q0 = grp * kQPT;
+      const int64_t cell = c0 + cl;
+      const CellGeo& cg = s_geo[cl];
+      const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
+      double zq[kQPT], om[kQPT];
       #pragma unroll
-      for (int k = 0; k < 9; ++k) dst[k] = __ldg(src + k);
-    }
-    const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
-    double zq[kQPT], om[kQPT];
-    #pragma unroll
-    for (int j = 0; j < kQPT; ++j) {
-      const int q = q0 + j;
-      zq[j] = 1.0;
-      om[j] = 0.0;  // padding points (q >= n_q) produce exact zeros
-      if (q < nq) {
-        om[j] = P.rule_w[q];  // already rounded to u_g on the host
-        const double* xi = P.rule_x + 3 * q;
-        if constexpr (COEF == 1 && UG == kFP32) {
-          zq[j] = double(coef_sincosexp_f(cg.v0, cg.e, xi));
-        } else if constexpr (COEF == 1) {
-          zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
-        } else if constexpr (COEF == 2) {
-          zq[j] = droundT<UG>(coef_exp10_affine(coef, xi), fl);
-        } else if constexpr (COEF == 3) {
-          double acc = 0.0;
-          for (int k = 0; k < P.n_phi; ++k)
-            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
-          zq[j] = droundT<UG>(acc, fl);
-        }
-      }
-    }
-    constexpr bool have_z = COEF != 0;
-    T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
-    // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192)
-    #pragma unroll
-    for (int b = 0; b < 6; ++b) {
-      if (b < nb) {
-        Pack8<T> pk;
-        #pragma unroll
-        for (int j = 0; j < kQPT; ++j) {
-          if constexpr (UG == kFP32) {
-            float val = __fmul_rn(float(om[j]), float(cg.g[b]));  // fp32 values: exact-then-round
-            if (have_z) val = __fmul_rn(val, float(zq[j]));
-            pk.v[j] = to_storage<T, US>(val, sf);
-          } else if constexpr (UG == kFP64) {
-            double val = __dmul_rn(om[j], cg.g[b]);
-            if (have_z) val = __dmul_rn(val, zq[j]);
-            pk.v[j] = to_storage<T, US>(val, sf);
+      for (int j = 0; j < kQPT; ++j) {
+        const int pq = j * ngroups + grp;
+        om[j] = sW[pq];
+        zq[j] = 1.0;
+        if constexpr (COEF != 0) {
+          const double xi[3] = {sX[pq], sX[nqp + pq], sX[2 * nqp + pq]};
+          if constexpr (COEF == 1 && UG == kFP32) {
+            zq[j] = double(coef_sincosexp_f(cg.v0, cg.e, xi));
+          } else if constexpr (COEF == 1) {
+            zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
+          } else if constexpr (COEF == 2) {
+            zq[j] = droundT<UG>(coef_exp10_affine(coef, xi), fl);
           } else {
-            double val = droundT<UG>(__dmul_rn(om[j], cg.g[b]), fl);
-            if (have_z) val = droundT<UG>(__dmul_rn(val, zq[j]), fl);
-            pk.v[j] = to_storage<T, US>(val, sf);
+            const int q = q0 + j;
+            if (q < nq) {
+              double acc = 0.0;
+              for (int k = 0; k < P.n_phi; ++k)
+                acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[int64_t(k) * nq + q], P.up, fl), P.up, fl);
+              zq[j] = droundT<UG>(acc, fl);
+            }
           }
         }
-        // one 16-byte store per block for 16-bit storage (2 / 4 for fp32 / fp64)
-        const uint4* srcv = reinterpret_cast<const uint4*>(&pk);
-        uint4* dstv = reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp);
-        #pragma unroll
-        for (int k = 0; k < int(sizeof(Pack8<T>) / 16); ++k) dstv[k] = srcv[k];
       }
-    }
-    // tail K..K_pad of the row: zeros (the group that owns the last block's start writes it)
-    if (q0 == 0) {
-      T* tail = static_cast<T*>(P.W) + cell * P.k_pad;
-      for (int64_t k = int64_t(nb) * nqp; k < P.k_pad; ++k) tail[k] = T(0.0f);
+      constexpr bool have_z = COEF != 0;
+      T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
+      // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192).
+      // Points q >= n_q (only in a cell's last group) are exact zeros whatever G is.
+      bool pad[kQPT];
+      #pragma unroll
+      for (int j = 0; j < kQPT; ++j) pad[j] = q0 + j >= nq;
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        if (b < nb) {
+          const double gb = cg.g[b];
+          Pack8<T> pk;
+          #pragma unroll
+          for (int j = 0; j < kQPT; ++j) {
+            if constexpr (UG == kFP32) {
+              float val = __fmul_rn(float(om[j]), float(gb));  // fp32 values: exact-then-round
+              if (have_z) val = __fmul_rn(val, float(zq[j]));
+              if (pad[j]) val = 0.0f;
+              pk.v[j] = to_storage<T, US>(val, sf);
+            } else if constexpr (UG == kFP64) {
+              double val = __dmul_rn(om[j], gb);
+              if (have_z) val = __dmul_rn(val, zq[j]);
+              if (pad[j]) val = 0.0;
+              pk.v[j] = to_storage<T, US>(val, sf);
+            } else {
+              double val = droundT<UG>(__dmul_rn(om[j], gb), fl);
+              if (have_z) val = droundT<UG>(__dmul_rn(val, zq[j]), fl);
+              if (pad[j]) val = 0.0;
+              pk.v[j] = to_storage<T, US>(val, sf);
+            }
+          }
+          // one 16-byte store per block for 16-bit storage (2 / 4 for fp32 / fp64)
+          const uint4* srcv = reinterpret_cast<const uint4*>(&pk);
+          uint4* dstv = reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp);
+          #pragma unroll
+          for (int k = 0; k < int(sizeof(Pack8<T>) / 16); ++k) dstv[k] = srcv[k];
+        }
+      }
+      // tail K..K_pad of the row: zeros (the group that owns the last block's start writes it)
+      if (q0 == 0) {
+        T* tail = static_cast<T*>(P.W) + cell * P.k_pad;
+        for (int64_t k = int64_t(nb) * nqp; k < P.k_pad; ++k) tail[k] = T(0.0f);
+      }
     }
   }
   publish_flags(P.flags, fl | store_flags_bits(sf));

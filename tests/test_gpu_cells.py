@@ -138,6 +138,31 @@ def test_cell_matrices_within_bound(oracle, tets, mode, form):
                 assert d_same <= 2 * S * b[0], (p, kind, c, d_same, b[0])
 
 
+@pytest.mark.parametrize("mode", ["fp64", "mixed"])
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_extreme_geometry_fp_events_match_build_C(oracle, tets, mode, form):
+    """Cells whose fp64 geometry overflows (1e160 coordinates), underflows |det| to zero
+    while inv(J) overflows (1e-160: |det| * inf -> NaN), or carries a NaN vertex: the
+    fast binary64 geometry must hand these to the flagged sequence, so W and the FP-event
+    flags equal build_C's (kernels.cpp:177-197, geometry.cpp:12-118) bit for bit."""
+    cfg = kconfig(mode, form, geometry_fp64=True)
+    s = mp.make_setup(2, cfg)
+    nan_cell = tets[1].copy()
+    nan_cell[2, 1] = np.nan
+    cases = [tets[0] * 1e160, tets[2] * 1e-160, nan_cell, tets[3] * 1e150, tets[4]]
+    for i, cell in enumerate(cases):
+        w, fl = s.scaled_weights(dev(cell[None]), None, COEF_ONE)
+        ref, rfl = oracle.build_C(2, form, cfg_tuple(cfg), cell, COEF_ONE)
+        nd = 3 if form == POISSON else 1
+        blocks = PACK if form == POISSON else [(0, 0)]
+        ref = ref.reshape(nd, nd, nq(2))
+        want = np.concatenate([ref[a, b] for a, b in blocks])
+        got = w.cpu().numpy().reshape(len(blocks), -1)[:, :nq(2)].reshape(-1)
+        same = (got.view(np.uint64) == want.view(np.uint64)) | (np.isnan(got) & np.isnan(want))
+        assert np.all(same), (i, got[:4], want[:4])
+        assert fl == rfl, (i, hex(fl), hex(rfl))
+
+
 @pytest.mark.parametrize("p", [5, 6, 7, 8])
 @pytest.mark.parametrize("form", [MASS, POISSON])
 def test_high_degree_mixed_and_fp64(oracle, tets, p, form):
