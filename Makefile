@@ -28,7 +28,15 @@ $(LIB): $(OBJS)
 oracle:
 	$(MAKE) -s -C oracle all
 
+# Diagnostic variant (not shipped): K2 epilogue without global stores, to separate the
+# operand feed from the output write path. Load with MPFEM_B200_LIB=<path>.
+DIAG_LIB := $(PKG)/lib/diag/libmpfem_b200_nostore.so
+diag: $(OBJS)
+	@mkdir -p $(PKG)/lib/diag
+	$(NVCC) $(NVFLAGS) -DMPFEM_TC2_NOSTORE -c -o $(PKG)/lib/diag/capi.o $(PKG)/csrc/capi.cu 2> /dev/null
+	$(NVCC) $(ARCH) -shared -o $(DIAG_LIB) $(PKG)/lib/diag/capi.o $(filter-out $(OBJDIR)/capi.o,$(OBJS))
+
 clean:
 	rm -rf $(LIB) $(OBJDIR)
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean diag

@@ -150,8 +150,47 @@ __global__ void dof_count_kernel(const int32_t* __restrict__ cell_dofs, int64_t 
 }
 
 // ---------------------------------------------------------------- CSR pattern
-// One warp per row; shared-memory buffer of `cap` ints per warp. Pass 0 writes the unique
-// count of row r to row_nnz[r]; pass 1 writes the sorted unique columns at row_ptr[r].
+// One warp per row r. The row's candidate columns are the dofs of its incident cells
+// (inc lists, ascending cell); duplicates are removed in a shared-memory open-addressing
+// table sized to the row (H = next_pow2(2 * candidates)), so the count pass never sorts
+// and the fill pass sorts only the row's unique columns (~50-70 at P3) instead of its
+// candidate list (up to multiplicity x n_loc, 480 at P3).
+__device__ __forceinline__ uint32_t next_pow2_u32(uint32_t v) {
+  return v <= 1u ? 1u : 1u << (32 - __clz(v - 1u));
+}
+
+__device__ __forceinline__ int hash_insert(int32_t* table, uint32_t mask, int32_t v) {
+  uint32_t h = (uint32_t(v) * 2654435761u) & mask;
+  while (true) {
+    const int32_t old = atomicCAS(&table[h], -1, v);
+    if (old == -1) return 1;
+    if (old == v) return 0;
+    h = (h + 1u) & mask;
+  }
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Inserts the row's candidates; returns the number of unique columns (all lanes).
+__device__ __forceinline__ int row_dedup(const int32_t* __restrict__ cell_dofs, int n_loc,
+                                         const int64_t* __restrict__ inc, int64_t b, int64_t m,
+                                         int32_t* table, uint32_t H) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t i = lane; i < H; i += 32) table[i] = -1;
+  __syncwarp();
+  int cnt = 0;
+  for (int64_t k = 0; k < m; ++k) {
+    const int64_t cell = inc[b + k] / n_loc;
+    for (int j = lane; j < n_loc; j += 32) cnt += hash_insert(table, H - 1u, cell_dofs[cell * n_loc + j]);
+  }
+  __syncwarp();
+  return warp_sum_i(cnt);
+}
+
 __device__ __forceinline__ void warp_bitonic_sort(int32_t* buf, int cap) {
   const int lane = threadIdx.x & 31;
   for (int size = 2; size <= cap; size <<= 1) {
@@ -171,40 +210,120 @@ __device__ __forceinline__ void warp_bitonic_sort(int32_t* buf, int cap) {
   }
 }
 
+// pass 0: row_nnz[r] = unique count. pass 1: sorted unique columns at col_idx[row_ptr[r]].
+// Shared memory per warp: hcap ints (table) + hcap / 2 ints (unique list).
 __global__ void csr_rows_kernel(const int32_t* __restrict__ cell_dofs, int n_loc,
                                 const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
-                                int32_t n_rows, int cap, int pass, int64_t* __restrict__ row_nnz,
+                                int32_t n_rows, int hcap, int pass, int64_t* __restrict__ row_nnz,
                                 const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
   extern __shared__ int32_t sbuf[];
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* buf = sbuf + w * cap;
+  int32_t* table = sbuf + int64_t(w) * (hcap + hcap / 2);
+  int32_t* list = table + hcap;
   for (int64_t r = int64_t(blockIdx.x) * warps + w; r < n_rows; r += int64_t(gridDim.x) * warps) {
-    const int64_t b = inc_ptr[r], e = inc_ptr[r + 1];
-    const int64_t total = (e - b) * n_loc;
-    for (int i = lane; i < cap; i += 32) {
-      int32_t v = INT32_MAX;
-      if (i < total) {
-        const int64_t pk = inc[b + i / n_loc];
-        const int64_t cell = pk / n_loc;
-        v = cell_dofs[cell * n_loc + (i % n_loc)];
-      }
-      buf[i] = v;
+    const int64_t b = inc_ptr[r], m = inc_ptr[r + 1] - b;
+    const int64_t t2 = 2 * m * n_loc;
+    const uint32_t H = next_pow2_u32(uint32_t(t2 < 32 ? 32 : t2));
+    const int u = row_dedup(cell_dofs, n_loc, inc, b, m, table, H);
+    if (pass == 0) {
+      if (lane == 0) row_nnz[r] = u;
+      continue;
+    }
+    // compact the table (any order), pad to a power of two, sort, write
+    int base = 0;
+    for (uint32_t i0 = 0; i0 < H; i0 += 32) {
+      const int32_t v = table[i0 + lane];
+      const unsigned msk = __ballot_sync(0xffffffffu, v != -1);
+      if (v != -1) list[base + __popc(msk & ((1u << lane) - 1u))] = v;
+      base += __popc(msk);
+    }
+    const int cap = int(next_pow2_u32(uint32_t(max(u, 32))));
+    for (int i = u + lane; i < cap; i += 32) list[i] = INT32_MAX;
+    __syncwarp();
+    warp_bitonic_sort(list, cap);
+    const int64_t o = row_ptr[r];
+    for (int i = lane; i < u; i += 32) col_idx[o + i] = list[i];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------- scatter plan
+// Per row (one warp): the row's sorted columns in shared memory; every incident local row
+// (cell, i) maps its n_loc entries by binary search -> pos_map, and (counts != NULL) the
+// number of contributions per CSR position (distinct positions within one cell; the warp
+// walks the incident cells in order, so plain shared-memory increments suffice).
+__device__ __forceinline__ int lower_bound_i32(const int32_t* L, int n, int32_t v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (L[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc,
+                                const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
+                                const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                int32_t n_rows, int rcap, int32_t* __restrict__ pos_map,
+                                int64_t* __restrict__ counts) {
+  extern __shared__ int32_t sbuf[];
+  const int warps = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* L = sbuf + int64_t(w) * 2 * rcap;
+  int32_t* cnt = L + rcap;
+  for (int64_t r = int64_t(blockIdx.x) * warps + w; r < n_rows; r += int64_t(gridDim.x) * warps) {
+    const int64_t o = row_ptr[r];
+    const int u = int(row_ptr[r + 1] - o);
+    for (int i = lane; i < u; i += 32) {
+      L[i] = col_idx[o + i];
+      cnt[i] = 0;
     }
     __syncwarp();
-    warp_bitonic_sort(buf, cap);
-    // unique count (and write)
-    int64_t base = pass ? row_ptr[r] : 0;
-    int64_t count = 0;
-    for (int i0 = 0; i0 < cap; i0 += 32) {
-      const int i = i0 + lane;
-      const int32_t v = buf[i];
-      const bool keep = v != INT32_MAX && (i == 0 || buf[i - 1] != v);
-      const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (pass && keep) col_idx[base + count + __popc(m & ((1u << lane) - 1u))] = v;
-      count += __popc(m);
+    const int64_t b = inc_ptr[r], m = inc_ptr[r + 1] - b;
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t pk = inc[b + k];
+      const int64_t cell = pk / n_loc;
+      for (int j = lane; j < n_loc; j += 32) {
+        const int idx = lower_bound_i32(L, u, cell_dofs[cell * n_loc + j]);
+        pos_map[pk * n_loc + j] = int32_t(o + idx);
+        if (counts) cnt[idx] += 1;
+      }
+      __syncwarp();
     }
-    if (!pass && lane == 0) row_nnz[r] = count;
+    if (counts)
+      for (int i = lane; i < u; i += 32) counts[o + i] = cnt[i];
+    __syncwarp();
+  }
+}
+
+// perm: for every CSR position, its contributions' local indices (c*n_loc + i)*n_loc + j
+// in ascending cell order (the reference's summation order), written through per-position
+// cursors that start at seg_ptr. Same walk as plan_pos_kernel; positions from pos_map.
+__global__ void plan_perm_kernel(int n_loc, const int64_t* __restrict__ inc_ptr,
+                                 const int64_t* __restrict__ inc, const int64_t* __restrict__ row_ptr,
+                                 const int32_t* __restrict__ pos_map, const int64_t* __restrict__ seg_ptr,
+                                 int32_t n_rows, int rcap, uint32_t* __restrict__ perm) {
+  extern __shared__ int64_t cursor_buf[];
+  const int warps = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int64_t* cur = cursor_buf + int64_t(w) * rcap;
+  for (int64_t r = int64_t(blockIdx.x) * warps + w; r < n_rows; r += int64_t(gridDim.x) * warps) {
+    const int64_t o = row_ptr[r];
+    const int u = int(row_ptr[r + 1] - o);
+    for (int i = lane; i < u; i += 32) cur[i] = seg_ptr[o + i];
+    __syncwarp();
+    const int64_t b = inc_ptr[r], m = inc_ptr[r + 1] - b;
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t pk = inc[b + k];
+      for (int j = lane; j < n_loc; j += 32) {
+        const int64_t e = pk * n_loc + j;
+        const int idx = int(pos_map[e] - o);
+        perm[cur[idx]++] = uint32_t(e);
+      }
+      __syncwarp();
+    }
     __syncwarp();
   }
 }
@@ -214,31 +333,6 @@ template <typename TL, typename TV>
 __device__ __forceinline__ TV cast_value(TL x) {
   if constexpr (sizeof(TV) == 4 && sizeof(TL) == 8) return __double2float_rn(x);
   else return TV(x);
-}
-
-// Scatter plan, part 1: CSR position of every local entry (c, i, j), found once by binary
-// search in row dof(c, i). One warp per local row (c, i), lanes over j.
-__global__ void pos_map_kernel(const int32_t* __restrict__ cell_dofs, int64_t n_cells, int n_loc,
-                               const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                               int32_t* __restrict__ pos_map) {
-  const int warps = blockDim.x >> 5;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t total = n_cells * n_loc;
-  for (int64_t t = int64_t(blockIdx.x) * warps + w; t < total; t += int64_t(gridDim.x) * warps) {
-    const int64_t cell = t / n_loc;
-    const int32_t r = cell_dofs[t];
-    int64_t lo0 = row_ptr[r], hi0 = row_ptr[r + 1];
-    for (int j = lane; j < n_loc; j += 32) {
-      const int32_t col = cell_dofs[cell * n_loc + j];
-      int64_t lo = lo0, hi = hi0;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (col_idx[mid] < col) lo = mid + 1;
-        else hi = mid;
-      }
-      pos_map[t * n_loc + j] = int32_t(lo);
-    }
-  }
 }
 
 // Deterministic scatter: thread per CSR entry (all rows) walks its contributions in the

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/mpfem_b200.h"
@@ -235,15 +236,18 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
     int64_t* inc = S.get<int64_t>(n);
     build_incidence(cell_dofs, n, n_dofs, inc_ptr, inc, S);
     const int64_t mmax = max_count(inc_ptr, n_dofs, S);
-    int cap = 32;
-    while (cap < mmax * n_loc) cap <<= 1;
-    if (cap > 8192) throw AsmError{2, "row candidate list exceeds 8192 (multiplicity x n_loc)"};
-    const int warps = std::max(1, std::min(8, 32768 / (cap * 4)));
-    const size_t smem = size_t(warps) * cap * 4;
-    const unsigned grid = unsigned(std::min<int64_t>((n_dofs + warps - 1) / warps, 148 * 16));
+    if (mmax * n_loc > 8192) throw AsmError{2, "row candidate list exceeds 8192 (multiplicity x n_loc)"};
+    int hcap = 32;
+    while (hcap < 2 * mmax * n_loc) hcap <<= 1;
+    const size_t per_warp = size_t(hcap + hcap / 2) * 4;
+    const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (48u << 10) / per_warp)));
+    const size_t smem = size_t(warps) * per_warp;
+    if (smem > (48u << 10))
+      ACUDA(cudaFuncSetAttribute(asmb::csr_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const unsigned grid = unsigned(std::min<int64_t>((n_dofs + warps - 1) / warps, 148 * 32));
     int64_t* row_nnz = S.get<int64_t>(size_t(n_dofs) + 1);
     ACUDA(cudaMemsetAsync(row_nnz + n_dofs, 0, sizeof(int64_t), st));
-    asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs, cap,
+    asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs, hcap,
                                                           0, row_nnz, nullptr, nullptr);
     ACUDA(cudaGetLastError());
     size_t tb = 0;
@@ -251,10 +255,11 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
     void* tmp = S.get<char>(tb);
     ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, row_nnz, row_ptr, n_dofs + 1, st));
     const int64_t total = read1(row_ptr + n_dofs, st);
+    if (total >= (int64_t(1) << 31)) throw AsmError{2, "nnz must fit int32 positions (split the mesh)"};
     if (nnz) *nnz = total;
     if (col_idx) {
       asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs,
-                                                            cap, 1, nullptr, row_ptr, col_idx);
+                                                            hcap, 1, nullptr, row_ptr, col_idx);
       ACUDA(cudaGetLastError());
     }
   });
@@ -267,33 +272,46 @@ int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc
     if (n_loc < 1 || n_dofs < 1 || !pos_map) throw AsmError{2, "scatter plan needs a dof map and pos_map"};
     const int64_t nk = n_cells * n_loc * n_loc;
     if (nk > int64_t(UINT32_MAX)) throw AsmError{2, "n_cells * n_loc^2 must fit 32 bits"};
+    if ((seg_ptr == nullptr) != (perm == nullptr))
+      throw AsmError{2, "deterministic plan needs both seg_ptr and perm"};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch S(st);
-    const int64_t rows_total = n_cells * n_loc;
-    asmb::pos_map_kernel<<<unsigned(std::min<int64_t>((rows_total + 7) / 8, 148 * 64)), 256, 0, st>>>(
-        cell_dofs, n_cells, n_loc, row_ptr, col_idx, pos_map);
-    ACUDA(cudaGetLastError());
-    if (!seg_ptr && !perm) return;
-    if (!seg_ptr || !perm) throw AsmError{2, "deterministic plan needs both seg_ptr and perm"};
+    const int64_t n = n_cells * n_loc;
+    int64_t* inc_ptr = S.get<int64_t>(size_t(n_dofs) + 1);
+    int64_t* inc = S.get<int64_t>(n);
+    build_incidence(cell_dofs, n, n_dofs, inc_ptr, inc, S);
+    int rcap = 32;
+    const int64_t umax = max_count(row_ptr, n_dofs, S);
+    while (rcap < umax) rcap <<= 1;
     const int64_t nnz = read1(row_ptr + n_dofs, st);
-    // segment offsets: every entry has >= 1 contribution; counts by position, then scan
-    int64_t* counts = S.get<int64_t>(size_t(nnz) + 1);
-    ACUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * (size_t(nnz) + 1), st));
-    asmb::dof_count_kernel<<<grid_for(nk), 256, 0, st>>>(pos_map, nk, counts);
+    int64_t* counts = nullptr;
+    if (seg_ptr) counts = S.get<int64_t>(size_t(nnz) + 1);
+    auto launch_dims = [&](size_t per_warp, const void* fn) {
+      const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (48u << 10) / per_warp)));
+      const size_t smem = size_t(warps) * per_warp;
+      if (smem > (48u << 10))
+        ACUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      const unsigned grid = unsigned(std::min<int64_t>((n_dofs + warps - 1) / warps, 148 * 32));
+      return std::make_tuple(grid, warps, smem);
+    };
+    {
+      auto [grid, warps, smem] = launch_dims(size_t(rcap) * 8, reinterpret_cast<const void*>(asmb::plan_pos_kernel));
+      asmb::plan_pos_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, row_ptr, col_idx,
+                                                            n_dofs, rcap, pos_map, counts);
+      ACUDA(cudaGetLastError());
+    }
+    if (!seg_ptr) return;
+    ACUDA(cudaMemsetAsync(counts + nnz, 0, sizeof(int64_t), st));
     size_t tb = 0;
     ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, seg_ptr, nnz + 1, st));
     void* tmp = S.get<char>(tb);
     ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, seg_ptr, nnz + 1, st));
-    // perm = local indices sorted stably by CSR position
-    uint32_t* idx = S.get<uint32_t>(nk);
-    int32_t* keys_out = S.get<int32_t>(nk);
-    iota_kernel<<<grid_for(nk), 256, 0, st>>>(idx, nk);
-    size_t tb2 = 0;
-    const int bits = bits_for(nnz);
-    ACUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb2, pos_map, keys_out, idx, perm, nk, 0, bits, st));
-    void* tmp2 = S.get<char>(tb2);
-    ACUDA(cub::DeviceRadixSort::SortPairs(tmp2, tb2, pos_map, keys_out, idx, perm, nk, 0, bits, st));
-    ACUDA(cudaGetLastError());
+    {
+      auto [grid, warps, smem] = launch_dims(size_t(rcap) * 8, reinterpret_cast<const void*>(asmb::plan_perm_kernel));
+      asmb::plan_perm_kernel<<<grid, warps * 32, smem, st>>>(n_loc, inc_ptr, inc, row_ptr, pos_map, seg_ptr,
+                                                             n_dofs, rcap, perm);
+      ACUDA(cudaGetLastError());
+    }
   });
 }
 
