@@ -68,63 +68,6 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
-// tcgen05.ld without the wait: the wait below names the destination registers as
-// read-write operands, so no use of them can be scheduled before it.
-__device__ __forceinline__ void tmem_ld_issue(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-        "=r"(r[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
-                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
-                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]),
-                 "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]),
-                 "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]),
-                 "+r"(r[31])
-               :
-               : "memory");
-}
-
-// Stores one 32-cell chunk of an output row: cell c0 + j gets v_j at dst + j * pitch.
-// chk accumulates v * 0: it turns NaN iff some v is inf or NaN (one FFMA per value).
-template <bool ACC_F16>
-__device__ __forceinline__ void store_chunk(const uint32_t (&r)[32], float* dst, int pitch, int64_t left,
-                                            float& chk) {
-  if (left >= 32) {
-    #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float v;
-      if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
-      else v = __uint_as_float(r[j]);
-      chk = fmaf(v, 0.0f, chk);
-#ifndef MPFEM_TC2_NOSTORE
-      __stcs(dst + j * pitch, v);
-#endif
-    }
-  } else {
-    #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < left) {
-        float v;
-        if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
-        else v = __uint_as_float(r[j]);
-        chk = fmaf(v, 0.0f, chk);
-        __stcs(dst + j * pitch, v);
-      }
-    }
-  }
-}
-
 template <bool ACC_F16>
 __global__ void __launch_bounds__(THREADS, 1)
     cellmat_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -211,44 +154,49 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // Epilogue: warp (quarter, half) drains TMEM lanes quarter*32.. (its output rows) and
-    // columns half*128.. (cells) of the accumulator; output row o is entry (i, j) of each
-    // cell's matrix (row table), so a warp store is 32 consecutive entries of one cell.
     const int quarter = warp & 3;
     const int half = (warp - 4) >> 2;
-    const int pitch = int(P.out_pitch);
     int acc = 0;
     uint32_t acc_phase = 0;
-    float chk = 0.0f;
+    uint32_t expo_or = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
       const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
-      const int32_t e = P.rows[ot * BM + int(rank) * BMC + quarter * 32 + lane];  // before the wait
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
+      const int o = ot * BM + int(rank) * BMC + quarter * 32 + lane;
+      const int32_t e = P.rows[o];
       const bool o_ok = e >= 0;
       const int off = (e & 0xffff) * P.n_phi + ((e >> 16) & 0x3fff);
-      const uint32_t tbase = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + half * (BN / 2));
-      const int64_t cell_base = int64_t(ct) * BN + half * (BN / 2);
-      float* row = P.out + off;
-      uint32_t ra[32], rb[32];
-      tmem_ld_issue(tbase, ra);
-      tmem_ld_wait(ra);
-      #pragma unroll
-      for (int chunk = 0; chunk < BN / 64; ++chunk) {
-        uint32_t (&cur)[32] = (chunk & 1) ? rb : ra;
-        uint32_t (&nxt)[32] = (chunk & 1) ? ra : rb;
-        if (chunk + 1 < BN / 64) tmem_ld_issue(tbase + uint32_t((chunk + 1) * 32), nxt);
-        const int64_t cell0 = cell_base + chunk * 32;
-        if (o_ok) store_chunk<ACC_F16>(cur, row + cell0 * pitch, pitch, P.n_cells - cell0, chk);
-        if (chunk + 1 < BN / 64) tmem_ld_wait(nxt);
+      #pragma unroll 1
+      for (int chunk = half * (BN / 64); chunk < (half + 1) * (BN / 64); ++chunk) {
+        uint32_t r[32];
+        tc::tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
+        const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
+        if (o_ok) {
+          float* dst = P.out + cell0 * P.out_pitch + off;
+          const int64_t left = P.n_cells - cell0;
+          #pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (left >= 32 || j < left) {
+              float v;
+              if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
+              else v = __uint_as_float(r[j]);
+              expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+#ifndef MPFEM_TC2_NOSTORE  // diagnostic build only (make diag)
+              __stcs(dst, v);
+#endif
+            }
+            dst += P.out_pitch;
+          }
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_leader(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
-    const uint32_t bad = __any_sync(0xffffffffu, chk != chk);
-    if (lane == 0 && bad && !(*reinterpret_cast<volatile uint32_t*>(P.flags) & 4u)) atomicOr(P.flags, 4u);
+    expo_or = __reduce_or_sync(0xffffffffu, expo_or);
+    if (lane == 0 && expo_or && !(*reinterpret_cast<volatile uint32_t*>(P.flags) & 4u)) atomicOr(P.flags, 4u);
   }
   tc::tc_fence_before();
   __syncthreads();
