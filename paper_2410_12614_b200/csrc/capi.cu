@@ -246,7 +246,7 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.flags = static_cast<uint32_t*>(S.d_flags.p);
   P.error = static_cast<int*>(S.d_error.p);
   const int64_t tiles = (n + kTileCells - 1) / kTileCells;
-  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * 3));
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * MPFEM_K1_MINB));
   launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
   CUDA_OK(cudaGetLastError());
 }
@@ -497,7 +497,7 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->n_q = S->rule.n_q;
     S->n_d = form ? 3 : 1;
     S->n_blocks = form ? 6 : 1;
-    S->nq_pad = (S->n_q + kQPT - 1) / kQPT * kQPT;
+    S->nq_pad = (S->n_q + kWAlign - 1) / kWAlign * kWAlign;
     S->k = int64_t(S->n_blocks) * S->nq_pad;
     const int64_t kal = S->path == kPathTC ? tc::BK : 16;
     S->k_pad = (S->k + kal - 1) / kal * kal;

@@ -88,12 +88,13 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
     if (!tet_geometry<UG>(v, FORM != 0, g, fl)) {
       atomicExch(F.error, 3);
     } else {
-      double v0[3], E[9];
+      double v0[3], E[9];  // x, y pre-doubled (coef_sincosexp_*)
       #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        v0[a] = v[0][a];
+        const double sc = a < 2 ? 2.0 : 1.0;
+        v0[a] = sc * v[0][a];
         #pragma unroll
-        for (int s = 0; s < 3; ++s) E[s * 3 + a] = __dsub_rn(v[s + 1][a], v[0][a]);
+        for (int s = 0; s < 3; ++s) E[s * 3 + a] = sc * __dsub_rn(v[s + 1][a], v[0][a]);
       }
       const double* zc = F.coef ? F.coef + cell * F.coef_stride : nullptr;
       float acc[NOUT];

@@ -562,29 +562,23 @@ __device__ __forceinline__ double coef_sincosexp(const double v[4][3], const dou
 }
 
 // Branch-free binary64 transcendentals for the bounded arguments of the analytic
-// coefficient (|2x| < 2^30, |z| < 700): range reduction by an exact rint, then fp64 Horner
-// on Taylor series truncated below 2^-60 relative. Measured against 120-bit mpmath over the
-// configs' coordinate range: sinpi/cospi <= 1.6 ulp, exp <= 1 ulp (the glibc/CUDA libm
-// functions are within 1-2 ulp of the same values; analytic-coefficient parity with the
-// oracle is tolerance-based for that reason).
-// Coefficients live in constant memory so DFMA reads them as constant-bank operands
-// (fp64 immediates would otherwise be materialised with two UMOVs each).
-__constant__ double kSinPiC[13] = {3.141592653589793, -5.16771278004997, 2.5501640398773455,
-                                   -0.5992645293207921, 0.08214588661112823, -0.0073704309457143504,
-                                   0.00046630280576761255, -2.1915353447830217e-05, 7.952054001475513e-07,
-                                   -2.2948428997269873e-08, 5.392664662608129e-10,
-                                   -1.0518471716932065e-11, 1.7302192458361107e-13};
-__constant__ double kExpC[15] = {1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664,
-                                 0.008333333333333333, 0.001388888888888889, 0.0001984126984126984,
-                                 2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07,
-                                 2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10,
-                                 1.1470745597729725e-11};
-
+// coefficient (|2x| < 2^30, |z| < 700): range reduction by exact rounding, then fp64
+// Horner. Measured (scripts/coef_ulp_check.c, long double references): sinpi/cospi
+// <= 2.4 ulp, exp <= 0.56 ulp. The glibc/CUDA libm functions are within 1-2 ulp of the
+// same values, so analytic-coefficient parity with the oracle is tolerance-based.
+// Polynomial coefficients live in constant memory so DFMA reads them as constant-bank
+// operands (fp64 immediates would otherwise be materialised with two UMOVs each).
+// sin(pi r) = r P(r^2), |r| <= 1/2: near-minimax P of degree 8 in r^2 (Chebyshev fit in
+// mpmath, scripts/fit_coef_polys.py; approximation error 2e-19 relative, below the fp64
+// evaluation rounding).
+__constant__ double kSinPiC[9] = {3.141592653589793, -5.167712780049969, 2.5501640398773007,
+                                  -0.5992645293189447, 0.0821458865731029, -0.007370430505916944,
+                                  0.0004662998161898394, -2.1903497074626018e-05, 7.697826768224191e-07};
 __device__ __forceinline__ double sinpi_poly(double r) {  // sin(pi r), |r| <= 0.5
   const double s = r * r;
-  double p = kSinPiC[12];
+  double p = kSinPiC[8];
   #pragma unroll
-  for (int k = 11; k >= 0; --k) p = fma(p, s, kSinPiC[k]);
+  for (int k = 7; k >= 0; --k) p = fma(p, s, kSinPiC[k]);
   return r * p;
 }
 // Rounding to an integer without the fp64 conversion pipe (FRND / F2I run at a fraction
@@ -605,15 +599,43 @@ __device__ __forceinline__ double fast_cospi(double a) {  // cos(pi r) = sin(pi 
   const double n = __dsub_rn(t, kRoundMagic);
   return flip_if_odd(sinpi_poly(__dsub_rn(0.5, fabs(__dsub_rn(a, n)))), uint32_t(__double2loint(t)));
 }
+// e^z * 2^-h (h = 0 or 1 folds a factor 1/2 into the exponent): n = rint(32 z / ln2),
+// r = z - n ln2/32 (Cody-Waite, |r| <= ln2/64), e^r - 1 by degree-6 Taylor (error 3e-18),
+// 2^(j/32) from a double-double table: hi + fma(hi, e^r - 1, lo). <= 0.56 ulp
+// (scripts/coef_ulp_check.c). Table in global memory, read through L1 (lanes differ).
+__device__ const double2 kExp2Tab[32] = {
+    {1.0, 0.0}, {1.0218971486541166, 5.109225028973444e-17}, {1.0442737824274138, 8.551889705537965e-17},
+    {1.0671404006768237, -7.899853966841582e-17}, {1.0905077326652577, -3.046782079812471e-17},
+    {1.1143867425958924, 1.0410278456845571e-16}, {1.1387886347566916, 8.912812676025408e-17},
+    {1.1637248587775775, 3.8292048369240935e-17}, {1.189207115002721, 3.982015231465646e-17},
+    {1.215247359980469, -7.712630692681488e-17}, {1.241857812073484, 4.658027591836937e-17},
+    {1.2690509571917332, 2.667932131342186e-18}, {1.2968395546510096, 2.5382502794888315e-17},
+    {1.3252366431597413, -2.8587312100388614e-17}, {1.3542555469368927, 7.70094837980299e-17},
+    {1.383909881963832, -6.770511658794786e-17}, {1.4142135623730951, -9.667293313452913e-17},
+    {1.4451808069770467, -3.0237581349939873e-17}, {1.4768261459394993, -3.483994556892796e-17},
+    {1.5091644275934228, -1.016455327754295e-16}, {1.5422108254079407, 7.949834809697621e-17},
+    {1.5759808451078865, -1.0136916471278304e-17}, {1.6104903319492543, 2.4707192569797888e-17},
+    {1.645755478153965, -1.0125679913674773e-16}, {1.681792830507429, 8.199010020581497e-17},
+    {1.718619298122478, -1.851380418263111e-17}, {1.7562521603732995, 2.960140695448873e-17},
+    {1.7947090750031072, 1.8227458427912087e-17}, {1.8340080864093424, 3.283107224245627e-17},
+    {1.8741676341103, -6.122763413004143e-17}, {1.9152065613971474, -1.0619946056195963e-16},
+    {1.9571441241754002, 8.960767791036668e-17}};
+template <int H = 0>
 __device__ __forceinline__ double fast_exp(double z) {
-  const double t = __dadd_rn(__dmul_rn(z, 1.4426950408889634), kRoundMagic);
+  const double t = __dadd_rn(__dmul_rn(z, 46.16624130844683), kRoundMagic);
   const double n = __dsub_rn(t, kRoundMagic);
-  double r = fma(-n, 6.93147180369123816490e-01, z);  // ln2 hi: n * hi is exact
-  r = fma(-n, 1.90821492927058770002e-10, r);
-  double p = kExpC[14];
-  #pragma unroll
-  for (int k = 13; k >= 0; --k) p = fma(p, r, kExpC[k]);
-  return p * __hiloint2double((__double2loint(t) + 1023) << 20, 0);
+  double r = fma(-n, 0.021660849390173098, z);  // ln2/32 hi (trailing zeros: n * hi exact)
+  r = fma(-n, 2.325192846878874e-12, r);
+  double q = fma(1.0 / 720, r, 1.0 / 120);
+  q = fma(q, r, 1.0 / 24);
+  q = fma(q, r, 1.0 / 6);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  const double p1 = q * r;  // e^r - 1
+  const int ni = __double2loint(t);
+  const double2 tj = __ldg(&kExp2Tab[ni & 31]);
+  const double v = __dadd_rn(tj.x, fma(tj.x, p1, tj.y));
+  return v * __hiloint2double(((ni >> 5) - H + 1023) << 20, 0);
 }
 
 // fp32 counterparts for u_g = fp32 (the coefficient is rounded to fp32 anyway): same
@@ -653,37 +675,40 @@ __device__ __forceinline__ float fast_exp_f(float z) {
   return p * __int_as_float((static_cast<int>(n) + 127) << 23);
 }
 
+// The analytic coefficient from a cell's origin and edge vectors with the x and y components
+// pre-doubled (v0d = (2 v0x, 2 v0y, v0z), Ed[s] likewise): the FMA chain then yields 2x and
+// 2y exactly (scaling by 2 commutes with rounding), the sinpi/cospi arguments.
 // c(x_q) with the physical point in binary64 and the transcendentals in fp32, for u_g = fp32.
-__device__ __forceinline__ float coef_sincosexp_f(const double* v0, const double* E, const double* xi) {
+__device__ __forceinline__ float coef_sincosexp_f(const double* v0d, const double* Ed, const double* xi) {
   double x[3];
   #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double acc = v0[i];
+    double acc = v0d[i];
     #pragma unroll
-    for (int s = 0; s < 3; ++s) acc = fma(E[s * 3 + i], xi[s], acc);
+    for (int s = 0; s < 3; ++s) acc = fma(Ed[s * 3 + i], xi[s], acc);
     x[i] = acc;
   }
-  const float sn = fast_sinpi_f(float(2.0 * x[0]));
-  const float cs = fast_cospi_f(float(2.0 * x[1]));
+  const float sn = fast_sinpi_f(float(x[0]));
+  const float cs = fast_cospi_f(float(x[1]));
   const float e = fast_exp_f(float(x[2]));
   return fmaf(0.5f * sn * cs, e, 1.0f);
 }
 
-// Same, from the cell's origin v0 and edge vectors E[s] = v_{s+1} - v0 (precomputed).
-__device__ __forceinline__ double coef_sincosexp_e(const double* v0, const double* E,
+// binary64: c = 1 + 0.5 sin(2 pi x) cos(2 pi y) e^z as fma(sn cs, e^z / 2, 1)
+// (<= 5.3 ulp of max(1, |0.5 sn cs e^z|) against a long double reference).
+__device__ __forceinline__ double coef_sincosexp_e(const double* v0d, const double* Ed,
                                                    const double* xi) {
   double x[3];
   #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    double acc = v0[i];
+    double acc = v0d[i];
     #pragma unroll
-    for (int s = 0; s < 3; ++s) acc = fma(E[s * 3 + i], xi[s], acc);
+    for (int s = 0; s < 3; ++s) acc = fma(Ed[s * 3 + i], xi[s], acc);
     x[i] = acc;
   }
-  double sn = fast_sinpi(__dmul_rn(2.0, x[0]));
-  double cs = fast_cospi(__dmul_rn(2.0, x[1]));
-  double e = fast_exp(x[2]);
-  return __dadd_rn(1.0, __dmul_rn(__dmul_rn(__dmul_rn(0.5, sn), cs), e));
+  const double sn = fast_sinpi(x[0]);
+  const double cs = fast_cospi(x[1]);
+  return fma(__dmul_rn(sn, cs), fast_exp<1>(x[2]), 1.0);
 }
 
 // Config-3 coefficient: c = 10^(6 u(x_q)), u affine with vertex values u4.

@@ -142,22 +142,50 @@ __device__ __forceinline__ void store_w<double>(void* W, int64_t idx, double v) 
 // single conversion for fp32.
 struct __align__(16) CellGeo {
   double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson) or |det| (mass)
-  double v0[3];
-  double e[9];  // e[s*3 + i] = v_{s+1}[i] - v0[i]
+  double v0[3];  // (2 v0x, 2 v0y, v0z)
+  double e[9];   // e[s*3 + i] = (v_{s+1}[i] - v0[i]), x and y components doubled
 };
 
-constexpr int kQPT = 8;
-constexpr int kTileCells = 32;
+#ifndef MPFEM_K1_QPT
+#define MPFEM_K1_QPT 4
+#endif
+constexpr int kWAlign = 8;             // W / T block stride: nq_pad = round_up(n_q, kWAlign)
+constexpr int kQPT = MPFEM_K1_QPT;      // quadrature points per thread (divides kWAlign)
+static_assert(kWAlign % kQPT == 0 && kQPT % 2 == 0, "points per thread must divide the W block alignment");
+#ifndef MPFEM_K1_TILE
+#define MPFEM_K1_TILE 32
+#endif
+#ifndef MPFEM_K1_MINB
+#define MPFEM_K1_MINB 4
+#endif
+constexpr int kTileCells = MPFEM_K1_TILE;
 constexpr int kGeomThreads = 256;
 
 template <typename T>
-struct Pack8 {
-  T v[8];
+struct alignas(sizeof(T) * kQPT) PackQ {
+  T v[kQPT];
 };
+// one store of a thread's kQPT consecutive entries (16 B for 8 x 16-bit)
+template <typename T>
+__device__ __forceinline__ void store_pack(T* dst, const PackQ<T>& pk) {
+  constexpr int bytes = int(sizeof(PackQ<T>));
+  if constexpr (bytes % 16 == 0) {
+    #pragma unroll
+    for (int k = 0; k < bytes / 16; ++k) reinterpret_cast<uint4*>(dst)[k] = reinterpret_cast<const uint4*>(&pk)[k];
+  } else {
+    #pragma unroll
+    for (int k = 0; k < bytes / 8; ++k) reinterpret_cast<uint2*>(dst)[k] = reinterpret_cast<const uint2*>(&pk)[k];
+  }
+}
 
+#ifdef MPFEM_K1_GEOM_NOINLINE
+#define MPFEM_K1_GEOM_INLINE __noinline__
+#else
+#define MPFEM_K1_GEOM_INLINE __forceinline__
+#endif
 template <int UG>
-__device__ __forceinline__ void cell_geometry(const GeomWParams& P, int64_t cell, CellGeo& o,
-                                              uint32_t& fl) {
+__device__ MPFEM_K1_GEOM_INLINE void cell_geometry(const GeomWParams& P, int64_t cell, CellGeo& o,
+                                                   uint32_t& fl) {
   double v[4][3];
   if (P.cells) {
     #pragma unroll
@@ -180,12 +208,57 @@ __device__ __forceinline__ void cell_geometry(const GeomWParams& P, int64_t cell
   }
   #pragma unroll
   for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
+  // origin and edges with x, y pre-doubled (the coefficient's sinpi(2x), cospi(2y) arguments)
   #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    o.v0[a] = v[0][a];
+    const double sc = a < 2 ? 2.0 : 1.0;
+    o.v0[a] = sc * v[0][a];
     #pragma unroll
-    for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = __dsub_rn(v[s2 + 1][a], v[0][a]);
+    for (int s2 = 0; s2 < 3; ++s2) o.e[s2 * 3 + a] = sc * __dsub_rn(v[s2 + 1][a], v[0][a]);
   }
+}
+
+// W value at u_g: round_ug(round_ug(omega G_b) zhat_q) in float (u_g = fp32, IEEE fp32 ops are
+// the correctly rounded binary64 results) or double (u_g = fp64).
+template <int UG, bool HAVE_Z>
+__device__ __forceinline__ auto w_value(double om, double gb, double zq) {
+  if constexpr (UG == kFP32) {
+    float v = __fmul_rn(float(om), float(gb));
+    if (HAVE_Z) v = __fmul_rn(v, float(zq));
+    return v;
+  } else {
+    double v = __dmul_rn(om, gb);
+    if (HAVE_Z) v = __dmul_rn(v, zq);
+    return v;
+  }
+}
+template <typename T>
+struct Storage16;
+template <>
+struct Storage16<__half> {
+  static constexpr uint32_t kInf = 0x7c00u, kMinNormal = 0x0400u;
+};
+template <>
+struct Storage16<__nv_bfloat16> {
+  static constexpr uint32_t kInf = 0x7f80u, kMinNormal = 0x0080u;
+};
+// round_us (one RNE conversion) -> storage bits
+template <typename T, typename V>
+__device__ __forceinline__ uint32_t storage_bits16(V v) {
+  if constexpr (std::is_same_v<T, __half>) {
+    if constexpr (std::is_same_v<V, float>) return __half_as_ushort(__float2half_rn(v));
+    else return __half_as_ushort(__double2half(v));
+  } else {
+    if constexpr (std::is_same_v<V, float>) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    else return __bfloat16_as_ushort(__double2bfloat16(v));
+  }
+}
+// FP-event bits of the packed path: sf.amax holds the packed (u16x2) max of |bits|
+template <typename T>
+__device__ __forceinline__ uint32_t packed_store_flags(const StoreFlags& sf) {
+  const uint32_t a = max(sf.amax & 0xffffu, sf.amax >> 16);
+  return (a == Storage16<T>::kInf ? kOverflow : 0u) | (a > Storage16<T>::kInf ? kInvalid : 0u) |
+         (sf.tiny ? kUnderflow : 0u);
 }
 
 // dynamic shared memory of geom_w_kernel: weights and the three point coordinates,
@@ -193,9 +266,10 @@ __device__ __forceinline__ void cell_geometry(const GeomWParams& P, int64_t cell
 __host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad) { return size_t(4) * nq_pad * sizeof(double); }
 
 template <typename T, int UG, int US, int COEF>
-__global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) {
+__global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
   extern __shared__ double s_rule[];
-  __shared__ CellGeo s_geo[kTileCells];
+  __shared__ CellGeo s_geo[2][kTileCells];
+  __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
@@ -212,20 +286,38 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
   uint32_t fl = 0;
   StoreFlags sf;
   const int64_t n_tiles = (P.n_cells + kTileCells - 1) / kTileCells;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int lane = threadIdx.x & 31;
+  auto tile_cells = [&](int64_t t) {
+    const int64_t left = P.n_cells - t * kTileCells;
+    return left < kTileCells ? int(left) : kTileCells;
+  };
+  // Tile pipeline: warp 0 computes the geometry of the CTA's next tile into the other
+  // buffer while every warp (warp 0 once done) takes 32-item grabs of the current tile.
+  if (blockIdx.x < n_tiles && threadIdx.x < tile_cells(blockIdx.x))
+    cell_geometry<UG>(P, int64_t(blockIdx.x) * kTileCells + threadIdx.x, s_geo[0][threadIdx.x], fl);
+  if (threadIdx.x < 2) s_next[threadIdx.x] = 0;
+  __syncthreads();  // first tile's geometry, s_rule and the counters are ready
+  int buf = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
     const int64_t c0 = tile * kTileCells;
-    const int64_t left = P.n_cells - c0;
-    const int nc = left < kTileCells ? int(left) : kTileCells;
-    __syncthreads();  // previous tile's readers of s_geo are done (and s_rule is staged)
-    if (threadIdx.x < nc) cell_geometry<UG>(P, c0 + threadIdx.x, s_geo[threadIdx.x], fl);
-    __syncthreads();
+    const int nc = tile_cells(tile);
+    const int64_t nt = tile + gridDim.x;
+    if (threadIdx.x < 32 && nt < n_tiles && lane < tile_cells(nt))
+      cell_geometry<UG>(P, nt * kTileCells + lane, s_geo[buf ^ 1][lane], fl);
     const uint32_t items = uint32_t(nc * ngroups);
-    for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+    const CellGeo* geo_t = s_geo[buf];
+    while (true) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&s_next[buf], 32u);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= items) break;
+      const uint32_t it = base + lane;
+      if (it >= items) continue;
       const uint32_t cl = P.div_nq.div(it);
       const int grp = int(it - cl * uint32_t(ngroups));
       const int q0 = grp * kQPT;
       const int64_t cell = c0 + cl;
-      const CellGeo& cg = s_geo[cl];
+      const CellGeo& cg = geo_t[cl];
       const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
       double zq[kQPT], om[kQPT];
       #pragma unroll
@@ -259,11 +351,54 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
       bool pad[kQPT];
       #pragma unroll
       for (int j = 0; j < kQPT; ++j) pad[j] = q0 + j >= nq;
+      if constexpr (sizeof(T) == 2 && (UG == kFP32 || UG == kFP64)) {
+        // 16-bit storage: convert, pack two values per word, zero the padding halfwords
+        // (keep mask), and derive the FP events from the packed words: packed max of |bits|
+        // (>= the inf pattern: overflow / NaN) and packed min (below the smallest normal:
+        // candidate underflow, confirmed exactly on the rare block where it happens).
+        constexpr int KW = kQPT / 2;  // packed words per block
+        uint32_t keep[KW];
+        #pragma unroll
+        for (int k = 0; k < KW; ++k)
+          keep[k] = (pad[2 * k] ? 0u : 0x0000ffffu) | (pad[2 * k + 1] ? 0u : 0xffff0000u);
+        #pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          if (b < nb) {
+            const double gb = cg.g[b];
+            uint32_t wd[KW];
+            #pragma unroll
+            for (int k = 0; k < KW; ++k) {
+              const uint32_t lo = storage_bits16<T>(w_value<UG, have_z>(om[2 * k], gb, zq[2 * k]));
+              const uint32_t hi = storage_bits16<T>(w_value<UG, have_z>(om[2 * k + 1], gb, zq[2 * k + 1]));
+              wd[k] = (lo | (hi << 16)) & keep[k];
+            }
+            uint32_t bmin = 0xffffffffu;
+            #pragma unroll
+            for (int k = 0; k < KW; ++k) {
+              const uint32_t m = wd[k] & 0x7fff7fffu;
+              sf.amax = __vmaxu2(sf.amax, m);
+              bmin = __vminu2(bmin, m | ~keep[k]);
+            }
+            if (min(bmin & 0xffffu, bmin >> 16) < Storage16<T>::kMinNormal && gb != 0.0) {
+              #pragma unroll
+              for (int j = 0; j < kQPT; ++j) {
+                const auto v = w_value<UG, have_z>(om[j], gb, zq[j]);
+                const uint32_t a16 = storage_bits16<T>(v) & 0x7fffu;
+                if (!pad[j] && a16 < Storage16<T>::kMinNormal && v != decltype(v)(0)) sf.tiny = 1;
+              }
+            }
+            if constexpr (KW == 4)
+              *reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            else
+              *reinterpret_cast<uint2*>(wrow + int64_t(b) * nqp) = make_uint2(wd[0], wd[1]);
+          }
+        }
+      } else {
       #pragma unroll
       for (int b = 0; b < 6; ++b) {
         if (b < nb) {
           const double gb = cg.g[b];
-          Pack8<T> pk;
+          PackQ<T> pk;
           #pragma unroll
           for (int j = 0; j < kQPT; ++j) {
             if constexpr (UG == kFP32) {
@@ -283,12 +418,9 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
               pk.v[j] = to_storage<T, US>(val, sf);
             }
           }
-          // one 16-byte store per block for 16-bit storage (2 / 4 for fp32 / fp64)
-          const uint4* srcv = reinterpret_cast<const uint4*>(&pk);
-          uint4* dstv = reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp);
-          #pragma unroll
-          for (int k = 0; k < int(sizeof(Pack8<T>) / 16); ++k) dstv[k] = srcv[k];
+          store_pack(wrow + int64_t(b) * nqp, pk);
         }
+      }
       }
       // tail K..K_pad of the row: zeros (the group that owns the last block's start writes it)
       if (q0 == 0) {
@@ -296,8 +428,13 @@ __global__ void __launch_bounds__(kGeomThreads, 3) geom_w_kernel(GeomWParams P) 
         for (int64_t k = int64_t(nb) * nqp; k < P.k_pad; ++k) tail[k] = T(0.0f);
       }
     }
+    __syncthreads();  // tile done, next tile's geometry written
+    if (threadIdx.x == 0) s_next[buf] = 0;
   }
-  publish_flags(P.flags, fl | store_flags_bits(sf));
+  if constexpr (sizeof(T) == 2 && (UG == kFP32 || UG == kFP64))
+    publish_flags(P.flags, fl | packed_store_flags<T>(sf));
+  else
+    publish_flags(P.flags, fl | store_flags_bits(sf));
 }
 
 // Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
