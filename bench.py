@@ -43,7 +43,7 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def profiled_traffic(kernel_prefix="cellmat_tc_kernel"):
+def profiled_traffic(kernel_prefix="cellmat_tc2_kernel"):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from
     the committed `ncu --set full` capture summary (profiles/r*_ncu_summary.json), or None."""
     import glob
@@ -446,7 +446,7 @@ def main():
                      "traffic": (lambda t: t["bytes"] if t else None)(profiled_traffic()),
                      "traffic_source": (lambda t: t["source"] if t else None)(profiled_traffic()),
                      "algorithmic_bytes": N_CELLS * b_cell,
-                     "kernel": "cellmat_tc_kernel",
+                     "kernel": "cellmat_tc2_kernel",
                      "note": (f"achieved = dense-equivalent F_cell {f_cell:.0f} flop x {N_CELLS} cells / "
                               f"K2 duration; peak = {peak_src} bf16 burst; the kernel executes the "
                               f"(s<=t)-packed depth, {executed / flops_launch:.3f} of F_cell"),

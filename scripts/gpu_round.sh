@@ -10,5 +10,5 @@ if [ "${NCU:-1}" = "1" ]; then
   $CMD > $OUT/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
   $CMD > $OUT/plain2.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"cellmat_tc|scaled_weights|cell_geometry" -s 6 -c 3 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:"cellmat_tc|geom_w" -s 6 -c 2 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
