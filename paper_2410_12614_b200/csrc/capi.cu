@@ -137,7 +137,7 @@ struct mpfem_b200_setup_s {
   int64_t k = 0, k_pad = 0, n_out = 0, n_out_pad = 0;
   int path = kPathF64;
   int acc_f16 = 0;
-  int pair = 0;    // tcgen05 path on CTA pairs (cellmat_tc2.cuh); 0 = one CTA per tile
+  int pair = 0;    // tcgen05 path: 0 = one CTA per tile, 1 = CTA pairs, 2 = two pairs per cluster
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
   Rule rule;
   DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
@@ -259,13 +259,13 @@ void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, 
     throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
 }
 
-template <bool ACC_F16>
+template <bool ACC_F16, int NP>
 void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = 2 * NP;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(tc2::THREADS);
@@ -274,15 +274,15 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!max_clusters) {
-    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16>,
+    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES));
     cfg.gridDim = dim3(unsigned(device_sm_count()));
-    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16>, &cfg));
-    if (max_clusters < 1) throw Error(MPFEM_B200_RUNTIME_ERROR, "tcgen05 pair kernel does not fit an SM pair");
+    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, NP>, &cfg));
+    if (max_clusters < 1) throw Error(MPFEM_B200_RUNTIME_ERROR, "tcgen05 pair kernel does not fit an SM cluster");
   }
-  const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
-  cfg.gridDim = dim3(unsigned(2 * std::min<int64_t>(tiles, max_clusters)));
-  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16>, ta, tb, P));
+  const int64_t tiles = int64_t(P.n_out_tiles) * ((P.n_cell_tiles + NP - 1) / NP);
+  cfg.gridDim = dim3(unsigned(2 * NP * std::min<int64_t>(tiles, max_clusters)));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, NP>, ta, tb, P));
 }
 
 void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t out_pitch,
@@ -290,9 +290,10 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
   if (S.path == kPathTC && S.pair) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc2::BK, tc2::BMC);
+    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc2::BK,
+                                 tc2::BMC / S.pair);
     CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc2::BK, tc2::BNC);
-    tc::Params P;
+    tc::Params P{};
     P.n_cells = n;
     P.n_out = int(S.n_out);
     P.n_phi = S.n_phi;
@@ -304,14 +305,19 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     P.out_pitch = out_pitch;
     P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc2::BM, tc2::BN);
     P.flags = static_cast<uint32_t*>(S.d_flags.p);
-    if (S.acc_f16) launch_tc2<true>(ta, tb, P, st);
-    else launch_tc2<false>(ta, tb, P, st);
+    if (S.pair == 2) {
+      if (S.acc_f16) launch_tc2<true, 2>(ta, tb, P, st);
+      else launch_tc2<false, 2>(ta, tb, P, st);
+    } else {
+      if (S.acc_f16) launch_tc2<true, 1>(ta, tb, P, st);
+      else launch_tc2<false, 1>(ta, tb, P, st);
+    }
   } else if (S.path == kPathTC) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc::BM);
     CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc::BN);
-    tc::Params P;
+    tc::Params P{};
     P.n_cells = n;
     P.n_out = int(S.n_out);
     P.n_phi = S.n_phi;
@@ -486,6 +492,9 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     if (S->path == kPathTC) {
       const char* tc1 = std::getenv("MPFEM_B200_TC1");
       S->pair = !(tc1 && std::atoi(tc1) != 0);
+      // pairs per cluster (2: the two pairs share the Tt tile by TMA multicast)
+      const char* np = std::getenv("MPFEM_B200_TC_PAIRS");
+      if (S->pair && np && std::atoi(np) == 2) S->pair = 2;
     }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
