@@ -115,6 +115,11 @@ int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 int mpfem_b200_set_timing(mpfem_b200_setup_t setup, int enable);
 int mpfem_b200_last_timings(mpfem_b200_setup_t setup, float* ms, int max_n);
 
+/* Debug timeline of the last cell_matrices call (only with MPFEM_B200_TRACE=1 in the
+ * environment): per CTA {start ns, end ns, SM id}; K1 CTAs in slots 0..1023, K2 CTAs in
+ * slots 1024..2047, 3 words per slot. Not a reference interface (diagnostics only). */
+int mpfem_b200_debug_trace(mpfem_b200_setup_t setup, unsigned long long* host, int max_n);
+
 /* ---------------------------------------------------------------- mesh & assembly */
 
 /* Seeded synthetic cells on the host (std::mt19937_64 = the reference Rng, common.hpp:21-35).

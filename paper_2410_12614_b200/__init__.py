@@ -133,6 +133,7 @@ def lib():
         "mpfem_b200_last_launch_count": (C.c_int, [vp]),
         "mpfem_b200_set_timing": (C.c_int, [vp, C.c_int]),
         "mpfem_b200_last_timings": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
+        "mpfem_b200_debug_trace": (C.c_int, [vp, vp, C.c_int]),
         "mpfem_b200_gen_tets": (C.c_int, [C.c_int, C.c_uint64, C.c_int64, vp, vp]),
         "mpfem_b200_structured_tet_mesh": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
                                                      C.c_double, C.c_uint64, vp, vp]),
@@ -305,6 +306,15 @@ class KernelSetup:
         if n < 0:
             check(-n)
         return [buf[i] for i in range(n)]
+
+    def debug_trace(self):
+        """Per-CTA timeline of the last call (MPFEM_B200_TRACE=1): arrays (k1, k2) of
+        rows (start_ns, end_ns, sm) for the CTAs that ran."""
+        buf = np.zeros(3 * 2048, dtype=np.uint64)
+        check(lib().mpfem_b200_debug_trace(self._h, buf.ctypes.data, buf.size))
+        rows = buf.reshape(2048, 3)
+        k1, k2 = rows[:1024], rows[1024:]
+        return k1[k1[:, 0] > 0], k2[k2[:, 0] > 0]
 
 
 def make_setup(p: int, config: KernelConfig, cell_kind: int = 0, dim: int = 3) -> KernelSetup:

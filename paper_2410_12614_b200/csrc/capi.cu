@@ -143,6 +143,11 @@ struct mpfem_b200_setup_s {
   DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
   int n_rows = 0;  // tcgen05 path: rows of Tt (upper-triangle 8x4 blocks, padded to 128)
   DevBuf d_W, d_flags, d_error;
+  // concurrent K1/K2 (tcgen05 pair path): per-K1-tile W stamps and the call's epoch
+  DevBuf d_ready;
+  DevBuf d_trace;  // MPFEM_B200_TRACE=1: per-CTA timeline of the last call
+  uint32_t epoch = 0;
+  uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
   // host-API staging
   DevBuf h_verts, h_cells, h_coef, h_out;
   int last_launches = 0;
@@ -245,8 +250,14 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.W = W;
   P.flags = static_cast<uint32_t*>(S.d_flags.p);
   P.error = static_cast<int*>(S.d_error.p);
+  P.ready = S.cur_ready;
+  P.epoch = S.epoch;
+  P.trace = static_cast<unsigned long long*>(S.d_trace.p);
   const int64_t tiles = (n + kTileCells - 1) / kTileCells;
-  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * MPFEM_K1_MINB));
+  // concurrent with K2 (one 384-thread CTA per SM): two 256-thread K1 CTAs fit beside it
+  int per_sm = S.cur_ready ? 2 : MPFEM_K1_MINB;
+  if (const char* e = std::getenv("MPFEM_B200_K1_PER_SM")) per_sm = std::max(1, std::atoi(e));
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * per_sm));
   launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
   CUDA_OK(cudaGetLastError());
 }
@@ -276,6 +287,12 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   if (!max_clusters) {
     CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES));
+    // Full carveout: with the default the driver configures an SM that K2 reaches first for
+    // the smallest shared-memory size holding its 198 KB (196 KB), leaving no room for the
+    // two concurrent K1 CTAs (2 x 14 KB) -- K1 would then wait for K2, which waits for K1.
+    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 int(cudaSharedmemCarveoutMaxShared)));
     cfg.gridDim = dim3(unsigned(device_sm_count()));
     CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, NP>, &cfg));
     if (max_clusters < 1) throw Error(MPFEM_B200_RUNTIME_ERROR, "tcgen05 pair kernel does not fit an SM cluster");
@@ -305,6 +322,11 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     P.out_pitch = out_pitch;
     P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc2::BM, tc2::BN);
     P.flags = static_cast<uint32_t*>(S.d_flags.p);
+    P.ready = S.cur_ready;
+    P.epoch = S.epoch;
+    P.k1_tile = kTileCells;
+    P.error = static_cast<int*>(S.d_error.p);
+    P.trace = static_cast<unsigned long long*>(S.d_trace.p);
     if (S.pair == 2) {
       if (S.acc_f16) launch_tc2<true, 2>(ta, tb, P, st);
       else launch_tc2<false, 2>(ta, tb, P, st);
@@ -397,6 +419,10 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   }
   S.n_ev = 0;
   if (n == 0) return;
+  if (const char* tr = std::getenv("MPFEM_B200_TRACE"); tr && std::atoi(tr) != 0) {
+    S.d_trace.ensure(3 * 2048 * sizeof(unsigned long long));
+    CUDA_OK(cudaMemsetAsync(S.d_trace.p, 0, S.d_trace.bytes, st));
+  }
   if (S.path == kPathFused) {
     if (n * int64_t(S.n_q) >= (int64_t(1) << 40)) throw Error(MPFEM_B200_CONFIG_ERROR, "batch too large");
     S.mark(st);
@@ -416,7 +442,45 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   (void)out_tiles;
   if (const char* env = std::getenv("MPFEM_B200_CHUNKS")) n_chunks = std::max(1, std::min(8, std::atoi(env)));
   if (S.timing) n_chunks = 1;  // per-kernel timing measures K1 and K2 unoverlapped
-  const int64_t tiles_per_chunk = (cell_tiles + n_chunks - 1) / n_chunks;
+  // Concurrent K1/K2 (experimental, MPFEM_B200_OVERLAP=1 on the tcgen05 pair path): K1 on
+  // the caller's stream and K2 on a side stream start together and share every SM (one K2
+  // CTA + two K1 CTAs); K2's producer acquires K1's per-tile W stamps before each TMA read.
+  // Correct, but measured no faster on B200: next to K2's MMAs K1 runs 2x slower (1.1x with
+  // the MMAs compiled out), so the fp64 and tensor work do not overlap.
+  const char* ov_env = std::getenv("MPFEM_B200_OVERLAP");
+  const bool concurrent = S.path == kPathTC && S.pair && !S.timing && n_chunks == 1 &&
+                          ov_env && std::atoi(ov_env) != 0;
+  if (concurrent) {
+    const int64_t k1_tiles = (n + kTileCells - 1) / kTileCells;
+    const size_t need = size_t(k1_tiles) * sizeof(uint32_t);
+    if (++S.epoch == 0) S.epoch = 1;
+    if (need > S.d_ready.bytes || S.epoch == 1) {
+      S.d_ready.ensure(need);
+      CUDA_OK(cudaMemsetAsync(S.d_ready.p, 0, S.d_ready.bytes, st));
+    }
+    if (!S.side) {
+      CUDA_OK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
+      CUDA_OK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&S.join, cudaEventDisableTiming));
+      for (auto& e : S.chunk_ready) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    S.cur_ready = static_cast<uint32_t*>(S.d_ready.p);
+    CUDA_OK(cudaEventRecord(S.fork, st));
+    CUDA_OK(cudaStreamWaitEvent(S.side, S.fork, 0));
+    try {
+      launch_geom(S, verts, cells, n, coef_kind, coef, coef_stride, S.d_W.p, S.k_pad, S.w_type, st);
+      launch_gemm(S, S.d_W.p, n, out, out_pitch, S.side);
+    } catch (...) {
+      S.cur_ready = nullptr;
+      throw;
+    }
+    S.cur_ready = nullptr;
+    S.last_launches += 2;
+    CUDA_OK(cudaEventRecord(S.join, S.side));
+    CUDA_OK(cudaStreamWaitEvent(st, S.join, 0));
+    n_chunks = 0;  // done
+  }
+  const int64_t tiles_per_chunk = (cell_tiles + std::max(n_chunks, 1) - 1) / std::max(n_chunks, 1);
   if (n_chunks > 1) {
     if (!S.side) {
       CUDA_OK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
@@ -464,6 +528,10 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     CUDA_OK(cudaStreamSynchronize(st));
     *flags |= h[0];
     if (h[1] == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+    if (h[1] == 5)
+      throw Error(MPFEM_B200_RUNTIME_ERROR,
+                  "concurrent K1/K2: W stamps never arrived (K1 not co-resident with K2); "
+                  "set MPFEM_B200_OVERLAP=0");
   }
 }
 
@@ -687,6 +755,16 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t S, const double* verts, const i
 }
 
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t S) { return S ? S->last_launches : 0; }
+
+int mpfem_b200_debug_trace(mpfem_b200_setup_t S, unsigned long long* host, int max_n) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (!S->d_trace.p) throw Error(MPFEM_B200_CONFIG_ERROR, "tracing off (MPFEM_B200_TRACE=1)");
+    const size_t n = std::min<size_t>(size_t(max_n), S->d_trace.bytes / sizeof(unsigned long long));
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaMemcpy(host, S->d_trace.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  });
+}
 
 int mpfem_b200_set_timing(mpfem_b200_setup_t S, int enable) {
   return guarded([&] {

@@ -31,6 +31,9 @@
 namespace mpfem_b200 {
 namespace tc {
 
+#ifndef MPFEM_TC_BACKOFF_NS
+#define MPFEM_TC_BACKOFF_NS 256
+#endif
 constexpr int BM = 128;  // output entries per tile (MMA M, TMEM lanes)
 #ifndef MPFEM_TC_BN
 #define MPFEM_TC_BN 256
@@ -62,7 +65,43 @@ struct Params {
   int64_t out_pitch;
   uint32_t idesc;
   uint32_t* flags;
+  // Concurrent K1/K2: per-K1-tile W stamps (NULL: W complete at launch, stream order)
+  const uint32_t* ready;
+  uint32_t epoch;
+  int k1_tile;         // cells per K1 tile (stamp granularity)
+  int* error;          // set to 5 if a stamp never arrives (K1 not co-resident); error[1]
+                       // holds the epoch of the last timed-out call (later waits skip)
+  unsigned long long* trace;  // debug timeline (slots 1024..2047), NULL normally
 };
+
+// Producer-side wait for K1's W rows [c0, c1): acquire each K1 tile stamp, then order the
+// generic-proxy writes before this thread's async-proxy (TMA) reads. Bounded: after ~0.2 s
+// without progress it flags error 5 and returns, so a scheduling failure cannot hang the GPU.
+__device__ __forceinline__ void wait_w_ready(const Params& P, int64_t c0, int64_t c1) {
+  if (!P.ready) return;
+  if (c1 > P.n_cells) c1 = P.n_cells;
+  if (c0 >= c1) return;
+  const int64_t t0 = c0 / P.k1_tile, t1 = (c1 - 1) / P.k1_tile;
+  uint64_t start = 0;
+  for (int64_t t = t0; t <= t1; ++t) {
+    if (reinterpret_cast<volatile uint32_t*>(P.error)[1] == P.epoch) return;  // this call timed out
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.ready + t) : "memory");
+      if (v == P.epoch) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (!start) start = now;
+      else if (now - start > 200000000ull) {
+        atomicExch(P.error, 5);
+        atomicExch(reinterpret_cast<uint32_t*>(P.error) + 1, P.epoch);
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -89,6 +128,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Waits that are not on the MMA critical path back off with nanosleep, so warps parked on
+// a barrier leave the issue slots to co-resident K1 CTAs.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(MPFEM_TC_BACKOFF_NS);
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
+  trace_mark(P.trace, 1024 + (blockIdx.x & 1023), 0);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t crank = cluster_rank();
@@ -140,8 +141,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
         const int ct = (tile / P.n_out_tiles) * NP + int(pr), ot = tile % P.n_out_tiles;
+        // K1 running concurrently: this CTA's 128 W rows of the tile must be stamped
+        tc::wait_w_ready(P, int64_t(ct) * BN + int(rank) * BNC, int64_t(ct) * BN + int(rank + 1) * BNC);
         for (int kb = 0; kb < P.num_k_blocks; ++kb) {
-          tc::mbar_wait(&empty[stage], phase ^ 1u);
+          tc::mbar_wait_backoff(&empty[stage], phase ^ 1u);
           if (leader) tc::mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           if constexpr (NP == 1) {
             tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, ot * BM + int(rank) * BMC, &full[stage]);
@@ -168,9 +171,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tc_fence_after();
           const uint64_t ad = tc::make_smem_desc(sA + stage * A_BYTES);
           const uint64_t bd = tc::make_smem_desc(sB + stage * B_BYTES);
+#ifndef MPFEM_TC2_NOMMA  // diagnostic build only: operand stream + epilogue without MMAs
           #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             mma_pair(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), P.idesc, (kb | kk) != 0);
+#else
+          (void)ad; (void)bd;
+#endif
           commit_pair(&empty[stage], NP == 1 ? uint16_t(0x3) : uint16_t(0xF));
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t expo_or = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
       const int ct = (tile / P.n_out_tiles) * NP + int(pr), ot = tile % P.n_out_tiles;
-      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::mbar_wait_backoff(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int o = ot * BM + int(rank) * BMC + quarter * 32 + lane;
       const int32_t e = P.rows[o];
@@ -226,6 +233,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::tc_fence_before();
   __syncthreads();
   cluster_sync();  // the pair's MMAs and peer arrivals are done before TMEM is released
+  trace_mark(P.trace, 1024 + (blockIdx.x & 1023), 1);
   if (warp == 2) {
     tc::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),

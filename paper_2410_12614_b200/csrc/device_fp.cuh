@@ -11,6 +11,20 @@
 
 namespace mpfem_b200 {
 
+// Debug timeline (MPFEM_B200_TRACE=1): per CTA {start ns, end ns, SM id} in 3 words at
+// trace[3 * slot]. No-op when trace is NULL.
+__device__ __forceinline__ void trace_mark(unsigned long long* trace, int slot, int end) {
+  if (!trace || threadIdx.x != 0) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  trace[3 * slot + end] = t;
+  if (!end) {
+    unsigned int sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    trace[3 * slot + 2] = sm;
+  }
+}
+
 enum Fmt : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };
 enum FlagBits : uint32_t { kOverflow = 1u, kUnderflow = 2u, kInvalid = 4u, kDivzero = 8u };
 

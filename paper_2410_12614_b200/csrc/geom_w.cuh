@@ -63,7 +63,17 @@ struct GeomWParams {
   void* W;
   uint32_t* flags;
   int* error;              // set to 3 on a singular cell
+  // Concurrent K1/K2 (see run_cell_matrices): after a tile's W rows are written, its
+  // stamp ready[tile] is set to `epoch` with release semantics; K2 acquires it before its
+  // TMA reads those rows. NULL: K2 runs after K1 in stream order.
+  uint32_t* ready;
+  uint32_t epoch;
+  unsigned long long* trace;  // debug timeline (slots 0..1023), NULL normally
 };
+
+__device__ __forceinline__ void store_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // Storage rounding round_us(v) (one RNE conversion, subnormals kept) of a u_g value held
 // in double or float, returned in the element type T. FP events are accumulated cheaply
@@ -269,6 +279,7 @@ template <typename T, int UG, int US, int COEF>
 __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
   extern __shared__ double s_rule[];
   __shared__ CellGeo s_geo[2][kTileCells];
+  trace_mark(P.trace, blockIdx.x & 1023, 0);
   __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
@@ -429,8 +440,14 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       }
     }
     __syncthreads();  // tile done, next tile's geometry written
-    if (threadIdx.x == 0) s_next[buf] = 0;
+    if (threadIdx.x == 0) {
+      s_next[buf] = 0;
+      // cumulative release: the CTA's W stores (ordered before thread 0 by the barrier)
+      // are visible to a gpu-scope acquire of the stamp
+      if (P.ready) store_release_gpu(P.ready + tile, P.epoch);
+    }
   }
+  trace_mark(P.trace, blockIdx.x & 1023, 1);
   if constexpr (sizeof(T) == 2 && (UG == kFP32 || UG == kFP64))
     publish_flags(P.flags, fl | packed_store_flags<T>(sf));
   else

@@ -21,6 +21,11 @@ void launch_one(unsigned grid, cudaStream_t st, const GeomWParams& P) {
     // P8 has nq_pad = 736 (23.5 KB); keep three CTAs per SM for every degree
     CUDA_CHECK_K1(cudaFuncSetAttribute(geom_w_kernel<T, UG, US, COEF>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // full shared-memory carveout: an SM configured by K1 must still fit K2's 197 KB CTA
+    // when the two run concurrently
+    CUDA_CHECK_K1(cudaFuncSetAttribute(geom_w_kernel<T, UG, US, COEF>,
+                                       cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       int(cudaSharedmemCarveoutMaxShared)));
     smem_set = smem;
   }
   geom_w_kernel<T, UG, US, COEF><<<grid, kGeomThreads, smem, st>>>(P);
