@@ -146,6 +146,7 @@ struct mpfem_b200_setup_s {
   // concurrent K1/K2 (tcgen05 pair path): per-K1-tile W stamps and the call's epoch
   DevBuf d_ready;
   DevBuf d_trace;  // MPFEM_B200_TRACE=1: per-CTA timeline of the last call
+  DevBuf d_tile_ctr;  // K1 dynamic tile schedule (2 words, zero between launches)
   uint32_t epoch = 0;
   uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
   // host-API staging
@@ -253,6 +254,11 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
   P.ready = S.cur_ready;
   P.epoch = S.epoch;
   P.trace = static_cast<unsigned long long*>(S.d_trace.p);
+  static const bool dyn = [] {
+    const char* e = std::getenv("MPFEM_B200_K1_DYNAMIC");
+    return !(e && std::atoi(e) == 0);
+  }();
+  P.tile_ctr = dyn ? static_cast<uint32_t*>(S.d_tile_ctr.p) : nullptr;
   const int64_t tiles = (n + kTileCells - 1) / kTileCells;
   // concurrent with K2 (one 384-thread CTA per SM): two 256-thread K1 CTAs fit beside it
   int per_sm = S.cur_ready ? 2 : MPFEM_K1_MINB;
@@ -628,6 +634,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     CUDA_OK(cudaMemcpy(S->d_B.p, B.data(), sizeof(double) * B.size(), cudaMemcpyHostToDevice));
     S->d_flags.ensure(16);
     S->d_error.ensure(16);
+    S->d_tile_ctr.ensure(16);
+    CUDA_OK(cudaMemset(S->d_tile_ctr.p, 0, 16));
     CUDA_OK(cudaMemset(S->d_flags.p, 0, 16));
     CUDA_OK(cudaMemset(S->d_error.p, 0, 16));
     size_t tbytes = size_t(S->k_pad) * size_t(S->n_out_pad) * elem_size(S->w_type);

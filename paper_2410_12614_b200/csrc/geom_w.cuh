@@ -69,6 +69,10 @@ struct GeomWParams {
   uint32_t* ready;
   uint32_t epoch;
   unsigned long long* trace;  // debug timeline (slots 0..1023), NULL normally
+  // Dynamic tile schedule: tile_ctr[0] hands out tiles gridDim.x, gridDim.x + 1, ... to
+  // CTAs as they free up (static blockIdx.x first); tile_ctr[1] counts finished CTAs and
+  // the last one resets both to zero (no per-call memset). NULL: static grid stride.
+  uint32_t* tile_ctr;
 };
 
 __device__ __forceinline__ void store_release_gpu(uint32_t* p, uint32_t v) {
@@ -281,6 +285,7 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
   __shared__ CellGeo s_geo[2][kTileCells];
   trace_mark(P.trace, blockIdx.x & 1023, 0);
   __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
+  __shared__ int64_t s_tile[2];   // tile held by each geometry buffer
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
@@ -309,17 +314,27 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
   if (threadIdx.x < 2) s_next[threadIdx.x] = 0;
   __syncthreads();  // first tile's geometry, s_rule and the counters are ready
   int buf = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, buf ^= 1) {
+  for (int64_t tile = blockIdx.x; tile < n_tiles; buf ^= 1) {
     const int64_t c0 = tile * kTileCells;
     const int nc = tile_cells(tile);
-    const int64_t nt = tile + gridDim.x;
-    if (threadIdx.x < 32 && nt < n_tiles && lane < tile_cells(nt))
-      cell_geometry<UG>(P, nt * kTileCells + lane, s_geo[buf ^ 1][lane], fl);
+    if (threadIdx.x < 32) {
+      // warp 0: claim the next tile and compute its geometry into the other buffer
+      int64_t nt = tile + gridDim.x;
+      if (P.tile_ctr) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(P.tile_ctr, 1u);
+        nt = int64_t(gridDim.x) + __shfl_sync(0xffffffffu, g, 0);
+      }
+      if (lane == 0) s_tile[buf ^ 1] = nt;
+      if (nt < n_tiles && lane < tile_cells(nt))
+        cell_geometry<UG>(P, nt * kTileCells + lane, s_geo[buf ^ 1][lane], fl);
+    }
     const uint32_t items = uint32_t(nc * ngroups);
     const CellGeo* geo_t = s_geo[buf];
     while (true) {
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&s_next[buf], 32u);
+      if (lane == 0)  // plain shared atomic (atomicAdd would add warp-aggregation code)
+        asm volatile("atom.shared.add.u32 %0, [%1], 32;" : "=r"(base) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(&s_next[buf]))) : "memory");
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= items) break;
       const uint32_t it = base + lane;
@@ -359,19 +374,27 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
       // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192).
       // Points q >= n_q (only in a cell's last group) are exact zeros whatever G is.
-      bool pad[kQPT];
+      bool pad[kQPT];  // (the 16-bit path below uses the packed keep mask instead)
       #pragma unroll
       for (int j = 0; j < kQPT; ++j) pad[j] = q0 + j >= nq;
       if constexpr (sizeof(T) == 2 && (UG == kFP32 || UG == kFP64)) {
         // 16-bit storage: convert, pack two values per word, zero the padding halfwords
-        // (keep mask), and derive the FP events from the packed words: packed max of |bits|
-        // (>= the inf pattern: overflow / NaN) and packed min (below the smallest normal:
-        // candidate underflow, confirmed exactly on the rare block where it happens).
+        // (only in a cell's last group), and derive the FP events from the packed words:
+        // packed max of |bits| (>= the inf pattern: overflow / NaN) and packed min (below the
+        // smallest normal: candidate underflow, confirmed exactly on that block). The
+        // underflow flag is sticky, so once a thread has raised it the check is skipped
+        // (fp16 W underflows on most cells from p = 3 on).
         constexpr int KW = kQPT / 2;  // packed words per block
-        uint32_t keep[KW];
+        static_assert(kQPT == 4, "the packed keep mask assumes 4 points per thread");
+        // entries j < nv are quadrature points, the rest padding (only in a cell's last group)
+        const int nv = min(max(nq - q0, 0), kQPT);
+        const uint64_t km = nv >= kQPT ? ~0ull : ((1ull << (16 * nv)) - 1ull);
+        const uint32_t keep[KW] = {uint32_t(km), uint32_t(km >> 32)};
+        // points whose coefficient is exactly zero (their W entries are exact zeros)
+        uint32_t zqz[KW];
         #pragma unroll
         for (int k = 0; k < KW; ++k)
-          keep[k] = (pad[2 * k] ? 0u : 0x0000ffffu) | (pad[2 * k + 1] ? 0u : 0xffff0000u);
+          zqz[k] = (zq[2 * k] == 0.0 ? 0x0000ffffu : 0u) | (zq[2 * k + 1] == 0.0 ? 0xffff0000u : 0u);
         #pragma unroll
         for (int b = 0; b < 6; ++b) {
           if (b < nb) {
@@ -383,20 +406,23 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
               const uint32_t hi = storage_bits16<T>(w_value<UG, have_z>(om[2 * k + 1], gb, zq[2 * k + 1]));
               wd[k] = (lo | (hi << 16)) & keep[k];
             }
-            uint32_t bmin = 0xffffffffu;
             #pragma unroll
-            for (int k = 0; k < KW; ++k) {
-              const uint32_t m = wd[k] & 0x7fff7fffu;
-              sf.amax = __vmaxu2(sf.amax, m);
-              bmin = __vminu2(bmin, m | ~keep[k]);
-            }
-            if (min(bmin & 0xffffu, bmin >> 16) < Storage16<T>::kMinNormal && gb != 0.0) {
+            for (int k = 0; k < KW; ++k) sf.amax = __vmaxu2(sf.amax, wd[k] & 0x7fff7fffu);
+            if (!sf.tiny) {
+              // A nonzero stored value below the smallest normal is an underflow. A stored
+              // zero is one unless the exact value was zero: omega > 0 at quadrature points,
+              // so that needs G_b == 0 or a zero coefficient (an fp64 product underflowing
+              // to zero counts as underflow, as in fp_op).
+              uint32_t bmin = 0xffffffffu, zmask = 0;
               #pragma unroll
-              for (int j = 0; j < kQPT; ++j) {
-                const auto v = w_value<UG, have_z>(om[j], gb, zq[j]);
-                const uint32_t a16 = storage_bits16<T>(v) & 0x7fffu;
-                if (!pad[j] && a16 < Storage16<T>::kMinNormal && v != decltype(v)(0)) sf.tiny = 1;
+              for (int k = 0; k < KW; ++k) {
+                const uint32_t m = wd[k] & 0x7fff7fffu;
+                const uint32_t z = __vcmpeq2(m, 0u) & keep[k];
+                zmask |= z & ~zqz[k];
+                bmin = __vminu2(bmin, m | z | ~keep[k]);
               }
+              if (min(bmin & 0xffffu, bmin >> 16) < Storage16<T>::kMinNormal || (zmask && gb != 0.0))
+                sf.tiny = 1;
             }
             if constexpr (KW == 4)
               *reinterpret_cast<uint4*>(wrow + int64_t(b) * nqp) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
@@ -445,6 +471,15 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       // cumulative release: the CTA's W stores (ordered before thread 0 by the barrier)
       // are visible to a gpu-scope acquire of the stamp
       if (P.ready) store_release_gpu(P.ready + tile, P.epoch);
+    }
+    tile = s_tile[buf ^ 1];  // written by warp 0 before the barrier; rewritten only after the next one
+  }
+  if (P.tile_ctr && threadIdx.x == 0) {
+    // every CTA made its final (failing) claim before counting itself done
+    __threadfence();
+    if (atomicAdd(P.tile_ctr + 1, 1u) == gridDim.x - 1) {
+      P.tile_ctr[0] = 0;
+      P.tile_ctr[1] = 0;
     }
   }
   trace_mark(P.trace, blockIdx.x & 1023, 1);
