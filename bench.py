@@ -199,7 +199,7 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_sweep(mp, torch, dev):
+def run_sweep(mp, torch, dev, only=None):
     """BASELINE config 2: p = 1..8, mass and Poisson, mixed (bf16 storage) and fp64; cell
     count per p chosen so the outputs total 4 GiB (fp32: 2^32 / (4 n_phi^2))."""
     hbm, tc_peak, _, _ = peaks()
@@ -207,6 +207,8 @@ def run_sweep(mp, torch, dev):
     for p in range(1, 9):
         for form in (0, 1):
             for mode in ("mixed", "fp64"):
+                if only and (p, form, mode) not in only:
+                    continue
                 if mode == "mixed":
                     cfg = mp.KernelConfig(form=form, u_p=2, u_g=2, u_q=2, u_s=0, engine=2)
                     ob = 4
@@ -232,13 +234,18 @@ def run_sweep(mp, torch, dev):
                 e1.record()
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / reps
+                s.set_timing(True)
+                s.cell_matrices(vd, None, 1, out=out)
+                kt = s.last_timings()
+                s.set_timing(False)
                 f, b = work_per_cell(p, form, ob)
                 t_roof = max(n * f / (tc_peak * 1e12) if mode == "mixed" else 0.0, n * b / (hbm * 1e9))
                 res.append({"p": p, "form": "poisson" if form else "mass", "mode": mode, "cells": n,
                             "ms": ms, "cells_per_s": n / (ms * 1e-3),
                             "tflops_dense_equiv": n * f / (ms * 1e-3) / 1e12,
                             "hbm_gbs_algorithmic": n * b / (ms * 1e-3) / 1e9,
-                            "roofline_frac": (t_roof / (ms * 1e-3)) if mode == "mixed" else None})
+                            "roofline_frac": (t_roof / (ms * 1e-3)) if mode == "mixed" else None,
+                            "path": s.path, "kernels_ms": kt})
                 del s, out, vd
                 torch.cuda.empty_cache()
     return res
@@ -429,6 +436,21 @@ def main():
         e2e_ms = max_over_ranks(torch, e2e_ms, dev)
     e2e_value = world * N_CELLS / (e2e_ms * 1e-3)
 
+    # ---- accuracy of the timed output against the device fp64 mode (u_p = u_g = u_q = u_s =
+    # fp64, the path pinned to the fp64 oracle by tests/test_gpu_cells.py) on the same cells
+    s64 = mp.make_setup(P_DEG, mp.KernelConfig(form=mp.FormKind.poisson))
+    a64 = s64.cell_matrices(vd, None, mp.CoefKind.sincosexp)
+    step()
+    torch.cuda.synchronize()
+    diff = (out.view(N_CELLS, -1).double() - a64.view(N_CELLS, -1)).abs().amax(dim=1)
+    err = (diff / a64.view(N_CELLS, -1).abs().amax(dim=1)).cpu().numpy()
+    del a64, s64, diff
+    u_s = 2.0 ** -11  # fp16 unit roundoff
+    accuracy = {"vs": "device fp64 mode (oracle-pinned), same cells",
+                "metric": "per-cell max|A - A64| / max|A64| (errorlab.cpp:90-99)",
+                "max_err_rel": float(err.max()), "median_err_rel": float(np.median(err)),
+                "max_err_over_u_s": float(err.max() / u_s), "u_s": "fp16"}
+
     f_cell, b_cell = work_per_cell(P_DEG, 1, 4)
     flops_launch = N_CELLS * f_cell
     achieved_tflops = flops_launch / (k2_ms * 1e-3) / 1e12
@@ -456,6 +478,7 @@ def main():
                 "d2h_bytes_per_step": int(out_host_np.nbytes), "ms_per_step": e2e_ms},
         "gpu_launches": launches,
         "clocks": clocks,
+        "accuracy": accuracy,
     }
     if not args.no_assembly:
         line["assembly"] = {"workload": "config4: 96^3 x 6 tets, poisson P2/P3, mixed-bf16 kernels, "

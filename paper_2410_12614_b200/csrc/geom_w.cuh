@@ -385,11 +385,12 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
         // underflow flag is sticky, so once a thread has raised it the check is skipped
         // (fp16 W underflows on most cells from p = 3 on).
         constexpr int KW = kQPT / 2;  // packed words per block
-        static_assert(kQPT == 4, "the packed keep mask assumes 4 points per thread");
         // entries j < nv are quadrature points, the rest padding (only in a cell's last group)
-        const int nv = min(max(nq - q0, 0), kQPT);
-        const uint64_t km = nv >= kQPT ? ~0ull : ((1ull << (16 * nv)) - 1ull);
-        const uint32_t keep[KW] = {uint32_t(km), uint32_t(km >> 32)};
+        const int nv = nq - q0;
+        uint32_t keep[KW];
+        #pragma unroll
+        for (int k = 0; k < KW; ++k)
+          keep[k] = (2 * k < nv ? 0x0000ffffu : 0u) | (2 * k + 1 < nv ? 0xffff0000u : 0u);
         // points whose coefficient is exactly zero (their W entries are exact zeros)
         uint32_t zqz[KW];
         #pragma unroll
