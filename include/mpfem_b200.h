@@ -179,6 +179,16 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
                         void* values, int fmt, int mode, int accumulate, const int32_t* rows,
                         int64_t n_rows, void* stream);
 
+/* Deterministic assemble_matrix without the seg_ptr/perm plan (the default full-matrix
+ * deterministic path): rows pull their incident (cell, local row) pairs from the
+ * incidence lists (mpfem_b200_incidence, ascending cell order) and the CSR positions from
+ * pos_map; values are bitwise those of mode 1 of mpfem_b200_assemble (the reference's
+ * ascending-cell sequential sum, assembly.cpp:50-67). Arguments as mpfem_b200_assemble. */
+int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
+                             int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
+                             const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
+                             void* values, int fmt, int accumulate, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,12 +98,17 @@ def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: 
 
 def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
                     mode: int = DETERMINISTIC, cell_begin: int = 0, cell_end: int | None = None,
-                    rows=None, accumulate: bool = False, values=None, stream=None):
+                    rows=None, accumulate: bool = False, values=None, stream=None,
+                    pull: bool | None = None):
     """assemble_matrix (assembly.cpp:41-88) into CSR values at fmt (fp32/fp64).
 
     `local` holds the local matrices of cells [cell_begin, cell_end), (n, n_loc, n_loc)
     fp32 or fp64. Deterministic mode reproduces the reference's ascending-cell sequential
-    sum bitwise; atomic mode is order-free (within gamma_{m+1} of the exact sum)."""
+    sum bitwise; atomic mode is order-free (within gamma_{m+1} of the exact sum).
+    Deterministic mode gathers each entry's segment through the seg_ptr/perm plan (block-
+    staged in shared memory). Patterns built with deterministic_plan=False (no seg_ptr/perm:
+    18 GB less at config-4 P3) use the row-pull kernel instead (pull=True forces it), which
+    replays the incidence lists in ascending cell order -- the same bits, about 2x slower."""
     import torch
     if cell_end is None:
         cell_end = cell_begin + int(local.shape[0])
@@ -119,6 +124,16 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
     n_rows = 0 if rows is None else int(rows.numel())
     if pat.pos_map is None:
         raise ConfigError("assemble_matrix needs a pattern built with plan=True")
+    if pull is None:
+        pull = pat.seg_ptr is None
+    if mode == DETERMINISTIC and rows is None and pull:
+        # row-pull: incidence lists + pos_map, no seg_ptr/perm plan needed
+        check(lib().mpfem_b200_assemble_pull(_ptr(local), lf, int(cell_begin), int(cell_end),
+                                             dm.n_local, _ptr(pat.row_ptr), dm.n_dofs,
+                                             _ptr(pat.inc_ptr), _ptr(pat.inc), _ptr(pat.pos_map),
+                                             _ptr(values), int(fmt), int(accumulate),
+                                             _stream_handle(stream)))
+        return values
     check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), dm.n_local,
                                     _ptr(pat.row_ptr), dm.n_dofs, _ptr(pat.pos_map),
                                     _ptr(pat.seg_ptr), _ptr(pat.perm), _ptr(values), int(fmt),

@@ -367,6 +367,196 @@ __global__ void assemble_seg_kernel(const TL* __restrict__ locals, int64_t per_c
     entry_sum(locals, per_cell, seg_ptr, perm, e, cell_begin, cell_end, init, values);
 }
 
+// Block-staged deterministic scatter: a CTA takes kSegBlock consecutive CSR entries, stages
+// their segment offsets, gathers every contribution of the block into shared memory with
+// independent coalesced perm loads (4 in flight per thread), then each thread sums its
+// entries' segments sequentially from shared memory. Contributions of cells outside
+// [cell_begin, cell_end) are replaced by -0.0, which leaves any IEEE sum unchanged
+// (x + -0 == x, +0 + -0 == +0), so values are bitwise those of entry_sum. Blocks with more
+// than `cap` contributions fall back to entry_sum.
+#ifndef MPFEM_SEG_BLOCK
+#define MPFEM_SEG_BLOCK 512
+#endif
+#ifndef MPFEM_SEG_SMEM_KB
+#define MPFEM_SEG_SMEM_KB 24
+#endif
+#ifndef MPFEM_SEG_CTAS
+#define MPFEM_SEG_CTAS 8
+#endif
+constexpr int kSegBlock = MPFEM_SEG_BLOCK;
+constexpr int kSegSmem = MPFEM_SEG_SMEM_KB * 1024;  // dynamic shared memory per CTA
+constexpr int kSegCtasPerSm = MPFEM_SEG_CTAS;
+template <typename TL, typename TV>
+__global__ void __launch_bounds__(256) assemble_seg_block_kernel(
+    const TL* __restrict__ locals, int64_t per_cell, const int64_t* __restrict__ seg_ptr,
+    const uint32_t* __restrict__ perm, int64_t nnz, int64_t cell_begin, int64_t cell_end, int init,
+    int cap, TV* __restrict__ values) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int64_t* s_seg = reinterpret_cast<int64_t*>(smem_raw);
+  TV* s_val = reinterpret_cast<TV*>(s_seg + kSegBlock + 1);
+  const int64_t kb = cell_begin * per_cell, ke = cell_end * per_cell;
+  const int64_t n_blocks = (nnz + kSegBlock - 1) / kSegBlock;
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
+    const int64_t e0 = blk * kSegBlock;
+    const int n = int((nnz - e0 < kSegBlock ? nnz - e0 : int64_t(kSegBlock)));
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) s_seg[i] = seg_ptr[e0 + i];
+    __syncthreads();
+    const int64_t t0 = s_seg[0];
+    const int64_t tn = s_seg[n] - t0;
+    if (tn <= cap) {
+      const int T = int(tn);
+      for (int t = threadIdx.x; t < T; t += 4 * blockDim.x) {
+        int64_t k[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tt = t + u * int(blockDim.x);
+          k[u] = tt < T ? int64_t(perm[t0 + tt]) : -1;
+        }
+        TV x[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u)
+          x[u] = (k[u] >= kb && k[u] < ke) ? cast_value<TL, TV>(locals[k[u]]) : TV(-0.0);
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tt = t + u * int(blockDim.x);
+          if (tt < T) s_val[tt] = x[u];
+        }
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        TV acc = init ? TV(-0.0) : values[e0 + i];
+        const int b = int(s_seg[i] - t0), en = int(s_seg[i + 1] - t0);
+        for (int t = b; t < en; ++t) acc = acc + s_val[t];
+        values[e0 + i] = acc;
+      }
+    } else {
+      for (int i = threadIdx.x; i < n; i += blockDim.x)
+        entry_sum(locals, per_cell, seg_ptr, perm, e0 + i, cell_begin, cell_end, init, values);
+    }
+    __syncthreads();
+  }
+}
+
+// Row-pull deterministic scatter (no seg_ptr/perm plan): a CTA takes kPullRows rows; for
+// each row its incident (cell, local row i) pairs come from the incidence list in ascending
+// cell order (inc is sorted by (dof, position)). All local entries of those pairs -- the
+// contiguous n_loc-wide rows of the local matrices -- and their CSR positions (pos_map) are
+// gathered into shared memory with independent coalesced loads; then one warp per row
+// replays the pairs in ascending cell order, lanes adding the pair's n_loc entries into
+// distinct accumulators. Each CSR entry therefore receives its contributions in ascending
+// cell order starting from -0.0: bitwise the reference's sequential sum (assembly.cpp:50-67)
+// and entry_sum. Batches beyond the shared-memory caps run the same replay on global memory.
+constexpr int kPullRows = 16;
+struct PullCaps {
+  int entries, pairs, inc;
+};
+template <typename TV>
+__host__ __device__ constexpr PullCaps pull_caps() {
+  return PullCaps{2048, 4096, 256};
+}
+template <typename TV>
+__host__ __device__ constexpr size_t pull_smem_bytes() {
+  constexpr PullCaps c = pull_caps<TV>();
+  return sizeof(TV) * (c.entries + c.pairs) + sizeof(int32_t) * c.pairs + sizeof(int64_t) * c.inc +
+         2 * sizeof(int64_t) * (kPullRows + 1);
+}
+template <typename TL, typename TV>
+__global__ void __launch_bounds__(256) assemble_pull_kernel(
+    const TL* __restrict__ locals, int64_t per_cell, int n_loc, const int64_t* __restrict__ row_ptr,
+    const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
+    const int32_t* __restrict__ pos_map, int32_t n_rows, int64_t cell_begin, int64_t cell_end,
+    int init, TV* __restrict__ values) {
+  constexpr PullCaps cap = pull_caps<TV>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TV* s_acc = reinterpret_cast<TV*>(smem_raw);
+  TV* s_x = s_acc + cap.entries;
+  int64_t* s_inc = reinterpret_cast<int64_t*>(s_x + cap.pairs);
+  int64_t* s_rp = s_inc + cap.inc;
+  int64_t* s_ip = s_rp + (kPullRows + 1);
+  int32_t* s_p = reinterpret_cast<int32_t*>(s_ip + (kPullRows + 1));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int64_t n_batches = (int64_t(n_rows) + kPullRows - 1) / kPullRows;
+  const uint32_t nl = uint32_t(n_loc);
+  for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
+    const int64_t r0 = b * kPullRows;
+    const int nr = int(int64_t(n_rows) - r0 < kPullRows ? int64_t(n_rows) - r0 : int64_t(kPullRows));
+    if (threadIdx.x <= nr) {
+      s_rp[threadIdx.x] = row_ptr[r0 + threadIdx.x];
+      s_ip[threadIdx.x] = inc_ptr[r0 + threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t e0 = s_rp[0], i0 = s_ip[0];
+    const int64_t ne = s_rp[nr] - e0, ni = s_ip[nr] - i0, np = ni * n_loc;
+    if (ne <= cap.entries && ni <= cap.inc && np <= cap.pairs) {
+      for (int e = threadIdx.x; e < int(ne); e += blockDim.x) s_acc[e] = init ? TV(-0.0) : values[e0 + e];
+      for (int t = threadIdx.x; t < int(ni); t += blockDim.x) s_inc[t] = inc[i0 + t];
+      __syncthreads();
+      for (int q = threadIdx.x; q < int(np); q += 4 * blockDim.x) {
+        int64_t k[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = q + u * int(blockDim.x);
+          k[u] = -1;
+          if (qq < int(np)) {
+            const uint32_t t = uint32_t(qq) / nl, j = uint32_t(qq) - t * nl;
+            const int64_t ki = s_inc[t];
+            const int64_t cell = ki / n_loc;
+            if (cell >= cell_begin && cell < cell_end) k[u] = cell * per_cell + (ki - cell * n_loc) * n_loc + j;
+          }
+        }
+        TV x[4];
+        int32_t pp[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          x[u] = k[u] >= 0 ? cast_value<TL, TV>(locals[k[u]]) : TV(-0.0);
+          pp[u] = k[u] >= 0 ? int32_t(int64_t(pos_map[k[u]]) - e0) : -1;
+        }
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = q + u * int(blockDim.x);
+          if (qq < int(np)) {
+            s_x[qq] = x[u];
+            s_p[qq] = pp[u];
+          }
+        }
+      }
+      __syncthreads();
+      for (int rr = warp; rr < nr; rr += nwarps) {
+        const int t1 = int(s_ip[rr + 1] - i0);
+        for (int t = int(s_ip[rr] - i0); t < t1; ++t) {
+          for (int j = lane; j < n_loc; j += 32) {
+            const int q = t * n_loc + j, pq = s_p[q];
+            if (pq >= 0) s_acc[pq] = s_acc[pq] + s_x[q];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < int(ne); e += blockDim.x) values[e0 + e] = s_acc[e];
+    } else {
+      // oversized batch: the same ordered replay, one warp per row, on global memory
+      for (int rr = warp; rr < nr; rr += nwarps) {
+        const int64_t ra = s_rp[rr], rb = s_rp[rr + 1];
+        if (init)
+          for (int64_t e = ra + lane; e < rb; e += 32) values[e] = TV(-0.0);
+        __syncwarp();
+        for (int64_t t = s_ip[rr]; t < s_ip[rr + 1]; ++t) {
+          const int64_t ki = inc[t], cell = ki / n_loc;
+          if (cell >= cell_begin && cell < cell_end) {
+            const int64_t kbase = cell * per_cell + (ki - cell * n_loc) * n_loc;
+            for (int j = lane; j < n_loc; j += 32) {
+              const int64_t pos = pos_map[kbase + j];
+              values[pos] = values[pos] + cast_value<TL, TV>(locals[kbase + j]);
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Same for a list of rows: one warp per row, lanes over the row's entries.
 template <typename TL, typename TV>
 __global__ void assemble_seg_rows_kernel(const TL* __restrict__ locals, int64_t per_cell,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -315,6 +316,46 @@ int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc
   });
 }
 
+int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
+                             int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
+                             const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
+                             void* values, int fmt, int accumulate, void* stream) {
+  return aguard([&] {
+    if (locals_fmt != 2 && locals_fmt != 3) throw AsmError{2, "local matrices must be fp32 or fp64"};
+    if (fmt != 2 && fmt != 3) throw AsmError{2, "CSR values must be fp32 or fp64"};
+    if (cell_end < cell_begin || n_loc < 1) throw AsmError{2, "bad cell range"};
+    if (!row_ptr || !inc_ptr || !inc || !pos_map)
+      throw AsmError{2, "row-pull assembly needs row_ptr, the incidence lists and pos_map"};
+    if (n_dofs == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t per_cell = int64_t(n_loc) * n_loc;
+    const size_t esz = locals_fmt == 2 ? 4 : 8;
+    const char* base = static_cast<const char*>(locals) - size_t(cell_begin) * size_t(per_cell) * esz;
+    const int init = accumulate ? 0 : 1;
+    const int64_t batches = (int64_t(n_dofs) + asmb::kPullRows - 1) / asmb::kPullRows;
+#define MPFEM_PULL(TL, TV)                                                                         \
+  {                                                                                                \
+    constexpr size_t smem = asmb::pull_smem_bytes<TV>();                                           \
+    static bool attr = false;                                                                      \
+    if (!attr) {                                                                                   \
+      ACUDA(cudaFuncSetAttribute(asmb::assemble_pull_kernel<TL, TV>,                               \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));         \
+      attr = true;                                                                                 \
+    }                                                                                              \
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(batches, 148 * 8)));    \
+    asmb::assemble_pull_kernel<TL, TV><<<grid, 256, smem, st>>>(                                   \
+        reinterpret_cast<const TL*>(base), per_cell, n_loc, row_ptr, inc_ptr, inc, pos_map,        \
+        n_dofs, cell_begin, cell_end, init, static_cast<TV*>(values));                             \
+  }
+    if (locals_fmt == 2 && fmt == 2) MPFEM_PULL(float, float)
+    else if (locals_fmt == 2) MPFEM_PULL(float, double)
+    else if (fmt == 2) MPFEM_PULL(double, float)
+    else MPFEM_PULL(double, double)
+#undef MPFEM_PULL
+    ACUDA(cudaGetLastError());
+  });
+}
+
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, int64_t cell_end,
                         int n_loc, const int64_t* row_ptr, int32_t n_dofs, const int32_t* pos_map,
                         const int64_t* seg_ptr, const uint32_t* perm, void* values, int fmt,
@@ -360,8 +401,26 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, 
 #undef MPFEM_SEG_ROWS
       } else {
         const int64_t nnz = read1(row_ptr + n_dofs, st);
-        const unsigned grid = grid_for(nnz);
-#define MPFEM_SEG(TL, TV) asmb::assemble_seg_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, static_cast<TV*>(values))
+        // block-staged gather (bitwise the per-entry sum); MPFEM_B200_SEG_BLOCK=0: per entry
+        static const bool blocked = [] {
+          const char* e = std::getenv("MPFEM_B200_SEG_BLOCK");
+          return !(e && std::atoi(e) == 0);
+        }();
+        const size_t vsz = fmt == 2 ? 4 : 8;
+        const int cap = int((asmb::kSegSmem - (asmb::kSegBlock + 1) * 8) / vsz);
+        const size_t smem = (asmb::kSegBlock + 1) * 8 + size_t(cap) * vsz;
+        const unsigned grid =
+            blocked ? unsigned(std::max<int64_t>(1, std::min<int64_t>((nnz + asmb::kSegBlock - 1) / asmb::kSegBlock,
+                                                                      148 * asmb::kSegCtasPerSm)))
+                    : grid_for(nnz);
+#define MPFEM_SEG(TL, TV)                                                                          \
+  if (blocked)                                                                                     \
+    asmb::assemble_seg_block_kernel<TL, TV><<<grid, 256, smem, st>>>(                              \
+        reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end,     \
+        init, cap, static_cast<TV*>(values));                                                      \
+  else                                                                                             \
+    asmb::assemble_seg_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base),    \
+        per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, static_cast<TV*>(values))
         if (locals_fmt == 2 && fmt == 2) MPFEM_SEG(float, float);
         else if (locals_fmt == 2) MPFEM_SEG(float, double);
         else if (fmt == 2) MPFEM_SEG(double, float);

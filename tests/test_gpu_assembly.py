@@ -38,9 +38,11 @@ def test_dofmap_known_answers(oracle):
         assert gpu_dofmap(p, verts, cells).n_dofs == (p * n + 1) ** 3
 
 
-@pytest.mark.parametrize("p", [1, 2, 3])
-def test_csr_pattern_and_values_bitwise(oracle, p):
-    verts, cells = oracle.structured_tet_mesh(4, 3, 3, 1.0, 0.15, 11)
+@pytest.mark.parametrize("p,dims", [(1, (4, 3, 3)), (2, (4, 3, 3)), (3, (4, 3, 3)), (6, (2, 2, 1))])
+def test_csr_pattern_and_values_bitwise(oracle, p, dims):
+    # p = 6 (n_loc = 84): row batches exceed the row-pull kernel's shared-memory caps, so its
+    # global-memory replay is exercised too
+    verts, cells = oracle.structured_tet_mesh(*dims, 1.0, 0.15, 11)
     cd, nd, _ = oracle.build_dofmap(p, verts, cells)
     dm = gpu_dofmap(p, verts, cells)
     pat = am.csr_pattern(dm)
@@ -56,6 +58,10 @@ def test_csr_pattern_and_values_bitwise(oracle, p):
         torch.cuda.synchronize()
         got = v.double().cpu().numpy()
         assert np.array_equal(got.view(np.uint64), vals.view(np.uint64)), fmt
+        # the plan-free row-pull path gives the same bits
+        vs = am.assemble_matrix(torch.from_numpy(loc32).cuda(), dm, pat, fmt, am.DETERMINISTIC,
+                                pull=True)
+        assert np.array_equal(vs.double().cpu().numpy().view(np.uint64), vals.view(np.uint64)), fmt
         # atomic mode: gamma_{m+1} * sum |contrib|
         va = am.assemble_matrix(torch.from_numpy(loc32).cuda(), dm, pat, fmt, am.ATOMIC)
         torch.cuda.synchronize()
@@ -81,11 +87,12 @@ def test_partial_cell_ranges_compose_bitwise(oracle):
     loc = torch.from_numpy(rng.uniform(-1, 1, size=(cells.shape[0], 10, 10)).astype(np.float32)).cuda()
     full = am.assemble_matrix(loc, dm, pat, 2)
     k = cells.shape[0] // 2
-    part = am.assemble_matrix(loc[:k], dm, pat, 2, cell_begin=0, cell_end=k)
-    part = am.assemble_matrix(loc[k:], dm, pat, 2, cell_begin=k, cell_end=cells.shape[0],
-                              accumulate=True, values=part)
-    torch.cuda.synchronize()
-    assert torch.equal(full.view(torch.int32), part.view(torch.int32))
+    for pull in (False, True):
+        part = am.assemble_matrix(loc[:k], dm, pat, 2, cell_begin=0, cell_end=k, pull=pull)
+        part = am.assemble_matrix(loc[k:], dm, pat, 2, cell_begin=k, cell_end=cells.shape[0],
+                                  accumulate=True, values=part, pull=pull)
+        torch.cuda.synchronize()
+        assert torch.equal(full.view(torch.int32), part.view(torch.int32)), pull
 
 
 def test_config4_reduced_end_to_end(oracle):
