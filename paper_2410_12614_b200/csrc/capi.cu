@@ -225,6 +225,18 @@ void choose_path(mpfem_b200_setup_s& S) {
   }
 }
 
+// K1 tile height: one geometry lane per cell, so a tile of 32 G cells has G geometry warps.
+// Low degrees have few quadrature groups per cell and would wait on a single geometry warp.
+int k1_geom_warps(const mpfem_b200_setup_s& S) {
+  static const int env = [] {
+    const char* e = std::getenv("MPFEM_B200_K1_GEOM_WARPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return std::min(env, 8);
+  const int ngroups = S.nq_pad / kQPT;
+  return std::max(1, std::min(4, 32 / ngroups));
+}
+
 void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
                  int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
                  int w_type, cudaStream_t st) {
@@ -259,7 +271,9 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
     return !(e && std::atoi(e) == 0);
   }();
   P.tile_ctr = dyn ? static_cast<uint32_t*>(S.d_tile_ctr.p) : nullptr;
-  const int64_t tiles = (n + kTileCells - 1) / kTileCells;
+  P.geom_warps = k1_geom_warps(S);
+  const int64_t tile_cells = 32 * P.geom_warps;
+  const int64_t tiles = (n + tile_cells - 1) / tile_cells;
   // concurrent with K2 (one 384-thread CTA per SM): two 256-thread K1 CTAs fit beside it
   int per_sm = S.cur_ready ? 2 : MPFEM_K1_MINB;
   if (const char* e = std::getenv("MPFEM_B200_K1_PER_SM")) per_sm = std::max(1, std::atoi(e));
@@ -330,7 +344,7 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     P.flags = static_cast<uint32_t*>(S.d_flags.p);
     P.ready = S.cur_ready;
     P.epoch = S.epoch;
-    P.k1_tile = kTileCells;
+    P.k1_tile = 32 * k1_geom_warps(S);
     P.error = static_cast<int*>(S.d_error.p);
     P.trace = static_cast<unsigned long long*>(S.d_trace.p);
     if (S.pair == 2) {
@@ -457,7 +471,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   const bool concurrent = S.path == kPathTC && S.pair && !S.timing && n_chunks == 1 &&
                           ov_env && std::atoi(ov_env) != 0;
   if (concurrent) {
-    const int64_t k1_tiles = (n + kTileCells - 1) / kTileCells;
+    const int64_t k1_tiles = (n + 32 * k1_geom_warps(S) - 1) / (32 * k1_geom_warps(S));
     const size_t need = size_t(k1_tiles) * sizeof(uint32_t);
     if (++S.epoch == 0) S.epoch = 1;
     if (need > S.d_ready.bytes || S.epoch == 1) {
@@ -638,7 +652,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     CUDA_OK(cudaMemset(S->d_tile_ctr.p, 0, 16));
     CUDA_OK(cudaMemset(S->d_flags.p, 0, 16));
     CUDA_OK(cudaMemset(S->d_error.p, 0, 16));
-    size_t tbytes = size_t(S->k_pad) * size_t(S->n_out_pad) * elem_size(S->w_type);
+    const int64_t t_rows = S->n_out_pad;
+    size_t tbytes = size_t(S->k_pad) * size_t(t_rows) * elem_size(S->w_type);
     if (S->path == kPathFused) {
       // fp32 T[k][o] with k = block * n_q + q (no padding), values rounded to u_s
       const int64_t kf = int64_t(S->n_blocks) * S->n_q;
@@ -650,12 +665,12 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     }
     if (tbytes) S->d_T.ensure(tbytes);
     const int transposed = S->path == kPathTC;
-    const int64_t total = tbytes ? S->k_pad * S->n_out_pad : 0;
+    const int64_t total = tbytes ? S->k_pad * t_rows : 0;
     const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
     const double* dB = static_cast<const double*>(S->d_B.p);
     if (total) switch (S->w_type) {
-      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
-      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
+      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, t_rows, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
+      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, t_rows, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
       case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
       default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
     }

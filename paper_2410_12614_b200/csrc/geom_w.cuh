@@ -73,6 +73,7 @@ struct GeomWParams {
   // CTAs as they free up (static blockIdx.x first); tile_ctr[1] counts finished CTAs and
   // the last one resets both to zero (no per-call memset). NULL: static grid stride.
   uint32_t* tile_ctr;
+  int geom_warps;          // warps computing the next tile's geometry; tile = 32 * geom_warps cells
 };
 
 __device__ __forceinline__ void store_release_gpu(uint32_t* p, uint32_t v) {
@@ -275,19 +276,22 @@ __device__ __forceinline__ uint32_t packed_store_flags(const StoreFlags& sf) {
          (sf.tiny ? kUnderflow : 0u);
 }
 
-// dynamic shared memory of geom_w_kernel: weights and the three point coordinates,
-// each nq_pad doubles in [j][group] order
-__host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad) { return size_t(4) * nq_pad * sizeof(double); }
+// dynamic shared memory of geom_w_kernel: weights and the three point coordinates, each
+// nq_pad doubles in [j][group] order, then the two geometry buffers of 32 * geom_warps cells
+__host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad, int geom_warps = 1) {
+  return size_t(4) * nq_pad * sizeof(double) + size_t(2) * 32 * geom_warps * sizeof(CellGeo);
+}
 
 template <typename T, int UG, int US, int COEF>
 __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
   extern __shared__ double s_rule[];
-  __shared__ CellGeo s_geo[2][kTileCells];
   trace_mark(P.trace, blockIdx.x & 1023, 0);
   __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
-  __shared__ int64_t s_tile[2];   // tile held by each geometry buffer
+  __shared__ int64_t s_tile[3];   // claimed tiles, ring indexed by iteration mod 3
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
+  const int tcells = 32 * P.geom_warps;  // cells per tile
+  CellGeo* s_geo0 = reinterpret_cast<CellGeo*>(s_rule + 4 * nqp);  // [2][tcells]
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
   const int nb = P.poisson ? 6 : 1;
   double* sW = s_rule;
@@ -301,36 +305,40 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
   }
   uint32_t fl = 0;
   StoreFlags sf;
-  const int64_t n_tiles = (P.n_cells + kTileCells - 1) / kTileCells;
+  const int64_t n_tiles = (P.n_cells + tcells - 1) / tcells;
   const int lane = threadIdx.x & 31;
   auto tile_cells = [&](int64_t t) {
-    const int64_t left = P.n_cells - t * kTileCells;
-    return left < kTileCells ? int(left) : kTileCells;
+    const int64_t left = P.n_cells - t * tcells;
+    return left < tcells ? int(left) : tcells;
   };
-  // Tile pipeline: warp 0 computes the geometry of the CTA's next tile into the other
-  // buffer while every warp (warp 0 once done) takes 32-item grabs of the current tile.
+  // Tiles are claimed one iteration ahead of their geometry: static blockIdx.x first, then
+  // gridDim.x + atomicAdd(tile_ctr) (or the grid stride without a counter).
+  int64_t static_next = int64_t(blockIdx.x) + gridDim.x;
+  auto claim = [&]() -> int64_t {
+    if (P.tile_ctr) return int64_t(gridDim.x) + atomicAdd(P.tile_ctr, 1u);
+    const int64_t t = static_next;
+    static_next += gridDim.x;
+    return t;
+  };
+  // Tile pipeline: the first geom_warps warps compute the geometry of the CTA's next tile
+  // (one lane per cell) into the other buffer while every warp takes 32-item grabs of the
+  // current tile.
   if (blockIdx.x < n_tiles && threadIdx.x < tile_cells(blockIdx.x))
-    cell_geometry<UG>(P, int64_t(blockIdx.x) * kTileCells + threadIdx.x, s_geo[0][threadIdx.x], fl);
+    cell_geometry<UG>(P, int64_t(blockIdx.x) * tcells + threadIdx.x, s_geo0[threadIdx.x], fl);
   if (threadIdx.x < 2) s_next[threadIdx.x] = 0;
-  __syncthreads();  // first tile's geometry, s_rule and the counters are ready
+  if (threadIdx.x == 0) s_tile[1] = claim();
+  __syncthreads();  // first tile's geometry, s_rule, the counters and the next claim are ready
   int buf = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; buf ^= 1) {
-    const int64_t c0 = tile * kTileCells;
+  int slot = 0;  // iteration mod 3
+  for (int64_t tile = blockIdx.x; tile < n_tiles; buf ^= 1, slot = slot == 2 ? 0 : slot + 1) {
+    const int64_t c0 = tile * tcells;
     const int nc = tile_cells(tile);
-    if (threadIdx.x < 32) {
-      // warp 0: claim the next tile and compute its geometry into the other buffer
-      int64_t nt = tile + gridDim.x;
-      if (P.tile_ctr) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(P.tile_ctr, 1u);
-        nt = int64_t(gridDim.x) + __shfl_sync(0xffffffffu, g, 0);
-      }
-      if (lane == 0) s_tile[buf ^ 1] = nt;
-      if (nt < n_tiles && lane < tile_cells(nt))
-        cell_geometry<UG>(P, nt * kTileCells + lane, s_geo[buf ^ 1][lane], fl);
-    }
+    const int64_t nt = s_tile[slot == 2 ? 0 : slot + 1];
+    if (threadIdx.x == 0) s_tile[slot == 0 ? 2 : slot - 1] = claim();  // the tile after next
+    if (threadIdx.x < tcells && nt < n_tiles && int(threadIdx.x) < tile_cells(nt))
+      cell_geometry<UG>(P, nt * tcells + threadIdx.x, s_geo0[(buf ^ 1) * tcells + threadIdx.x], fl);
     const uint32_t items = uint32_t(nc * ngroups);
-    const CellGeo* geo_t = s_geo[buf];
+    const CellGeo* geo_t = s_geo0 + buf * tcells;
     while (true) {
       uint32_t base = 0;
       if (lane == 0)  // plain shared atomic (atomicAdd would add warp-aggregation code)
@@ -473,7 +481,7 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       // are visible to a gpu-scope acquire of the stamp
       if (P.ready) store_release_gpu(P.ready + tile, P.epoch);
     }
-    tile = s_tile[buf ^ 1];  // written by warp 0 before the barrier; rewritten only after the next one
+    tile = nt;
   }
   if (P.tile_ctr && threadIdx.x == 0) {
     // every CTA made its final (failing) claim before counting itself done

@@ -15,7 +15,7 @@ namespace mpfem_b200 {
 namespace {
 template <typename T, int UG, int US, int COEF>
 void launch_one(unsigned grid, cudaStream_t st, const GeomWParams& P) {
-  const size_t smem = geom_w_smem_bytes(P.nq_pad);
+  const size_t smem = geom_w_smem_bytes(P.nq_pad, P.geom_warps);
   static size_t smem_set = 0;
   if (smem > smem_set) {
     // P8 has nq_pad = 736 (23.5 KB); keep three CTAs per SM for every degree
