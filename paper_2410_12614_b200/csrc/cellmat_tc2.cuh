@@ -3,7 +3,7 @@
 // Same GEMM as cellmat_tc.cuh (D^T[o, c] = sum_k Tt[o, k] W[c, k]), but each 2-CTA cluster
 // computes a 256-output x 256-cell tile with one M=256 MMA per K=16 step:
 //   * each CTA stages its own 128 output rows of Tt and its own 128 cells of W per stage
-//     (32 KB, 6 stages in 192 KB): per-SM operand traffic is 2/3 of the 1-CTA kernel's and
+//     (32 KB, 7 stages in 224 KB): per-SM operand traffic is 2/3 of the 1-CTA kernel's and
 //     the pipeline holds 1.5x more MMA work in flight;
 //   * only the leader (cluster rank 0) arms the full barriers (expect_tx of both CTAs'
 //     bytes; the peer's TMA completes on the leader's barrier) and issues the MMAs;
@@ -21,7 +21,10 @@ constexpr int BMC = 128;       // outputs per CTA (TMEM lanes)
 constexpr int BN = 256;        // cells per pair tile (MMA N; each CTA stages 128)
 constexpr int BNC = 128;
 constexpr int BK = 64;
-constexpr int STAGES = 6;
+#ifndef MPFEM_TC2_STAGES
+#define MPFEM_TC2_STAGES 7  // 7 x 32 KB + barriers = 225 KB (measured 119 -> 115 us at config 1)
+#endif
+constexpr int STAGES = MPFEM_TC2_STAGES;
 constexpr int A_BYTES = BMC * BK * 2;
 constexpr int B_BYTES = BNC * BK * 2;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
