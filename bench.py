@@ -251,6 +251,99 @@ def run_sweep(mp, torch, dev, only=None):
     return res
 
 
+UNIT_ROUNDOFF = {0: 2.0 ** -8, 1: 2.0 ** -11, 2: 2.0 ** -24, 3: 2.0 ** -53}  # bf16 fp16 fp32 fp64
+
+
+def timed_ms(torch, fn, reps=20, flush=None):
+    """Mean CUDA-event time of fn on the current stream, L2 flushed before each call."""
+    fn()
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        tot += e0.elapsed_time(e1)
+    return tot / reps
+
+
+def fin(x):
+    """JSON-safe float: non-finite values as strings."""
+    x = float(x)
+    return x if np.isfinite(x) else str(x)
+
+
+def err_rel(torch, a, a64):
+    """Per-cell max|A - A64| / max|A64| (errorlab.cpp:90-99), NaN as +inf."""
+    n = a64.shape[0]
+    d = (a.reshape(n, -1).double() - a64.reshape(n, -1)).abs().amax(dim=1)
+    e = d / a64.reshape(n, -1).abs().amax(dim=1)
+    return torch.nan_to_num(e, nan=float("inf")).cpu().numpy()
+
+
+def run_modes(mp, torch, dev, flush):
+    """BASELINE configs 0 (mass) and 1 (Poisson): 65,536 seeded P4 tets, c(x) at the quadrature
+    points, every precision mode: cells/s of the device step and the per-cell error against
+    the device fp64 mode (itself pinned to the fp64 oracle by tests/test_gpu_cells.py).
+    Config 1 computes G_K at u_g = fp64 in every mode."""
+    verts, _ = mp.gen_tets(0, 1, N_CELLS)
+    vd = torch.from_numpy(verts).to(dev)
+    res = []
+    for form, name in ((0, "config0 mass"), (1, "config1 poisson")):
+        ref = None
+        for mode in ("fp64", "fp32", "fp16", "mixed", "mixed_bf16"):
+            cfg = mp.mode_config(mode, form, geometry_fp64=(form == 1))
+            s = mp.make_setup(P_DEG, cfg)
+            s.reserve(N_CELLS)
+            out = torch.empty((N_CELLS, s.n_phi ** 2), dtype=torch.float64 if s.path == 2 else torch.float32,
+                              device=dev)
+            ms = timed_ms(torch, lambda: s.cell_matrices(vd, None, mp.CoefKind.sincosexp, out=out), flush=flush)
+            if mode == "fp64":
+                ref = out.clone()
+                e = np.zeros(1)
+            else:
+                e = err_rel(torch, out, ref)
+            us = UNIT_ROUNDOFF[int(cfg.u_s)]
+            res.append({"config": name, "mode": mode, "u_p/u_g/u_q/u_s": [int(cfg.u_p), int(cfg.u_g), int(cfg.u_q), int(cfg.u_s)],
+                        "ms": ms, "cells_per_s": N_CELLS / (ms * 1e-3),
+                        "max_err_rel": fin(e.max()), "max_err_over_u_s": fin(e.max() / us)})
+            del s, out
+        del ref
+        torch.cuda.empty_cache()
+    return res
+
+
+def run_robustness(mp, torch, dev):
+    """BASELINE config 3: 65,536 anisotropic rotated tets, c = 10^(6 u(x)) with u affine per
+    cell; P1-P6 mass and Poisson in fp16 and mixed (fp16 and bf16 storage): max per-cell error
+    against the device fp64 mode, and over the storage unit roundoff."""
+    verts, coef = mp.gen_tets(1, 1, N_CELLS)
+    vd = torch.from_numpy(verts).to(dev)
+    cd = torch.from_numpy(coef).to(dev)
+    res = []
+    for p in range(1, 7):
+        for form in (0, 1):
+            s64 = mp.make_setup(p, mp.mode_config("fp64", form))
+            a64 = s64.cell_matrices(vd, None, mp.CoefKind.exp10_affine, cd)
+            for mode in ("fp16", "mixed", "mixed_bf16"):
+                cfg = mp.mode_config(mode, form)
+                s = mp.make_setup(p, cfg)
+                a, fl = s.cell_matrices(vd, None, mp.CoefKind.exp10_affine, cd, want_flags=True)
+                e = err_rel(torch, a, a64)
+                res.append({"p": p, "form": "poisson" if form else "mass", "mode": mode,
+                            "max_err_rel": fin(e.max()), "median_err_rel": fin(np.median(e)),
+                            "max_err_over_u_s": fin(e.max() / UNIT_ROUNDOFF[int(cfg.u_s)]),
+                            "fp_flags": int(fl)})
+                del s, a
+            del s64, a64
+            torch.cuda.empty_cache()
+    return res
+
+
 def max_over_ranks(torch, value, dev):
     import torch.distributed as dist
     on_cpu = dist.get_backend() == "gloo"
@@ -335,6 +428,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-assembly", action="store_true", help="skip the config-4 assembly key")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-modes", action="store_true", help="skip the configs 0/1 precision-mode table")
+    ap.add_argument("--robustness", action="store_true", help="add the config-3 error table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -484,6 +579,10 @@ def main():
         line["assembly"] = {"workload": "config4: 96^3 x 6 tets, poisson P2/P3, mixed-bf16 kernels, "
                                         "deterministic CSR, z-slabs over ranks",
                             "results": run_assembly(mp, torch, dev, rank, world)}
+    if not args.no_modes and rank == 0:
+        line["modes"] = run_modes(mp, torch, dev, flush)
+    if args.robustness and rank == 0:
+        line["robustness"] = run_robustness(mp, torch, dev)
     if args.sweep and rank == 0:
         line["sweep"] = run_sweep(mp, torch, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
