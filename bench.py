@@ -412,6 +412,13 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
             t_at, _ = timed(lambda: am.assemble_matrix(local, dm, pat, 2, am.ATOMIC, values=vals))
             res["assemble_atomic_fp32_ms"] = t_at
         res["kernels_plus_assembly_fp32_ms"] = t_cell + res["assemble_fp32_ms"]
+        if world == 1:
+            # cell kernels fused with the atomic scatter (K2 adds from TMEM, no locals in HBM)
+            vals = torch.zeros(pat.nnz, dtype=torch.float32, device=dev)
+            t_fused, _ = timed(lambda: am.assemble_cells(s, vd, cdev, dm, pat, 2, mp.CoefKind.sincosexp,
+                                                         accumulate=True, values=vals))
+            res["fused_kernels_atomic_scatter_fp32_ms"] = t_fused
+            del vals
         out.append(res)
         del local, pat, dm, s
         torch.cuda.empty_cache()

@@ -106,6 +106,18 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t setup, const double* verts,
                               const double* coef, int64_t coef_stride, double* out,
                               void* stream, uint32_t* flags);
 
+/* Fused cell kernels + atomic CSR scatter (replaces run_assemble's per-cell
+ * bilinear_kernel -> assemble_matrix loop, mpfem_cli.cpp:322-332, in the order-free atomic
+ * mode): values[pos_map[c * n_phi^2 + i * n_phi + j]] += A_c[i][j] for the n_cells cells
+ * (pos_map from mpfem_b200_scatter_plan, already offset to the first cell of this call).
+ * On the tcgen05 path the local matrices never reach HBM (K2's epilogue adds from TMEM);
+ * other paths stage them and run the atomic scatter. values_fmt 2 = fp32, 3 = fp64. */
+int mpfem_b200_cell_matrices_scatter(mpfem_b200_setup_t setup, const double* verts,
+                                     const int32_t* cells, int64_t n_cells, int coef_kind,
+                                     const double* coef, int64_t coef_stride,
+                                     const int32_t* pos_map, void* values, int values_fmt,
+                                     void* stream, uint32_t* flags);
+
 /* Number of kernel launches the last cell_matrices call on this setup issued. */
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 

@@ -125,6 +125,8 @@ def lib():
         "mpfem_b200_setup_rule": (C.c_int, [vp, dp, dp]),
         "mpfem_b200_cell_matrices": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
                                                C.c_int64, vp, u32p]),
+        "mpfem_b200_cell_matrices_scatter": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64,
+                                                       vp, vp, C.c_int, vp, u32p]),
         "mpfem_b200_cell_matrices_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
                                                     C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_reserve": (C.c_int, [vp, C.c_int64]),

@@ -140,3 +140,31 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
                                     int(mode), int(accumulate), _ptr(rows), n_rows,
                                     _stream_handle(stream)))
     return values
+
+
+def assemble_cells(setup, verts, cells, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
+                   coef_kind: int = 0, coef=None, cell_begin: int = 0, accumulate: bool = False,
+                   values=None, stream=None, want_flags: bool = False):
+    """Cell kernels fused with the atomic CSR scatter (run_assemble's bilinear_kernel ->
+    assemble_matrix loop, mpfem_cli.cpp:322-332, in the order-free atomic mode): adds the
+    local matrices of `cells` (global cells cell_begin .. cell_begin + len(cells)) into the
+    CSR values. On the tcgen05 path K2 adds straight from TMEM, so the local matrices never
+    reach HBM. Values are within gamma_{m+1}(fmt) * sum|contrib| of the exact sum."""
+    import torch
+    if pat.pos_map is None:
+        raise ConfigError("assemble_cells needs a pattern built with plan=True")
+    n = int(cells.shape[0])
+    per = dm.n_local * dm.n_local
+    if values is None:
+        values = torch.zeros(pat.nnz, dtype=torch.float32 if fmt == FP32 else torch.float64,
+                             device=cells.device)
+    elif not accumulate:
+        values.zero_()
+    stride = 0 if coef is None else int(coef.shape[-1]) if coef.dim() > 1 else 0
+    fl = C.c_uint32(0)
+    pm = pat.pos_map[cell_begin * per:(cell_begin + n) * per]
+    check(lib().mpfem_b200_cell_matrices_scatter(setup._h, _ptr(verts), _ptr(cells), n, int(coef_kind),
+                                                 _ptr(coef), stride, _ptr(pm), _ptr(values), int(fmt),
+                                                 _stream_handle(stream),
+                                                 C.byref(fl) if want_flags else None))
+    return (values, fl.value) if want_flags else values

@@ -147,6 +147,11 @@ struct mpfem_b200_setup_s {
   DevBuf d_ready;
   DevBuf d_trace;  // MPFEM_B200_TRACE=1: per-CTA timeline of the last call
   DevBuf d_tile_ctr;  // K1 dynamic tile schedule (2 words, zero between launches)
+  // fused scatter (mpfem_b200_cell_matrices_scatter) for the duration of one call
+  const int32_t* cur_pos_map = nullptr;
+  void* cur_values = nullptr;
+  int cur_values_fp64 = 0;
+  DevBuf d_locals;  // non-fused paths: local matrices staged before the atomic scatter
   uint32_t epoch = 0;
   uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
   // host-API staging
@@ -290,7 +295,7 @@ void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, 
     throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
 }
 
-template <bool ACC_F16, int NP>
+template <bool ACC_F16, int NP, int OUTK = 0>
 void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
@@ -305,21 +310,21 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!max_clusters) {
-    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP>,
+    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES));
     // Full carveout: with the default the driver configures an SM that K2 reaches first for
     // the smallest shared-memory size holding its 198 KB (196 KB), leaving no room for the
     // two concurrent K1 CTAs (2 x 14 KB) -- K1 would then wait for K2, which waits for K1.
-    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP>,
+    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout,
                                  int(cudaSharedmemCarveoutMaxShared)));
     cfg.gridDim = dim3(unsigned(device_sm_count()));
-    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, NP>, &cfg));
+    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>, &cfg));
     if (max_clusters < 1) throw Error(MPFEM_B200_RUNTIME_ERROR, "tcgen05 pair kernel does not fit an SM cluster");
   }
   const int64_t tiles = int64_t(P.n_out_tiles) * ((P.n_cell_tiles + NP - 1) / NP);
   cfg.gridDim = dim3(unsigned(2 * NP * std::min<int64_t>(tiles, max_clusters)));
-  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, NP>, ta, tb, P));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>, ta, tb, P));
 }
 
 void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t out_pitch,
@@ -347,7 +352,18 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     P.k1_tile = 32 * k1_geom_warps(S);
     P.error = static_cast<int*>(S.d_error.p);
     P.trace = static_cast<unsigned long long*>(S.d_trace.p);
-    if (S.pair == 2) {
+    if (S.cur_pos_map) {
+      // fused scatter: the local matrices go straight into the CSR values
+      P.pos_map = S.cur_pos_map;
+      P.values = S.cur_values;
+      if (S.cur_values_fp64) {
+        if (S.acc_f16) launch_tc2<true, 1, 2>(ta, tb, P, st);
+        else launch_tc2<false, 1, 2>(ta, tb, P, st);
+      } else {
+        if (S.acc_f16) launch_tc2<true, 1, 1>(ta, tb, P, st);
+        else launch_tc2<false, 1, 1>(ta, tb, P, st);
+      }
+    } else if (S.pair == 2) {
       if (S.acc_f16) launch_tc2<true, 2>(ta, tb, P, st);
       else launch_tc2<false, 2>(ta, tb, P, st);
     } else {
@@ -461,7 +477,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   (void)cell_tiles;
   (void)out_tiles;
   if (const char* env = std::getenv("MPFEM_B200_CHUNKS")) n_chunks = std::max(1, std::min(8, std::atoi(env)));
-  if (S.timing) n_chunks = 1;  // per-kernel timing measures K1 and K2 unoverlapped
+  if (S.timing || S.cur_pos_map) n_chunks = 1;  // timing: K1 and K2 unoverlapped; scatter: one pos_map base
   // Concurrent K1/K2 (experimental, MPFEM_B200_OVERLAP=1 on the tcgen05 pair path): K1 on
   // the caller's stream and K2 on a side stream start together and share every SM (one K2
   // CTA + two K1 CTAs); K2's producer acquires K1's per-tile W stamps before each TMA read.
@@ -720,6 +736,40 @@ int mpfem_b200_cell_matrices(mpfem_b200_setup_t S, const double* verts, const in
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
     run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, out, out_pitch,
                       static_cast<cudaStream_t>(stream), flags);
+  });
+}
+
+int mpfem_b200_cell_matrices_scatter(mpfem_b200_setup_t S, const double* verts,
+                                     const int32_t* cells, int64_t n_cells, int coef_kind,
+                                     const double* coef, int64_t coef_stride,
+                                     const int32_t* pos_map, void* values, int values_fmt,
+                                     void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (!pos_map || !values) throw Error(MPFEM_B200_CONFIG_ERROR, "scatter needs pos_map and values");
+    if (values_fmt != 2 && values_fmt != 3) throw Error(MPFEM_B200_CONFIG_ERROR, "CSR values must be fp32 or fp64");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (S->path == kPathTC && S->pair) {
+      struct Reset {
+        mpfem_b200_setup_s& s;
+        ~Reset() { s.cur_pos_map = nullptr; s.cur_values = nullptr; }
+      } reset{*S};
+      S->cur_pos_map = pos_map;
+      S->cur_values = values;
+      S->cur_values_fp64 = values_fmt == 3;
+      // out is unused by the fused epilogue (pitch n_out keeps the argument checks)
+      run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, nullptr, S->n_out,
+                        st, flags);
+    } else {
+      // other paths: stage the local matrices, then the atomic scatter (assemble mode 0)
+      const int lf = S->path == kPathF64 ? 3 : 2;
+      S->d_locals.ensure(size_t(n_cells) * size_t(S->n_out) * (lf == 3 ? 8 : 4) + 16);
+      run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, S->d_locals.p,
+                        S->n_out, st, flags);
+      const int rc = mpfem_b200_assemble(S->d_locals.p, lf, 0, n_cells, S->n_phi, nullptr, 0, pos_map,
+                                         nullptr, nullptr, values, values_fmt, 0, 1, nullptr, 0, stream);
+      if (rc) throw Error(rc, std::string("atomic scatter: ") + mpfem_b200_last_error());
+    }
   });
 }
 

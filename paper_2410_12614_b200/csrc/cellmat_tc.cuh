@@ -72,6 +72,10 @@ struct Params {
   int* error;          // set to 5 if a stamp never arrives (K1 not co-resident); error[1]
                        // holds the epoch of the last timed-out call (later waits skip)
   unsigned long long* trace;  // debug timeline (slots 1024..2047), NULL normally
+  // Fused CSR scatter (pair kernel, OUTK != 0): instead of storing, entry (i, j) of cell c
+  // is added into values[pos_map[c * n_out + i * n_phi + j]] (fp32 or fp64 values).
+  const int32_t* pos_map;
+  void* values;
 };
 
 // Producer-side wait for K1's W rows [c0, c1): acquire each K1 tile stamp, then order the

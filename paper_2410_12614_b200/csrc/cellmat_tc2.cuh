@@ -87,7 +87,9 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
 // counterpart in the other pair (A is read from L2 once per cluster), and a stage is
 // refilled only after both pair leaders committed it (empty barriers count NP arrivals,
 // commits multicast to every CTA of the cluster).
-template <bool ACC_F16, int NP>
+// OUTK: 0 = store the cell matrices (out, out_pitch); 1 / 2 = fused atomic CSR scatter into
+// fp32 / fp64 values through pos_map (the local matrices never reach HBM).
+template <bool ACC_F16, int NP, int OUTK = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     cellmat_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const tc::Params P) {
@@ -207,7 +209,27 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint32_t r[32];
         tc::tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
         const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
-        if (o_ok) {
+        if constexpr (OUTK != 0) {
+          if (o_ok) {
+            // all 32 positions first (independent coalesced loads), then the 32 reductions
+            const int32_t* pm = P.pos_map + cell0 * P.n_out + off;
+            const int64_t left = P.n_cells - cell0;
+            int32_t pos[32];
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) pos[j] = (left >= 32 || j < left) ? __ldcs(pm + j * P.n_out) : -1;
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (pos[j] >= 0) {
+                float v;
+                if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
+                else v = __uint_as_float(r[j]);
+                expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+                if constexpr (OUTK == 1) atomicAdd(static_cast<float*>(P.values) + pos[j], v);
+                else atomicAdd(static_cast<double*>(P.values) + pos[j], double(v));
+              }
+            }
+          }
+        } else if (o_ok) {
           float* dst = P.out + cell0 * P.out_pitch + off;
           const int64_t left = P.n_cells - cell0;
           #pragma unroll

@@ -137,3 +137,32 @@ def test_config4_full_size_p2_properties():
     key = rows.to(torch.int64) * dm.n_dofs + pat.col_idx.to(torch.int64)
     keyt = pat.col_idx.to(torch.int64) * dm.n_dofs + rows.to(torch.int64)
     assert torch.equal(torch.sort(key).values, torch.sort(keyt).values)
+
+
+@pytest.mark.parametrize("mode,p", [("mixed", 2), ("mixed_bf16", 3), ("fp64", 2), ("mixed", 1)])
+def test_fused_cell_kernels_scatter(oracle, mode, p):
+    """assemble_cells (cell kernels fused with the atomic scatter; on the tcgen05 path K2 adds
+    from TMEM) against the deterministic assembly of the same cell matrices: per entry within
+    gamma_{m+1}(fmt) * sum|contrib| (test_assembly.cpp:165-167), and with cell ranges that
+    compose (z-slab style)."""
+    verts, cells = oracle.structured_tet_mesh(4, 3, 3, 1.0, 0.15, 11)
+    dm = gpu_dofmap(p, verts, cells)
+    pat = am.csr_pattern(dm)
+    s = mp.make_setup(p, mp.mode_config(mode, mp.FormKind.poisson))
+    vd = torch.from_numpy(verts).cuda()
+    cd = torch.from_numpy(np.ascontiguousarray(cells)).cuda()
+    local = s.cell_matrices(vd, cd, mp.CoefKind.sincosexp)
+    ab = local.abs().double()
+    for fmt in (2, 3):
+        det = am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC).double()
+        mag = am.assemble_matrix(ab.to(local.dtype), dm, pat, fmt, am.DETERMINISTIC).double()
+        u = 2.0 ** -24 if fmt == 2 else 2.0 ** -53
+        m = dm.max_multiplicity
+        tol = (m + 1) * u / (1 - (m + 1) * u) * mag + 1e-300
+        fused = am.assemble_cells(s, vd, cd, dm, pat, fmt, mp.CoefKind.sincosexp).double()
+        assert bool(((fused - det).abs() <= tol).all()), (mode, fmt)
+        k = cells.shape[0] // 3
+        part = am.assemble_cells(s, vd, cd[:k], dm, pat, fmt, mp.CoefKind.sincosexp)
+        part = am.assemble_cells(s, vd, cd[k:], dm, pat, fmt, mp.CoefKind.sincosexp, cell_begin=k,
+                                 accumulate=True, values=part).double()
+        assert bool(((part - det).abs() <= tol).all()), (mode, fmt)
