@@ -191,8 +191,8 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
                         void* values, int fmt, int mode, int accumulate, const int32_t* rows,
                         int64_t n_rows, void* stream);
 
-/* Deterministic assemble_matrix without the seg_ptr/perm plan (the default full-matrix
- * deterministic path): rows pull their incident (cell, local row) pairs from the
+/* Deterministic assemble_matrix without the seg_ptr/perm plan (for patterns built without
+ * it: 18 GB less at config-4 P3; about 2x slower than mode 1 with the plan): rows pull their incident (cell, local row) pairs from the
  * incidence lists (mpfem_b200_incidence, ascending cell order) and the CSR positions from
  * pos_map; values are bitwise those of mode 1 of mpfem_b200_assemble (the reference's
  * ascending-cell sequential sum, assembly.cpp:50-67). Arguments as mpfem_b200_assemble. */
