@@ -1091,6 +1091,199 @@ int orc_bound(int p, int form, const int* cfg, const double* verts, int kind,
   return 0;
 }
 
+/* ------------------------------------------------------------------ action (Algorithm 2) */
+/* action_kernel (kernels.cpp:269-304) for one cell: w-evaluation eval_w_at_ug
+ * (kernels.cpp:145-173: round w to u_s, k-ascending matmul against the u_s store slabs at
+ * u_p, cast to u_g), the integrand r (kernels.cpp:280-301 / build_r 214-240: (G w)_s with t
+ * ascending at u_g, times omega, times zhat, rounded to u_s) and v = b_cat_action r at u_q
+ * ((s, q) ascending, kernels.cpp:303). The matrix engine flushes subnormal accumulates
+ * (mm_units.cpp:43-62). Coefficient kinds as orc_build_C (Q path: zhat = c(x_q) at u_g). */
+static int action_one(const setup_t* S, const double* verts, int kind, const double* coef,
+                      const double* w, double* v, uint32_t* fl) {
+  int nq = S->nq, nd = S->nd, nphi = S->nphi;
+  double geom[ORC_GEOM_SIZE];
+  int st = orc_cell_geometry(verts, S->form, S->ug, geom, fl);
+  if (st) return st;
+  const double* ten = geom + 20;
+  int ftz = S->engine == 2;
+  double* zhat = malloc(sizeof(double) * nq);
+  int have_z = coef_zhat(S, verts, kind, coef, zhat, fl);
+  double wm[165];
+  for (int k = 0; k < nphi; ++k) wm[k] = RND(w[k], S->us);
+  double* what = malloc(sizeof(double) * nd * nq);
+  for (int s = 0; s < nd; ++s)
+    for (int q = 0; q < nq; ++q) {
+      double acc = 0.0;
+      for (int k = 0; k < nphi; ++k) {
+        double prod = orc_op(wm[k], S->tab_store[((size_t)s * nphi + k) * nq + q], 2, S->up, 0, fl);
+        acc = orc_op(acc, prod, 0, S->up, ftz, fl);
+      }
+      what[(size_t)s * nq + q] = RND(acc, S->ug);
+    }
+  double* r = malloc(sizeof(double) * nd * nq);
+  for (int q = 0; q < nq; ++q) {
+    double omega = RND(S->wts[q], S->ug);
+    for (int s = 0; s < nd; ++s) {
+      double t1 = 0.0;
+      for (int t = 0; t < nd; ++t)
+        t1 = ADD(t1, MUL(ten[s * 3 + t], what[(size_t)t * nq + q], S->ug), S->ug);
+      double m1 = MUL(omega, t1, S->ug);
+      if (have_z) m1 = MUL(m1, zhat[q], S->ug);
+      r[(size_t)s * nq + q] = RND(m1, S->us);
+    }
+  }
+  for (int i = 0; i < nphi; ++i) {
+    double acc = 0.0;
+    for (int s = 0; s < nd; ++s)
+      for (int q = 0; q < nq; ++q) {
+        double prod = orc_op(S->tab_store[((size_t)s * nphi + i) * nq + q], r[(size_t)s * nq + q],
+                             2, S->uq, 0, fl);
+        acc = orc_op(acc, prod, 0, S->uq, ftz, fl);
+      }
+    v[i] = acc;
+  }
+  free(zhat); free(what); free(r);
+  return 0;
+}
+
+int orc_action(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+               const double* coef, int coef_stride, const double* w, int w_stride,
+               double* v_out, uint32_t* fl) {
+  uint32_t dummy = 0;
+  if (!fl) fl = &dummy;
+  setup_t S;
+  int st = make_setup(p, form, cfg, &S);
+  if (!st) {
+    for (int64_t c = 0; c < m && !st; ++c)
+      st = action_one(&S, verts + 12 * c, kind, coef ? coef + (int64_t)coef_stride * c : NULL,
+                      w + (int64_t)w_stride * c, v_out + (int64_t)S.nphi * c, fl);
+  }
+  free_setup(&S);
+  return st;
+}
+
+/* kernel_bounds, action part (bounds.cpp:29-281: the r stage 128-155 and the v
+ * accumulation 222-240, bound_v 269-279). Q path as orc_bound: z_at = c(x_q), and the
+ * coefficient-evaluation budget term (kv z_norm) is zero because c enters at >= u_g.
+ * out4 = {bound_v, kappa_q_v, kappa_p_v, kappa_g_v}; v64 = the exact binary64 v. */
+int orc_action_bound(int p, int form, const int* cfg, const double* verts, int kind,
+                     const double* coef, const double* w, double* out4, double* v64) {
+  setup_t S;
+  int st = make_setup(p, form, cfg, &S);
+  if (st) { free_setup(&S); return st; }
+  int nq = S.nq, nd = S.nd, nphi = S.nphi;
+  int poisson = form == ORC_POISSON;
+  uint32_t scratch = 0;
+  uint32_t* fl = &scratch;
+  double geom[ORC_GEOM_SIZE];
+  st = orc_cell_geometry(verts, form, ORC_FP64, geom, fl);
+  if (st) { free_setup(&S); return st; }
+  const double* ten = geom + 20;
+  const double* tt = geom + 31;
+  double kk2 = geom[30] * geom[29];
+  size_t nb = (size_t)nd * nphi * nq;
+  double* tab = malloc(sizeof(double) * nb);
+  tabulate_b(&S.B, S.pts, nq, ORC_FP64, ORC_FP64, poisson, tab, fl);
+  cond_t* bc = malloc(sizeof *bc);
+  basis_conditioning(&S.B, S.pts, nq, bc);
+  double dp = 3.0 * p, pd = pow((double)p, 3), kv = bc->lebesgue;
+  double z_norm = 0.0, w_norm = 0.0;
+  if (kind == ORC_COEF_NODAL)
+    for (int i = 0; i < nphi; ++i) if (fabs(coef[i]) > z_norm) z_norm = fabs(coef[i]);
+  for (int i = 0; i < nphi; ++i) if (fabs(w[i]) > w_norm) w_norm = fabs(w[i]);
+  double* theta_b = calloc(nb, sizeof(double));
+  if (poisson) {
+    for (int s = 0; s < nd; ++s)
+      for (int k = 0; k < nphi; ++k) {
+        double peak = 0.0;
+        for (int q = 0; q < nq; ++q) {
+          double a = fabs(tab[((size_t)s * nphi + k) * nq + q]);
+          if (a > peak) peak = a;
+        }
+        for (int q = 0; q < nq; ++q)
+          theta_b[((size_t)s * nphi + k) * nq + q] = dp * bc->grad_kappa[k][s] * peak;
+      }
+  } else {
+    for (size_t i = 0; i < nb; ++i) theta_b[i] = dp * fabs(tab[i]);
+  }
+  double* r = malloc(sizeof(double) * nd * nq);
+  double* thr = malloc(sizeof(double) * nd * nq);
+  double* gr = malloc(sizeof(double) * nd * nq);
+  for (int q = 0; q < nq; ++q) {
+    const double* x = S.pts + 3 * q;
+    double z_at = 1.0;
+    if (kind == ORC_COEF_NODAL) {
+      z_at = 0.0;
+      for (int i = 0; i < nphi; ++i) z_at += coef[i] * eval_basis(&S.B, i, x, ORC_FP64, fl);
+    } else if (kind == ORC_COEF_SINCOSEXP) {
+      double xp[3];
+      phys_point(verts, x, xp);
+      z_at = coef_sincosexp(xp);
+    } else if (kind == ORC_COEF_EXP10_AFFINE) {
+      z_at = coef_exp10_affine(coef, x);
+    }
+    double omega = S.wts[q];
+    if (poisson) {
+      double gw[3] = {0.0, 0.0, 0.0};  /* eval_fe_gradient (elements.cpp:224-236) */
+      for (int i = 0; i < nphi; ++i) {
+        double g[3];
+        eval_basis_gradient(&S.B, i, x, ORC_FP64, g, fl);
+        for (int a = 0; a < 3; ++a) gw[a] += w[i] * g[a];
+      }
+      for (int s = 0; s < 3; ++s) {
+        double gw_s = 0.0, gtw_s = 0.0, kappa_s = 0.0;
+        for (int t = 0; t < 3; ++t) {
+          gw_s += ten[s * 3 + t] * gw[t];
+          gtw_s += fabs(tt[s * 3 + t]) * fabs(gw[t]);
+          kappa_s += fabs(ten[s * 3 + t]) * bc->grad_kappa_max[t] * bc->grad_lebesgue[t];
+        }
+        size_t idx = (size_t)s * nq + q;
+        r[idx] = omega * z_at * gw_s;
+        thr[idx] = pd * fabs(omega) * (kv * z_norm * fabs(gw_s) + fabs(z_at) * w_norm * kappa_s);
+        gr[idx] = kk2 * fabs(omega * z_at) * gtw_s;
+      }
+    } else {
+      double w_at = 0.0;
+      for (int i = 0; i < nphi; ++i) w_at += w[i] * eval_basis(&S.B, i, x, ORC_FP64, fl);
+      double g = ten[0];
+      r[q] = omega * z_at * g * w_at;
+      thr[q] = pd * kv * (fabs(w_at) * z_norm + fabs(z_at) * w_norm) * fabs(omega * g);
+      gr[q] = kk2 * fabs(r[q]);
+    }
+  }
+  double vmax = 0, svmax = 0, tvmax = 0, gvmax = 0;
+  for (int i = 0; i < nphi; ++i) {
+    double acc = 0.0, sv = 0.0, tv = 0.0, gv = 0.0;
+    for (int s = 0; s < nd; ++s)
+      for (int q = 0; q < nq; ++q) {
+        double b = tab[((size_t)s * nphi + i) * nq + q];
+        double tb = theta_b[((size_t)s * nphi + i) * nq + q];
+        size_t idx = (size_t)s * nq + q;
+        acc += b * r[idx];
+        sv += fabs(b) * fabs(r[idx]);
+        tv += fabs(b) * thr[idx] + tb * fabs(r[idx]);
+        gv += fabs(b) * gr[idx];
+      }
+    if (v64) v64[i] = acc;
+    if (fabs(acc) > vmax) vmax = fabs(acc);
+    if (sv > svmax) svmax = sv;
+    if (tv > tvmax) tvmax = tv;
+    if (gv > gvmax) gvmax = gv;
+  }
+  double u_p = FMT[S.up].u, u_g = FMT[S.ug].u, u_q = FMT[S.uq].u, u_s = FMT[S.us].u;
+  if (vmax > 0.0) {
+    out4[1] = svmax / vmax;
+    out4[2] = tvmax / vmax;
+    out4[3] = gvmax / vmax;
+    out4[0] = (u_s + nq * u_q) * out4[1] + u_p * out4[2] + u_g * out4[3];
+  } else {
+    out4[0] = out4[1] = out4[2] = out4[3] = NAN;
+  }
+  free(tab); free(bc); free(theta_b); free(r); free(thr); free(gr);
+  free_setup(&S);
+  return 0;
+}
+
 /* ------------------------------------------------------------------ synthetic inputs */
 static double det3(const double j[3][3]) { /* mesh.cpp:21-25 */
   return j[0][0] * (j[1][1] * j[2][2] - j[1][2] * j[2][1]) -

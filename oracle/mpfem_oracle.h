@@ -84,6 +84,18 @@ int orc_bilinear(int p, int form, const int* cfg, int64_t m, const double* verts
 int orc_bound(int p, int form, const int* cfg, const double* verts, int coef_kind,
               const double* coef, double* out4, double* a64);
 
+/* Reference Algorithm 2, action_kernel (kernels.cpp:269-304) incl. eval_w_at_ug
+ * (kernels.cpp:145-173): v (n_phi per cell) for M cells, w (n_phi per cell, row stride
+ * w_stride). Coefficient kinds as orc_bilinear. */
+int orc_action(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+               const double* coef, int coef_stride, const double* w, int w_stride,
+               double* v_out, uint32_t* flags);
+
+/* Restated kernel_bounds, action part (bounds.cpp:128-155,222-279): out4 = {bound_v,
+ * kappa_q_v, kappa_p_v, kappa_g_v}; v64 = exact binary64 v (report.v). */
+int orc_action_bound(int p, int form, const int* cfg, const double* verts, int kind,
+                     const double* coef, const double* w, double* out4, double* v64);
+
 /* Physical quadrature points x_q = v0 + J (xi_q) in fp64 and the coefficient there. */
 int orc_coef_at_q(int p, const double* verts, int coef_kind, const double* coef,
                   double* c_q /* n_q */);

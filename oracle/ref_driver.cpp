@@ -52,10 +52,10 @@ int guard(F&& f) {
 
 const ReferenceCell kTet{CellKind::simplex, 3};
 
-KernelConfig make_cfg(int form, const int* cfg) {
+KernelConfig make_cfg(int form, const int* cfg, ModeKind mode = ModeKind::bilinear) {
   KernelConfig c;
   c.form = form ? FormKind::poisson : FormKind::mass;
-  c.mode = ModeKind::bilinear;
+  c.mode = mode;
   c.u_p = Fmt(cfg[0]);
   c.u_g = Fmt(cfg[1]);
   c.u_q = Fmt(cfg[2]);
@@ -126,6 +126,50 @@ Mat cell_matrix(const KernelSetup& setup, const double* v, int kind, const doubl
         for (int k = 0; k < n_phi; ++k) h_cat(row0 + q, k) = h(q, k);
     }
   return blocked_matmul(setup.b_cat_bilinear, h_cat, cfg.engine, cfg.u_q, flags);
+}
+
+// Same-mode action v (n_phi) for one cell through the reference's public API. Nodal /
+// constant coefficients call action_kernel itself (kernels.cpp:269-304). The quadrature-
+// point coefficient path composes the same stages from public pieces: the w evaluation as
+// eval_w_at_ug does it (blocked_matmul of the u_s-rounded w against setup.store_slabs at
+// u_p, cast to u_g; kernels.cpp:145-173), the integrand with z_q := c(x_q) at u_g
+// (kernels.cpp:280-301), and blocked_matmul(setup.b_cat_action, r, engine, u_q).
+std::vector<double> cell_action(const KernelSetup& setup, const double* v, int kind,
+                                const double* coef, const double* w, FpFlags& flags) {
+  Mesh mesh = single_tet(v);
+  const KernelConfig& cfg = setup.config;
+  GeometryData geom = cell_geometry(mesh, 0, setup.rule, cfg.form, cfg.u_g, flags);
+  int n_d = setup.n_d, n_q = setup.rule.n_points, n_phi = setup.basis.n_phi;
+  Coefficients wv(w, w + n_phi);
+  if (kind == 0 || kind == 3) {
+    Coefficients z;
+    if (kind == 3) z.assign(coef, coef + n_phi);
+    Mat out = action_kernel(setup, {geom}, {wv}, z, flags);
+    return out.a;
+  }
+  Mat wmat(1, n_phi);
+  for (int k = 0; k < n_phi; ++k) wmat(0, k) = fp_cast(w[k], Fmt::fp64, cfg.u_s, flags);
+  std::vector<double> what(std::size_t(n_d) * n_q);
+  for (int s = 0; s < n_d; ++s) {
+    Mat vals = blocked_matmul(wmat, setup.store_slabs[s], cfg.engine, cfg.u_p, flags);
+    for (int q = 0; q < n_q; ++q) what[std::size_t(s) * n_q + q] = fp_cast(vals(0, q), cfg.u_p, cfg.u_g, flags);
+  }
+  Mat r_cat(n_d * n_q, 1);
+  for (int q = 0; q < n_q; ++q) {
+    double zq = round_to(coef_at(kind, v, coef, setup.rule.point(q)), cfg.u_g, flags);
+    double omega = fp_cast(setup.rule.weights[q], Fmt::fp64, cfg.u_g, flags);
+    const GeometryPoint& gp = geom.at(q);
+    for (int s = 0; s < n_d; ++s) {
+      double t1 = 0.0;
+      for (int t = 0; t < n_d; ++t)
+        t1 = fp_add(t1, fp_mul(gp.tensor(s, t), what[std::size_t(t) * n_q + q], cfg.u_g, flags),
+                    cfg.u_g, flags);
+      double m1 = fp_mul(omega, t1, cfg.u_g, flags);
+      m1 = fp_mul(m1, zq, cfg.u_g, flags);
+      r_cat(s * n_q + q, 0) = fp_cast(m1, cfg.u_g, cfg.u_s, flags);
+    }
+  }
+  return blocked_matmul(setup.b_cat_action, r_cat, cfg.engine, cfg.u_q, flags).a;
 }
 
 uint32_t pack(const FpFlags& f) {
@@ -276,6 +320,44 @@ int ref_bound(int p, int form, const int* cfg, const double* verts, int kind,
     out4[2] = r.kappa_p_a;
     out4[3] = r.kappa_g_a;
     if (a64) std::memcpy(a64, r.a.a.data(), sizeof(double) * r.a.a.size());
+  });
+}
+
+int ref_action(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+               const double* coef, int coef_stride, const double* w, int w_stride,
+               double* v_out, uint32_t* flags) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kTet, p, make_cfg(form, cfg, ModeKind::action));
+    int n_phi = setup.basis.n_phi;
+    for (int64_t c = 0; c < m; ++c) {
+      std::vector<double> v = cell_action(setup, verts + 12 * c, kind,
+                                          coef ? coef + int64_t(coef_stride) * c : nullptr,
+                                          w + int64_t(w_stride) * c, f);
+      std::memcpy(v_out + int64_t(n_phi) * c, v.data(), sizeof(double) * n_phi);
+    }
+    if (flags) *flags |= pack(f);
+  });
+}
+
+// kernel_bounds with w (bound_v, report.v) for constant / nodal coefficients.
+int ref_action_bound(int p, int form, const int* cfg, const double* verts, int kind,
+                     const double* coef, const double* w, double* out4, double* v64) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kTet, p, make_cfg(form, cfg, ModeKind::action));
+    BasisConditioning bc = basis_condition_numbers(setup.basis);
+    Mesh mesh = single_tet(verts);
+    GeometryData g64 = cell_geometry(mesh, 0, setup.rule, setup.config.form, Fmt::fp64, f);
+    Coefficients z;
+    if (kind == 3) z.assign(coef, coef + setup.basis.n_phi);
+    Coefficients wv(w, w + setup.basis.n_phi);
+    BoundReport r = kernel_bounds(setup, bc, g64, z, wv);
+    out4[0] = r.bound_v;
+    out4[1] = r.kappa_q_v;
+    out4[2] = r.kappa_p_v;
+    out4[3] = r.kappa_g_v;
+    if (v64) std::memcpy(v64, r.v.data(), sizeof(double) * r.v.size());
   });
 }
 

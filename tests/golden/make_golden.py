@@ -105,6 +105,33 @@ def main() -> None:
     v2, c2 = R.structured_tet_mesh(2, 2, 2, 1.0, 0.15, 7)
     cd2, nd2, mm2 = R.build_dofmap(1, v2, c2)
     out["dofmap222_p1_meta"] = np.array([nd2, mm2], dtype=np.int64)
+    # Algorithm 2 (action_kernel, kernels.cpp:269-304) and its bound (bounds.cpp:128-279).
+    arng = np.random.default_rng(2410)
+    for mode, cfg in MODES.items():
+        for form in (MASS, POISSON):
+            for p in (1, 2, 3, 4):
+                for kind in (COEF_ONE, 1, COEF_NODAL):
+                    m = 2
+                    w = arng.uniform(-1.0, 1.0, size=(m, nphi(p)))
+                    coef = arng.uniform(0.5, 1.5, size=(m, nphi(p))) if kind == COEF_NODAL else None
+                    v, fl = R.action(p, form, cfg, V[:m], w, kind, coef)
+                    key = f"V_{mode}_f{form}_p{p}_k{kind}"
+                    out[key] = v
+                    out[key + "_w"] = w
+                    out[key + "_flags"] = np.array([fl], dtype=np.uint32)
+                    if coef is not None:
+                        out[key + "_coef"] = coef
+            for p in (1, 2, 3):
+                for kind in (COEF_ONE, COEF_NODAL):
+                    w = arng.uniform(-1.0, 1.0, size=nphi(p))
+                    coef = arng.uniform(0.5, 1.5, size=nphi(p)) if kind == COEF_NODAL else None
+                    b, v64 = R.action_bound(p, form, cfg, V[7], w, kind, coef)
+                    key = f"vbound_{mode}_f{form}_p{p}_k{kind}"
+                    out[key] = b
+                    out[key + "_v64"] = v64
+                    out[key + "_w"] = w
+                    if coef is not None:
+                        out[key + "_coef"] = coef
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
 

@@ -75,6 +75,10 @@ class _Lib:
         self._sig("bilinear", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
                                          C.c_int, _d, _u32])
         self._sig("bound", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d])
+        self._sig("action", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
+                                      C.c_int, _d, C.c_int, _d, _u32])
+        self._sig("action_bound", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d,
+                                            _d])
         self._sig("structured_tet_mesh", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
                                                    C.c_double, C.c_uint64, _d, _i32])
         self._sig("build_dofmap", C.c_int, [C.c_int, C.c_int64, _d, C.c_int64, _i32, _i32,
@@ -176,6 +180,35 @@ class _Lib:
         self._check(self._bound(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(out, _d),
                                 _ptr(a64, _d)))
         return out, a64
+
+    def action(self, p, form, cfg, verts, w, kind=COEF_ONE, coef=None):
+        """action_kernel (kernels.cpp:269-304): v (m, n_phi) and the FP flag mask."""
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 12)
+        m = v.shape[0]
+        wv = np.ascontiguousarray(w, dtype=np.float64).reshape(m, -1)
+        out = np.zeros((m, nphi(p)))
+        c = (C.c_int * 5)(*cfg)
+        cf = None
+        stride = 0
+        if coef is not None:
+            cf = np.ascontiguousarray(coef, dtype=np.float64).reshape(m, -1)
+            stride = cf.shape[1]
+        fl = C.c_uint32(0)
+        self._check(self._action(p, form, c, m, _ptr(v, _d), kind, _ptr(cf, _d), stride,
+                                 _ptr(wv, _d), wv.shape[1], _ptr(out, _d), C.byref(fl)))
+        return out, fl.value
+
+    def action_bound(self, p, form, cfg, verts, w, kind=COEF_ONE, coef=None):
+        """kernel_bounds action part: ({bound_v, kappa_q, kappa_p, kappa_g}, exact v)."""
+        out = np.zeros(4)
+        v64 = np.zeros(nphi(p))
+        c = (C.c_int * 5)(*cfg)
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(12)
+        wv = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+        cf = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+        self._check(self._action_bound(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(wv, _d),
+                                       _ptr(out, _d), _ptr(v64, _d)))
+        return out, v64
 
     def structured_tet_mesh(self, nx, ny, nz, extent=1.0, jitter=0.15, seed=1):
         nv = (nx + 1) * (ny + 1) * (nz + 1)

@@ -131,3 +131,49 @@ def test_config0_generator_properties(oracle):
     e = v[:, 1:, :] - v[:, :1, :]
     det = np.linalg.det(np.transpose(e, (0, 2, 1)))
     assert np.all(det >= 1e-3)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_action_bitwise(oracle, golden, mode, form):
+    """Algorithm 2 (action_kernel, kernels.cpp:269-304) restated bit for bit, FP flags too."""
+    V = golden["verts"]
+    cfg = MODES[mode]
+    for p in (1, 2, 3, 4):
+        for kind in (COEF_ONE, 1, COEF_NODAL):
+            key = f"V_{mode}_f{form}_p{p}_k{kind}"
+            coef = golden[key + "_coef"] if kind == COEF_NODAL else None
+            v, fl = oracle.action(p, form, cfg, V[:2], golden[key + "_w"], kind, coef)
+            assert np.array_equal(bits(v), bits(golden[key])), key
+            assert fl == golden[key + "_flags"][0], key
+
+
+def test_action_bounds_bitwise(oracle, golden):
+    """kernel_bounds with w: bound_v and the exact v (bounds.cpp:128-279)."""
+    V = golden["verts"]
+    for form in (MASS, POISSON):
+        for mode, cfg in MODES.items():
+            for p in (1, 2, 3):
+                for kind in (COEF_ONE, COEF_NODAL):
+                    key = f"vbound_{mode}_f{form}_p{p}_k{kind}"
+                    coef = golden[key + "_coef"] if kind == COEF_NODAL else None
+                    b, v64 = oracle.action_bound(p, form, cfg, V[7], golden[key + "_w"], kind, coef)
+                    assert np.array_equal(bits(b), bits(golden[key])), key
+                    assert np.array_equal(bits(v64), bits(golden[key + "_v64"])), key
+
+
+def test_action_known_answers(oracle, golden):
+    # test_kernels.cpp:281-290: reference tet, P1 mass action of w = 1 -> 1/24 per function
+    ref = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], dtype=np.float64)
+    v, _ = oracle.action(1, MASS, MODES["fp64"], ref[None], np.ones((1, 4)))
+    assert np.max(np.abs(v - 1.0 / 24.0)) <= 1e-13
+    # the action is the bilinear matrix applied to w (fp64: both are exact to rounding)
+    V = golden["verts"]
+    rng = np.random.default_rng(3)
+    for form in (MASS, POISSON):
+        for p in (2, 3):
+            w = rng.uniform(-1, 1, size=(2, nphi(p)))
+            v, _ = oracle.action(p, form, MODES["fp64"], V[:2], w)
+            a, _ = oracle.bilinear(p, form, MODES["fp64"], V[:2])
+            av = np.einsum("cij,cj->ci", a, w)
+            assert np.max(np.abs(v - av)) <= 1e-13 * np.max(np.abs(av))
