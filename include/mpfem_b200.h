@@ -118,6 +118,29 @@ int mpfem_b200_cell_matrices_scatter(mpfem_b200_setup_t setup, const double* ver
                                      const int32_t* pos_map, void* values, int values_fmt,
                                      void* stream, uint32_t* flags);
 
+/* Batched replacement for action_kernel (kernels.hpp:90-92, kernels.cpp:269-304; Algorithm
+ * 2 of the paper): v_c = sum_s B_s r_s for n_cells cells in ONE launch, on DEVICE buffers,
+ * bit-identical to the reference in every mode (same op order and roundings: eval_w_at_ug
+ * kernels.cpp:145-173, integrand kernels.cpp:280-301, b_cat_action contraction :303).
+ *   verts/cells/coef: as mpfem_b200_cell_matrices (the reference takes one nodal z for the
+ *           batch: pass coef_stride 0 to share it)
+ *   w:      n_cells rows of n_phi fp64 FE coefficients (row stride w_stride >= n_phi)
+ *   out:    n_cells rows of n_phi (row pitch out_pitch) -- row c is column c of the
+ *           reference's n_phi x batch result; fp64 if u_q = fp64, else fp32 carriers of u_q
+ * Errors as the reference: ConfigError (2) for a short w / coefficient, CheckError (3) for a
+ * singular cell (reported when flags != NULL, which synchronizes). */
+int mpfem_b200_action(mpfem_b200_setup_t setup, const double* verts, const int32_t* cells,
+                      int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
+                      const double* w, int64_t w_stride, void* out, int64_t out_pitch,
+                      void* stream, uint32_t* flags);
+
+/* Same on HOST buffers (H2D of vertices, coefficients and w; D2H of v inside the call). */
+int mpfem_b200_action_host(mpfem_b200_setup_t setup, const double* verts, int64_t n_verts,
+                           const int32_t* cells, int64_t n_cells, int coef_kind,
+                           const double* coef, int64_t coef_stride, const double* w,
+                           int64_t w_stride, void* out, int64_t out_pitch, void* stream,
+                           uint32_t* flags);
+
 /* Number of kernel launches the last cell_matrices call on this setup issued. */
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 

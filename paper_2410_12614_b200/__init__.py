@@ -19,7 +19,7 @@ import numpy as np
 __all__ = [
     "Fmt", "FormKind", "ModeKind", "EngineKind", "CoefKind", "KernelConfig", "KernelSetup",
     "ConfigError", "CheckError", "RuntimeFailure", "reference_config", "make_setup",
-    "bilinear_kernel", "mode_config", "lib", "LIB_PATH",
+    "bilinear_kernel", "action_kernel", "mode_config", "lib", "LIB_PATH",
 ]
 
 LIB_PATH = os.environ.get("MPFEM_B200_LIB") or os.path.join(
@@ -130,6 +130,10 @@ def lib():
         "mpfem_b200_cell_matrices_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
                                                     C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_reserve": (C.c_int, [vp, C.c_int64]),
+        "mpfem_b200_action": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
+                                        C.c_int64, vp, C.c_int64, vp, u32p]),
+        "mpfem_b200_action_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
+                                             C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_scaled_weights": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
                                                 vp, u32p]),
         "mpfem_b200_last_launch_count": (C.c_int, [vp]),
@@ -297,6 +301,50 @@ class KernelSetup:
                                               C.byref(fl)))
         return out, fl.value
 
+    def action(self, verts, w, cells=None, coef_kind: int = CoefKind.one, coef=None, out=None,
+               stream=None, want_flags: bool = False):
+        """Batched action_kernel (Algorithm 2) on device tensors: w (n, n_phi) float64 FE
+        coefficients per cell -> v (n, n_phi), row c = the reference's column c. Bitwise the
+        reference's result in every mode. A 1-D coef (one nodal z for the whole batch, as the
+        reference's action_kernel takes it) is shared by all cells."""
+        import torch
+        n = int(cells.shape[0]) if cells is not None else int(verts.shape[0])
+        if w.dim() != 2 or w.shape[0] != n:
+            raise ConfigError("action batch needs one coefficient vector per cell")
+        dt = torch.float64 if self.config.u_q == Fmt.fp64 else torch.float32
+        if out is None:
+            out = torch.empty((n, self.n_phi), dtype=dt, device=w.device)
+        # a 1-D coef is one vector shared by the batch (stride 0), as the reference's z
+        stride = 0 if coef is None or coef.dim() == 1 else int(coef.stride(0))
+        fl = C.c_uint32(0)
+        check(lib().mpfem_b200_action(self._h, _ptr(verts), _ptr(cells), n, int(coef_kind),
+                                      _ptr(coef), stride, _ptr(w), int(w.stride(0)), _ptr(out),
+                                      int(out.stride(0)), _stream_handle(stream),
+                                      C.byref(fl) if want_flags else None))
+        return (out, fl.value) if want_flags else out
+
+    def action_host(self, verts: np.ndarray, w: np.ndarray, cells: np.ndarray | None = None,
+                    coef_kind: int = CoefKind.one, coef: np.ndarray | None = None, stream=None,
+                    want_flags: bool = False):
+        """Same on host (numpy) buffers: H2D, compute, D2H inside the call."""
+        verts = np.ascontiguousarray(verts, dtype=np.float64)
+        n = cells.shape[0] if cells is not None else verts.shape[0]
+        n_verts = verts.reshape(-1, 3).shape[0] if cells is not None else 0
+        if cells is not None:
+            cells = np.ascontiguousarray(cells, dtype=np.int32)
+        w = np.ascontiguousarray(w, dtype=np.float64).reshape(n, -1)
+        stride = 0
+        if coef is not None:
+            coef = np.ascontiguousarray(coef, dtype=np.float64).reshape(n, -1)
+            stride = coef.shape[1]
+        out = np.empty((n, self.n_phi), dtype=np.float64 if self.config.u_q == Fmt.fp64 else np.float32)
+        fl = C.c_uint32(0)
+        check(lib().mpfem_b200_action_host(self._h, _ptr(verts), n_verts, _ptr(cells), n,
+                                           int(coef_kind), _ptr(coef), stride, _ptr(w), w.shape[1],
+                                           _ptr(out), self.n_phi, _stream_handle(stream),
+                                           C.byref(fl) if want_flags else None))
+        return (out, fl.value) if want_flags else out
+
     def last_launch_count(self) -> int:
         return lib().mpfem_b200_last_launch_count(self._h)
 
@@ -322,9 +370,7 @@ class KernelSetup:
 
 
 def make_setup(p: int, config: KernelConfig, cell_kind: int = 0, dim: int = 3) -> KernelSetup:
-    """make_setup (kernels.hpp:60-62) for affine tetrahedra."""
-    if config.mode != ModeKind.bilinear:
-        raise ConfigError("configuration is not a bilinear-mode config")
+    """make_setup (kernels.hpp:60-62) for affine tetrahedra (bilinear or action mode)."""
     return KernelSetup(p, config, cell_kind, dim)
 
 
@@ -334,6 +380,14 @@ def bilinear_kernel(setup: KernelSetup, verts, cells=None, coef_kind: int = Coef
     if setup.config.mode != ModeKind.bilinear:
         raise ConfigError("configuration is not a bilinear-mode config")
     return setup.cell_matrices(verts, cells, coef_kind, coef, **kw)
+
+
+def action_kernel(setup: KernelSetup, verts, w, cells=None, coef_kind: int = CoefKind.one,
+                  coef=None, **kw):
+    """Batched action_kernel (kernels.hpp:90-92): v (n, n_phi), bitwise the reference's."""
+    if setup.config.mode != ModeKind.action:
+        raise ConfigError("configuration is not an action-mode config")
+    return setup.action(verts, w, cells, coef_kind, coef, **kw)
 
 
 def gen_tets(kind: int, seed: int, n: int):

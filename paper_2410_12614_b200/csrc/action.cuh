@@ -1,0 +1,310 @@
+// action.cuh -- KA: the reference's Algorithm 2 (action_kernel, kernels.cpp:269-304),
+// batched over cells in one fused launch, bit-identical to the reference in every mode.
+//
+//   what[c][s][q] = round_ug( sum_k  round_us(w_ck) * Bs[s][k][q]   at u_p, k ascending )
+//                   (eval_w_at_ug, kernels.cpp:145-173)
+//   r[c][s][q]    = round_us( (omega_q * (sum_t G_st what_t)) * zhat_q   at u_g, t ascending )
+//                   (kernels.cpp:280-301; build_r 214-240)
+//   v[c][i]       = sum_(s,q) Bs[s][i][q] * r[c][s][q]   at u_q, (s, q) ascending
+//                   (blocked_matmul(b_cat_action, r_cat), kernels.cpp:303)
+//
+// Bs is the setup's store tabulation (evaluated at u_p, stored at u_s). Every product and
+// every sum is rounded once to its format, in the reference's order, so the results are
+// the reference's bits: the two contractions are sequential per output and cannot use FMA
+// or a tensor-core tree (both would change the rounding). The product is therefore an
+// issue-bound SIMT kernel: a CTA holds a tile of cells in shared memory, each thread keeps
+// CB cells of one output column in registers so that one coalesced tabulation load (L1/L2
+// resident, shared by all cells) feeds CB multiply-adds.
+//
+// Arithmetic per format (exact-rounding arguments as device_fp.cuh):
+//   fp64: hardware DMUL/DADD;  fp32: FMUL/FADD with _rn (no contraction) -- the binary64
+//   product of two fp32 values is exact, so one fp32 rounding equals the reference's;
+//   fp16: fp32 op then one RNE conversion to fp16 (24 >= 2*11+2: no double-rounding error)
+//   for fp16-representable operands; anything else (bf16 accumulation, operands wider than
+//   the accumulate format, FTZ fp64) runs the generic binary64-carrier emulation.
+// The matrix engine (engine 2) flushes subnormal accumulates to signed zero
+// (mm_units.cpp:43-62, flush_output_subnormals).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "device_fp.cuh"
+
+namespace mpfem_b200 {
+
+enum ArithKind : int { kArF64 = 0, kArF32 = 1, kArF16 = 2, kArGen = 3 };
+
+struct ActionParams {
+  const double* verts;
+  const int32_t* cells;  // optional mesh indexing (n_cells x 4)
+  int64_t n_cells;
+  int coef_kind;
+  const double* coef;
+  int64_t coef_stride;
+  const double* w;  // n_cells rows of n_phi fp64 (row stride w_stride)
+  int64_t w_stride;
+  const void* tab_a;  // [k][s * n_q + q]  store tabulation, u_p compute type
+  const void* tab_c;  // [s * n_q + q][i]  store tabulation, u_q compute type
+  const double* tab_up;    // value tabulation at u_p, [k][q] (nodal coefficient)
+  const double* rule_w_ug; // omega_q rounded to u_g
+  const double* rule_x;    // xi_q, [q][3]
+  int n_phi, n_q, n_d;
+  int up, ug, uq, us;
+  int ftz;
+  int tile;  // cells per CTA tile
+  void* out;  // n_cells x out_pitch, fp32 (u_q != fp64) or fp64
+  int64_t out_pitch;
+  uint32_t* flags;
+  int* error;
+};
+
+constexpr int kActionThreads = 256;
+constexpr int kActionCB = 4;  // cells per thread in the contractions
+
+template <int A>
+struct Arith;
+template <>
+struct Arith<kArF64> {
+  using T = double;
+  __device__ static T mul(T a, T b, int, uint32_t&) { return __dmul_rn(a, b); }
+  __device__ static T add(T a, T b, int, bool ftz, uint32_t&) {
+    T r = __dadd_rn(a, b);
+    if (ftz && fabs(r) < 0x1.0p-1022) r = copysign(0.0, r);
+    return r;
+  }
+};
+template <>
+struct Arith<kArF32> {
+  using T = float;
+  __device__ static T mul(T a, T b, int, uint32_t&) { return __fmul_rn(a, b); }
+  __device__ static T add(T a, T b, int, bool ftz, uint32_t&) {
+    T r = __fadd_rn(a, b);
+    if (ftz && fabsf(r) < 0x1.0p-126f) r = copysignf(0.0f, r);
+    return r;
+  }
+};
+template <>
+struct Arith<kArF16> {
+  using T = float;
+  __device__ static T mul(T a, T b, int, uint32_t&) { return __half2float(__float2half_rn(__fmul_rn(a, b))); }
+  __device__ static T add(T a, T b, int, bool ftz, uint32_t&) {
+    T r = __half2float(__float2half_rn(__fadd_rn(a, b)));
+    if (ftz && fabsf(r) < 0x1.0p-14f) r = copysignf(0.0f, r);
+    return r;
+  }
+};
+template <>
+struct Arith<kArGen> {
+  using T = double;
+  __device__ static T mul(T a, T b, int f, uint32_t& fl) { return dmul(a, b, f, fl); }
+  __device__ static T add(T a, T b, int f, bool ftz, uint32_t& fl) {
+    T r = dadd(a, b, f, fl);
+    if (ftz && r != 0.0 && fabs(r) < fmt_min_normal(f)) {
+      fl |= kUnderflow;
+      r = copysign(0.0, r);
+    }
+    return r;
+  }
+  __device__ static double fmt_min_normal(int f) {
+    return f == kFP64 ? 0x1.0p-1022 : (f == kFP16 ? 0x1.0p-14 : 0x1.0p-126);
+  }
+};
+
+// Geometry at a runtime u_g (the op sequence of cell_geometry, geometry.cpp:12-118).
+static __device__ __noinline__ bool action_geometry(const double v[4][3], bool poisson, int ug,
+                                             TetGeometry& g, uint32_t& fl) {
+  switch (ug) {
+    case kFP64: return tet_geometry<kFP64>(v, poisson, g, fl);
+    case kFP32: return tet_geometry<kFP32>(v, poisson, g, fl);
+    case kFP16: return tet_geometry<kFP16>(v, poisson, g, fl);
+    default: return tet_geometry<kBF16>(v, poisson, g, fl);
+  }
+}
+
+// Shared-memory layout of one tile (C cells), all 8-byte aligned:
+//   sWH  C x n_d n_q  double   what at u_g, then reused for nothing (r lives in sR)
+//   sR   C x n_d n_q  TQ       r at u_s (exact in the u_q compute type)
+//   sWm  C x n_phi    TP       round_us(w)
+//   sGeo C x 16       double   G (6), v0 doubled (3), edges doubled (9 -> 16 padded: v0 3 + e 9 + g 6 = 18)
+constexpr int kGeoWords = 18;
+
+template <int AP, int AQ>
+__host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q, int n_d) {
+  using TP = typename Arith<AP>::T;
+  using TQ = typename Arith<AQ>::T;
+  const size_t n1 = size_t(n_d) * n_q;
+  size_t b = size_t(tile) * n1 * sizeof(double);
+  b += (size_t(tile) * n1 * sizeof(TQ) + 7) / 8 * 8;
+  b += (size_t(tile) * n_phi * sizeof(TP) + 7) / 8 * 8;
+  b += size_t(tile) * kGeoWords * sizeof(double);
+  return b;
+}
+
+template <int AP, int AQ>
+__global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionParams P) {
+  using TP = typename Arith<AP>::T;
+  using TQ = typename Arith<AQ>::T;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int C = P.tile, nphi = P.n_phi, nq = P.n_q, nd = P.n_d;
+  const int n1 = nd * nq;
+  double* sWH = reinterpret_cast<double*>(smem);
+  TQ* sR = reinterpret_cast<TQ*>(sWH + size_t(C) * n1);
+  TP* sWm = reinterpret_cast<TP*>(reinterpret_cast<unsigned char*>(sR) + (size_t(C) * n1 * sizeof(TQ) + 7) / 8 * 8);
+  double* sGeo = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(sWm) + (size_t(C) * nphi * sizeof(TP) + 7) / 8 * 8);
+  const TP* tabA = static_cast<const TP*>(P.tab_a);
+  const TQ* tabC = static_cast<const TQ*>(P.tab_c);
+  const bool ftz = P.ftz != 0;
+  const bool poisson = nd == 3;
+  uint32_t fl = 0;
+  const int64_t n_tiles = (P.n_cells + C - 1) / C;
+  const int groups = (C + kActionCB - 1) / kActionCB;
+
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t c0 = tile * C;
+    const int nc = int((P.n_cells - c0 < int64_t(C) ? P.n_cells - c0 : int64_t(C)));
+    // -- stage: geometry (one thread per cell) and the u_s-rounded w
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      double* geo = sGeo + c * kGeoWords;
+      if (c >= nc) {
+        for (int j = 0; j < kGeoWords; ++j) geo[j] = 0.0;
+        continue;
+      }
+      const int64_t cell = c0 + c;
+      double v[4][3];
+      #pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t base = P.cells ? int64_t(P.cells[cell * 4 + k]) * 3 : cell * 12 + k * 3;
+        #pragma unroll
+        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[base + a];
+      }
+      TetGeometry g;
+      if (!action_geometry(v, poisson, P.ug, g, fl)) {
+        atomicExch(P.error, 3);
+        for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+      }
+      for (int b = 0; b < 6; ++b) geo[b] = g.g[b];
+      // origin and edges with x, y pre-doubled (the analytic coefficient's arguments, as K1)
+      #pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double sc = a < 2 ? 2.0 : 1.0;
+        geo[6 + a] = sc * v[0][a];
+        #pragma unroll
+        for (int s2 = 0; s2 < 3; ++s2) geo[9 + s2 * 3 + a] = sc * __dsub_rn(v[s2 + 1][a], v[0][a]);
+      }
+    }
+    for (int e = threadIdx.x; e < C * nphi; e += blockDim.x) {
+      const int c = e / nphi, k = e - c * nphi;
+      double wv = c < nc ? P.w[(c0 + c) * P.w_stride + k] : 0.0;
+      sWm[e] = TP(dround(wv, P.us, fl));
+    }
+    __syncthreads();
+
+    // -- what (eval_w_at_ug): column n = s n_q + q, CB cells per thread, k ascending at u_p
+    for (int item = threadIdx.x; item < groups * n1; item += blockDim.x) {
+      const int cg = item / n1, n = item - cg * n1;
+      TP acc[kActionCB];
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) acc[j] = TP(0);
+      const TP* wrow = sWm + cg * kActionCB * nphi;
+      bool on[kActionCB];  // rows past the tile (C not a multiple of the block) stay idle
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) on[j] = cg * kActionCB + j < C;
+      for (int k = 0; k < nphi; ++k) {
+        const TP b = tabA[size_t(k) * n1 + n];
+        #pragma unroll
+        for (int j = 0; j < kActionCB; ++j)
+          if (on[j])
+            acc[j] = Arith<AP>::add(acc[j], Arith<AP>::mul(wrow[j * nphi + k], b, P.up, fl), P.up, ftz, fl);
+      }
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) {
+        const int c = cg * kActionCB + j;
+        if (c < C) sWH[size_t(c) * n1 + n] = dround(double(acc[j]), P.ug, fl);
+      }
+    }
+    __syncthreads();
+
+    // -- integrand r at u_g, stored at u_s: one thread per (cell, q)
+    for (int item = threadIdx.x; item < C * nq; item += blockDim.x) {
+      const int c = item / nq, q = item - c * nq;
+      const double* geo = sGeo + c * kGeoWords;
+      const double* wh = sWH + size_t(c) * n1;
+      const double om = P.rule_w_ug[q];
+      double zq = 1.0;
+      bool have_z = P.coef_kind != 0;
+      if (c < nc && have_z) {
+        const double xi[3] = {P.rule_x[3 * q], P.rule_x[3 * q + 1], P.rule_x[3 * q + 2]};
+        const double* coef = P.coef ? P.coef + (c0 + c) * P.coef_stride : nullptr;
+        if (P.coef_kind == 1) {
+          zq = P.ug == kFP32 ? double(coef_sincosexp_f(geo + 6, geo + 9, xi))
+                             : dround(coef_sincosexp_e(geo + 6, geo + 9, xi), P.ug, fl);
+        } else if (P.coef_kind == 2) {
+          zq = dround(coef_exp10_affine(coef, xi), P.ug, fl);
+        } else {
+          double acc = 0.0;  // eval_z_at_ug (kernels.cpp:114-136)
+          for (int k = 0; k < nphi; ++k)
+            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[size_t(k) * nq + q], P.up, fl), P.up, fl);
+          zq = dround(acc, P.ug, fl);
+        }
+      }
+      for (int s = 0; s < nd; ++s) {
+        double t1 = 0.0;
+        if (poisson) {
+          for (int t = 0; t < 3; ++t) {
+            const int gi = s <= t ? (s * (5 - s)) / 2 + t : (t * (5 - t)) / 2 + s;  // upper-tri index
+            t1 = dadd(t1, dmul(geo[gi], wh[t * nq + q], P.ug, fl), P.ug, fl);
+          }
+        } else {
+          t1 = dadd(t1, dmul(geo[0], wh[q], P.ug, fl), P.ug, fl);
+        }
+        double m1 = dmul(om, t1, P.ug, fl);
+        if (have_z) m1 = dmul(m1, zq, P.ug, fl);
+        double r = c < nc ? dround(m1, P.us, fl) : 0.0;
+        sR[size_t(c) * n1 + s * nq + q] = TQ(r);
+      }
+    }
+    __syncthreads();
+
+    // -- v = b_cat_action r at u_q: output i, CB cells per thread, (s, q) ascending
+    for (int item = threadIdx.x; item < groups * nphi; item += blockDim.x) {
+      const int cg = item / nphi, i = item - cg * nphi;
+      TQ acc[kActionCB];
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) acc[j] = TQ(0);
+      const TQ* rrow = sR + size_t(cg) * kActionCB * n1;
+      bool on[kActionCB];
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) on[j] = cg * kActionCB + j < nc;
+      for (int kk = 0; kk < n1; ++kk) {
+        const TQ b = tabC[size_t(kk) * nphi + i];
+        #pragma unroll
+        for (int j = 0; j < kActionCB; ++j)
+          if (on[j])
+            acc[j] = Arith<AQ>::add(acc[j], Arith<AQ>::mul(b, rrow[size_t(j) * n1 + kk], P.uq, fl), P.uq, ftz, fl);
+      }
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) {
+        const int c = cg * kActionCB + j;
+        if (c < nc) {
+          double v = double(acc[j]);
+          if (!isfinite(v)) fl |= isnan(v) ? kInvalid : kOverflow;
+          // NaN leaves as the reference's canonical quiet NaN (softfloat.hpp round_to)
+          if (isnan(v)) v = canonical_nan_d();
+          if (P.uq == kFP64)
+            static_cast<double*>(P.out)[(c0 + c) * P.out_pitch + i] = v;
+          else
+            static_cast<float*>(P.out)[(c0 + c) * P.out_pitch + i] = float(v);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  publish_flags(P.flags, fl);
+}
+
+// Host launcher (launch_action.cu): picks the arithmetic instantiation and the tile.
+void launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st);
+
+}  // namespace mpfem_b200

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/mpfem_b200.h"
+#include "action.cuh"
 #include "cellmat_fused.cuh"
 #include "cellmat_simt.cuh"
 #include "cellmat_tc.cuh"
@@ -152,6 +153,9 @@ struct mpfem_b200_setup_s {
   void* cur_values = nullptr;
   int cur_values_fp64 = 0;
   DevBuf d_locals;  // non-fused paths: local matrices staged before the atomic scatter
+  // action (Algorithm 2): store tabulation in the u_p / u_q compute types, built on first use
+  DevBuf d_act_a, d_act_c;
+  int act_ap = -1, act_aq = -1;
   uint32_t epoch = 0;
   uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
   // host-API staging
@@ -571,6 +575,110 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   }
 }
 
+// Compute type of a contraction accumulating at `acc` over operands stored at u_s
+// (action.cuh): hardware fp64 / fp32, fp16 through fp32 for fp16 operands, else emulation.
+int action_arith(int acc, int us) {
+  if (acc == 3) return kArF64;
+  if (acc == 2 && us <= 2) return kArF32;
+  if (acc == 1 && us == 1) return kArF16;
+  return kArGen;
+}
+
+template <typename T>
+void upload_typed(DevBuf& buf, const std::vector<double>& v) {
+  std::vector<T> t(v.begin(), v.end());
+  buf.ensure(sizeof(T) * t.size());
+  CUDA_OK(cudaMemcpy(buf.p, t.data(), sizeof(T) * t.size(), cudaMemcpyHostToDevice));
+}
+
+// make_setup's store tabulation (tab_store: evaluated at u_p, stored at u_s,
+// kernels.cpp:86-98) in the two layouts of the action contractions.
+void prepare_action(mpfem_b200_setup_s& S) {
+  int ap = action_arith(S.up, S.us), aq = action_arith(S.uq, S.us);
+  if (ap != aq) ap = aq = kArGen;
+  if (ap == S.act_ap) return;
+  uint32_t fl = 0;
+  const Basis basis = simplex_basis(S.p);
+  const std::vector<double> tab = tabulate(basis, S.rule, S.up, S.us, S.form == 1, fl);
+  const int nphi = S.n_phi, nq = S.n_q, nd = S.n_d, n1 = nd * nq;
+  std::vector<double> a(size_t(nphi) * n1), c(size_t(n1) * nphi);
+  for (int s = 0; s < nd; ++s)
+    for (int k = 0; k < nphi; ++k)
+      for (int q = 0; q < nq; ++q) {
+        const double v = tab[(size_t(s) * nphi + k) * nq + q];
+        a[size_t(k) * n1 + s * nq + q] = v;
+        c[size_t(s * nq + q) * nphi + k] = v;
+      }
+  if (ap == kArF32 || ap == kArF16) {
+    upload_typed<float>(S.d_act_a, a);
+    upload_typed<float>(S.d_act_c, c);
+  } else {
+    upload_typed<double>(S.d_act_a, a);
+    upload_typed<double>(S.d_act_c, c);
+  }
+  S.act_ap = ap;
+  S.act_aq = aq;
+}
+
+void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
+                int coef_kind, const double* coef, int64_t coef_stride, const double* w,
+                int64_t w_stride, void* out, int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+  // one nodal z may be shared by the batch (stride 0), as the reference's action_kernel takes it
+  check_coef(S, coef_kind, coef, coef_kind == 3 && coef_stride == 0 ? S.n_phi : coef_stride);
+  if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative batch");
+  if (n > 0 && (!verts || !w || !out)) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+  if (w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+  if (out_pitch < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
+  prepare_action(S);
+  S.last_launches = 0;
+  if (flags) {
+    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
+    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
+  }
+  if (n > 0) {
+    ActionParams P{};
+    P.verts = verts;
+    P.cells = cells;
+    P.n_cells = n;
+    P.coef_kind = coef_kind;
+    P.coef = coef;
+    P.coef_stride = coef_stride;
+    P.w = w;
+    P.w_stride = w_stride;
+    P.tab_a = S.d_act_a.p;
+    P.tab_c = S.d_act_c.p;
+    P.tab_up = static_cast<const double*>(S.d_tab_up.p);
+    P.rule_w_ug = static_cast<const double*>(S.d_rule_w_ug.p);
+    P.rule_x = static_cast<const double*>(S.d_rule_x.p);
+    P.n_phi = S.n_phi;
+    P.n_q = S.n_q;
+    P.n_d = S.n_d;
+    P.up = S.up;
+    P.ug = S.ug;
+    P.uq = S.uq;
+    P.us = S.us;
+    P.ftz = S.engine == 2;
+    P.out = out;
+    P.out_pitch = out_pitch;
+    P.flags = static_cast<uint32_t*>(S.d_flags.p);
+    P.error = static_cast<int*>(S.d_error.p);
+    S.n_ev = 0;
+    S.mark(st);
+    launch_action(S.act_ap, S.act_aq, P, device_sm_count(), st);
+    CUDA_OK(cudaGetLastError());
+    S.mark(st);
+    S.last_launches = 1;
+  }
+  if (flags) {
+    uint32_t h[2] = {0, 0};
+    CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaMemcpyAsync(&h[1], S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    *flags |= h[0];
+    if (h[1] == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -824,6 +932,58 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t S, const double* verts, const i
       CUDA_OK(cudaStreamSynchronize(st));
       *flags |= h;
     }
+  });
+}
+
+int mpfem_b200_action(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
+                      int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
+                      const double* w, int64_t w_stride, void* out, int64_t out_pitch,
+                      void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    run_action(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, w, w_stride, out, out_pitch,
+               static_cast<cudaStream_t>(stream), flags);
+  });
+}
+
+int mpfem_b200_action_host(mpfem_b200_setup_t S, const double* verts, int64_t n_verts,
+                           const int32_t* cells, int64_t n_cells, int coef_kind, const double* coef,
+                           int64_t coef_stride, const double* w, int64_t w_stride, void* out,
+                           int64_t out_pitch, void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    check_coef(*S, coef_kind, coef, coef_stride);  // host path: per-cell rows only
+    if (w_stride < S->n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 12);
+    S->h_verts.ensure(vbytes + 8);
+    CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
+    const int32_t* dcells = nullptr;
+    if (cells) {
+      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * 4 + 8);
+      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * 4,
+                              cudaMemcpyHostToDevice, st));
+      dcells = static_cast<const int32_t*>(S->h_cells.p);
+    }
+    const double* dcoef = nullptr;
+    if (coef && (coef_kind == 2 || coef_kind == 3)) {
+      const size_t cb = sizeof(double) * size_t(n_cells) * size_t(coef_stride);
+      S->h_coef.ensure(cb + 8);
+      CUDA_OK(cudaMemcpyAsync(S->h_coef.p, coef, cb, cudaMemcpyHostToDevice, st));
+      dcoef = static_cast<const double*>(S->h_coef.p);
+    }
+    // w and the result share one staging buffer: [w (n x w_stride fp64) | v]
+    const size_t wbytes = sizeof(double) * size_t(n_cells) * size_t(w_stride);
+    const size_t esz = S->uq == 3 ? 8 : 4;
+    const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
+    S->h_out.ensure(wbytes + obytes + 16);
+    char* base = static_cast<char*>(S->h_out.p);
+    CUDA_OK(cudaMemcpyAsync(base, w, wbytes, cudaMemcpyHostToDevice, st));
+    void* dout = base + (wbytes + 15) / 16 * 16;
+    run_action(*S, static_cast<const double*>(S->h_verts.p), dcells, n_cells, coef_kind, dcoef,
+               coef_stride, reinterpret_cast<const double*>(base), w_stride, dout, out_pitch, st, flags);
+    CUDA_OK(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
   });
 }
 

@@ -62,8 +62,8 @@ def test_config_validation_before_device():
         mp.make_setup(2, mp.KernelConfig(n_batch=0))
     with pytest.raises(mp.ConfigError):
         mp.make_setup(0, mp.KernelConfig())
-    with pytest.raises(mp.ConfigError):
-        mp.make_setup(2, mp.KernelConfig(mode=mp.ModeKind.action))
+    with pytest.raises(mp.ConfigError):  # action_kernel needs an action-mode config
+        mp.action_kernel(type("S", (), {"config": mp.KernelConfig()})(), None, None)
     with pytest.raises(mp.ConfigError):  # bf16 accumulation has no B200 path
         mp.make_setup(2, mp.KernelConfig(u_q=mp.Fmt.bf16, u_s=mp.Fmt.bf16))
 
