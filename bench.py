@@ -317,6 +317,51 @@ def run_modes(mp, torch, dev, flush):
     return res
 
 
+def run_action(mp, torch, dev, flush, sm_mhz):
+    """Algorithm 2 (action_kernel, kernels.cpp:269-304) on the config-0/1 workloads: 65,536
+    seeded P4 tets, c(x) at the quadrature points, one w per cell, every precision mode.
+    One launch per step (KA, bitwise the reference's op order); cells/s, error against the
+    device fp64 action, and the issue roof: the reference rounds every product and sum, so
+    each of the 2 n_phi n_d n_q multiply-adds per cell is two instructions (FMUL+FADD at 128
+    lanes/clk/SM, or DMUL+DADD at 64/clk/SM in fp64 mode)."""
+    verts, _ = mp.gen_tets(0, 1, N_CELLS)
+    vd = torch.from_numpy(verts).to(dev)
+    rng = np.random.default_rng(1)
+    res = []
+    clk = sm_mhz * 1e6
+    for form, name in ((0, "config0 mass"), (1, "config1 poisson")):
+        n_phi, n_q, n_d = nphi(P_DEG), (P_DEG + 1) ** 3, 3 if form else 1
+        wd = torch.from_numpy(rng.uniform(-1.0, 1.0, size=(N_CELLS, n_phi))).to(dev)
+        ref = None
+        pairs = 2.0 * n_phi * n_d * n_q * N_CELLS
+        for mode in ("fp64", "fp32", "fp16", "mixed", "mixed_bf16"):
+            cfg = mp.mode_config(mode, form, geometry_fp64=(form == 1))
+            cfg.mode = mp.ModeKind.action
+            s = mp.make_setup(P_DEG, cfg)
+            out = torch.empty((N_CELLS, n_phi), dtype=torch.float64 if mode == "fp64" else torch.float32,
+                              device=dev)
+            ms = timed_ms(torch, lambda: mp.action_kernel(s, vd, wd, coef_kind=mp.CoefKind.sincosexp, out=out),
+                          flush=flush)
+            if mode == "fp64":
+                ref = out.clone()
+                e = np.zeros(1)
+            else:
+                e = err_rel(torch, out, ref)
+            lanes = 64.0 if mode == "fp64" else 128.0
+            t_issue = 2.0 * pairs / (148 * lanes * clk) * 1e3
+            res.append({"config": name, "mode": mode, "ms": ms, "cells_per_s": N_CELLS / (ms * 1e-3),
+                        "launches": s.last_launch_count(),
+                        "gflop_per_s": 2.0 * pairs / (ms * 1e-3) / 1e9,
+                        "issue_roof_ms": t_issue, "issue_frac": t_issue / ms,
+                        "hbm_bytes": N_CELLS * (96 + 8 * n_phi + out.element_size() * n_phi),
+                        "max_err_rel_vs_fp64": fin(e.max()),
+                        "max_err_over_u_s": fin(e.max() / UNIT_ROUNDOFF[int(cfg.u_s)])})
+            del s, out
+        del ref, wd
+        torch.cuda.empty_cache()
+    return res
+
+
 def run_robustness(mp, torch, dev):
     """BASELINE config 3: 65,536 anisotropic rotated tets, c = 10^(6 u(x)) with u affine per
     cell; P1-P6 mass and Poisson in fp16 and mixed (fp16 and bf16 storage): max per-cell error
@@ -437,6 +482,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-modes", action="store_true", help="skip the configs 0/1 precision-mode table")
     ap.add_argument("--robustness", action="store_true", help="add the config-3 error table")
+    ap.add_argument("--no-action", action="store_true", help="skip the Algorithm-2 action table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -588,6 +634,10 @@ def main():
                             "results": run_assembly(mp, torch, dev, rank, world)}
     if not args.no_modes and rank == 0:
         line["modes"] = run_modes(mp, torch, dev, flush)
+    if not args.no_action and rank == 0:
+        line["action"] = {"workload": "configs 0/1 as action_kernel (Algorithm 2): 65536 P4 tets, "
+                                      "c(x) at quadrature points, one random w per cell",
+                          "results": run_action(mp, torch, dev, flush, clocks.get("sm_max_mhz") or 1965.0)}
     if args.robustness and rank == 0:
         line["robustness"] = run_robustness(mp, torch, dev)
     if args.sweep and rank == 0:

@@ -112,6 +112,34 @@ struct Arith<kArGen> {
   }
 };
 
+// The integrand stage at u_g: hardware ops when u_g is fp64 or fp32 (every operand -- G,
+// what, omega, zhat -- is already a u_g value, so the fp32 op is the reference's rounded
+// binary64 op), the flagged emulation otherwise.
+enum UgKind : int { kUg64 = 0, kUg32 = 1, kUgGen = 2 };
+template <int UGK>
+__device__ __forceinline__ double ug_mul(double a, double b, int ug, uint32_t& fl) {
+  if constexpr (UGK == kUg64) return __dmul_rn(a, b);
+  else if constexpr (UGK == kUg32) return double(__fmul_rn(float(a), float(b)));
+  else return dmul(a, b, ug, fl);
+}
+template <int UGK>
+__device__ __forceinline__ double ug_add(double a, double b, int ug, uint32_t& fl) {
+  if constexpr (UGK == kUg64) return __dadd_rn(a, b);
+  else if constexpr (UGK == kUg32) return double(__fadd_rn(float(a), float(b)));
+  else return dadd(a, b, ug, fl);
+}
+
+// round_to at a runtime format through the compile-time conversions (one cvt for fp16 /
+// bf16 / fp32; bitwise dround, device_fp.cuh).
+__device__ __forceinline__ double dround_fast(double x, int f, uint32_t& fl) {
+  switch (f) {
+    case kBF16: return droundT<kBF16>(x, fl);
+    case kFP16: return droundT<kFP16>(x, fl);
+    case kFP32: return droundT<kFP32>(x, fl);
+    default: return droundT<kFP64>(x, fl);
+  }
+}
+
 // Geometry at a runtime u_g (the op sequence of cell_geometry, geometry.cpp:12-118).
 static __device__ __noinline__ bool action_geometry(const double v[4][3], bool poisson, int ug,
                                              TetGeometry& g, uint32_t& fl) {
@@ -123,146 +151,153 @@ static __device__ __noinline__ bool action_geometry(const double v[4][3], bool p
   }
 }
 
-// Shared-memory layout of one tile (C cells), all 8-byte aligned:
-//   sWH  C x n_d n_q  double   what at u_g, then reused for nothing (r lives in sR)
-//   sR   C x n_d n_q  TQ       r at u_s (exact in the u_q compute type)
-//   sWm  C x n_phi    TP       round_us(w)
-//   sGeo C x 16       double   G (6), v0 doubled (3), edges doubled (9 -> 16 padded: v0 3 + e 9 + g 6 = 18)
+// Shared-memory layout of one tile of C cells (C a multiple of kActionCB; rows past the last
+// cell are zeros), cell index fastest so that the CB cells of a thread are one vector load
+// and the per-(cell, q) integrand stage is bank-conflict free:
+//   sWm  [k][C]          TP      round_us(w)
+//   sWH  [s n_q + q][C]  double  what at u_g
+//   sR   [s n_q + q][C]  TQ      r at u_s (exact in the u_q compute type)
+//   sGeo [C][18]         double  G (6: G00 G01 G02 G11 G12 G22 / |det|), 2v0x 2v0y v0z, edges
 constexpr int kGeoWords = 18;
 
-template <int AP, int AQ>
+template <int A>
 __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q, int n_d) {
-  using TP = typename Arith<AP>::T;
-  using TQ = typename Arith<AQ>::T;
+  using T = typename Arith<A>::T;
   const size_t n1 = size_t(n_d) * n_q;
-  size_t b = size_t(tile) * n1 * sizeof(double);
-  b += (size_t(tile) * n1 * sizeof(TQ) + 7) / 8 * 8;
-  b += (size_t(tile) * n_phi * sizeof(TP) + 7) / 8 * 8;
-  b += size_t(tile) * kGeoWords * sizeof(double);
-  return b;
+  return size_t(tile) * (size_t(n_phi) * sizeof(T) + n1 * (sizeof(double) + sizeof(T)) +
+                         kGeoWords * sizeof(double));
 }
 
-template <int AP, int AQ>
+// One cell's geometry row at u_g: G (6, upper triangle; mass: |det|), then K1's coefficient
+// inputs (2 v0x, 2 v0y, v0z and the edges with x, y doubled).
+__device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell, double* geo,
+                                             uint32_t& fl) {
+  double v[4][3];
+  #pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t base = P.cells ? int64_t(P.cells[cell * 4 + k]) * 3 : cell * 12 + k * 3;
+    #pragma unroll
+    for (int a = 0; a < 3; ++a) v[k][a] = P.verts[base + a];
+  }
+  TetGeometry g;
+  if (!action_geometry(v, P.n_d == 3, P.ug, g, fl)) {
+    atomicExch(P.error, 3);
+    for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+  }
+  for (int b = 0; b < 6; ++b) geo[b] = g.g[b];
+  #pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double sc = a < 2 ? 2.0 : 1.0;
+    geo[6 + a] = sc * v[0][a];
+    #pragma unroll
+    for (int s2 = 0; s2 < 3; ++s2) geo[9 + s2 * 3 + a] = sc * __dsub_rn(v[s2 + 1][a], v[0][a]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void load_cb(const T* p, T (&v)[kActionCB]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const double2 x = reinterpret_cast<const double2*>(p)[0], y = reinterpret_cast<const double2*>(p)[1];
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+  }
+}
+
+template <int A, bool FTZ, int UGK>
 __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionParams P) {
-  using TP = typename Arith<AP>::T;
-  using TQ = typename Arith<AQ>::T;
+  using T = typename Arith<A>::T;
+  using Ar = Arith<A>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int C = P.tile, nphi = P.n_phi, nq = P.n_q, nd = P.n_d;
   const int n1 = nd * nq;
-  double* sWH = reinterpret_cast<double*>(smem);
-  TQ* sR = reinterpret_cast<TQ*>(sWH + size_t(C) * n1);
-  TP* sWm = reinterpret_cast<TP*>(reinterpret_cast<unsigned char*>(sR) + (size_t(C) * n1 * sizeof(TQ) + 7) / 8 * 8);
-  double* sGeo = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(sWm) + (size_t(C) * nphi * sizeof(TP) + 7) / 8 * 8);
-  const TP* tabA = static_cast<const TP*>(P.tab_a);
-  const TQ* tabC = static_cast<const TQ*>(P.tab_c);
-  const bool ftz = P.ftz != 0;
+  T* sWm = reinterpret_cast<T*>(smem);
+  double* sWH = reinterpret_cast<double*>(sWm + size_t(C) * nphi);
+  T* sR = reinterpret_cast<T*>(sWH + size_t(C) * n1);
+  double* sGeo = reinterpret_cast<double*>(sR + size_t(C) * n1);
+  const T* tabA = static_cast<const T*>(P.tab_a);
+  const T* tabC = static_cast<const T*>(P.tab_c);
   const bool poisson = nd == 3;
   uint32_t fl = 0;
   const int64_t n_tiles = (P.n_cells + C - 1) / C;
-  const int groups = (C + kActionCB - 1) / kActionCB;
+  const int groups = C / kActionCB;
 
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t c0 = tile * C;
     const int nc = int((P.n_cells - c0 < int64_t(C) ? P.n_cells - c0 : int64_t(C)));
     // -- stage: geometry (one thread per cell) and the u_s-rounded w
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      double* geo = sGeo + c * kGeoWords;
-      if (c >= nc) {
-        for (int j = 0; j < kGeoWords; ++j) geo[j] = 0.0;
-        continue;
-      }
-      const int64_t cell = c0 + c;
-      double v[4][3];
-      #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t base = P.cells ? int64_t(P.cells[cell * 4 + k]) * 3 : cell * 12 + k * 3;
-        #pragma unroll
-        for (int a = 0; a < 3; ++a) v[k][a] = P.verts[base + a];
-      }
-      TetGeometry g;
-      if (!action_geometry(v, poisson, P.ug, g, fl)) {
-        atomicExch(P.error, 3);
-        for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
-      }
-      for (int b = 0; b < 6; ++b) geo[b] = g.g[b];
-      // origin and edges with x, y pre-doubled (the analytic coefficient's arguments, as K1)
-      #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double sc = a < 2 ? 2.0 : 1.0;
-        geo[6 + a] = sc * v[0][a];
-        #pragma unroll
-        for (int s2 = 0; s2 < 3; ++s2) geo[9 + s2 * 3 + a] = sc * __dsub_rn(v[s2 + 1][a], v[0][a]);
-      }
+      if (c < nc) cell_geo_row(P, c0 + c, sGeo + c * kGeoWords, fl);
+      else for (int j = 0; j < kGeoWords; ++j) sGeo[c * kGeoWords + j] = 0.0;
     }
     for (int e = threadIdx.x; e < C * nphi; e += blockDim.x) {
-      const int c = e / nphi, k = e - c * nphi;
-      double wv = c < nc ? P.w[(c0 + c) * P.w_stride + k] : 0.0;
-      sWm[e] = TP(dround(wv, P.us, fl));
+      const int c = e / nphi, k = e - c * nphi;  // coalesced over the w rows
+      const double wv = c < nc ? P.w[(c0 + c) * P.w_stride + k] : 0.0;
+      sWm[k * C + c] = T(dround_fast(wv, P.us, fl));
     }
     __syncthreads();
 
     // -- what (eval_w_at_ug): column n = s n_q + q, CB cells per thread, k ascending at u_p
     for (int item = threadIdx.x; item < groups * n1; item += blockDim.x) {
       const int cg = item / n1, n = item - cg * n1;
-      TP acc[kActionCB];
+      T acc[kActionCB];
       #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) acc[j] = TP(0);
-      const TP* wrow = sWm + cg * kActionCB * nphi;
-      bool on[kActionCB];  // rows past the tile (C not a multiple of the block) stay idle
-      #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) on[j] = cg * kActionCB + j < C;
-      for (int k = 0; k < nphi; ++k) {
-        const TP b = tabA[size_t(k) * n1 + n];
+      for (int j = 0; j < kActionCB; ++j) acc[j] = T(0);
+      const T* bp = tabA + n;
+      const T* wp = sWm + cg * kActionCB;
+      #pragma unroll 4
+      for (int k = 0; k < nphi; ++k, bp += n1, wp += C) {
+        const T b = __ldg(bp);
+        T wv[kActionCB];
+        load_cb(wp, wv);
         #pragma unroll
         for (int j = 0; j < kActionCB; ++j)
-          if (on[j])
-            acc[j] = Arith<AP>::add(acc[j], Arith<AP>::mul(wrow[j * nphi + k], b, P.up, fl), P.up, ftz, fl);
+          acc[j] = Ar::add(acc[j], Ar::mul(wv[j], b, P.up, fl), P.up, FTZ, fl);
       }
       #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) {
-        const int c = cg * kActionCB + j;
-        if (c < C) sWH[size_t(c) * n1 + n] = dround(double(acc[j]), P.ug, fl);
-      }
+      for (int j = 0; j < kActionCB; ++j)
+        sWH[size_t(n) * C + cg * kActionCB + j] = dround_fast(double(acc[j]), P.ug, fl);
     }
     __syncthreads();
 
-    // -- integrand r at u_g, stored at u_s: one thread per (cell, q)
+    // -- integrand r at u_g, stored at u_s: one thread per (q, cell), cell fastest
+    const bool have_z = P.coef_kind != 0;
     for (int item = threadIdx.x; item < C * nq; item += blockDim.x) {
-      const int c = item / nq, q = item - c * nq;
+      const int q = item / C, c = item - q * C;
       const double* geo = sGeo + c * kGeoWords;
-      const double* wh = sWH + size_t(c) * n1;
       const double om = P.rule_w_ug[q];
       double zq = 1.0;
-      bool have_z = P.coef_kind != 0;
       if (c < nc && have_z) {
         const double xi[3] = {P.rule_x[3 * q], P.rule_x[3 * q + 1], P.rule_x[3 * q + 2]};
         const double* coef = P.coef ? P.coef + (c0 + c) * P.coef_stride : nullptr;
         if (P.coef_kind == 1) {
           zq = P.ug == kFP32 ? double(coef_sincosexp_f(geo + 6, geo + 9, xi))
-                             : dround(coef_sincosexp_e(geo + 6, geo + 9, xi), P.ug, fl);
+                             : dround_fast(coef_sincosexp_e(geo + 6, geo + 9, xi), P.ug, fl);
         } else if (P.coef_kind == 2) {
-          zq = dround(coef_exp10_affine(coef, xi), P.ug, fl);
+          zq = dround_fast(coef_exp10_affine(coef, xi), P.ug, fl);
         } else {
           double acc = 0.0;  // eval_z_at_ug (kernels.cpp:114-136)
           for (int k = 0; k < nphi; ++k)
-            acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[size_t(k) * nq + q], P.up, fl), P.up, fl);
-          zq = dround(acc, P.ug, fl);
+            acc = dadd(acc, dmul(dround_fast(coef[k], P.up, fl), P.tab_up[size_t(k) * nq + q], P.up, fl), P.up, fl);
+          zq = dround_fast(acc, P.ug, fl);
         }
       }
       for (int s = 0; s < nd; ++s) {
         double t1 = 0.0;
         if (poisson) {
+          #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int gi = s <= t ? (s * (5 - s)) / 2 + t : (t * (5 - t)) / 2 + s;  // upper-tri index
-            t1 = dadd(t1, dmul(geo[gi], wh[t * nq + q], P.ug, fl), P.ug, fl);
+            t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[gi], sWH[size_t(t * nq + q) * C + c], P.ug, fl), P.ug, fl);
           }
         } else {
-          t1 = dadd(t1, dmul(geo[0], wh[q], P.ug, fl), P.ug, fl);
+          t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[0], sWH[size_t(q) * C + c], P.ug, fl), P.ug, fl);
         }
-        double m1 = dmul(om, t1, P.ug, fl);
-        if (have_z) m1 = dmul(m1, zq, P.ug, fl);
-        double r = c < nc ? dround(m1, P.us, fl) : 0.0;
-        sR[size_t(c) * n1 + s * nq + q] = TQ(r);
+        double m1 = ug_mul<UGK>(om, t1, P.ug, fl);
+        if (have_z) m1 = ug_mul<UGK>(m1, zq, P.ug, fl);
+        const double r = c < nc ? dround_fast(m1, P.us, fl) : 0.0;
+        sR[size_t(s * nq + q) * C + c] = T(r);
       }
     }
     __syncthreads();
@@ -270,19 +305,19 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
     // -- v = b_cat_action r at u_q: output i, CB cells per thread, (s, q) ascending
     for (int item = threadIdx.x; item < groups * nphi; item += blockDim.x) {
       const int cg = item / nphi, i = item - cg * nphi;
-      TQ acc[kActionCB];
+      T acc[kActionCB];
       #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) acc[j] = TQ(0);
-      const TQ* rrow = sR + size_t(cg) * kActionCB * n1;
-      bool on[kActionCB];
-      #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) on[j] = cg * kActionCB + j < nc;
-      for (int kk = 0; kk < n1; ++kk) {
-        const TQ b = tabC[size_t(kk) * nphi + i];
+      for (int j = 0; j < kActionCB; ++j) acc[j] = T(0);
+      const T* bp = tabC + i;
+      const T* rp = sR + cg * kActionCB;
+      #pragma unroll 4
+      for (int kk = 0; kk < n1; ++kk, bp += nphi, rp += C) {
+        const T b = __ldg(bp);
+        T rv[kActionCB];
+        load_cb(rp, rv);
         #pragma unroll
         for (int j = 0; j < kActionCB; ++j)
-          if (on[j])
-            acc[j] = Arith<AQ>::add(acc[j], Arith<AQ>::mul(b, rrow[size_t(j) * n1 + kk], P.uq, fl), P.uq, ftz, fl);
+          acc[j] = Ar::add(acc[j], Ar::mul(b, rv[j], P.uq, fl), P.uq, FTZ, fl);
       }
       #pragma unroll
       for (int j = 0; j < kActionCB; ++j) {

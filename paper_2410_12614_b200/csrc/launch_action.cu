@@ -7,39 +7,73 @@
 
 namespace mpfem_b200 {
 namespace {
-constexpr size_t kActionSmemBudget = 100 * 1024;  // two CTAs per SM
+constexpr size_t kActionSmemBudget = 110 * 1024;  // two CTAs per SM
+constexpr size_t kActionSmemMax = 227 * 1024;
 
+// Tile height C (cells per CTA, a multiple of the per-thread block): both contractions run
+// ceil(items / threads) rounds of a sequential loop (the reference's order forbids splitting
+// an output's sum), so C is chosen to minimise the rounds per cell, e.g. P4: C = 28 gives
+// 7 x 35 = 245 output items for 256 threads where C = 32 would need two rounds of 280.
 template <int A>
+int pick_tile(int n_phi, int n_q, int n_d, size_t budget) {
+  const int n1 = n_d * n_q;
+  int best = 0;
+  double best_cost = 0.0;
+  for (int c = kActionCB; c <= 32; c += kActionCB) {
+    if (action_smem_bytes<A>(c, n_phi, n_q, n_d) > budget) break;
+    const int g = c / kActionCB;
+    const double rounds_a = double((g * n1 + kActionThreads - 1) / kActionThreads) * n_phi;
+    const double rounds_c = double((g * n_phi + kActionThreads - 1) / kActionThreads) * n1;
+    const double rounds_b = double((c * n_q + kActionThreads - 1) / kActionThreads) * 8.0 * n_d;
+    const double cost = (rounds_a + rounds_c + rounds_b) / c;
+    if (!best || cost < best_cost * 0.999) {
+      best = c;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+template <int A, bool FTZ, int UGK>
 void launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   ActionParams P = P0;
-  // tile: as many cells as fit the budget, a multiple of the per-thread cell block
-  int tile = 32;
-  while (tile > kActionCB && action_smem_bytes<A, A>(tile, P.n_phi, P.n_q, P.n_d) > kActionSmemBudget)
-    tile -= kActionCB;
-  while (tile > 1 && action_smem_bytes<A, A>(tile, P.n_phi, P.n_q, P.n_d) > kActionSmemBudget) --tile;
+  int tile = pick_tile<A>(P.n_phi, P.n_q, P.n_d, kActionSmemBudget);
+  int per_sm = 2;
+  if (!tile) {  // high degree in fp64: one CTA of kActionCB cells per SM
+    tile = kActionCB;
+    per_sm = 1;
+  }
+  const size_t smem = action_smem_bytes<A>(tile, P.n_phi, P.n_q, P.n_d);
+  if (smem > kActionSmemMax) return;  // not reachable for p <= 8
   P.tile = tile;
-  const size_t smem = action_smem_bytes<A, A>(tile, P.n_phi, P.n_q, P.n_d);
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    if (cudaFuncSetAttribute(action_kernel<A, A>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(action_kernel<A, FTZ, UGK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(std::max<size_t>(smem, 48 * 1024))) != cudaSuccess)
       return;  // reported by the caller's launch check
     smem_set = smem;
   }
   const int64_t tiles = (P.n_cells + tile - 1) / tile;
-  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sm_count) * 2));
-  action_kernel<A, A><<<grid, kActionThreads, smem, st>>>(P);
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sm_count) * per_sm));
+  action_kernel<A, FTZ, UGK><<<grid, kActionThreads, smem, st>>>(P);
 }
 }  // namespace
 
 void launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st) {
   const int a = ap == aq ? ap : kArGen;
-  switch (a) {
-    case kArF64: launch_one<kArF64>(P, sm_count, st); break;
-    case kArF32: launch_one<kArF32>(P, sm_count, st); break;
-    case kArF16: launch_one<kArF16>(P, sm_count, st); break;
-    default: launch_one<kArGen>(P, sm_count, st); break;
-  }
+  const bool ftz = P.ftz != 0;
+  if (a == kArF64 && P.ug == kFP64) return launch_one<kArF64, false, kUg64>(P, sm_count, st);
+  if (a == kArF16 && P.ug == kFP32) return launch_one<kArF16, false, kUg32>(P, sm_count, st);
+  if (a == kArF32 && P.ug == kFP32)
+    return ftz ? launch_one<kArF32, true, kUg32>(P, sm_count, st) : launch_one<kArF32, false, kUg32>(P, sm_count, st);
+  if (a == kArF32 && P.ug == kFP64)
+    return ftz ? launch_one<kArF32, true, kUg64>(P, sm_count, st) : launch_one<kArF32, false, kUg64>(P, sm_count, st);
+  // every other format combination: binary64 carriers with the flagged emulation
+  if (a == kArF64) return launch_one<kArF64, false, kUgGen>(P, sm_count, st);
+  if (a == kArF32)
+    return ftz ? launch_one<kArF32, true, kUgGen>(P, sm_count, st) : launch_one<kArF32, false, kUgGen>(P, sm_count, st);
+  if (a == kArF16) return launch_one<kArF16, false, kUgGen>(P, sm_count, st);
+  return ftz ? launch_one<kArGen, true, kUgGen>(P, sm_count, st) : launch_one<kArGen, false, kUgGen>(P, sm_count, st);
 }
 
 }  // namespace mpfem_b200

@@ -120,6 +120,11 @@ def test_action_analytic_coefficient_within_bound(oracle, tets, mode, form):
                 b, v64 = oracle.action_bound(p, form, cfg_tuple(cfg), vv[c], w[c], kind,
                                              None if cf is None else cf[c])
                 scale = np.max(np.abs(v64))
+                fin = np.isfinite(same[c])
+                if not fin.all():  # u_s overflow (fp16 storage, config 3): same events as the reference
+                    assert np.array_equal(np.isfinite(got[c]), fin), (mode, form, p, c)
+                    assert np.array_equal(got[c][~fin], same[c][~fin], equal_nan=True)
+                    continue
                 err64 = np.max(np.abs(got[c] - v64)) / scale
                 errsm = np.max(np.abs(got[c] - same[c])) / scale
                 assert errsm <= 2 * S * b[0], (mode, form, p, kind, c, errsm, b[0])
