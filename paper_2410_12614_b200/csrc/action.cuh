@@ -61,7 +61,8 @@ struct ActionParams {
 };
 
 constexpr int kActionThreads = 256;
-constexpr int kActionCB = 4;  // cells per thread in the contractions
+constexpr int kActionCB = 4;   // cells per thread in the b_cat_action contraction (few outputs)
+constexpr int kActionCBA = 4;  // cells per thread in the w evaluation (measured: 8 is slower)
 
 template <int A>
 struct Arith;
@@ -151,7 +152,7 @@ static __device__ __noinline__ bool action_geometry(const double v[4][3], bool p
   }
 }
 
-// Shared-memory layout of one tile of C cells (C a multiple of kActionCB; rows past the last
+// Shared-memory layout of one tile of C cells (C a multiple of kActionCBA; rows past the last
 // cell are zeros), cell index fastest so that the CB cells of a thread are one vector load
 // and the per-(cell, q) integrand stage is bank-conflict free:
 //   sWm  [k][C]          TP      round_us(w)
@@ -164,7 +165,10 @@ template <int A>
 __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q, int n_d) {
   using T = typename Arith<A>::T;
   const size_t n1 = size_t(n_d) * n_q;
-  return size_t(tile) * (size_t(n_phi) * sizeof(T) + n1 * (sizeof(double) + sizeof(T)) +
+  // a double r overwrites what in place (each (q, cell) item reads its own three what values
+  // before writing its r values), so fp64 compute types need one n1 array per cell
+  const size_t r_bytes = sizeof(T) == 8 ? 0 : sizeof(T);
+  return size_t(tile) * (size_t(n_phi) * sizeof(T) + n1 * (sizeof(double) + r_bytes) +
                          kGeoWords * sizeof(double));
 }
 
@@ -194,14 +198,17 @@ __device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell
   }
 }
 
-template <typename T>
-__device__ __forceinline__ void load_cb(const T* p, T (&v)[kActionCB]) {
-  if constexpr (sizeof(T) == 4) {
-    const float4 x = *reinterpret_cast<const float4*>(p);
-    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-  } else {
-    const double2 x = reinterpret_cast<const double2*>(p)[0], y = reinterpret_cast<const double2*>(p)[1];
-    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+template <typename T, int N>
+__device__ __forceinline__ void load_cb(const T* p, T (&v)[N]) {
+  #pragma unroll
+  for (int h = 0; h < N / 4; ++h) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 x = reinterpret_cast<const float4*>(p)[h];
+      v[4 * h] = x.x; v[4 * h + 1] = x.y; v[4 * h + 2] = x.z; v[4 * h + 3] = x.w;
+    } else {
+      const double2 x = reinterpret_cast<const double2*>(p)[2 * h], y = reinterpret_cast<const double2*>(p)[2 * h + 1];
+      v[4 * h] = x.x; v[4 * h + 1] = x.y; v[4 * h + 2] = y.x; v[4 * h + 3] = y.y;
+    }
   }
 }
 
@@ -214,8 +221,8 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
   const int n1 = nd * nq;
   T* sWm = reinterpret_cast<T*>(smem);
   double* sWH = reinterpret_cast<double*>(sWm + size_t(C) * nphi);
-  T* sR = reinterpret_cast<T*>(sWH + size_t(C) * n1);
-  double* sGeo = reinterpret_cast<double*>(sR + size_t(C) * n1);
+  T* sR = sizeof(T) == 8 ? reinterpret_cast<T*>(sWH) : reinterpret_cast<T*>(sWH + size_t(C) * n1);
+  double* sGeo = sizeof(T) == 8 ? sWH + size_t(C) * n1 : reinterpret_cast<double*>(sR + size_t(C) * n1);
   const T* tabA = static_cast<const T*>(P.tab_a);
   const T* tabC = static_cast<const T*>(P.tab_c);
   const bool poisson = nd == 3;
@@ -238,26 +245,27 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
     }
     __syncthreads();
 
-    // -- what (eval_w_at_ug): column n = s n_q + q, CB cells per thread, k ascending at u_p
-    for (int item = threadIdx.x; item < groups * n1; item += blockDim.x) {
+    // -- what (eval_w_at_ug): column n = s n_q + q, CBA cells per thread, k ascending at u_p
+    const int groups_a = C / kActionCBA;
+    for (int item = threadIdx.x; item < groups_a * n1; item += blockDim.x) {
       const int cg = item / n1, n = item - cg * n1;
-      T acc[kActionCB];
+      T acc[kActionCBA];
       #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) acc[j] = T(0);
+      for (int j = 0; j < kActionCBA; ++j) acc[j] = T(0);
       const T* bp = tabA + n;
-      const T* wp = sWm + cg * kActionCB;
-      #pragma unroll 4
+      const T* wp = sWm + cg * kActionCBA;
+      #pragma unroll 2
       for (int k = 0; k < nphi; ++k, bp += n1, wp += C) {
         const T b = __ldg(bp);
-        T wv[kActionCB];
+        T wv[kActionCBA];
         load_cb(wp, wv);
         #pragma unroll
-        for (int j = 0; j < kActionCB; ++j)
+        for (int j = 0; j < kActionCBA; ++j)
           acc[j] = Ar::add(acc[j], Ar::mul(wv[j], b, P.up, fl), P.up, FTZ, fl);
       }
       #pragma unroll
-      for (int j = 0; j < kActionCB; ++j)
-        sWH[size_t(n) * C + cg * kActionCB + j] = dround_fast(double(acc[j]), P.ug, fl);
+      for (int j = 0; j < kActionCBA; ++j)
+        sWH[size_t(n) * C + cg * kActionCBA + j] = dround_fast(double(acc[j]), P.ug, fl);
     }
     __syncthreads();
 
@@ -283,16 +291,18 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
           zq = dround_fast(acc, P.ug, fl);
         }
       }
+      double wt[3] = {0.0, 0.0, 0.0};  // read before r overwrites what (fp64: aliased)
+      for (int t = 0; t < nd; ++t) wt[t] = sWH[size_t(t * nq + q) * C + c];
       for (int s = 0; s < nd; ++s) {
         double t1 = 0.0;
         if (poisson) {
           #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int gi = s <= t ? (s * (5 - s)) / 2 + t : (t * (5 - t)) / 2 + s;  // upper-tri index
-            t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[gi], sWH[size_t(t * nq + q) * C + c], P.ug, fl), P.ug, fl);
+            t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[gi], wt[t], P.ug, fl), P.ug, fl);
           }
         } else {
-          t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[0], sWH[size_t(q) * C + c], P.ug, fl), P.ug, fl);
+          t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[0], wt[0], P.ug, fl), P.ug, fl);
         }
         double m1 = ug_mul<UGK>(om, t1, P.ug, fl);
         if (have_z) m1 = ug_mul<UGK>(m1, zq, P.ug, fl);
@@ -340,6 +350,7 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
 }
 
 // Host launcher (launch_action.cu): picks the arithmetic instantiation and the tile.
-void launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st);
+// Returns 0, 2 (the tile does not fit shared memory) or 4 (attribute/launch failure).
+int launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st);
 
 }  // namespace mpfem_b200

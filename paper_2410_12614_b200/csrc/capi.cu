@@ -664,7 +664,9 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
     P.error = static_cast<int*>(S.d_error.p);
     S.n_ev = 0;
     S.mark(st);
-    launch_action(S.act_ap, S.act_aq, P, device_sm_count(), st);
+    const int rc = launch_action(S.act_ap, S.act_aq, P, device_sm_count(), st);
+    if (rc == 2) throw Error(MPFEM_B200_CONFIG_ERROR, "action tile exceeds shared memory");
+    if (rc) throw Error(MPFEM_B200_RUNTIME_ERROR, "action kernel attribute setup failed");
     CUDA_OK(cudaGetLastError());
     S.mark(st);
     S.last_launches = 1;

@@ -19,10 +19,10 @@ int pick_tile(int n_phi, int n_q, int n_d, size_t budget) {
   const int n1 = n_d * n_q;
   int best = 0;
   double best_cost = 0.0;
-  for (int c = kActionCB; c <= 32; c += kActionCB) {
+  for (int c = kActionCBA; c <= 32; c += kActionCBA) {
     if (action_smem_bytes<A>(c, n_phi, n_q, n_d) > budget) break;
-    const int g = c / kActionCB;
-    const double rounds_a = double((g * n1 + kActionThreads - 1) / kActionThreads) * n_phi;
+    const int g = c / kActionCB, ga = c / kActionCBA;
+    const double rounds_a = double((ga * n1 + kActionThreads - 1) / kActionThreads) * n_phi;
     const double rounds_c = double((g * n_phi + kActionThreads - 1) / kActionThreads) * n1;
     const double rounds_b = double((c * n_q + kActionThreads - 1) / kActionThreads) * 8.0 * n_d;
     const double cost = (rounds_a + rounds_c + rounds_b) / c;
@@ -35,31 +35,32 @@ int pick_tile(int n_phi, int n_q, int n_d, size_t budget) {
 }
 
 template <int A, bool FTZ, int UGK>
-void launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
+int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   ActionParams P = P0;
   int tile = pick_tile<A>(P.n_phi, P.n_q, P.n_d, kActionSmemBudget);
   int per_sm = 2;
-  if (!tile) {  // high degree in fp64: one CTA of kActionCB cells per SM
-    tile = kActionCB;
+  if (!tile) {  // high degree in fp64: one CTA of kActionCBA cells per SM
+    tile = kActionCBA;
     per_sm = 1;
   }
   const size_t smem = action_smem_bytes<A>(tile, P.n_phi, P.n_q, P.n_d);
-  if (smem > kActionSmemMax) return;  // not reachable for p <= 8
+  if (smem > kActionSmemMax) return 2;  // tile does not fit shared memory (not reached for p <= 8)
   P.tile = tile;
   static size_t smem_set = 0;
   if (smem > smem_set) {
     if (cudaFuncSetAttribute(action_kernel<A, FTZ, UGK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(std::max<size_t>(smem, 48 * 1024))) != cudaSuccess)
-      return;  // reported by the caller's launch check
+      return 4;
     smem_set = smem;
   }
   const int64_t tiles = (P.n_cells + tile - 1) / tile;
   const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sm_count) * per_sm));
   action_kernel<A, FTZ, UGK><<<grid, kActionThreads, smem, st>>>(P);
+  return 0;
 }
 }  // namespace
 
-void launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st) {
+int launch_action(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_t st) {
   const int a = ap == aq ? ap : kArGen;
   const bool ftz = P.ftz != 0;
   if (a == kArF64 && P.ug == kFP64) return launch_one<kArF64, false, kUg64>(P, sm_count, st);

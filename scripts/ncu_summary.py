@@ -51,6 +51,9 @@ if __name__ == "__main__":
         res["launch_list_avg"] = launch_list(os.path.join(OUT, "launches.csv"))
     if os.path.exists(os.path.join(OUT, "prof.ncu-rep")):
         res["ncu_full"] = full(os.path.join(OUT, "prof.ncu-rep"))
-    with open(os.path.join(ROOT, "profiles", f"{rnd}_ncu_summary.json"), "w") as f:
+    if os.path.exists(os.path.join(OUT, "prof_action.ncu-rep")):
+        res["ncu_full_action"] = full(os.path.join(OUT, "prof_action.ncu-rep"))
+    dest = os.environ.get("NCU_SUMMARY_DIR", os.path.join(ROOT, "profiles"))
+    with open(os.path.join(dest, f"{rnd}_ncu_summary.json"), "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1)[:3000])
