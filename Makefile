@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2410_12614_b200
 LIB := $(PKG)/lib/libmpfem_b200.so
 OBJDIR := $(PKG)/lib/obj
-CU_SRCS := capi assembly_capi launch_geom launch_fused launch_action
+CU_SRCS := capi assembly_capi launch_geom launch_fused launch_action launch_bounds
 CPP_SRCS := host_setup host_mesh
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU_SRCS) $(CPP_SRCS)))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/mpfem_b200.h
@@ -12,6 +12,11 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off \
            --expt-relaxed-constexpr -Xptxas -v
 
 all: $(LIB) oracle
+
+# kernel_bounds on the GPU: binary64 without FMA contraction (the reference's roundings)
+$(OBJDIR)/launch_bounds.o: $(PKG)/csrc/launch_bounds.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) --fmad=false -c -o $@ $< 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
 
 $(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)

@@ -594,6 +594,22 @@ def main():
     err = (diff / a64.view(N_CELLS, -1).abs().amax(dim=1)).cpu().numpy()
     del a64, s64, diff
     u_s = 2.0 ** -11  # fp16 unit roundoff
+    # every cell against its own a-priori bound: kernel_bounds (bounds.cpp:29-281) on the GPU
+    # (bitwise the reference's for nodal/constant coefficients, tests/test_gpu_bounds.py)
+    torch.cuda.synchronize()
+    tb0 = time.perf_counter()
+    bnd, a_exact = setup.cell_bounds(vd, coef_kind=mp.CoefKind.sincosexp, want_a64=True)
+    torch.cuda.synchronize()
+    bound_ms = (time.perf_counter() - tb0) * 1e3
+    e_exact = (out.view(N_CELLS, -1).double() - a_exact.view(N_CELLS, -1)).abs().amax(dim=1) / \
+        a_exact.view(N_CELLS, -1).abs().amax(dim=1)
+    ratio = (e_exact / (4.0 * bnd[:, 0])).cpu().numpy()  # S = 4: u_s coarser than u_p, u_g, u_q
+    bound_check = {"cells": N_CELLS, "max_err_over_S_bound_a": float(ratio.max()),
+                   "median_err_over_S_bound_a": float(np.median(ratio)),
+                   "cells_violating": int((ratio > 1.0).sum()), "S": 4,
+                   "bound_kernel_ms": bound_ms,
+                   "note": "err vs the exact binary64 A of kernel_bounds, per cell, all cells"}
+    del a_exact, bnd
     accuracy = {"vs": "device fp64 mode (oracle-pinned), same cells",
                 "metric": "per-cell max|A - A64| / max|A64| (errorlab.cpp:90-99)",
                 "max_err_rel": float(err.max()), "median_err_rel": float(np.median(err)),
@@ -627,6 +643,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clocks,
         "accuracy": accuracy,
+        "bound_check": bound_check,
     }
     if not args.no_assembly:
         line["assembly"] = {"workload": "config4: 96^3 x 6 tets, poisson P2/P3, mixed-bf16 kernels, "

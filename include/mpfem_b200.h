@@ -141,6 +141,18 @@ int mpfem_b200_action_host(mpfem_b200_setup_t setup, const double* verts, int64_
                            int64_t w_stride, void* out, int64_t out_pitch, void* stream,
                            uint32_t* flags);
 
+/* Per-cell a-priori error bound on the GPU: replaces kernel_bounds (bounds.hpp, bounds.cpp:
+ * 29-281, bilinear part) with basis_condition_numbers (elements.cpp:278-359) over n_cells cells
+ * in binary64, so bound dominance can be checked on every cell of a mesh.
+ *   out: n_cells x 4 doubles {bound_a, kappa_q_a, kappa_p_a, kappa_g_a} (NaN when A = 0)
+ *   a64: optional n_cells x n_phi^2 doubles, the exact binary64 A of the report (report.a)
+ * For constant and nodal coefficients every value is the reference's bit for bit; the
+ * analytic coefficient (kinds 1, 2) enters at x_q as in the Q path (z_at = c(x_q),
+ * theta_c = 0). Synchronizes (CheckError 3 for a singular cell). */
+int mpfem_b200_cell_bounds(mpfem_b200_setup_t setup, const double* verts, const int32_t* cells,
+                           int64_t n_cells, int coef_kind, const double* coef,
+                           int64_t coef_stride, double* out, double* a64, void* stream);
+
 /* Number of kernel launches the last cell_matrices call on this setup issued. */
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 

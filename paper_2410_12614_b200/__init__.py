@@ -132,6 +132,8 @@ def lib():
         "mpfem_b200_reserve": (C.c_int, [vp, C.c_int64]),
         "mpfem_b200_action": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
                                         C.c_int64, vp, C.c_int64, vp, u32p]),
+        "mpfem_b200_cell_bounds": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
+                                             vp]),
         "mpfem_b200_action_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
                                              C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_scaled_weights": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
@@ -344,6 +346,20 @@ class KernelSetup:
                                            _ptr(out), self.n_phi, _stream_handle(stream),
                                            C.byref(fl) if want_flags else None))
         return (out, fl.value) if want_flags else out
+
+    def cell_bounds(self, verts, cells=None, coef_kind: int = CoefKind.one, coef=None,
+                    want_a64: bool = False, stream=None):
+        """kernel_bounds (bounds.cpp:29-281, bilinear part) for every cell on the GPU:
+        (n, 4) float64 {bound_a, kappa_q, kappa_p, kappa_g} [and the exact A (n, n_phi, n_phi)]."""
+        import torch
+        n = int(cells.shape[0]) if cells is not None else int(verts.shape[0])
+        out = torch.empty((n, 4), dtype=torch.float64, device=verts.device)
+        a64 = torch.empty((n, self.n_phi, self.n_phi), dtype=torch.float64, device=verts.device) if want_a64 else None
+        stride = 0 if coef is None else int(coef.shape[-1])
+        check(lib().mpfem_b200_cell_bounds(self._h, _ptr(verts), _ptr(cells), n, int(coef_kind),
+                                           _ptr(coef), stride, _ptr(out), _ptr(a64),
+                                           _stream_handle(stream)))
+        return (out, a64) if want_a64 else out
 
     def last_launch_count(self) -> int:
         return lib().mpfem_b200_last_launch_count(self._h)

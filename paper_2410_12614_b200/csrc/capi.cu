@@ -16,6 +16,7 @@
 
 #include "../../include/mpfem_b200.h"
 #include "action.cuh"
+#include "bounds.cuh"
 #include "cellmat_fused.cuh"
 #include "cellmat_simt.cuh"
 #include "cellmat_tc.cuh"
@@ -156,6 +157,10 @@ struct mpfem_b200_setup_s {
   // action (Algorithm 2): store tabulation in the u_p / u_q compute types, built on first use
   DevBuf d_act_a, d_act_c;
   int act_ap = -1, act_aq = -1;
+  // GPU bound evaluation (kernel_bounds): binary64 budgets of the tabulation, built on first use
+  DevBuf d_bnd_theta, d_bnd_vals;
+  double bnd_lebesgue = 0.0;
+  bool bnd_ready = false;
   uint32_t epoch = 0;
   uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
   // host-API staging
@@ -681,6 +686,43 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   }
 }
 
+// kernel_bounds' setup-level inputs (bounds.cpp:60-95): theta_b of the binary64 tabulation
+// (Poisson: 3p grad_kappa(k, s) max_q |d_s phi_k|; mass: 3p |phi_k(x_q)|), the binary64 value
+// tabulation for nodal coefficients and the basis Lebesgue constant.
+void prepare_bounds(mpfem_b200_setup_s& S) {
+  if (S.bnd_ready) return;
+  const Basis basis = simplex_basis(S.p);
+  const BasisCond bc = basis_conditioning(basis, S.rule);
+  uint32_t fl = 0;
+  const std::vector<double> tab = tabulate(basis, S.rule, 3, 3, S.form == 1, fl);
+  const std::vector<double> vals = tabulate(basis, S.rule, 3, 3, false, fl);
+  const int nphi = S.n_phi, nq = S.n_q, nd = S.n_d;
+  const double dp = 3.0 * S.p;
+  std::vector<double> theta(tab.size());
+  for (int s = 0; s < nd; ++s)
+    for (int k = 0; k < nphi; ++k) {
+      const size_t row = (size_t(s) * nphi + k) * nq;
+      if (S.form == 1) {
+        double peak = 0.0;
+        for (int q = 0; q < nq; ++q) peak = std::max(peak, std::fabs(tab[row + q]));
+        const double budget = dp * bc.grad_kappa[k][s] * peak;
+        for (int q = 0; q < nq; ++q) theta[row + q] = budget;
+      } else {
+        for (int q = 0; q < nq; ++q) theta[row + q] = dp * std::fabs(tab[row + q]);
+      }
+    }
+  S.d_bnd_theta.ensure(sizeof(double) * theta.size());
+  CUDA_OK(cudaMemcpy(S.d_bnd_theta.p, theta.data(), sizeof(double) * theta.size(), cudaMemcpyHostToDevice));
+  S.d_bnd_vals.ensure(sizeof(double) * vals.size());
+  CUDA_OK(cudaMemcpy(S.d_bnd_vals.p, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice));
+  S.bnd_lebesgue = bc.lebesgue;
+  S.bnd_ready = true;
+}
+
+double unit_roundoff(int f) {
+  return f == 0 ? 0x1.0p-8 : (f == 1 ? 0x1.0p-11 : (f == 2 ? 0x1.0p-24 : 0x1.0p-53));
+}
+
 }  // namespace
 
 extern "C" {
@@ -986,6 +1028,51 @@ int mpfem_b200_action_host(mpfem_b200_setup_t S, const double* verts, int64_t n_
                coef_stride, reinterpret_cast<const double*>(base), w_stride, dout, out_pitch, st, flags);
     CUDA_OK(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+int mpfem_b200_cell_bounds(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
+                           int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
+                           double* out, double* a64, void* stream) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    check_coef(*S, coef_kind, coef, coef_stride);
+    if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prepare_bounds(*S);
+    if (n_cells == 0) return;
+    BoundParams P{};
+    P.verts = verts;
+    P.cells = cells;
+    P.n_cells = n_cells;
+    P.coef_kind = coef_kind;
+    P.coef = coef;
+    P.coef_stride = coef_stride;
+    P.tab = static_cast<const double*>(S->d_B.p);
+    P.theta_b = static_cast<const double*>(S->d_bnd_theta.p);
+    P.vals = static_cast<const double*>(S->d_bnd_vals.p);
+    P.rule_w = static_cast<const double*>(S->d_rule_w.p);
+    P.rule_x = static_cast<const double*>(S->d_rule_x.p);
+    P.n_phi = S->n_phi;
+    P.n_q = S->n_q;
+    P.n_d = S->n_d;
+    P.p = S->p;
+    P.lebesgue = S->bnd_lebesgue;
+    P.u_p = unit_roundoff(S->up);
+    P.u_g = unit_roundoff(S->ug);
+    P.u_q = unit_roundoff(S->uq);
+    P.u_s = unit_roundoff(S->us);
+    P.out = out;
+    P.a64 = a64;
+    P.error = static_cast<int*>(S->d_error.p);
+    CUDA_OK(cudaMemsetAsync(S->d_error.p, 0, 4, st));
+    if (launch_bounds_kernel(P, device_sm_count(), st)) throw Error(MPFEM_B200_RUNTIME_ERROR, "bound kernel attribute setup failed");
+    CUDA_OK(cudaGetLastError());
+    int err = 0;
+    CUDA_OK(cudaMemcpyAsync(&err, S->d_error.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (err == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+    S->last_launches = 1;
   });
 }
 

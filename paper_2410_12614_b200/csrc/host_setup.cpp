@@ -10,7 +10,9 @@
 //     (elements.cpp:89-147), evaluated factor by factor (elements.cpp:165-211).
 #include "host_setup.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <random>
 #include <cstring>
 #include <stdexcept>
 
@@ -289,6 +291,68 @@ std::vector<double> tabulate(const Basis& b, const Rule& r, int ef, int sf, bool
     }
   }
   return out;
+}
+
+BasisCond basis_conditioning(const Basis& b, const Rule& r) {
+  const int m = b.p, nphi = b.n_phi, nq = r.n_q, n_random = 2000;
+  std::vector<std::array<double, 3>> pts;
+  pts.reserve(size_t(nq + nphi + n_random));
+  for (int q = 0; q < nq; ++q) pts.push_back({r.points[3 * q], r.points[3 * q + 1], r.points[3 * q + 2]});
+  for (int k = 0; k < nphi; ++k) pts.push_back(b.nodes[k]);
+  std::mt19937_64 eng(9001);  // common.hpp:21-35 Rng
+  auto uniform = [&eng](double lo, double hi) { return lo + (hi - lo) * (double(eng() >> 11) * 0x1.0p-53); };
+  for (int i = 0; i < n_random; ++i) {
+    std::array<double, 3> x{};
+    for (;;) {  // sample_point (elements.cpp:279-289)
+      double sum = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        x[a] = uniform(0.0, 1.0);
+        sum += x[a];
+      }
+      if (sum <= 1.0) break;
+    }
+    pts.push_back(x);
+  }
+  BasisCond bc;
+  std::vector<std::array<double, 3>> num_max(size_t(nphi), {0.0, 0.0, 0.0}), abs_max(size_t(nphi), {0.0, 0.0, 0.0});
+  std::vector<double> lv(m), prefix(m + 1), suffix(m + 1);
+  for (const auto& xs : pts) {
+    const double* x = xs.data();
+    double sum_abs_phi = 0.0, sum_abs_grad[3] = {0.0, 0.0, 0.0};
+    for (int i = 0; i < nphi; ++i) {
+      for (int j = 0; j < m; ++j) lv[j] = factor_at(b.factors[i][j], x);
+      prefix[0] = 1.0;
+      for (int j = 0; j < m; ++j) prefix[j + 1] = prefix[j] * lv[j];
+      suffix[m] = 1.0;
+      for (int j = m - 1; j >= 0; --j) suffix[j] = suffix[j + 1] * lv[j];
+      sum_abs_phi += std::fabs(b.weight[i] * prefix[m]);
+      for (int s = 0; s < 3; ++s) {
+        double grad = 0.0, numer = 0.0;
+        for (int j = 0; j < m; ++j) {
+          const int sign = b.factors[i][j].sign[s];
+          if (sign == 0) continue;
+          const double complement = b.weight[i] * prefix[j] * suffix[j + 1];
+          grad += sign * complement;
+          numer += std::fabs(complement);
+        }
+        sum_abs_grad[s] += std::fabs(grad);
+        abs_max[i][s] = std::max(abs_max[i][s], std::fabs(grad));
+        num_max[i][s] = std::max(num_max[i][s], numer);
+      }
+    }
+    bc.lebesgue = std::max(bc.lebesgue, sum_abs_phi);
+    for (int s = 0; s < 3; ++s) bc.grad_lebesgue[s] = std::max(bc.grad_lebesgue[s], sum_abs_grad[s]);
+  }
+  bc.grad_kappa.resize(size_t(nphi));
+  for (int i = 0; i < nphi; ++i)
+    for (int s = 0; s < 3; ++s) {
+      const double numer = num_max[i][s], denom = abs_max[i][s];
+      double kappa = 1.0;
+      if (numer > 0.0) kappa = denom > 0.0 ? numer / denom : INFINITY;
+      bc.grad_kappa[i][s] = kappa;
+      bc.grad_kappa_max[s] = std::max(bc.grad_kappa_max[s], kappa);
+    }
+  return bc;
 }
 
 }  // namespace mpfem_b200

@@ -44,4 +44,16 @@ Basis simplex_basis(int p);
 std::vector<double> tabulate(const Basis& b, const Rule& r, int eval_fmt, int store_fmt,
                              bool gradients, uint32_t& flags);
 
+// basis_condition_numbers (elements.cpp:278-359): Lebesgue constant of the values, per-axis
+// gradient Lebesgue constants and per-function gradient evaluation condition numbers, sampled
+// at the rule points, the nodes and 2000 seeded points (Rng(9001), rejection in the unit tet).
+// Host inputs of the GPU bound evaluation (kernel_bounds, bounds.cpp:29-281).
+struct BasisCond {
+  double lebesgue = 1.0;
+  std::array<double, 3> grad_lebesgue{0.0, 0.0, 0.0};
+  std::vector<std::array<double, 3>> grad_kappa;  // n_phi
+  std::array<double, 3> grad_kappa_max{0.0, 0.0, 0.0};
+};
+BasisCond basis_conditioning(const Basis& b, const Rule& r);
+
 }  // namespace mpfem_b200
