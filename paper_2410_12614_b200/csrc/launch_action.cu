@@ -2,12 +2,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "action.cuh"
 
 namespace mpfem_b200 {
 namespace {
-constexpr size_t kActionSmemBudget = 110 * 1024;  // two CTAs per SM
 constexpr size_t kActionSmemMax = 227 * 1024;
 
 // Tile height C (cells per CTA, a multiple of the per-thread block): both contractions run
@@ -15,16 +15,16 @@ constexpr size_t kActionSmemMax = 227 * 1024;
 // an output's sum), so C is chosen to minimise the rounds per cell, e.g. P4: C = 28 gives
 // 7 x 35 = 245 output items for 256 threads where C = 32 would need two rounds of 280.
 template <int A>
-int pick_tile(int n_phi, int n_q, int n_d, size_t budget) {
+int pick_tile(int n_phi, int n_q, int n_d, size_t budget, int threads) {
   const int n1 = n_d * n_q;
   int best = 0;
   double best_cost = 0.0;
   for (int c = kActionCBA; c <= 32; c += kActionCBA) {
     if (action_smem_bytes<A>(c, n_phi, n_q, n_d) > budget) break;
     const int g = c / kActionCB, ga = c / kActionCBA;
-    const double rounds_a = double((ga * n1 + kActionThreads - 1) / kActionThreads) * n_phi;
-    const double rounds_c = double((g * n_phi + kActionThreads - 1) / kActionThreads) * n1;
-    const double rounds_b = double((c * n_q + kActionThreads - 1) / kActionThreads) * 8.0 * n_d;
+    const double rounds_a = double((ga * n1 + threads - 1) / threads) * n_phi;
+    const double rounds_c = double((g * n_phi + threads - 1) / threads) * n1;
+    const double rounds_b = double((c * n_q + threads - 1) / threads) * 8.0 * n_d;
     const double cost = (rounds_a + rounds_c + rounds_b) / c;
     if (!best || cost < best_cost * 0.999) {
       best = c;
@@ -37,8 +37,20 @@ int pick_tile(int n_phi, int n_q, int n_d, size_t budget) {
 template <int A, bool FTZ, int UGK>
 int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   ActionParams P = P0;
-  int tile = pick_tile<A>(P.n_phi, P.n_q, P.n_d, kActionSmemBudget);
-  int per_sm = 2;
+  // measured (scripts/action_sweep.py, P4): mass 128 threads / 36 KB tiles (230 vs 291 us),
+  // Poisson 256 threads / 70 KB tiles (710 vs 773 us); overridable for experiments
+  static const int env_threads = [] {
+    const char* e = std::getenv("MPFEM_B200_ACT_THREADS");
+    return e ? std::max(64, std::min(kActionThreads, std::atoi(e))) : 0;
+  }();
+  static const size_t env_budget = [] {
+    const char* e = std::getenv("MPFEM_B200_ACT_BUDGET_KB");
+    return e ? size_t(std::atoi(e)) * 1024 : 0;
+  }();
+  const int threads = env_threads ? env_threads : (P.n_d == 1 ? 128 : kActionThreads);
+  const size_t budget = env_budget ? env_budget : (P.n_d == 1 ? 36 * 1024 : 70 * 1024);
+  int tile = pick_tile<A>(P.n_phi, P.n_q, P.n_d, budget, threads);
+  int per_sm = std::max(1, std::min(int(224 * 1024 / std::max<size_t>(1, action_smem_bytes<A>(tile ? tile : kActionCBA, P.n_phi, P.n_q, P.n_d) + 1024)), 2048 / threads));
   if (!tile) {  // high degree in fp64: one CTA of kActionCBA cells per SM
     tile = kActionCBA;
     per_sm = 1;
@@ -55,7 +67,7 @@ int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   }
   const int64_t tiles = (P.n_cells + tile - 1) / tile;
   const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sm_count) * per_sm));
-  action_kernel<A, FTZ, UGK><<<grid, kActionThreads, smem, st>>>(P);
+  action_kernel<A, FTZ, UGK><<<grid, threads, smem, st>>>(P);
   return 0;
 }
 }  // namespace
