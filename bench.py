@@ -347,6 +347,13 @@ def run_action(mp, torch, dev, flush, sm_mhz):
                 e = np.zeros(1)
             else:
                 e = err_rel(torch, out, ref)
+            bound = None
+            if mode in ("mixed", "mixed_bf16"):  # every cell against kernel_bounds' bound_v
+                b, v64 = s.action_bounds(vd, wd, coef_kind=mp.CoefKind.sincosexp, want_v64=True)
+                ev = (out.double() - v64).abs().amax(dim=1) / v64.abs().amax(dim=1)
+                r = (ev / (4.0 * b[:, 0])).cpu().numpy()
+                bound = {"max_err_over_S_bound_v": fin(r.max()), "cells_violating": int((r > 1.0).sum())}
+                del b, v64
             lanes = 64.0 if mode == "fp64" else 128.0
             t_issue = 2.0 * pairs / (148 * lanes * clk) * 1e3
             res.append({"config": name, "mode": mode, "ms": ms, "cells_per_s": N_CELLS / (ms * 1e-3),
@@ -355,7 +362,8 @@ def run_action(mp, torch, dev, flush, sm_mhz):
                         "issue_roof_ms": t_issue, "issue_frac": t_issue / ms,
                         "hbm_bytes": N_CELLS * (96 + 8 * n_phi + out.element_size() * n_phi),
                         "max_err_rel_vs_fp64": fin(e.max()),
-                        "max_err_over_u_s": fin(e.max() / UNIT_ROUNDOFF[int(cfg.u_s)])})
+                        "max_err_over_u_s": fin(e.max() / UNIT_ROUNDOFF[int(cfg.u_s)]),
+                        "bound_check": bound})
             del s, out
         del ref, wd
         torch.cuda.empty_cache()

@@ -153,6 +153,15 @@ int mpfem_b200_cell_bounds(mpfem_b200_setup_t setup, const double* verts, const 
                            int64_t n_cells, int coef_kind, const double* coef,
                            int64_t coef_stride, double* out, double* a64, void* stream);
 
+/* The action part of kernel_bounds (bounds.cpp:128-155,224-240,268-279; the bound of Algorithm
+ * 2) per cell on the GPU: out n_cells x 4 {bound_v, kappa_q_v, kappa_p_v, kappa_g_v}; v64
+ * (optional) n_cells x n_phi, the exact binary64 v. w: n_cells rows of n_phi (stride w_stride).
+ * Bitwise the reference's for constant and nodal coefficients. Synchronizes. */
+int mpfem_b200_action_bounds(mpfem_b200_setup_t setup, const double* verts, const int32_t* cells,
+                             int64_t n_cells, int coef_kind, const double* coef,
+                             int64_t coef_stride, const double* w, int64_t w_stride, double* out,
+                             double* v64, void* stream);
+
 /* Number of kernel launches the last cell_matrices call on this setup issued. */
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 

@@ -134,6 +134,8 @@ def lib():
                                         C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_cell_bounds": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
                                              vp]),
+        "mpfem_b200_action_bounds": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
+                                               C.c_int64, vp, vp, vp]),
         "mpfem_b200_action_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
                                              C.c_int64, vp, C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_scaled_weights": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
@@ -360,6 +362,20 @@ class KernelSetup:
                                            _ptr(coef), stride, _ptr(out), _ptr(a64),
                                            _stream_handle(stream)))
         return (out, a64) if want_a64 else out
+
+    def action_bounds(self, verts, w, cells=None, coef_kind: int = CoefKind.one, coef=None,
+                      want_v64: bool = False, stream=None):
+        """kernel_bounds' action part for every cell on the GPU: (n, 4) {bound_v, kappa_q,
+        kappa_p, kappa_g} [and the exact v (n, n_phi)]."""
+        import torch
+        n = int(cells.shape[0]) if cells is not None else int(verts.shape[0])
+        out = torch.empty((n, 4), dtype=torch.float64, device=verts.device)
+        v64 = torch.empty((n, self.n_phi), dtype=torch.float64, device=verts.device) if want_v64 else None
+        stride = 0 if coef is None else int(coef.shape[-1])
+        check(lib().mpfem_b200_action_bounds(self._h, _ptr(verts), _ptr(cells), n, int(coef_kind),
+                                             _ptr(coef), stride, _ptr(w), int(w.stride(0)), _ptr(out),
+                                             _ptr(v64), _stream_handle(stream)))
+        return (out, v64) if want_v64 else out
 
     def last_launch_count(self) -> int:
         return lib().mpfem_b200_last_launch_count(self._h)

@@ -34,11 +34,18 @@ struct BoundParams {
   double* out;            // n_cells x 4: bound_a, kappa_q, kappa_p, kappa_g
   double* a64;            // optional n_cells x n_phi^2: exact binary64 A (report.a)
   int* error;
+  // action part (bound_v): w per cell and the gradient conditioning of the basis
+  const double* w;        // n_cells rows of n_phi (row stride w_stride); NULL = bilinear
+  int64_t w_stride;
+  double grad_lebesgue[3], grad_kappa_max[3];
 };
 
 constexpr int kBoundThreads = 256;
 
-// Host launcher (launch_bounds.cu). Returns 0 or 4 (attribute failure).
+// Host launchers (launch_bounds.cu). Return 0 or 4 (attribute failure). The action launcher
+// evaluates the action part of kernel_bounds (bound_v, bounds.cpp:128-155,224-240,268-279)
+// with a64 receiving the exact v (n_cells x n_phi).
 int launch_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st);
+int launch_action_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st);
 
 }  // namespace mpfem_b200

@@ -160,6 +160,7 @@ struct mpfem_b200_setup_s {
   // GPU bound evaluation (kernel_bounds): binary64 budgets of the tabulation, built on first use
   DevBuf d_bnd_theta, d_bnd_vals;
   double bnd_lebesgue = 0.0;
+  double bnd_glebesgue[3] = {0.0, 0.0, 0.0}, bnd_gkmax[3] = {0.0, 0.0, 0.0};
   bool bnd_ready = false;
   uint32_t epoch = 0;
   uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
@@ -716,6 +717,10 @@ void prepare_bounds(mpfem_b200_setup_s& S) {
   S.d_bnd_vals.ensure(sizeof(double) * vals.size());
   CUDA_OK(cudaMemcpy(S.d_bnd_vals.p, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice));
   S.bnd_lebesgue = bc.lebesgue;
+  for (int a = 0; a < 3; ++a) {
+    S.bnd_glebesgue[a] = bc.grad_lebesgue[a];
+    S.bnd_gkmax[a] = bc.grad_kappa_max[a];
+  }
   S.bnd_ready = true;
 }
 
@@ -1031,48 +1036,77 @@ int mpfem_b200_action_host(mpfem_b200_setup_t S, const double* verts, int64_t n_
   });
 }
 
+namespace {
+void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n_cells,
+                int coef_kind, const double* coef, int64_t coef_stride, const double* w,
+                int64_t w_stride, double* out, double* a64, cudaStream_t st) {
+  check_coef(S, coef_kind, coef, coef_stride);
+  if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+  if (w && w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+  prepare_bounds(S);
+  if (n_cells == 0) return;
+  BoundParams P{};
+  P.verts = verts;
+  P.cells = cells;
+  P.n_cells = n_cells;
+  P.coef_kind = coef_kind;
+  P.coef = coef;
+  P.coef_stride = coef_stride;
+  P.tab = static_cast<const double*>(S.d_B.p);
+  P.theta_b = static_cast<const double*>(S.d_bnd_theta.p);
+  P.vals = static_cast<const double*>(S.d_bnd_vals.p);
+  P.rule_w = static_cast<const double*>(S.d_rule_w.p);
+  P.rule_x = static_cast<const double*>(S.d_rule_x.p);
+  P.n_phi = S.n_phi;
+  P.n_q = S.n_q;
+  P.n_d = S.n_d;
+  P.p = S.p;
+  P.lebesgue = S.bnd_lebesgue;
+  for (int a = 0; a < 3; ++a) {
+    P.grad_lebesgue[a] = S.bnd_glebesgue[a];
+    P.grad_kappa_max[a] = S.bnd_gkmax[a];
+  }
+  P.u_p = unit_roundoff(S.up);
+  P.u_g = unit_roundoff(S.ug);
+  P.u_q = unit_roundoff(S.uq);
+  P.u_s = unit_roundoff(S.us);
+  P.out = out;
+  P.a64 = a64;
+  P.w = w;
+  P.w_stride = w_stride;
+  P.error = static_cast<int*>(S.d_error.p);
+  CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
+  const int rc = w ? launch_action_bounds_kernel(P, device_sm_count(), st)
+                   : launch_bounds_kernel(P, device_sm_count(), st);
+  if (rc) throw Error(MPFEM_B200_RUNTIME_ERROR, "bound kernel attribute setup failed");
+  CUDA_OK(cudaGetLastError());
+  int err = 0;
+  CUDA_OK(cudaMemcpyAsync(&err, S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  if (err == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+  S.last_launches = 1;
+}
+}  // namespace
+
 int mpfem_b200_cell_bounds(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
                            int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
                            double* out, double* a64, void* stream) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    check_coef(*S, coef_kind, coef, coef_stride);
-    if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    prepare_bounds(*S);
-    if (n_cells == 0) return;
-    BoundParams P{};
-    P.verts = verts;
-    P.cells = cells;
-    P.n_cells = n_cells;
-    P.coef_kind = coef_kind;
-    P.coef = coef;
-    P.coef_stride = coef_stride;
-    P.tab = static_cast<const double*>(S->d_B.p);
-    P.theta_b = static_cast<const double*>(S->d_bnd_theta.p);
-    P.vals = static_cast<const double*>(S->d_bnd_vals.p);
-    P.rule_w = static_cast<const double*>(S->d_rule_w.p);
-    P.rule_x = static_cast<const double*>(S->d_rule_x.p);
-    P.n_phi = S->n_phi;
-    P.n_q = S->n_q;
-    P.n_d = S->n_d;
-    P.p = S->p;
-    P.lebesgue = S->bnd_lebesgue;
-    P.u_p = unit_roundoff(S->up);
-    P.u_g = unit_roundoff(S->ug);
-    P.u_q = unit_roundoff(S->uq);
-    P.u_s = unit_roundoff(S->us);
-    P.out = out;
-    P.a64 = a64;
-    P.error = static_cast<int*>(S->d_error.p);
-    CUDA_OK(cudaMemsetAsync(S->d_error.p, 0, 4, st));
-    if (launch_bounds_kernel(P, device_sm_count(), st)) throw Error(MPFEM_B200_RUNTIME_ERROR, "bound kernel attribute setup failed");
-    CUDA_OK(cudaGetLastError());
-    int err = 0;
-    CUDA_OK(cudaMemcpyAsync(&err, S->d_error.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
-    if (err == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
-    S->last_launches = 1;
+    run_bounds(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, nullptr, 0, out, a64,
+               static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mpfem_b200_action_bounds(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
+                             int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
+                             const double* w, int64_t w_stride, double* out, double* v64,
+                             void* stream) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (n_cells > 0 && !w) throw Error(MPFEM_B200_CONFIG_ERROR, "action bound needs w");
+    run_bounds(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, w, w_stride, out, v64,
+               static_cast<cudaStream_t>(stream));
   });
 }
 

@@ -268,6 +268,121 @@ __global__ void __launch_bounds__(kBoundThreads) cell_bounds_kernel(const BoundP
   }
 }
 
+// Action part of kernel_bounds: one CTA per cell; threads over the rule points build r,
+// theta_r, gamma_r (bounds.cpp:128-155) in shared memory, then one thread per output i runs the
+// (s, q) accumulation (bounds.cpp:224-240).
+__global__ void __launch_bounds__(kBoundThreads) cell_action_bounds_kernel(const BoundParams P) {
+  extern __shared__ __align__(16) double sb[];
+  const int nq = P.n_q, nd = P.n_d, nphi = P.n_phi;
+  const int nr = nd * nq;
+  double* rr = sb;        // r_sq
+  double* thr = rr + nr;  // theta_r
+  double* gr = thr + nr;  // gamma_r
+  double* red = gr + nr;  // 4 x 32
+  __shared__ CellDiag sd;
+  __shared__ int s_ok;
+  const bool poisson = nd == 3;
+  const double pd = double(P.p) * double(P.p) * double(P.p);
+  const double kv = P.lebesgue;
+  for (int64_t cell = blockIdx.x; cell < P.n_cells; cell += gridDim.x) {
+    if (threadIdx.x == 0) {
+      s_ok = cell_diag(P, cell, poisson, sd);
+      if (!s_ok) atomicExch(P.error, 3);
+    }
+    __syncthreads();
+    const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
+    const double* w = P.w + cell * P.w_stride;
+    double z_norm = 0.0, w_norm = 0.0;
+    if (P.coef_kind == 3)
+      for (int i = 0; i < nphi; ++i) z_norm = fmax(z_norm, fabs(coef[i]));
+    for (int i = 0; i < nphi; ++i) w_norm = fmax(w_norm, fabs(w[i]));
+    for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+      double z = 1.0;
+      const double* xi = P.rule_x + 3 * q;
+      if (P.coef_kind == 3) {
+        z = 0.0;
+        for (int i = 0; i < nphi; ++i) z += coef[i] * P.vals[size_t(i) * nq + q];
+      } else if (P.coef_kind == 1) {
+        double x[3];
+        for (int i = 0; i < 3; ++i) {
+          double acc = sd.v[0][i];
+          for (int s = 0; s < 3; ++s) acc = acc + (sd.v[s + 1][i] - sd.v[0][i]) * xi[s];
+          x[i] = acc;
+        }
+        const double two_pi = 6.283185307179586476925286766559;
+        z = 1.0 + 0.5 * sin(two_pi * x[0]) * cos(two_pi * x[1]) * exp(x[2]);
+      } else if (P.coef_kind == 2) {
+        const double l0 = ((1.0 - xi[0]) - xi[1]) - xi[2];
+        const double u = coef[0] * l0 + coef[1] * xi[0] + coef[2] * xi[1] + coef[3] * xi[2];
+        z = pow(10.0, 6.0 * u);
+      }
+      const double omega = P.rule_w[q];
+      if (poisson) {
+        double gw[3] = {0.0, 0.0, 0.0};  // eval_fe_gradient at binary64 (elements.cpp:224-236)
+        for (int i = 0; i < nphi; ++i)
+          for (int a = 0; a < 3; ++a) gw[a] += w[i] * P.tab[(size_t(a) * nphi + i) * nq + q];
+        for (int s = 0; s < 3; ++s) {
+          double gw_s = 0.0, gtw_s = 0.0, kappa_s = 0.0;
+          for (int t = 0; t < 3; ++t) {
+            gw_s += sd.ten[s * 3 + t] * gw[t];
+            gtw_s += fabs(sd.tt[s * 3 + t]) * fabs(gw[t]);
+            kappa_s += fabs(sd.ten[s * 3 + t]) * P.grad_kappa_max[t] * P.grad_lebesgue[t];
+          }
+          const int idx = s * nq + q;
+          rr[idx] = omega * z * gw_s;
+          thr[idx] = pd * fabs(omega) * (kv * z_norm * fabs(gw_s) + fabs(z) * w_norm * kappa_s);
+          gr[idx] = sd.kk2 * fabs(omega * z) * gtw_s;
+        }
+      } else {
+        double w_at = 0.0;
+        for (int i = 0; i < nphi; ++i) w_at += w[i] * P.vals[size_t(i) * nq + q];
+        const double g = sd.ten[0];
+        rr[q] = omega * z * g * w_at;
+        thr[q] = pd * kv * (fabs(w_at) * z_norm + fabs(z) * w_norm) * fabs(omega * g);
+        gr[q] = sd.kk2 * fabs(rr[q]);
+      }
+    }
+    __syncthreads();
+    double vmax = 0.0, svmax = 0.0, tvmax = 0.0, gvmax = 0.0;
+    for (int i = threadIdx.x; i < nphi; i += blockDim.x) {
+      double acc = 0.0, sv = 0.0, tv = 0.0, gv = 0.0;
+      for (int s = 0; s < nd; ++s) {
+        const double* bi = P.tab + (size_t(s) * nphi + i) * nq;
+        const double* tbi = P.theta_b + (size_t(s) * nphi + i) * nq;
+        for (int q = 0; q < nq; ++q) {
+          const double b = __ldg(bi + q), tb = __ldg(tbi + q);
+          const int idx = s * nq + q;
+          acc += b * rr[idx];
+          sv += fabs(b) * fabs(rr[idx]);
+          tv += fabs(b) * thr[idx] + tb * fabs(rr[idx]);
+          gv += fabs(b) * gr[idx];
+        }
+      }
+      if (P.a64) P.a64[cell * nphi + i] = acc;
+      vmax = fmax(vmax, fabs(acc));
+      svmax = fmax(svmax, sv);
+      tvmax = fmax(tvmax, tv);
+      gvmax = fmax(gvmax, gv);
+    }
+    vmax = block_max(vmax, red);
+    svmax = block_max(svmax, red + 32);
+    tvmax = block_max(tvmax, red + 64);
+    gvmax = block_max(gvmax, red + 96);
+    if (threadIdx.x == 0) {
+      double* o = P.out + cell * 4;
+      if (s_ok && vmax > 0.0) {  // bounds.cpp:268-279
+        o[1] = svmax / vmax;
+        o[2] = tvmax / vmax;
+        o[3] = gvmax / vmax;
+        o[0] = (P.u_s + nq * P.u_q) * o[1] + P.u_p * o[2] + P.u_g * o[3];
+      } else {
+        o[0] = o[1] = o[2] = o[3] = __longlong_as_double(0x7ff8000000000000ll);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 int launch_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st) {
@@ -282,6 +397,20 @@ int launch_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st) {
   }
   const unsigned grid = unsigned(std::min<int64_t>(P.n_cells, int64_t(sm_count) * 4));
   cell_bounds_kernel<<<grid, kBoundThreads, smem, st>>>(P);
+  return 0;
+}
+
+int launch_action_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (3 * size_t(P.n_d) * P.n_q + 128);
+  static size_t smem_set = 0;
+  if (smem > smem_set) {
+    if (cudaFuncSetAttribute(cell_action_bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(std::max<size_t>(smem, 48 * 1024))) != cudaSuccess)
+      return 4;
+    smem_set = smem;
+  }
+  const unsigned grid = unsigned(std::min<int64_t>(P.n_cells, int64_t(sm_count) * 8));
+  cell_action_bounds_kernel<<<grid, 128, smem, st>>>(P);
   return 0;
 }
 

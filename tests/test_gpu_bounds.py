@@ -103,3 +103,47 @@ def test_bound_dominance_every_cell_at_baseline_size(oracle, form, mode):
     for c in (0, 4097, 65535):
         ref, _ = oracle.bound(4, form, cfg_tuple(cfg), verts[c], COEF_SINCOSEXP)
         assert np.allclose(b[c].cpu().numpy(), ref, rtol=1e-12)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_action_bounds_bitwise(oracle, mode, form):
+    """bound_v and the exact v (bounds.cpp:128-279 action part) bitwise the restatement's
+    (pinned to ref_action_bound, tests/test_oracle_golden.py::test_action_bounds_bitwise)."""
+    verts, _ = oracle.gen_tets(0, 1, 8)
+    rng = np.random.default_rng(8 + form)
+    cfg = kconfig(mode, form)
+    for p in range(1, 6):
+        s = mp.make_setup(p, cfg)
+        n = 3
+        w = rng.uniform(-1, 1, size=(n, nphi(p)))
+        for kind in (COEF_ONE, COEF_NODAL):
+            z = rng.uniform(0.5, 1.5, size=(n, nphi(p))) if kind == COEF_NODAL else None
+            out, v64 = s.action_bounds(dev(verts[:n]), dev(w), coef_kind=kind,
+                                       coef=None if z is None else dev(z), want_v64=True)
+            out, v64 = out.cpu().numpy(), v64.cpu().numpy()
+            for c in range(n):
+                ref, rv = oracle.action_bound(p, form, cfg_tuple(cfg), verts[c], w[c], kind,
+                                              None if z is None else z[c])
+                assert np.array_equal(bits(out[c]), bits(ref)), (mode, form, p, kind, c, out[c], ref)
+                assert np.array_equal(bits(v64[c]), bits(rv)), (mode, form, p, kind, c)
+
+
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_action_bound_dominance_every_cell(oracle, form):
+    """Algorithm 2 at config scale: every one of the 65,536 config-0/1 cells satisfies
+    err_rel(v_gpu) <= S bound_v against the exact v of kernel_bounds, both on the GPU."""
+    verts, _ = oracle.gen_tets(0, 1, 65536)
+    dv = dev(verts)
+    w = dev(np.random.default_rng(12).uniform(-1, 1, size=(65536, nphi(4))))
+    for mode in ("mixed", "mixed_bf16"):
+        up, ug, uq, us, eng = MODES[mode]
+        cfg = mp.KernelConfig(form=mp.FormKind(form), mode=mp.ModeKind.action, u_p=mp.Fmt(up),
+                              u_g=mp.Fmt(3 if form == POISSON else ug), u_q=mp.Fmt(uq),
+                              u_s=mp.Fmt(us), engine=mp.EngineKind(eng))
+        s = mp.make_setup(4, cfg)
+        v = mp.action_kernel(s, dv, w, coef_kind=COEF_SINCOSEXP).double()
+        b, v64 = s.action_bounds(dv, w, coef_kind=COEF_SINCOSEXP, want_v64=True)
+        err = (v - v64).abs().amax(dim=1) / v64.abs().amax(dim=1)
+        ratio = (err / (4.0 * b[:, 0])).cpu().numpy()
+        assert np.isfinite(ratio).all() and ratio.max() <= 1.0, (mode, form, float(ratio.max()))
