@@ -319,15 +319,33 @@ int orc_rule_simplex3(int p, double* pts, double* wts) {
   return 0;
 }
 
+/* rule_for(box, p): quadrature.cpp:171-224, Gauss-Legendre on every axis, axis 0 fastest. */
+static int orc_rule_box3_(int p, double* pts, double* wts) {
+  if (p < 1) return fail(2, "element degree must be at least 1");
+  int n = p + 1;
+  double fx[64], fw[64];
+  int st = orc_gauss_legendre_1d(n, fx, fw);
+  if (st) return st;
+  for (int q = 0; q < n * n * n; ++q) {
+    int idx[3], rem = q;
+    for (int a = 0; a < 3; ++a) { idx[a] = rem % n; rem /= n; }
+    double w = 1.0;
+    for (int a = 0; a < 3; ++a) { pts[q * 3 + a] = fx[idx[a]]; w *= fw[idx[a]]; }
+    wts[q] = w;
+  }
+  return 0;
+}
+int orc_rule_box3(int p, double* pts, double* wts) { return orc_rule_box3_(p, pts, wts); }
+
 /* ------------------------------------------------------------------ elements */
 /* Product-form Lagrange basis on the unit tet: elements.cpp:89-147. */
 typedef struct {
-  int p, n_phi, m;
+  int p, n_phi, m, box;
   double nodes[165][3];
   double weight[165];
-  double fa[165][8][3]; /* factor linear coefficients */
-  double fb[165][8];    /* factor constants */
-  int fs[165][8][3];    /* derivative signs */
+  double fa[165][12][3]; /* factor linear coefficients (m <= 12: tets p <= 8, boxes p <= 4) */
+  double fb[165][12];    /* factor constants */
+  int fs[165][12][3];    /* derivative signs */
 } basis_t;
 
 int orc_nphi(int p) { return (p + 1) * (p + 2) * (p + 3) / 6; }
@@ -373,6 +391,40 @@ static int build_basis(int p, basis_t* B) {
     if (a == 3) break;
   }
   B->n_phi = nf;
+  return 0;
+}
+
+/* Tensor-product Lagrange basis on the unit box, equispaced nodes: elements.cpp:26-31,50-87.
+ * Axis 0 fastest; per axis the p factors (x_a - x_j), j != i_a, weight 1 / prod (x_i - x_j). */
+static int build_box_basis(int p, basis_t* B) {
+  if (p < 1) return fail(2, "element degree must be at least 1");
+  if (p > 4) return fail(2, "oracle supports box cells with p <= 4");
+  memset(B, 0, sizeof *B);
+  B->p = p;
+  B->m = 3 * p;
+  B->box = 1;
+  int n1 = p + 1;
+  double xs[5];
+  for (int j = 0; j <= p; ++j) xs[j] = (double)j / (double)p;
+  B->n_phi = n1 * n1 * n1;
+  for (int idx = 0; idx < B->n_phi; ++idx) {
+    int iax[3], rem = idx;
+    for (int a = 0; a < 3; ++a) { iax[a] = rem % n1; rem /= n1; }
+    double w = 1.0;
+    int f = 0;
+    for (int a = 0; a < 3; ++a) {
+      B->nodes[idx][a] = xs[iax[a]];
+      for (int j = 0; j <= p; ++j) {
+        if (j == iax[a]) continue;
+        B->fa[idx][f][a] = 1.0;
+        B->fb[idx][f] = -xs[j];
+        B->fs[idx][f][a] = 1;
+        ++f;
+        w /= xs[iax[a]] - xs[j];
+      }
+    }
+    B->weight[idx] = w;
+  }
   return 0;
 }
 
@@ -481,7 +533,7 @@ static void basis_conditioning(const basis_t* B, const double* pts, int nq, cond
     for (;;) {  /* sample_point: elements.cpp:279-289 */
       double sum = 0.0;
       for (int a = 0; a < 3; ++a) { x[a] = orc_rng_uniform(&rng, 0.0, 1.0); sum += x[a]; }
-      if (sum <= 1.0) break;
+      if (B->box || sum <= 1.0) break;  /* sample_point: rejection for simplices only */
     }
     for (int a = 0; a < 3; ++a) S[ip * 3 + a] = x[a];
   }
@@ -555,17 +607,21 @@ int orc_basis_conditioning(int p, double* leb, double* gleb, double* gk, double*
 
 /* ------------------------------------------------------------------ geometry */
 /* jacobian through the P1 geometry basis at the centroid: geometry.cpp:12-27 */
-static void jacobian(const basis_t* G1, const double* verts, int f, double* jac, uint32_t* fl) {
-  double centroid[3] = {0.25, 0.25, 0.25};
+static void jacobian_at(const basis_t* G1, const double* verts, const double* xref, int f, double* jac,
+                        uint32_t* fl) {
   for (int i = 0; i < 9; ++i) jac[i] = 0.0;
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < G1->n_phi; ++k) {
     double g[3];
-    eval_basis_gradient(G1, k, centroid, f, g, fl);
+    eval_basis_gradient(G1, k, xref, f, g, fl);
     for (int i = 0; i < 3; ++i) {
       double x = RND(verts[k * 3 + i], f);
       for (int s = 0; s < 3; ++s) jac[i * 3 + s] = ADD(jac[i * 3 + s], MUL(x, g[s], f), f);
     }
   }
+}
+static void jacobian(const basis_t* G1, const double* verts, int f, double* jac, uint32_t* fl) {
+  double centroid[3] = {0.25, 0.25, 0.25};
+  jacobian_at(G1, verts, centroid, f, jac, fl);
 }
 
 /* lu_decompose: geometry.cpp:33-57 */
@@ -690,11 +746,11 @@ static double kappa2_of(const double* jac) {
 }
 
 /* kappa_cell_of: geometry.cpp:171-186 */
-static double kappa_cell_of(const double* verts, const double* jac) {
+static double kappa_cell_nv(const double* verts, int nv, const double* jac) {
   double xnorm = 0.0;
   for (int i = 0; i < 3; ++i) {
     double row = 0.0;
-    for (int v = 0; v < 4; ++v) row += fabs(verts[v * 3 + i]);
+    for (int v = 0; v < nv; ++v) row += fabs(verts[v * 3 + i]);
     if (row > xnorm) xnorm = row;
   }
   double jnorm = 0.0;
@@ -703,7 +759,10 @@ static double kappa_cell_of(const double* verts, const double* jac) {
     for (int s = 0; s < 3; ++s) row += fabs(jac[i * 3 + s]);
     if (row > jnorm) jnorm = row;
   }
-  return 4.0 * xnorm / jnorm;
+  return (double)nv * xnorm / jnorm;
+}
+static double kappa_cell_of(const double* verts, const double* jac) {
+  return kappa_cell_nv(verts, 4, jac);
 }
 
 static basis_t g_geom1;
@@ -713,16 +772,21 @@ static const basis_t* geom_basis(void) {
   return &g_geom1;
 }
 
-/* point_geometry + cell_geometry (affine): geometry.cpp:190-245 */
-int orc_cell_geometry(const double* verts, int form, int f, double* out, uint32_t* fl) {
-  uint32_t dummy = 0;
-  if (!fl) fl = &dummy;
-  const basis_t* G1 = geom_basis();
+static basis_t g_geom1_box;
+static int g_geom1_box_ready = 0;
+static const basis_t* geom_basis_box(void) {
+  if (!g_geom1_box_ready) { build_box_basis(1, &g_geom1_box); g_geom1_box_ready = 1; }
+  return &g_geom1_box;
+}
+
+/* point_geometry: geometry.cpp:190-221 (J through the degree-1 geometry basis at xref). */
+static int point_geometry(const basis_t* G1, const double* verts, const double* xref, int form,
+                          int f, double* out, uint32_t* fl) {
   memset(out, 0, sizeof(double) * ORC_GEOM_SIZE);
   double* jac = out + 2;
   double* inv = out + 11;
   double* ten = out + 20;
-  jacobian(G1, verts, f, jac, fl);
+  jacobian_at(G1, verts, xref, f, jac, fl);
   double det;
   int st = det_lu(jac, f, &det, fl);
   if (st) return st;
@@ -746,9 +810,9 @@ int orc_cell_geometry(const double* verts, int form, int f, double* out, uint32_
   /* binary64 diagnostics */
   uint32_t wide = 0;
   double jac64[9], inv64[9], det64;
-  jacobian(G1, verts, ORC_FP64, jac64, &wide);
+  jacobian_at(G1, verts, xref, ORC_FP64, jac64, &wide);
   out[29] = kappa2_of(jac64);
-  out[30] = kappa_cell_of(verts, jac64);
+  out[30] = kappa_cell_nv(verts, G1->n_phi, jac64);
   st = det_lu(jac64, ORC_FP64, &det64, &wide);
   if (st) return st;
   det64 = fabs(det64);
@@ -766,6 +830,14 @@ int orc_cell_geometry(const double* verts, int form, int f, double* out, uint32_
       }
   }
   return 0;
+}
+
+/* cell_geometry, affine tets: geometry.cpp:226-245 (one point at the centroid). */
+int orc_cell_geometry(const double* verts, int form, int f, double* out, uint32_t* fl) {
+  uint32_t dummy = 0;
+  if (!fl) fl = &dummy;
+  double centroid[3] = {0.25, 0.25, 0.25};
+  return point_geometry(geom_basis(), verts, centroid, form, f, out, fl);
 }
 
 /* ------------------------------------------------------------------ coefficients */
@@ -801,8 +873,14 @@ typedef struct {
   double* tab_values; /* n_phi x n_q at (u_p -> u_p) */
 } setup_t;
 
-/* make_setup: kernels.cpp:78-108 */
+static int orc_rule_box3_(int p, double* pts, double* wts);
+
+/* make_setup: kernels.cpp:78-108 (box: tensor basis and Gauss-Legendre rule) */
+static int make_setup_kind(int p, int form, const int* cfg, setup_t* S, int box);
 static int make_setup(int p, int form, const int* cfg, setup_t* S) {
+  return make_setup_kind(p, form, cfg, S, 0);
+}
+static int make_setup_kind(int p, int form, const int* cfg, setup_t* S, int box) {
   memset(S, 0, sizeof *S);
   S->p = p; S->form = form;
   S->up = cfg[0]; S->ug = cfg[1]; S->uq = cfg[2]; S->us = cfg[3]; S->engine = cfg[4];
@@ -811,14 +889,14 @@ static int make_setup(int p, int form, const int* cfg, setup_t* S) {
   /* validate_config: kernels.cpp:29-40 (matrix engine => u_s bf16, u_q fp32) */
   if (S->engine == 2 && (S->us != ORC_BF16 || S->uq != ORC_FP32))
     return fail(2, "matrix engine requires the unit's native formats: u_s = bf16, u_q = fp32");
-  int st = build_basis(p, &S->B);
+  int st = box ? build_box_basis(p, &S->B) : build_basis(p, &S->B);
   if (st) return st;
   S->nphi = S->B.n_phi;
   S->nq = orc_nq(p);
   S->nd = form == ORC_POISSON ? 3 : 1;
   S->pts = malloc(sizeof(double) * 3 * S->nq);
   S->wts = malloc(sizeof(double) * S->nq);
-  st = orc_rule_simplex3(p, S->pts, S->wts);
+  st = box ? orc_rule_box3_(p, S->pts, S->wts) : orc_rule_simplex3(p, S->pts, S->wts);
   if (st) return st;
   S->tab_store = malloc(sizeof(double) * S->nd * S->nphi * S->nq);
   S->tab_values = malloc(sizeof(double) * S->nphi * S->nq);
@@ -876,13 +954,13 @@ int orc_coef_at_q(int p, const double* verts, int kind, const double* coef, doub
 }
 
 /* build_C: kernels.cpp:177-197 */
-static int build_C_s(const setup_t* S, const double* geom, const double* verts, int kind,
-                     const double* coef, double* c, uint32_t* fl) {
+static int build_C_g(const setup_t* S, const double* geom, int gstride, const double* verts,
+                     int kind, const double* coef, double* c, uint32_t* fl) {
   int nq = S->nq, nd = S->nd;
   double* zhat = malloc(sizeof(double) * nq);
   int have_z = coef_zhat(S, verts, kind, coef, zhat, fl);
-  const double* ten = geom + 20;
   for (int q = 0; q < nq; ++q) {
+    const double* ten = geom + (size_t)q * gstride + 20;
     double omega = RND(S->wts[q], S->ug);
     for (int s = 0; s < nd; ++s)
       for (int t = 0; t < nd; ++t) {
@@ -892,6 +970,29 @@ static int build_C_s(const setup_t* S, const double* geom, const double* verts, 
       }
   }
   free(zhat);
+  return 0;
+}
+static int build_C_s(const setup_t* S, const double* geom, const double* verts, int kind,
+                     const double* coef, double* c, uint32_t* fl) {
+  return build_C_g(S, geom, 0, verts, kind, coef, c, fl);
+}
+
+/* Geometry of one cell at every rule point: affine tets one point (stride 0), boxes one
+ * point per rule point (cell_geometry, geometry.cpp:226-245). Caller frees *geo. */
+static int cell_geometry_all(const setup_t* S, const double* verts, int f, double** geo,
+                             int* stride, uint32_t* fl) {
+  if (!S->B.box) {
+    *geo = malloc(sizeof(double) * ORC_GEOM_SIZE);
+    *stride = 0;
+    return orc_cell_geometry(verts, S->form, f, *geo, fl);
+  }
+  *geo = malloc(sizeof(double) * ORC_GEOM_SIZE * S->nq);
+  *stride = ORC_GEOM_SIZE;
+  for (int q = 0; q < S->nq; ++q) {
+    int st = point_geometry(geom_basis_box(), verts, S->pts + 3 * q, S->form, f,
+                            *geo + (size_t)q * ORC_GEOM_SIZE, fl);
+    if (st) return st;
+  }
   return 0;
 }
 
@@ -917,11 +1018,13 @@ static int bilinear_one(const setup_t* S, const double* verts, int kind, const d
                         double* a, uint32_t* fl) {
   int nq = S->nq, nd = S->nd, nphi = S->nphi;
   int K = nd * nd * nq;
-  double geom[ORC_GEOM_SIZE];
-  int st = orc_cell_geometry(verts, S->form, S->ug, geom, fl);
-  if (st) return st;
+  double* geom = NULL;
+  int gstride = 0;
+  int st = cell_geometry_all(S, verts, S->ug, &geom, &gstride, fl);
+  if (st) { free(geom); return st; }
   double* c = malloc(sizeof(double) * K);
-  build_C_s(S, geom, verts, kind, coef, c, fl);
+  build_C_g(S, geom, gstride, verts, kind, coef, c, fl);
+  free(geom);
   double* h = malloc(sizeof(double) * (size_t)K * nphi);
   for (int s = 0; s < nd; ++s)
     for (int t = 0; t < nd; ++t) {
@@ -973,21 +1076,19 @@ int orc_bilinear(int p, int form, const int* cfg, int64_t m, const double* verts
 /* ------------------------------------------------------------------ bounds */
 /* kernel_bounds, bilinear part: bounds.cpp:29-281. For the analytic coefficient path the
  * coefficient enters at >= u_g, so z_at = c(x_q) and theta_c = 0 (SURVEY 8.0, Q path). */
-int orc_bound(int p, int form, const int* cfg, const double* verts, int kind,
-              const double* coef, double* out4, double* a64) {
+static int bound_impl(int p, int form, const int* cfg, const double* verts, int kind,
+                      const double* coef, double* out4, double* a64, int box) {
   setup_t S;
-  int st = make_setup(p, form, cfg, &S);
+  int st = make_setup_kind(p, form, cfg, &S, box);
   if (st) { free_setup(&S); return st; }
   int nq = S.nq, nd = S.nd, nphi = S.nphi;
   int poisson = form == ORC_POISSON;
   uint32_t scratch = 0;
   uint32_t* fl = &scratch;
-  double geom[ORC_GEOM_SIZE];
-  st = orc_cell_geometry(verts, form, ORC_FP64, geom, fl);
-  if (st) { free_setup(&S); return st; }
-  const double* ten = geom + 20;
-  const double* tt = geom + 31;
-  double kappa2 = geom[29], kcell = geom[30];
+  double* geom = NULL;
+  int gstride = 0;
+  st = cell_geometry_all(&S, verts, ORC_FP64, &geom, &gstride, fl);
+  if (st) { free(geom); free_setup(&S); return st; }
 
   size_t nb = (size_t)nd * nphi * nq;
   double* tab = malloc(sizeof(double) * nb);
@@ -1044,6 +1145,10 @@ int orc_bound(int p, int form, const int* cfg, const double* verts, int kind,
     for (int t = 0; t < nd; ++t)
       for (int q = 0; q < nq; ++q) {
         double omega = S.wts[q];
+        const double* gq = geom + (size_t)q * gstride;
+        const double* ten = gq + 20;
+        const double* tt = gq + 31;
+        double kappa2 = gq[29], kcell = gq[30];
         size_t idx = ((size_t)s * nd + t) * nq + q;
         cc[idx] = omega * ten[s * 3 + t] * z_at[q];
         thc[idx] = (kind == ORC_COEF_NODAL && !z_const)
@@ -1086,9 +1191,67 @@ int orc_bound(int p, int form, const int* cfg, const double* verts, int kind,
   } else {
     out4[0] = out4[1] = out4[2] = out4[3] = NAN;
   }
-  free(tab); free(bc); free(theta_b); free(z_at); free(cc); free(thc); free(gc);
+  free(tab); free(bc); free(theta_b); free(z_at); free(cc); free(thc); free(gc); free(geom);
   free_setup(&S);
   return 0;
+}
+
+int orc_bound(int p, int form, const int* cfg, const double* verts, int kind,
+              const double* coef, double* out4, double* a64) {
+  return bound_impl(p, form, cfg, verts, kind, coef, out4, a64, 0);
+}
+
+/* ------------------------------------------------------------------ box cells */
+/* Hexahedra: per-point geometry through the trilinear map (geometry.cpp:12-27,190-245 with the
+ * degree-1 box basis), tensor Lagrange basis and Gauss-Legendre rule. Constant and nodal
+ * coefficients (the reference's own coefficient path). */
+static int box_coef_ok(int kind) {
+  return kind == ORC_COEF_ONE || kind == ORC_COEF_NODAL
+             ? 0 : fail(2, "box cells take constant or nodal coefficients");
+}
+
+int orc_bilinear_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                     const double* coef, int coef_stride, double* a_out, uint32_t* fl) {
+  uint32_t dummy = 0;
+  if (!fl) fl = &dummy;
+  int st = box_coef_ok(kind);
+  if (st) return st;
+  setup_t S;
+  st = make_setup_kind(p, form, cfg, &S, 1);
+  if (!st) {
+    size_t n2 = (size_t)S.nphi * S.nphi;
+    for (int64_t c = 0; c < m && !st; ++c)
+      st = bilinear_one(&S, verts + 24 * c, kind, coef ? coef + coef_stride * c : NULL,
+                        a_out + n2 * c, fl);
+  }
+  free_setup(&S);
+  return st;
+}
+
+int orc_build_C_box(int p, int form, const int* cfg, const double* verts, int kind,
+                    const double* coef, double* c_out, uint32_t* fl) {
+  uint32_t dummy = 0;
+  if (!fl) fl = &dummy;
+  int st = box_coef_ok(kind);
+  if (st) return st;
+  setup_t S;
+  st = make_setup_kind(p, form, cfg, &S, 1);
+  if (!st) {
+    double* geom = NULL;
+    int gstride = 0;
+    st = cell_geometry_all(&S, verts, S.ug, &geom, &gstride, fl);
+    if (!st) st = build_C_g(&S, geom, gstride, verts, kind, coef, c_out, fl);
+    free(geom);
+  }
+  free_setup(&S);
+  return st;
+}
+
+int orc_bound_box(int p, int form, const int* cfg, const double* verts, int kind,
+                  const double* coef, double* out4, double* a64) {
+  int st = box_coef_ok(kind);
+  if (st) return st;
+  return bound_impl(p, form, cfg, verts, kind, coef, out4, a64, 1);
 }
 
 /* ------------------------------------------------------------------ action (Algorithm 2) */

@@ -96,6 +96,18 @@ int orc_action(int p, int form, const int* cfg, int64_t m, const double* verts, 
 int orc_action_bound(int p, int form, const int* cfg, const double* verts, int kind,
                      const double* coef, const double* w, double* out4, double* v64);
 
+/* Box (hexahedral) cells: tensor Lagrange basis with equispaced nodes
+ * (elements.cpp:50-87), Gauss-Legendre rule (quadrature.cpp:171-224), geometry at every rule
+ * point through the trilinear map (geometry.cpp:12-27,190-245); p <= 4; coefficient kinds
+ * ONE or NODAL. verts: 8 x 3 per cell in the lattice's bit order (x fastest). */
+int orc_rule_box3(int p, double* points, double* weights);
+int orc_bilinear_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                     const double* coef, int coef_stride, double* a_out, uint32_t* flags);
+int orc_build_C_box(int p, int form, const int* cfg, const double* verts, int kind,
+                    const double* coef, double* c_out, uint32_t* flags);
+int orc_bound_box(int p, int form, const int* cfg, const double* verts, int kind,
+                  const double* coef, double* out4, double* a64);
+
 /* Physical quadrature points x_q = v0 + J (xi_q) in fp64 and the coefficient there. */
 int orc_coef_at_q(int p, const double* verts, int coef_kind, const double* coef,
                   double* c_q /* n_q */);

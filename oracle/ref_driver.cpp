@@ -361,6 +361,70 @@ int ref_action_bound(int p, int form, const int* cfg, const double* verts, int k
   });
 }
 
+// Box (hexahedral) cells through the reference's public API: a one-hex mesh, cell_geometry at
+// every rule point, bilinear_kernel / build_C / kernel_bounds (constant or nodal z).
+Mesh single_hex(const double* v) {
+  Mesh m;
+  m.kind = CellKind::box;
+  m.dim = 3;
+  for (int k = 0; k < 8; ++k) m.vertices.push_back({v[3 * k], v[3 * k + 1], v[3 * k + 2]});
+  m.cells.push_back({0, 1, 2, 3, 4, 5, 6, 7});
+  return m;
+}
+const ReferenceCell kHex{CellKind::box, 3};
+
+int ref_bilinear_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                     const double* coef, int coef_stride, double* a_out, uint32_t* flags) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kHex, p, make_cfg(form, cfg));
+    std::size_t n2 = std::size_t(setup.basis.n_phi) * setup.basis.n_phi;
+    for (int64_t c = 0; c < m; ++c) {
+      Mesh mesh = single_hex(verts + 24 * c);
+      GeometryData geom = cell_geometry(mesh, 0, setup.rule, setup.config.form, setup.config.u_g, f);
+      Coefficients z;
+      if (kind == 3) z.assign(coef + coef_stride * c, coef + coef_stride * c + setup.basis.n_phi);
+      Mat a = bilinear_kernel(setup, geom, z, f);
+      std::memcpy(a_out + n2 * c, a.a.data(), sizeof(double) * n2);
+    }
+    if (flags) *flags |= pack(f);
+  });
+}
+
+int ref_build_C_box(int p, int form, const int* cfg, const double* verts, int kind,
+                    const double* coef, double* c_out, uint32_t* flags) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kHex, p, make_cfg(form, cfg));
+    Mesh mesh = single_hex(verts);
+    GeometryData geom = cell_geometry(mesh, 0, setup.rule, setup.config.form, setup.config.u_g, f);
+    Coefficients z;
+    if (kind == 3) z.assign(coef, coef + setup.basis.n_phi);
+    std::vector<double> c = build_C(setup, geom, z, f);
+    std::memcpy(c_out, c.data(), sizeof(double) * c.size());
+    if (flags) *flags |= pack(f);
+  });
+}
+
+int ref_bound_box(int p, int form, const int* cfg, const double* verts, int kind,
+                  const double* coef, double* out4, double* a64) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kHex, p, make_cfg(form, cfg));
+    BasisConditioning bc = basis_condition_numbers(setup.basis);
+    Mesh mesh = single_hex(verts);
+    GeometryData g64 = cell_geometry(mesh, 0, setup.rule, setup.config.form, Fmt::fp64, f);
+    Coefficients z;
+    if (kind == 3) z.assign(coef, coef + setup.basis.n_phi);
+    BoundReport r = kernel_bounds(setup, bc, g64, z, {});
+    out4[0] = r.bound_a;
+    out4[1] = r.kappa_q_a;
+    out4[2] = r.kappa_p_a;
+    out4[3] = r.kappa_g_a;
+    if (a64) std::memcpy(a64, r.a.a.data(), sizeof(double) * r.a.a.size());
+  });
+}
+
 int ref_structured_tet_mesh(int nx, int ny, int nz, double extent, double jitter, uint64_t seed,
                             double* verts, int32_t* cells) {
   return guard([&] {

@@ -18,7 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
 from oracle_lib import (COEF_NODAL, COEF_ONE, MODES, MASS, POISSON, Oracle, Reference,  # noqa: E402
-                        ensure_built, nphi)
+                        box_mesh_cells, ensure_built, nphi)
 
 
 def sha(a: np.ndarray) -> str:
@@ -132,6 +132,29 @@ def main() -> None:
                     out[key + "_w"] = w
                     if coef is not None:
                         out[key + "_coef"] = coef
+    # Hexahedra: jittered 2x2x2 lattice, constant / nodal coefficients.
+    brng = np.random.default_rng(8)
+    lv, _ = R.structured_tet_mesh(2, 2, 2, 1.0, 0.15, 7)
+    hexes = lv[box_mesh_cells(2, 2, 2)]
+    out["hex_verts"] = hexes
+    for mode, cfg in MODES.items():
+        for form in (MASS, POISSON):
+            for p in (1, 2, 3):
+                n = (p + 1) ** 3
+                for kind in (COEF_ONE, COEF_NODAL):
+                    coef = brng.uniform(0.5, 1.5, size=(2, n)) if kind == COEF_NODAL else None
+                    a, fl = R.bilinear_box(p, form, cfg, hexes[:2], kind, coef)
+                    key = f"Ahex_{mode}_f{form}_p{p}_k{kind}"
+                    out[key] = a
+                    out[key + "_flags"] = np.array([fl], dtype=np.uint32)
+                    if coef is not None:
+                        out[key + "_coef"] = coef
+                    c, _ = R.build_C_box(p, form, cfg, hexes[0], kind, None if coef is None else coef[0])
+                    out[f"Chex_{mode}_f{form}_p{p}_k{kind}"] = c
+                    if p <= 2:
+                        b, a64 = R.bound_box(p, form, cfg, hexes[3], kind, None if coef is None else coef[1])
+                        out[f"boundhex_{mode}_f{form}_p{p}_k{kind}"] = b
+                        out[f"boundhex_{mode}_f{form}_p{p}_k{kind}_a64"] = a64
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **out)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), len(out), "arrays")
 

@@ -75,6 +75,10 @@ class _Lib:
         self._sig("bilinear", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
                                          C.c_int, _d, _u32])
         self._sig("bound", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d])
+        self._sig("bilinear_box", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
+                                            C.c_int, _d, _u32])
+        self._sig("build_C_box", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _u32])
+        self._sig("bound_box", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d])
         self._sig("action", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
                                       C.c_int, _d, C.c_int, _d, _u32])
         self._sig("action_bound", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d,
@@ -179,6 +183,43 @@ class _Lib:
         cf = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
         self._check(self._bound(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(out, _d),
                                 _ptr(a64, _d)))
+        return out, a64
+
+    def bilinear_box(self, p, form, cfg, verts, kind=COEF_ONE, coef=None):
+        """bilinear_kernel on hexahedra (verts (m, 8, 3)): A (m, (p+1)^3, (p+1)^3), flags."""
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 24)
+        m, n = v.shape[0], (p + 1) ** 3
+        out = np.zeros((m, n, n))
+        c = (C.c_int * 5)(*cfg)
+        cf, stride = None, 0
+        if coef is not None:
+            cf = np.ascontiguousarray(coef, dtype=np.float64).reshape(m, -1)
+            stride = cf.shape[1]
+        fl = C.c_uint32(0)
+        self._check(self._bilinear_box(p, form, c, m, _ptr(v, _d), kind, _ptr(cf, _d), stride,
+                                       _ptr(out, _d), C.byref(fl)))
+        return out, fl.value
+
+    def build_C_box(self, p, form, cfg, verts, kind=COEF_ONE, coef=None):
+        nd = 3 if form == POISSON else 1
+        out = np.zeros(nd * nd * (p + 1) ** 3)
+        c = (C.c_int * 5)(*cfg)
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(24)
+        cf = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+        fl = C.c_uint32(0)
+        self._check(self._build_C_box(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(out, _d),
+                                      C.byref(fl)))
+        return out, fl.value
+
+    def bound_box(self, p, form, cfg, verts, kind=COEF_ONE, coef=None):
+        n = (p + 1) ** 3
+        out = np.zeros(4)
+        a64 = np.zeros((n, n))
+        c = (C.c_int * 5)(*cfg)
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(24)
+        cf = None if coef is None else np.ascontiguousarray(coef, dtype=np.float64)
+        self._check(self._bound_box(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(out, _d),
+                                    _ptr(a64, _d)))
         return out, a64
 
     def action(self, p, form, cfg, verts, w, kind=COEF_ONE, coef=None):
@@ -295,6 +336,17 @@ class Reference(_Lib):
 
 def reference_available() -> bool:
     return os.path.exists(REF_SO)
+
+
+def box_mesh_cells(nx: int, ny: int, nz: int) -> np.ndarray:
+    """Hexahedra of the jittered lattice (mesh.cpp:78-123), vertex b = (x, y, z) bits."""
+    cells = []
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                cells.append([(i + (b & 1)) + (nx + 1) * ((j + ((b >> 1) & 1)) + (ny + 1) * (k + ((b >> 2) & 1)))
+                              for b in range(8)])
+    return np.array(cells, dtype=np.int32)
 
 
 def rel_err(approx: np.ndarray, exact: np.ndarray) -> np.ndarray:

@@ -177,3 +177,32 @@ def test_action_known_answers(oracle, golden):
             a, _ = oracle.bilinear(p, form, MODES["fp64"], V[:2])
             av = np.einsum("cij,cj->ci", a, w)
             assert np.max(np.abs(v - av)) <= 1e-13 * np.max(np.abs(av))
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_box_cells_bitwise(oracle, golden, mode):
+    """Hexahedra: bilinear_kernel, build_C and kernel_bounds with per-point
+    geometry through the trilinear map, bit for bit the reference's (flags too)."""
+    hexes = golden["hex_verts"]
+    cfg = MODES[mode]
+    for form in (MASS, POISSON):
+        for p in (1, 2, 3):
+            for kind in (COEF_ONE, COEF_NODAL):
+                key = f"Ahex_{mode}_f{form}_p{p}_k{kind}"
+                coef = golden[key + "_coef"] if kind == COEF_NODAL else None
+                a, fl = oracle.bilinear_box(p, form, cfg, hexes[:2], kind, coef)
+                assert np.array_equal(bits(a), bits(golden[key])), key
+                assert fl == golden[key + "_flags"][0], key
+                c, _ = oracle.build_C_box(p, form, cfg, hexes[0], kind, None if coef is None else coef[0])
+                assert np.array_equal(bits(c), bits(golden[f"Chex_{mode}_f{form}_p{p}_k{kind}"]))
+                if p <= 2:
+                    b, a64 = oracle.bound_box(p, form, cfg, hexes[3], kind, None if coef is None else coef[1])
+                    assert np.array_equal(bits(b), bits(golden[f"boundhex_{mode}_f{form}_p{p}_k{kind}"]))
+                    assert np.array_equal(bits(a64), bits(golden[f"boundhex_{mode}_f{form}_p{p}_k{kind}_a64"]))
+    # known answer: unit cube Q1 mass in closed form, prod_a (1 + delta_a) / 216 with
+    # delta_a = 1 when the two vertices share their axis-a coordinate
+    cube = np.array([[(b & 1), (b >> 1) & 1, (b >> 2) & 1] for b in range(8)], dtype=np.float64)
+    a, _ = oracle.bilinear_box(1, MASS, MODES["fp64"], cube[None])
+    want = np.array([[np.prod([2.0 if ((i >> k) & 1) == ((j >> k) & 1) else 1.0 for k in range(3)]) / 216.0
+                      for j in range(8)] for i in range(8)])
+    assert np.max(np.abs(a[0] - want)) <= 1e-15
