@@ -21,6 +21,7 @@
 #include "cellmat_simt.cuh"
 #include "cellmat_tc.cuh"
 #include "cellmat_tc2.cuh"
+#include "geom_box.cuh"
 #include "geom_w.cuh"
 #include "host_setup.hpp"
 
@@ -135,6 +136,8 @@ void mpfem_b200_set_last_error(const std::string& msg) { g_last_error = msg; }
 
 struct mpfem_b200_setup_s {
   int p = 0, form = 0, up = 3, ug = 3, uq = 3, us = 3, engine = 0;
+  int box = 0;         // hexahedral cells: per-point geometry in K1
+  DevBuf d_ggrad;      // box: degree-1 basis gradients at u_g, (s * 8 + k) * n_q + q
   int n_phi = 0, n_q = 0, n_d = 1, n_blocks = 1, nq_pad = 0;
   int64_t k = 0, k_pad = 0, n_out = 0, n_out_pad = 0;
   int path = kPathF64;
@@ -198,9 +201,10 @@ namespace {
 size_t elem_size(int w_type) { return w_type <= 1 ? 2 : (w_type == 2 ? 4 : 8); }
 
 void validate(int cell_kind, int dim, int p, int form, const int* fmts, int engine, int n_batch) {
-  if (cell_kind != 0 || dim != 3)
-    throw Error(MPFEM_B200_CONFIG_ERROR, "the B200 path supports affine tetrahedra (simplex, dim 3)");
+  if ((cell_kind != 0 && cell_kind != 1) || dim != 3)
+    throw Error(MPFEM_B200_CONFIG_ERROR, "the B200 path supports tetrahedra and hexahedra (dim 3)");
   if (p < 1 || p > 8) throw Error(MPFEM_B200_CONFIG_ERROR, "element degree must be in [1, 8]");
+  if (cell_kind == 1 && p > 4) throw Error(MPFEM_B200_CONFIG_ERROR, "hexahedra support p <= 4");
   if (form != 0 && form != 1) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown form");
   for (int i = 0; i < 4; ++i)
     if (fmts[i] < 0 || fmts[i] > 3) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown float format");
@@ -216,7 +220,7 @@ void choose_path(mpfem_b200_setup_s& S) {
   const int us = S.us, uq = S.uq;
   // Tiny GEMM depth (K <= 48) and small matrices: one thread per cell runs the whole
   // path in registers (cellmat_fused.cuh); fp32 accumulation of u_s-rounded operands.
-  if (uq == 2 && us <= 2 && (S.ug == 2 || S.ug == 3) && (S.p == 1 || (S.p == 2 && S.form == 0))) {
+  if (!S.box && uq == 2 && us <= 2 && (S.ug == 2 || S.ug == 3) && (S.p == 1 || (S.p == 2 && S.form == 0))) {
     S.path = kPathFused;
     S.w_type = us == 2 ? 2 : (us == 1 ? 0 : 1);
     return;
@@ -252,9 +256,45 @@ int k1_geom_warps(const mpfem_b200_setup_s& S) {
   return std::max(1, std::min(4, 32 / ngroups));
 }
 
+void launch_geom_tet(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
+                     int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
+                     int w_type, cudaStream_t st);
+
+// K1: per-cell geometry (tets, geom_w.cuh) or per-point geometry (boxes, geom_box.cuh).
 void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
                  int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
                  int w_type, cudaStream_t st) {
+  if (!S.box) return launch_geom_tet(S, verts, cells, n, coef_kind, coef, coef_stride, W, k_pad, w_type, st);
+  GeomBoxParams P{};
+  P.verts = verts;
+  P.cells = cells;
+  P.n_cells = n;
+  P.coef_kind = coef_kind;
+  P.coef = coef;
+  P.coef_stride = coef_stride;
+  P.rule_w_ug = static_cast<const double*>(S.d_rule_w_ug.p);
+  P.ggrad = static_cast<const double*>(S.d_ggrad.p);
+  P.tab_up = static_cast<const double*>(S.d_tab_up.p);
+  P.n_phi = S.n_phi;
+  P.n_q = S.n_q;
+  P.nq_pad = S.nq_pad;
+  P.n_blocks = S.n_blocks;
+  P.k = S.k;
+  P.k_pad = k_pad;
+  P.up = S.up;
+  P.ug = S.ug;
+  P.us = S.us;
+  P.poisson = S.form;
+  P.W = W;
+  P.flags = static_cast<uint32_t*>(S.d_flags.p);
+  P.error = static_cast<int*>(S.d_error.p);
+  launch_geom_box(w_type, P, device_sm_count(), st);
+  CUDA_OK(cudaGetLastError());
+}
+
+void launch_geom_tet(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
+                     int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
+                     int w_type, cudaStream_t st) {
   GeomWParams P;
   P.verts = verts;
   P.cells = cells;
@@ -299,6 +339,8 @@ void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cell
 
 void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, int64_t stride) {
   if (coef_kind < 0 || coef_kind > 3) throw Error(MPFEM_B200_CONFIG_ERROR, "unknown coefficient kind");
+  if (S.box && (coef_kind == 1 || coef_kind == 2))
+    throw Error(MPFEM_B200_CONFIG_ERROR, "hexahedra take constant or nodal coefficients");
   if (coef_kind == 2 && (!coef || stride < 4))
     throw Error(MPFEM_B200_CONFIG_ERROR, "affine coefficient needs 4 values per cell");
   if (coef_kind == 3 && (!coef || stride < S.n_phi))
@@ -493,7 +535,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
   // CTA + two K1 CTAs); K2's producer acquires K1's per-tile W stamps before each TMA read.
   // Correct, but measured no faster on B200: next to K2's MMAs K1 runs 2x slower (1.1x with
   // the MMAs compiled out), so the fp64 and tensor work do not overlap.
-  const char* ov_env = std::getenv("MPFEM_B200_OVERLAP");
+  const char* ov_env = S.box ? nullptr : std::getenv("MPFEM_B200_OVERLAP");
   const bool concurrent = S.path == kPathTC && S.pair && !S.timing && n_chunks == 1 &&
                           ov_env && std::atoi(ov_env) != 0;
   if (concurrent) {
@@ -544,8 +586,9 @@ void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t
     const int64_t m = c1 - c0;
     const size_t wb = size_t(S.k_pad) * elem_size(S.w_type);
     void* Wc = static_cast<char*>(S.d_W.p) + size_t(c0) * wb;
-    const double* vc = cells ? verts : verts + c0 * 12;
-    const int32_t* cc = cells ? cells + c0 * 4 : nullptr;
+    const int nv = S.box ? 8 : 4;
+    const double* vc = cells ? verts : verts + c0 * 3 * nv;
+    const int32_t* cc = cells ? cells + c0 * nv : nullptr;
     const double* coefc = coef ? coef + c0 * coef_stride : nullptr;
     S.mark(st);
     launch_geom(S, vc, cc, m, coef_kind, coefc, coef_stride, Wc, S.k_pad, S.w_type, st);
@@ -635,6 +678,7 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   if (n > 0 && (!verts || !w || !out)) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
   if (out_pitch < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
+  if (S.box) throw Error(MPFEM_B200_CONFIG_ERROR, "the action kernel supports tetrahedra");
   prepare_action(S);
   S.last_launches = 0;
   if (flags) {
@@ -749,6 +793,7 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->uq = u_q;
     S->us = u_s;
     S->engine = engine;
+    S->box = cell_kind == 1;
     choose_path(*S);
     if (S->path == kPathTC) {
       const char* tc1 = std::getenv("MPFEM_B200_TC1");
@@ -761,8 +806,8 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw Error(MPFEM_B200_RUNTIME_ERROR, "no CUDA device: the B200 path has no CPU fallback");
     CUDA_OK(cudaGetDevice(&S->device));
-    S->rule = simplex_rule(p);
-    Basis basis = simplex_basis(p);
+    S->rule = S->box ? box_rule(p) : simplex_rule(p);
+    Basis basis = S->box ? box_basis(p) : simplex_basis(p);
     S->n_phi = basis.n_phi;
     S->n_q = S->rule.n_q;
     S->n_d = form ? 3 : 1;
@@ -819,6 +864,11 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     CUDA_OK(cudaMemcpy(S->d_rule_x.p, S->rule.points.data(), sizeof(double) * 3 * S->n_q, cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(S->d_tab_up.p, tab_up.data(), sizeof(double) * tab_up.size(), cudaMemcpyHostToDevice));
     CUDA_OK(cudaMemcpy(S->d_B.p, B.data(), sizeof(double) * B.size(), cudaMemcpyHostToDevice));
+    if (S->box) {  // jacobian() at every rule point: degree-1 box gradients at u_g
+      const std::vector<double> gg = tabulate(box_basis(1), S->rule, u_g, u_g, true, fl);
+      S->d_ggrad.ensure(sizeof(double) * gg.size());
+      CUDA_OK(cudaMemcpy(S->d_ggrad.p, gg.data(), sizeof(double) * gg.size(), cudaMemcpyHostToDevice));
+    }
     S->d_flags.ensure(16);
     S->d_error.ensure(16);
     S->d_tile_ctr.ensure(16);
@@ -938,13 +988,14 @@ int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t S, const double* verts, int
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
     check_coef(*S, coef_kind, coef, coef_stride);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 12);
+    const int nv = S->box ? 8 : 4;
+    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 3 * nv);
     S->h_verts.ensure(vbytes);
     CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
     const int32_t* dcells = nullptr;
     if (cells) {
-      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * 4);
-      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * 4,
+      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * nv);
+      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * nv,
                               cudaMemcpyHostToDevice, st));
       dcells = static_cast<const int32_t*>(S->h_cells.p);
     }
@@ -1043,6 +1094,7 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   check_coef(S, coef_kind, coef, coef_stride);
   if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w && w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+  if (S.box) throw Error(MPFEM_B200_CONFIG_ERROR, "the GPU bound kernel supports tetrahedra");
   prepare_bounds(S);
   if (n_cells == 0) return;
   BoundParams P{};

@@ -335,27 +335,11 @@ __device__ __forceinline__ bool tet_geometry_f64_fast(const double v[4][3], bool
   return true;
 }
 
+// LU, det, inverse and geometry tensor at format F from a Jacobian (geometry.cpp:29-118):
+// shared by affine tets (J from the P1 gradients) and boxes (J at every rule point).
 template <int F>
-__device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poisson, TetGeometry& out,
-                                                     uint32_t& fl) {
-  // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
-  double jac[3][3];
-  #pragma unroll
-  for (int i = 0; i < 3; ++i)
-    #pragma unroll
-    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
-  #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      double x = droundT<F>(v[k][i], fl);
-      #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
-        jac[i][s] = daddT<F>(jac[i][s], dmulT<F>(x, g, fl), fl);
-      }
-    }
-  }
+__device__ __noinline__ bool jac_geometry_flagged(const double jac[3][3], bool poisson,
+                                                     TetGeometry& out, uint32_t& fl) {
   // lu_decompose (geometry.cpp:33-57)
   double lu[3][3];
   int perm[3] = {0, 1, 2};
@@ -444,6 +428,30 @@ __device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poi
       out.g[idx++] = dmulT<F>(out.abs_det, dot, fl);
     }
   return true;
+}
+
+template <int F>
+__device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poisson, TetGeometry& out,
+                                                     uint32_t& fl) {
+  // P1 gradient signs: vertex 0 -> -1 on every axis, vertex k -> +1 on axis k-1.
+  double jac[3][3];
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+  #pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    #pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double x = droundT<F>(v[k][i], fl);
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) {
+        double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
+        jac[i][s] = daddT<F>(jac[i][s], dmulT<F>(x, g, fl), fl);
+      }
+    }
+  }
+  return jac_geometry_flagged<F>(jac, poisson, out, fl);
 }
 
 // u_g = fp32: the same op sequence in native fp32 arithmetic. IEEE fp32 +,-,*,/ are the

@@ -241,7 +241,62 @@ Basis simplex_basis(int p) {
         b.factors.push_back(std::move(fs));
       }
   b.n_phi = int(b.weight.size());
+  b.m = p;
   return b;
+}
+
+Basis box_basis(int p) {
+  Basis b;
+  b.p = p;
+  b.m = 3 * p;
+  b.box = true;
+  const int n1 = p + 1;
+  std::vector<double> xs(n1);
+  for (int j = 0; j <= p; ++j) xs[j] = double(j) / double(p);
+  b.n_phi = n1 * n1 * n1;
+  for (int idx = 0; idx < b.n_phi; ++idx) {
+    int iax[3], rem = idx;
+    for (int a = 0; a < 3; ++a) {
+      iax[a] = rem % n1;
+      rem /= n1;
+    }
+    std::vector<Factor> fs;
+    double w = 1.0;
+    for (int a = 0; a < 3; ++a)
+      for (int j = 0; j <= p; ++j) {
+        if (j == iax[a]) continue;
+        Factor f;
+        f.a[a] = 1.0;
+        f.b = -xs[j];
+        f.sign[a] = 1;
+        fs.push_back(f);
+        w /= xs[iax[a]] - xs[j];
+      }
+    b.nodes.push_back({xs[iax[0]], xs[iax[1]], xs[iax[2]]});
+    b.weight.push_back(w);
+    b.factors.push_back(std::move(fs));
+  }
+  return b;
+}
+
+Rule box_rule(int p) {
+  const int n = p + 1;
+  double fx[64], fw[64];
+  gauss_legendre(n, fx, fw);
+  Rule r;
+  r.n_q = n * n * n;
+  r.points.resize(std::size_t(r.n_q) * 3);
+  r.weights.resize(r.n_q);
+  for (int q = 0; q < r.n_q; ++q) {
+    const int ix[3] = {q % n, (q / n) % n, q / (n * n)};
+    double w = 1.0;
+    for (int a = 0; a < 3; ++a) {
+      r.points[std::size_t(q) * 3 + a] = fx[ix[a]];
+      w *= fw[ix[a]];
+    }
+    r.weights[q] = w;
+  }
+  return r;
 }
 
 namespace {
@@ -258,7 +313,7 @@ double mul_at(double a, double b, int fmt, uint32_t& fl) { return host_round(a *
 
 std::vector<double> tabulate(const Basis& b, const Rule& r, int ef, int sf, bool grads,
                              uint32_t& fl) {
-  int nd = grads ? 3 : 1, m = b.p, nphi = b.n_phi, nq = r.n_q;
+  int nd = grads ? 3 : 1, m = b.m, nphi = b.n_phi, nq = r.n_q;
   std::vector<double> out(std::size_t(nd) * nphi * nq);
   std::vector<double> l(m);
   for (int k = 0; k < nphi; ++k) {
@@ -294,7 +349,7 @@ std::vector<double> tabulate(const Basis& b, const Rule& r, int ef, int sf, bool
 }
 
 BasisCond basis_conditioning(const Basis& b, const Rule& r) {
-  const int m = b.p, nphi = b.n_phi, nq = r.n_q, n_random = 2000;
+  const int m = b.m, nphi = b.n_phi, nq = r.n_q, n_random = 2000;
   std::vector<std::array<double, 3>> pts;
   pts.reserve(size_t(nq + nphi + n_random));
   for (int q = 0; q < nq; ++q) pts.push_back({r.points[3 * q], r.points[3 * q + 1], r.points[3 * q + 2]});
@@ -309,7 +364,7 @@ BasisCond basis_conditioning(const Basis& b, const Rule& r) {
         x[a] = uniform(0.0, 1.0);
         sum += x[a];
       }
-      if (sum <= 1.0) break;
+      if (b.box || sum <= 1.0) break;
     }
     pts.push_back(x);
   }

@@ -30,6 +30,8 @@ struct Factor {
 };
 struct Basis {
   int p = 0;
+  int m = 0;      // factors per function: p (tets), 3p (boxes)
+  bool box = false;
   int n_phi = 0;
   std::vector<std::array<double, 3>> nodes;
   std::vector<double> weight;
@@ -38,6 +40,10 @@ struct Basis {
 
 // build_basis(simplex 3D, p): elements.cpp:89-147.
 Basis simplex_basis(int p);
+// build_basis(box 3D, p), equispaced nodes: elements.cpp:26-31,50-87 (axis 0 fastest).
+Basis box_basis(int p);
+// rule_for(box, p): Gauss-Legendre (p+1)^3 points, axis 0 fastest (quadrature.cpp:171-224).
+Rule box_rule(int p);
 
 // tabulate(basis, rule, eval_fmt, store_fmt, gradients): elements.cpp:171-274.
 // Layout (s * n_phi + k) * n_q + q.

@@ -1,0 +1,109 @@
+// launch_geom_box.cu -- K1 for box cells (geom_box.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "geom_box.cuh"
+
+namespace mpfem_b200 {
+namespace {
+
+__device__ __forceinline__ double round_us_rt(double x, int f, uint32_t& fl) {
+  switch (f) {
+    case kBF16: return droundT<kBF16>(x, fl);
+    case kFP16: return droundT<kFP16>(x, fl);
+    case kFP32: return droundT<kFP32>(x, fl);
+    default: return droundT<kFP64>(x, fl);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T to_w(double v) {
+  if constexpr (sizeof(T) == 8) return v;
+  else if constexpr (sizeof(T) == 4) return float(v);
+  else return T(float(v));  // v is already a u_s value: the conversion is exact
+}
+
+template <typename T, int UG>
+__global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) {
+  uint32_t fl = 0;
+  T* W = static_cast<T*>(P.W);
+  const int64_t items = P.n_cells * P.nq_pad;
+  for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items;
+       it += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t cell = it / P.nq_pad;
+    const int q = int(it - cell * P.nq_pad);
+    T* wrow = W + cell * P.k_pad;
+    if (q == 0)
+      for (int64_t e = P.k; e < P.k_pad; ++e) wrow[e] = T(0.0f);
+    if (q >= P.n_q) {
+      for (int b = 0; b < P.n_blocks; ++b) wrow[b * P.nq_pad + q] = T(0.0f);
+      continue;
+    }
+    double jac[3][3];
+    #pragma unroll
+    for (int i = 0; i < 3; ++i)
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+    #pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+      const int64_t base = P.cells ? int64_t(P.cells[cell * 8 + k]) * 3 : cell * 24 + k * 3;
+      double g[3];
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) g[s] = P.ggrad[(size_t(s) * 8 + k) * P.n_q + q];
+      #pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double x = droundT<UG>(P.verts[base + i], fl);
+        #pragma unroll
+        for (int s = 0; s < 3; ++s) jac[i][s] = daddT<UG>(jac[i][s], dmulT<UG>(x, g[s], fl), fl);
+      }
+    }
+    TetGeometry geo;
+    if (!jac_geometry_flagged<UG>(jac, P.poisson != 0, geo, fl)) {
+      atomicExch(P.error, 3);
+      #pragma unroll
+      for (int b = 0; b < 6; ++b) geo.g[b] = 0.0;
+    }
+    double zq = 1.0;
+    const bool have_z = P.coef_kind != 0;
+    if (have_z) {  // eval_z_at_ug (kernels.cpp:114-136)
+      const double* coef = P.coef + cell * P.coef_stride;
+      double acc = 0.0;
+      for (int k = 0; k < P.n_phi; ++k)
+        acc = dadd(acc, dmul(dround(coef[k], P.up, fl), P.tab_up[size_t(k) * P.n_q + q], P.up, fl), P.up, fl);
+      zq = droundT<UG>(acc, fl);
+    }
+    const double om = P.rule_w_ug[q];
+    for (int b = 0; b < P.n_blocks; ++b) {
+      double v = dmulT<UG>(om, geo.g[b], fl);
+      if (have_z) v = dmulT<UG>(v, zq, fl);
+      wrow[b * P.nq_pad + q] = to_w<T>(round_us_rt(v, P.us, fl));
+    }
+  }
+  publish_flags(P.flags, fl);
+}
+
+template <typename T>
+void launch_ug(const GeomBoxParams& P, unsigned grid, cudaStream_t st) {
+  switch (P.ug) {
+    case kFP64: geom_w_box_kernel<T, kFP64><<<grid, 128, 0, st>>>(P); break;
+    case kFP32: geom_w_box_kernel<T, kFP32><<<grid, 128, 0, st>>>(P); break;
+    case kFP16: geom_w_box_kernel<T, kFP16><<<grid, 128, 0, st>>>(P); break;
+    default: geom_w_box_kernel<T, kBF16><<<grid, 128, 0, st>>>(P); break;
+  }
+}
+
+}  // namespace
+
+void launch_geom_box(int w_type, const GeomBoxParams& P, int sm_count, cudaStream_t st) {
+  const int64_t items = P.n_cells * P.nq_pad;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((items + 127) / 128, int64_t(sm_count) * 16)));
+  switch (w_type) {
+    case 0: launch_ug<__half>(P, grid, st); break;
+    case 1: launch_ug<__nv_bfloat16>(P, grid, st); break;
+    case 2: launch_ug<float>(P, grid, st); break;
+    default: launch_ug<double>(P, grid, st); break;
+  }
+}
+
+}  // namespace mpfem_b200

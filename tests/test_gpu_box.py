@@ -1,0 +1,110 @@
+"""Hexahedral (box) cells on the GPU, through the C-ABI.
+
+The geometry is evaluated at every rule point (trilinear map), so K1 writes per-point scaled
+weights; K2 (the tcgen05 / SIMT GEMM) is unchanged. Bars (tolerances written here):
+  * W (build_C with per-point G): BITWISE the reference's (oracle restatement pinned to the
+    compiled reference, tests/test_oracle_golden.py::test_box_cells_bitwise), constant and nodal
+    coefficients, every mode, p = 1..4;
+  * cell matrices vs the fp64 oracle: err_rel <= S bound_a per cell (kernel_bounds on the box
+    cell, S = 4 when u_s is coarser than every compute format), vs same mode <= 2 S bound_a;
+  * fp64 mode equals the oracle to rounding (<= 1e-13 relative); mesh-indexed == private.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2410_12614_b200 as mp  # noqa: E402
+from oracle_lib import (COEF_NODAL, COEF_ONE, MASS, MODES, POISSON, UNIT_ROUNDOFF,  # noqa: E402
+                        box_mesh_cells)
+
+PACK = [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+
+
+def kconfig(mode, form):
+    up, ug, uq, us, eng = MODES[mode]
+    return mp.KernelConfig(form=mp.FormKind(form), u_p=mp.Fmt(up), u_g=mp.Fmt(ug), u_q=mp.Fmt(uq),
+                           u_s=mp.Fmt(us), engine=mp.EngineKind(eng))
+
+
+def cfg_tuple(c):
+    return (int(c.u_p), int(c.u_g), int(c.u_q), int(c.u_s), int(c.engine))
+
+
+def dev(a, dtype=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+@pytest.fixture(scope="module")
+def hexes(oracle):
+    verts, _ = oracle.structured_tet_mesh(3, 3, 3, 1.0, 0.15, 11)
+    cells = box_mesh_cells(3, 3, 3)
+    return verts, cells, verts[cells]
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_box_scaled_weights_bitwise(oracle, hexes, mode, form):
+    _, _, hx = hexes
+    rng = np.random.default_rng(5 + form)
+    cfg = kconfig(mode, form)
+    nd = 3 if form == POISSON else 1
+    blocks = PACK if form == POISSON else [(0, 0)]
+    for p in (1, 2, 3, 4):
+        s = mp.make_setup(p, cfg, cell_kind=1)
+        n, nq = 5, (p + 1) ** 3
+        for kind in (COEF_ONE, COEF_NODAL):
+            z = rng.uniform(0.5, 1.5, size=(n, s.n_phi)) if kind == COEF_NODAL else None
+            w, _ = s.scaled_weights(dev(hx[:n]), None, kind, None if z is None else dev(z))
+            nqp = s.k // len(blocks)
+            w = w.cpu().numpy().reshape(n, len(blocks), nqp)
+            assert np.all(w[:, :, nq:] == 0.0)
+            w = np.ascontiguousarray(w[:, :, :nq]).reshape(n, -1)
+            for c in range(n):
+                ref, _ = oracle.build_C_box(p, form, cfg_tuple(cfg), hx[c], kind, None if z is None else z[c])
+                ref = ref.reshape(nd, nd, nq)
+                want = np.concatenate([ref[a, b] for a, b in blocks])
+                assert np.array_equal(w[c].view(np.uint64), want.view(np.uint64)), (mode, form, p, kind, c)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_box_cell_matrices_within_bound(oracle, hexes, mode, form):
+    _, _, hx = hexes
+    rng = np.random.default_rng(9)
+    cfg = kconfig(mode, form)
+    us = UNIT_ROUNDOFF[int(cfg.u_s)]
+    S = 4.0 if all(us > UNIT_ROUNDOFF[int(f)] for f in (cfg.u_p, cfg.u_g, cfg.u_q)) else 1.0
+    for p in (1, 2, 3):
+        s = mp.make_setup(p, cfg, cell_kind=1)
+        n = 6
+        for kind in (COEF_ONE, COEF_NODAL):
+            z = rng.uniform(0.5, 1.5, size=(n, s.n_phi)) if kind == COEF_NODAL else None
+            a = s.cell_matrices(dev(hx[:n]), None, kind, None if z is None else dev(z))
+            a = a.double().cpu().numpy()
+            same, _ = oracle.bilinear_box(p, form, cfg_tuple(cfg), hx[:n], kind, z)
+            for c in range(n):
+                b, a64 = oracle.bound_box(p, form, cfg_tuple(cfg), hx[c], kind, None if z is None else z[c])
+                scale = np.max(np.abs(a64))
+                e64 = np.max(np.abs(a[c] - a64)) / scale
+                esm = np.max(np.abs(a[c] - same[c])) / scale
+                assert e64 <= S * b[0], (mode, form, p, kind, c, e64, b[0])
+                assert esm <= 2 * S * b[0], (mode, form, p, kind, c, esm, b[0])
+                if mode == "fp64":
+                    assert e64 <= 1e-13
+
+
+def test_box_mesh_indexed_and_host_api(oracle, hexes):
+    verts, cells, hx = hexes
+    for mode in ("mixed", "fp64"):
+        s = mp.make_setup(2, kconfig(mode, POISSON), cell_kind=1)
+        a_mesh = s.cell_matrices(dev(verts), dev(cells, torch.int32), COEF_ONE)
+        a_priv = s.cell_matrices(dev(hx), None, COEF_ONE)
+        assert torch.equal(a_mesh, a_priv)
+        a_host = s.cell_matrices_host(hx, None, COEF_ONE)
+        assert np.array_equal(a_host, a_priv.cpu().numpy())
+    with pytest.raises(mp.ConfigError):  # analytic coefficients are defined for tets only
+        s.cell_matrices(dev(hx), None, 1)
+    with pytest.raises(mp.ConfigError):
+        mp.make_setup(5, kconfig("mixed", MASS), cell_kind=1)
