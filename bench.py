@@ -370,6 +370,45 @@ def run_action(mp, torch, dev, flush, sm_mhz):
     return res
 
 
+def run_hex(mp, torch, dev, flush, hbm, tc_peak):
+    """Hexahedral cells: the paper's 55,296-hex case size (48 x 48 x 24 jittered
+    lattice, seed 1), Q1-Q3 Poisson and mass, mixed (fp16 storage, fp32 accumulation), constant
+    coefficient; geometry at every Gauss-Legendre point in K1, the tets' tcgen05 GEMM in K2."""
+    lv, lc = mp.structured_tet_mesh(48, 48, 24, 1.0, 0.15, 1)
+    nx, ny, nz = 48, 48, 24
+    ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    base = (ii + (nx + 1) * (jj + (ny + 1) * kk)).transpose(2, 1, 0).reshape(-1)
+    offs = np.array([(b & 1) + (nx + 1) * (((b >> 1) & 1) + (ny + 1) * ((b >> 2) & 1)) for b in range(8)])
+    cells = (base[:, None] + offs[None, :]).astype(np.int32)
+    dv = torch.from_numpy(lv).to(dev)
+    dc = torch.from_numpy(cells).to(dev)
+    n = cells.shape[0]
+    res = []
+    for form in (0, 1):
+        for p in (1, 2, 3):
+            cfg = mp.mode_config("mixed", form)
+            s = mp.make_setup(p, cfg, cell_kind=1)
+            s.reserve(n)
+            out = torch.empty((n, s.n_phi ** 2), dtype=torch.float32, device=dev)
+            ms = timed_ms(torch, lambda: s.cell_matrices(dv, dc, mp.CoefKind.one, out=out), reps=10, flush=flush)
+            s.set_timing(True)
+            s.cell_matrices(dv, dc, mp.CoefKind.one, out=out)
+            t = s.last_timings()
+            s.set_timing(False)
+            nd = 3 if form else 1
+            f_cell = 2.0 * s.n_phi ** 2 * s.n_q * nd * nd
+            b_cell = 8 * 3 * 4 + 4 * s.n_phi ** 2  # vertex ids + output (mesh-indexed)
+            t_roof = max(f_cell * n / (tc_peak * 1e12), b_cell * n / (hbm * 1e9)) * 1e3
+            res.append({"form": "poisson" if form else "mass", "p": p, "n_phi": s.n_phi, "cells": n,
+                        "ms": ms, "cells_per_s": n / (ms * 1e-3), "k1_ms": t[0] if t else None,
+                        "k2_ms": t[1] if len(t) > 1 else None,
+                        "tflops_dense_equiv": f_cell * n / (ms * 1e-3) / 1e12,
+                        "roofline_frac": t_roof / ms, "path": s.path})
+            del s, out
+            torch.cuda.empty_cache()
+    return res
+
+
 def run_robustness(mp, torch, dev):
     """BASELINE config 3: 65,536 anisotropic rotated tets, c = 10^(6 u(x)) with u affine per
     cell; P1-P6 mass and Poisson in fp16 and mixed (fp16 and bf16 storage): max per-cell error
@@ -491,6 +530,7 @@ def main():
     ap.add_argument("--no-modes", action="store_true", help="skip the configs 0/1 precision-mode table")
     ap.add_argument("--robustness", action="store_true", help="add the config-3 error table")
     ap.add_argument("--no-action", action="store_true", help="skip the Algorithm-2 action table")
+    ap.add_argument("--no-hex", action="store_true", help="skip the hexahedral-cell table")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -663,6 +703,9 @@ def main():
         line["action"] = {"workload": "configs 0/1 as action_kernel (Algorithm 2): 65536 P4 tets, "
                                       "c(x) at quadrature points, one random w per cell",
                           "results": run_action(mp, torch, dev, flush, clocks.get("sm_max_mhz") or 1965.0)}
+    if not args.no_hex and rank == 0:
+        line["hex"] = {"workload": "55,296 jittered hexes (48x48x24 lattice), Q1-Q3, mixed, constant c",
+                       "results": run_hex(mp, torch, dev, flush, hbm, tc_peak)}
     if args.robustness and rank == 0:
         line["robustness"] = run_robustness(mp, torch, dev)
     if args.sweep and rank == 0:

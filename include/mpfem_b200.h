@@ -54,7 +54,9 @@ const char* mpfem_b200_last_error(void);
 const char* mpfem_b200_version(void);
 
 /* Replaces make_setup (kernels.hpp:60-62, kernels.cpp:78-108) + validate_config
- * (kernels.cpp:29-40). cell_kind must be 0 (simplex), dim 3, 1 <= p <= 8.
+ * (kernels.cpp:29-40). dim 3; cell_kind 0 (simplex, 1 <= p <= 8) or 1 (box / hexahedra,
+ * 1 <= p <= 4: tensor Lagrange basis, Gauss-Legendre rule, geometry at every rule point;
+ * vertices 8 per cell in lattice bit order, constant or nodal coefficients).
  * The handle owns device copies of the rule, the fp64 tabulations and the shared
  * basis-product operand T; it is immutable and may be shared by streams. */
 int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, int u_g,
