@@ -38,6 +38,9 @@ struct BoundParams {
   const double* w;        // n_cells rows of n_phi (row stride w_stride); NULL = bilinear
   int64_t w_stride;
   double grad_lebesgue[3], grad_kappa_max[3];
+  // hexahedra: geometry at every rule point through the degree-1 box gradients (binary64)
+  int box;
+  const double* ggrad64;  // (s * 8 + k) * n_q + q
 };
 
 constexpr int kBoundThreads = 256;

@@ -161,7 +161,7 @@ struct mpfem_b200_setup_s {
   DevBuf d_act_a, d_act_c;
   int act_ap = -1, act_aq = -1;
   // GPU bound evaluation (kernel_bounds): binary64 budgets of the tabulation, built on first use
-  DevBuf d_bnd_theta, d_bnd_vals;
+  DevBuf d_bnd_theta, d_bnd_vals, d_bnd_ggrad;
   double bnd_lebesgue = 0.0;
   double bnd_glebesgue[3] = {0.0, 0.0, 0.0}, bnd_gkmax[3] = {0.0, 0.0, 0.0};
   bool bnd_ready = false;
@@ -736,7 +736,7 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
 // tabulation for nodal coefficients and the basis Lebesgue constant.
 void prepare_bounds(mpfem_b200_setup_s& S) {
   if (S.bnd_ready) return;
-  const Basis basis = simplex_basis(S.p);
+  const Basis basis = S.box ? box_basis(S.p) : simplex_basis(S.p);
   const BasisCond bc = basis_conditioning(basis, S.rule);
   uint32_t fl = 0;
   const std::vector<double> tab = tabulate(basis, S.rule, 3, 3, S.form == 1, fl);
@@ -760,6 +760,11 @@ void prepare_bounds(mpfem_b200_setup_s& S) {
   CUDA_OK(cudaMemcpy(S.d_bnd_theta.p, theta.data(), sizeof(double) * theta.size(), cudaMemcpyHostToDevice));
   S.d_bnd_vals.ensure(sizeof(double) * vals.size());
   CUDA_OK(cudaMemcpy(S.d_bnd_vals.p, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice));
+  if (S.box) {  // degree-1 box gradients at binary64, for the per-point geometry
+    const std::vector<double> gg = tabulate(box_basis(1), S.rule, 3, 3, true, fl);
+    S.d_bnd_ggrad.ensure(sizeof(double) * gg.size());
+    CUDA_OK(cudaMemcpy(S.d_bnd_ggrad.p, gg.data(), sizeof(double) * gg.size(), cudaMemcpyHostToDevice));
+  }
   S.bnd_lebesgue = bc.lebesgue;
   for (int a = 0; a < 3; ++a) {
     S.bnd_glebesgue[a] = bc.grad_lebesgue[a];
@@ -1094,7 +1099,7 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   check_coef(S, coef_kind, coef, coef_stride);
   if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w && w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
-  if (S.box) throw Error(MPFEM_B200_CONFIG_ERROR, "the GPU bound kernel supports tetrahedra");
+  if (S.box && w) throw Error(MPFEM_B200_CONFIG_ERROR, "the action bound supports tetrahedra");
   prepare_bounds(S);
   if (n_cells == 0) return;
   BoundParams P{};
@@ -1126,6 +1131,8 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   P.a64 = a64;
   P.w = w;
   P.w_stride = w_stride;
+  P.box = S.box;
+  P.ggrad64 = static_cast<const double*>(S.d_bnd_ggrad.p);
   P.error = static_cast<int*>(S.d_error.p);
   CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
   const int rc = w ? launch_action_bounds_kernel(P, device_sm_count(), st)

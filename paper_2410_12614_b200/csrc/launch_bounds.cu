@@ -50,26 +50,13 @@ __device__ void sym_eigenvalues3(const double* sym, double* eig) {
 struct CellDiag {
   double ten[9], tt[9];
   double kk2;  // kappa_cell * kappa_2
-  double v[4][3];
+  double v[8][3];
 };
 
-// binary64 cell_geometry with the diagnostics fields (geometry.cpp:12-118,156-245).
-// Returns false on a zero pivot (CheckError, geometry.cpp:42).
-__device__ bool cell_diag(const BoundParams& P, int64_t cell, bool poisson, CellDiag& d) {
-  for (int k = 0; k < 4; ++k) {
-    const int64_t base = P.cells ? int64_t(P.cells[cell * 4 + k]) * 3 : cell * 12 + k * 3;
-    for (int a = 0; a < 3; ++a) d.v[k][a] = P.verts[base + a];
-  }
-  double jac[3][3];
-  for (int i = 0; i < 3; ++i)
-    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
-  for (int k = 0; k < 4; ++k)  // J through the P1 gradients at the centroid (exact +-1, 0)
-    for (int i = 0; i < 3; ++i)
-      for (int s = 0; s < 3; ++s) {
-        const double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
-        jac[i][s] = jac[i][s] + d.v[k][i] * g;
-      }
-  // LU with partial pivoting, det, inverse by three solves (geometry.cpp:29-95)
+// Binary64 geometry and diagnostics at one point from its Jacobian (geometry.cpp:29-118,
+// 156-221): G, G~, kappa_2(J), kappa_cell = nv ||X||_inf / ||J||_inf. False on a zero pivot.
+__device__ bool diag_from_jac(const double jac[3][3], const double (*v)[3], int nv, bool poisson,
+                              double* ten, double* tt, double& kk2) {
   double lu[3][3];
   int perm[3] = {0, 1, 2}, sign = 1;
   for (int i = 0; i < 3; ++i)
@@ -108,25 +95,24 @@ __device__ bool cell_diag(const BoundParams& P, int64_t cell, bool poisson, Cell
       inv[r][k] = s / lu[r][r];
     }
   }
-  for (int i = 0; i < 9; ++i) d.ten[i] = d.tt[i] = 0.0;
+  for (int i = 0; i < 9; ++i) ten[i] = tt[i] = 0.0;
   if (!poisson) {
-    d.ten[0] = adet;
-    d.tt[0] = adet;
+    ten[0] = adet;
+    tt[0] = adet;
   } else {
     for (int s = 0; s < 3; ++s)
       for (int t = s; t < 3; ++t) {
         double dot = 0.0;
         for (int k = 0; k < 3; ++k) dot = dot + inv[s][k] * inv[t][k];
-        d.ten[s * 3 + t] = d.ten[t * 3 + s] = adet * dot;
+        ten[s * 3 + t] = ten[t * 3 + s] = adet * dot;
       }
     for (int s = 0; s < 3; ++s)
       for (int t = 0; t < 3; ++t) {
         double dot = 0.0;
         for (int k = 0; k < 3; ++k) dot += fabs(inv[s][k]) * fabs(inv[t][k]);
-        d.tt[s * 3 + t] = adet * dot;
+        tt[s * 3 + t] = adet * dot;
       }
   }
-  // kappa_2(J) = sqrt(lambda_max / lambda_min) of J^T J (geometry.cpp:156-169)
   double jtj[9], eig[3];
   for (int s = 0; s < 3; ++s)
     for (int t = 0; t < 3; ++t) {
@@ -136,19 +122,50 @@ __device__ bool cell_diag(const BoundParams& P, int64_t cell, bool poisson, Cell
     }
   sym_eigenvalues3(jtj, eig);
   const double kappa2 = eig[0] <= 0.0 ? INFINITY : sqrt(eig[2] / eig[0]);
-  // kappa_cell = 4 ||X||_inf / ||J||_inf (geometry.cpp:171-186)
   double xnorm = 0.0, jnorm = 0.0;
   for (int i = 0; i < 3; ++i) {
     double row = 0.0;
-    for (int v = 0; v < 4; ++v) row += fabs(d.v[v][i]);
+    for (int w = 0; w < nv; ++w) row += fabs(v[w][i]);
     xnorm = fmax(xnorm, row);
     double jr = 0.0;
     for (int s = 0; s < 3; ++s) jr += fabs(jac[i][s]);
     jnorm = fmax(jnorm, jr);
   }
-  const double kcell = 4.0 * xnorm / jnorm;
-  d.kk2 = kcell * kappa2;
+  kk2 = double(nv) * xnorm / jnorm * kappa2;
   return true;
+}
+
+// Affine tets: one point (J through the P1 gradients at the centroid, exact +-1 / 0).
+__device__ bool cell_diag(const BoundParams& P, int64_t cell, bool poisson, CellDiag& d) {
+  const int nv = P.box ? 8 : 4;
+  for (int k = 0; k < nv; ++k) {
+    const int64_t base = P.cells ? int64_t(P.cells[cell * nv + k]) * 3 : cell * 3 * nv + k * 3;
+    for (int a = 0; a < 3; ++a) d.v[k][a] = P.verts[base + a];
+  }
+  if (P.box) return true;  // boxes: per-point diagnostics in box_point_diag
+  double jac[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+  for (int k = 0; k < 4; ++k)
+    for (int i = 0; i < 3; ++i)
+      for (int s = 0; s < 3; ++s) {
+        const double g = (k == 0) ? -1.0 : ((k - 1 == s) ? 1.0 : 0.0);
+        jac[i][s] = jac[i][s] + d.v[k][i] * g;
+      }
+  return diag_from_jac(jac, d.v, 4, poisson, d.ten, d.tt, d.kk2);
+}
+
+// Boxes: J(xi_q) = sum_k x_k (x) grad phi_k(xi_q) at binary64 (geometry.cpp:12-27).
+__device__ bool box_point_diag(const BoundParams& P, const CellDiag& d, int q, bool poisson,
+                               double* ten, double* tt, double& kk2) {
+  double jac[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+  for (int k = 0; k < 8; ++k)
+    for (int i = 0; i < 3; ++i)
+      for (int s = 0; s < 3; ++s)
+        jac[i][s] = jac[i][s] + d.v[k][i] * P.ggrad64[(size_t(s) * 8 + k) * P.n_q + q];
+  return diag_from_jac(jac, d.v, 8, poisson, ten, tt, kk2);
 }
 
 __device__ double block_max(double v, double* red) {
@@ -171,6 +188,9 @@ __global__ void __launch_bounds__(kBoundThreads) cell_bounds_kernel(const BoundP
   double* gc = thc + nc;       // gamma_c                         (bounds.cpp:123-124)
   double* zat = gc + nc;       // z(x_q) in binary64
   double* red = zat + nq;      // 4 x 32 reduction scratch
+  double* pten = red + 128;    // boxes: G, G~ and kappa_cell kappa_2 at every rule point
+  double* ptt = pten + (P.box ? 9 * nq : 0);
+  double* pkk = ptt + (P.box ? 9 * nq : 0);
   __shared__ CellDiag sd;
   __shared__ int s_ok;
   const bool poisson = nd == 3;
@@ -181,6 +201,14 @@ __global__ void __launch_bounds__(kBoundThreads) cell_bounds_kernel(const BoundP
       if (!s_ok) atomicExch(P.error, 3);
     }
     __syncthreads();
+    if (P.box) {
+      for (int q = threadIdx.x; q < nq; q += blockDim.x)
+        if (!box_point_diag(P, sd, q, poisson, pten + 9 * q, ptt + 9 * q, pkk[q])) {
+          s_ok = 0;
+          atomicExch(P.error, 3);
+        }
+      __syncthreads();
+    }
     const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
     double z_norm = 0.0;
     if (P.coef_kind == 3)
@@ -212,10 +240,12 @@ __global__ void __launch_bounds__(kBoundThreads) cell_bounds_kernel(const BoundP
       const int st = e / nq, q = e - st * nq;
       const int s = st / nd, t = st - s * nd;
       const double omega = P.rule_w[q];
-      const double ten = sd.ten[s * 3 + t];
+      const double ten = P.box ? pten[9 * q + s * 3 + t] : sd.ten[s * 3 + t];
+      const double tt = P.box ? ptt[9 * q + s * 3 + t] : sd.tt[s * 3 + t];
+      const double kk2 = P.box ? pkk[q] : sd.kk2;
       cc[e] = omega * ten * zat[q];
       thc[e] = P.coef_kind == 3 ? pd * P.lebesgue * z_norm * fabs(omega * ten) : 0.0;
-      gc[e] = sd.kk2 * fabs(omega * sd.tt[s * 3 + t] * zat[q]);
+      gc[e] = kk2 * fabs(omega * tt * zat[q]);
     }
     __syncthreads();
     double amax = 0.0, samax = 0.0, tamax = 0.0, gamax = 0.0;
@@ -387,7 +417,7 @@ __global__ void __launch_bounds__(kBoundThreads) cell_action_bounds_kernel(const
 
 int launch_bounds_kernel(const BoundParams& P, int sm_count, cudaStream_t st) {
   const size_t nc = size_t(P.n_d) * P.n_d * P.n_q;
-  const size_t smem = sizeof(double) * (3 * nc + P.n_q + 128);
+  const size_t smem = sizeof(double) * (3 * nc + P.n_q + 128 + (P.box ? 19 * size_t(P.n_q) : 0));
   static size_t smem_set = 0;
   if (smem > smem_set) {
     if (cudaFuncSetAttribute(cell_bounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

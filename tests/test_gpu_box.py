@@ -108,3 +108,33 @@ def test_box_mesh_indexed_and_host_api(oracle, hexes):
         s.cell_matrices(dev(hx), None, 1)
     with pytest.raises(mp.ConfigError):
         mp.make_setup(5, kconfig("mixed", MASS), cell_kind=1)
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_box_bounds_bitwise(oracle, hexes, mode, form):
+    """kernel_bounds on hexahedra (per-point geometry diagnostics) on the GPU: bound_a, the
+    kappas and the exact A bitwise the reference's (oracle restatement pinned by
+    test_box_cells_bitwise), p = 1..3; then every cell of the mesh against its bound."""
+    _, _, hx = hexes
+    rng = np.random.default_rng(2 + form)
+    cfg = kconfig(mode, form)
+    for p in (1, 2, 3):
+        s = mp.make_setup(p, cfg, cell_kind=1)
+        n = 3
+        for kind in (COEF_ONE, COEF_NODAL):
+            z = rng.uniform(0.5, 1.5, size=(n, s.n_phi)) if kind == COEF_NODAL else None
+            out, a64 = s.cell_bounds(dev(hx[:n]), coef_kind=kind, coef=None if z is None else dev(z),
+                                     want_a64=True)
+            out, a64 = out.cpu().numpy(), a64.cpu().numpy()
+            for c in range(n):
+                ref, ra = oracle.bound_box(p, form, cfg_tuple(cfg), hx[c], kind, None if z is None else z[c])
+                assert np.array_equal(out[c].view(np.uint64), ref.view(np.uint64)), (mode, form, p, kind, c)
+                assert np.array_equal(a64[c].view(np.uint64), ra.view(np.uint64)), (mode, form, p, kind, c)
+    us = UNIT_ROUNDOFF[int(cfg.u_s)]
+    S = 4.0 if all(us > UNIT_ROUNDOFF[int(f)] for f in (cfg.u_p, cfg.u_g, cfg.u_q)) else 1.0
+    s = mp.make_setup(2, cfg, cell_kind=1)
+    a = s.cell_matrices(dev(hx), None, COEF_ONE).double()
+    b, a64 = s.cell_bounds(dev(hx), want_a64=True)
+    err = (a - a64).abs().amax(dim=(1, 2)) / a64.abs().amax(dim=(1, 2))
+    assert float((err / (S * b[:, 0])).max()) <= 1.0
