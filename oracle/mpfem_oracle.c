@@ -1264,10 +1264,10 @@ int orc_bound_box(int p, int form, const int* cfg, const double* verts, int kind
 static int action_one(const setup_t* S, const double* verts, int kind, const double* coef,
                       const double* w, double* v, uint32_t* fl) {
   int nq = S->nq, nd = S->nd, nphi = S->nphi;
-  double geom[ORC_GEOM_SIZE];
-  int st = orc_cell_geometry(verts, S->form, S->ug, geom, fl);
-  if (st) return st;
-  const double* ten = geom + 20;
+  double* geom = NULL;
+  int gstride = 0;
+  int st = cell_geometry_all(S, verts, S->ug, &geom, &gstride, fl);
+  if (st) { free(geom); return st; }
   int ftz = S->engine == 2;
   double* zhat = malloc(sizeof(double) * nq);
   int have_z = coef_zhat(S, verts, kind, coef, zhat, fl);
@@ -1286,6 +1286,7 @@ static int action_one(const setup_t* S, const double* verts, int kind, const dou
   double* r = malloc(sizeof(double) * nd * nq);
   for (int q = 0; q < nq; ++q) {
     double omega = RND(S->wts[q], S->ug);
+    const double* ten = geom + (size_t)q * gstride + 20;
     for (int s = 0; s < nd; ++s) {
       double t1 = 0.0;
       for (int t = 0; t < nd; ++t)
@@ -1305,8 +1306,27 @@ static int action_one(const setup_t* S, const double* verts, int kind, const dou
       }
     v[i] = acc;
   }
-  free(zhat); free(what); free(r);
+  free(zhat); free(what); free(r); free(geom);
   return 0;
+}
+
+/* action_kernel on hexahedra (per-point geometry), constant or nodal coefficients. */
+int orc_action_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                   const double* coef, int coef_stride, const double* w, int w_stride,
+                   double* v_out, uint32_t* fl) {
+  uint32_t dummy = 0;
+  if (!fl) fl = &dummy;
+  if (kind != ORC_COEF_ONE && kind != ORC_COEF_NODAL)
+    return fail(2, "box cells take constant or nodal coefficients");
+  setup_t S;
+  int st = make_setup_kind(p, form, cfg, &S, 1);
+  if (!st) {
+    for (int64_t c = 0; c < m && !st; ++c)
+      st = action_one(&S, verts + 24 * c, kind, coef ? coef + (int64_t)coef_stride * c : NULL,
+                      w + (int64_t)w_stride * c, v_out + (int64_t)S.nphi * c, fl);
+  }
+  free_setup(&S);
+  return st;
 }
 
 int orc_action(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,

@@ -107,6 +107,9 @@ int orc_build_C_box(int p, int form, const int* cfg, const double* verts, int ki
                     const double* coef, double* c_out, uint32_t* flags);
 int orc_bound_box(int p, int form, const int* cfg, const double* verts, int kind,
                   const double* coef, double* out4, double* a64);
+int orc_action_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                   const double* coef, int coef_stride, const double* w, int w_stride,
+                   double* v_out, uint32_t* flags);
 
 /* Physical quadrature points x_q = v0 + J (xi_q) in fp64 and the coefficient there. */
 int orc_coef_at_q(int p, const double* verts, int coef_kind, const double* coef,

@@ -425,6 +425,26 @@ int ref_bound_box(int p, int form, const int* cfg, const double* verts, int kind
   });
 }
 
+int ref_action_box(int p, int form, const int* cfg, int64_t m, const double* verts, int kind,
+                   const double* coef, int coef_stride, const double* w, int w_stride,
+                   double* v_out, uint32_t* flags) {
+  return guard([&] {
+    FpFlags f;
+    KernelSetup setup = make_setup(kHex, p, make_cfg(form, cfg, ModeKind::action));
+    int n_phi = setup.basis.n_phi;
+    for (int64_t c = 0; c < m; ++c) {
+      Mesh mesh = single_hex(verts + 24 * c);
+      GeometryData geom = cell_geometry(mesh, 0, setup.rule, setup.config.form, setup.config.u_g, f);
+      Coefficients z;
+      if (kind == 3) z.assign(coef + coef_stride * c, coef + coef_stride * c + n_phi);
+      Coefficients wv(w + int64_t(w_stride) * c, w + int64_t(w_stride) * c + n_phi);
+      Mat v = action_kernel(setup, {geom}, {wv}, z, f);
+      std::memcpy(v_out + int64_t(n_phi) * c, v.a.data(), sizeof(double) * n_phi);
+    }
+    if (flags) *flags |= pack(f);
+  });
+}
+
 int ref_structured_tet_mesh(int nx, int ny, int nz, double extent, double jitter, uint64_t seed,
                             double* verts, int32_t* cells) {
   return guard([&] {

@@ -151,6 +151,11 @@ def main() -> None:
                         out[key + "_coef"] = coef
                     c, _ = R.build_C_box(p, form, cfg, hexes[0], kind, None if coef is None else coef[0])
                     out[f"Chex_{mode}_f{form}_p{p}_k{kind}"] = c
+                    wv = brng.uniform(-1.0, 1.0, size=(2, n))
+                    v, vfl = R.action_box(p, form, cfg, hexes[4:6], wv, kind, coef)
+                    out[f"Vhex_{mode}_f{form}_p{p}_k{kind}"] = v
+                    out[f"Vhex_{mode}_f{form}_p{p}_k{kind}_w"] = wv
+                    out[f"Vhex_{mode}_f{form}_p{p}_k{kind}_flags"] = np.array([vfl], dtype=np.uint32)
                     if p <= 2:
                         b, a64 = R.bound_box(p, form, cfg, hexes[3], kind, None if coef is None else coef[1])
                         out[f"boundhex_{mode}_f{form}_p{p}_k{kind}"] = b

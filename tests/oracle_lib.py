@@ -78,6 +78,8 @@ class _Lib:
         self._sig("bilinear_box", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
                                             C.c_int, _d, _u32])
         self._sig("build_C_box", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _u32])
+        self._sig("action_box", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
+                                          C.c_int, _d, C.c_int, _d, _u32])
         self._sig("bound_box", C.c_int, [C.c_int, C.c_int, _int, _d, C.c_int, _d, _d, _d])
         self._sig("action", C.c_int, [C.c_int, C.c_int, _int, C.c_int64, _d, C.c_int, _d,
                                       C.c_int, _d, C.c_int, _d, _u32])
@@ -209,6 +211,22 @@ class _Lib:
         fl = C.c_uint32(0)
         self._check(self._build_C_box(p, form, c, _ptr(v, _d), kind, _ptr(cf, _d), _ptr(out, _d),
                                       C.byref(fl)))
+        return out, fl.value
+
+    def action_box(self, p, form, cfg, verts, w, kind=COEF_ONE, coef=None):
+        """action_kernel on hexahedra: v (m, (p+1)^3), flags."""
+        v = np.ascontiguousarray(verts, dtype=np.float64).reshape(-1, 24)
+        m = v.shape[0]
+        wv = np.ascontiguousarray(w, dtype=np.float64).reshape(m, -1)
+        out = np.zeros((m, (p + 1) ** 3))
+        c = (C.c_int * 5)(*cfg)
+        cf, stride = None, 0
+        if coef is not None:
+            cf = np.ascontiguousarray(coef, dtype=np.float64).reshape(m, -1)
+            stride = cf.shape[1]
+        fl = C.c_uint32(0)
+        self._check(self._action_box(p, form, c, m, _ptr(v, _d), kind, _ptr(cf, _d), stride,
+                                     _ptr(wv, _d), wv.shape[1], _ptr(out, _d), C.byref(fl)))
         return out, fl.value
 
     def bound_box(self, p, form, cfg, verts, kind=COEF_ONE, coef=None):

@@ -195,6 +195,10 @@ def test_box_cells_bitwise(oracle, golden, mode):
                 assert fl == golden[key + "_flags"][0], key
                 c, _ = oracle.build_C_box(p, form, cfg, hexes[0], kind, None if coef is None else coef[0])
                 assert np.array_equal(bits(c), bits(golden[f"Chex_{mode}_f{form}_p{p}_k{kind}"]))
+                vkey = f"Vhex_{mode}_f{form}_p{p}_k{kind}"
+                v, vfl = oracle.action_box(p, form, cfg, hexes[4:6], golden[vkey + "_w"], kind, coef)
+                assert np.array_equal(bits(v), bits(golden[vkey])), vkey
+                assert vfl == golden[vkey + "_flags"][0], vkey
                 if p <= 2:
                     b, a64 = oracle.bound_box(p, form, cfg, hexes[3], kind, None if coef is None else coef[1])
                     assert np.array_equal(bits(b), bits(golden[f"boundhex_{mode}_f{form}_p{p}_k{kind}"]))
