@@ -58,6 +58,8 @@ struct ActionParams {
   int64_t out_pitch;
   uint32_t* flags;
   int* error;
+  int box;               // hexahedra: geometry at every rule point
+  const double* ggrad;   // box: degree-1 gradients at u_g, (s * 8 + k) * n_q + q
 };
 
 constexpr int kActionThreads = 256;
@@ -159,7 +161,7 @@ static __device__ __noinline__ bool action_geometry(const double v[4][3], bool p
 //   sWH  [s n_q + q][C]  double  what at u_g
 //   sR   [s n_q + q][C]  TQ      r at u_s (exact in the u_q compute type)
 //   sGeo [C][18]         double  G (6: G00 G01 G02 G11 G12 G22 / |det|), 2v0x 2v0y v0z, edges
-constexpr int kGeoWords = 18;
+constexpr int kGeoWords = 24;  // tets: G (6), 2v0x 2v0y v0z, edges (9); boxes: 8 vertices
 
 template <int A>
 __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q, int n_d) {
@@ -172,10 +174,43 @@ __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q
                          kGeoWords * sizeof(double));
 }
 
+// Box cells: G at rule point q of a cell whose 8 vertices sit in geo (u_g runtime for the
+// generic instantiation). False on a zero pivot.
+template <int UGK>
+__device__ __forceinline__ bool box_g_at(const ActionParams& P, const double* geo, int q,
+                                         TetGeometry& g, uint32_t& fl) {
+  double vx[8][3], gq[3][8];
+  #pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    #pragma unroll
+    for (int a = 0; a < 3; ++a) vx[k][a] = geo[k * 3 + a];
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) gq[s][k] = P.ggrad[(size_t(s) * 8 + k) * P.n_q + q];
+  }
+  const bool poisson = P.n_d == 3;
+  if constexpr (UGK == kUg64) return box_point_geometry<kFP64>(vx, gq, poisson, g, fl);
+  else if constexpr (UGK == kUg32) return box_point_geometry<kFP32>(vx, gq, poisson, g, fl);
+  else {
+    switch (P.ug) {
+      case kFP64: return box_point_geometry<kFP64>(vx, gq, poisson, g, fl);
+      case kFP32: return box_point_geometry<kFP32>(vx, gq, poisson, g, fl);
+      case kFP16: return box_point_geometry<kFP16>(vx, gq, poisson, g, fl);
+      default: return box_point_geometry<kBF16>(vx, gq, poisson, g, fl);
+    }
+  }
+}
+
 // One cell's geometry row at u_g: G (6, upper triangle; mass: |det|), then K1's coefficient
 // inputs (2 v0x, 2 v0y, v0z and the edges with x, y doubled).
 __device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell, double* geo,
                                              uint32_t& fl) {
+  if (P.box) {  // hexahedra: the vertices; the geometry is evaluated per point in the r stage
+    for (int k = 0; k < 8; ++k) {
+      const int64_t base = P.cells ? int64_t(P.cells[cell * 8 + k]) * 3 : cell * 24 + k * 3;
+      for (int a = 0; a < 3; ++a) geo[k * 3 + a] = P.verts[base + a];
+    }
+    return;
+  }
   double v[4][3];
   #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -293,16 +328,29 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
       }
       double wt[3] = {0.0, 0.0, 0.0};  // read before r overwrites what (fp64: aliased)
       for (int t = 0; t < nd; ++t) wt[t] = sWH[size_t(t * nq + q) * C + c];
+      double gbox[6];
+      const double* gsrc = geo;
+      if (P.box) {  // hexahedra: the geometry at this rule point
+        TetGeometry tg;
+        if (c < nc && !box_g_at<UGK>(P, geo, q, tg, fl)) {
+          atomicExch(P.error, 3);
+          for (int b = 0; b < 6; ++b) tg.g[b] = 0.0;
+        } else if (c >= nc) {
+          for (int b = 0; b < 6; ++b) tg.g[b] = 0.0;
+        }
+        for (int b = 0; b < 6; ++b) gbox[b] = tg.g[b];
+        gsrc = gbox;
+      }
       for (int s = 0; s < nd; ++s) {
         double t1 = 0.0;
         if (poisson) {
           #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int gi = s <= t ? (s * (5 - s)) / 2 + t : (t * (5 - t)) / 2 + s;  // upper-tri index
-            t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[gi], wt[t], P.ug, fl), P.ug, fl);
+            t1 = ug_add<UGK>(t1, ug_mul<UGK>(gsrc[gi], wt[t], P.ug, fl), P.ug, fl);
           }
         } else {
-          t1 = ug_add<UGK>(t1, ug_mul<UGK>(geo[0], wt[0], P.ug, fl), P.ug, fl);
+          t1 = ug_add<UGK>(t1, ug_mul<UGK>(gsrc[0], wt[0], P.ug, fl), P.ug, fl);
         }
         double m1 = ug_mul<UGK>(om, t1, P.ug, fl);
         if (have_z) m1 = ug_mul<UGK>(m1, zq, P.ug, fl);

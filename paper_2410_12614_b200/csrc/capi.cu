@@ -647,7 +647,7 @@ void prepare_action(mpfem_b200_setup_s& S) {
   if (ap != aq) ap = aq = kArGen;
   if (ap == S.act_ap) return;
   uint32_t fl = 0;
-  const Basis basis = simplex_basis(S.p);
+  const Basis basis = S.box ? box_basis(S.p) : simplex_basis(S.p);
   const std::vector<double> tab = tabulate(basis, S.rule, S.up, S.us, S.form == 1, fl);
   const int nphi = S.n_phi, nq = S.n_q, nd = S.n_d, n1 = nd * nq;
   std::vector<double> a(size_t(nphi) * n1), c(size_t(n1) * nphi);
@@ -678,7 +678,6 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   if (n > 0 && (!verts || !w || !out)) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
   if (out_pitch < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
-  if (S.box) throw Error(MPFEM_B200_CONFIG_ERROR, "the action kernel supports tetrahedra");
   prepare_action(S);
   S.last_launches = 0;
   if (flags) {
@@ -708,6 +707,8 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
     P.uq = S.uq;
     P.us = S.us;
     P.ftz = S.engine == 2;
+    P.box = S.box;
+    P.ggrad = static_cast<const double*>(S.d_ggrad.p);
     P.out = out;
     P.out_pitch = out_pitch;
     P.flags = static_cast<uint32_t*>(S.d_flags.p);
@@ -1060,13 +1061,14 @@ int mpfem_b200_action_host(mpfem_b200_setup_t S, const double* verts, int64_t n_
     check_coef(*S, coef_kind, coef, coef_stride);  // host path: per-cell rows only
     if (w_stride < S->n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 12);
+    const int nv = S->box ? 8 : 4;
+    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 3 * nv);
     S->h_verts.ensure(vbytes + 8);
     CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
     const int32_t* dcells = nullptr;
     if (cells) {
-      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * 4 + 8);
-      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * 4,
+      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * nv + 8);
+      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * nv,
                               cudaMemcpyHostToDevice, st));
       dcells = static_cast<const int32_t*>(S->h_cells.p);
     }

@@ -8,6 +8,7 @@
 #include <cuda_fp16.h>
 
 #include <cstdint>
+#include <type_traits>
 
 namespace mpfem_b200 {
 
@@ -452,6 +453,157 @@ __device__ __noinline__ bool tet_geometry_flagged(const double v[4][3], bool poi
     }
   }
   return jac_geometry_flagged<F>(jac, poisson, out, fl);
+}
+
+// Native-precision twin of the geometry sequence for u_g = fp32 / fp64: IEEE fp32 / fp64
+// +,-,*,/ (explicit _rn intrinsics, no contraction) are the correctly rounded results the
+// emulation computes, so the values are bit-identical (as tet_geometry_f32 / _f64_fast).
+// Returns false on a zero pivot or any non-finite value; the caller then reruns the flagged
+// emulation, which also produces the reference's FP flags for those events.
+template <typename F> struct NativeOps;
+template <> struct NativeOps<float> {
+  __device__ static float add(float a, float b) { return __fadd_rn(a, b); }
+  __device__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+  __device__ static float mul(float a, float b) { return __fmul_rn(a, b); }
+  __device__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+};
+template <> struct NativeOps<double> {
+  __device__ static double add(double a, double b) { return __dadd_rn(a, b); }
+  __device__ static double sub(double a, double b) { return __dsub_rn(a, b); }
+  __device__ static double mul(double a, double b) { return __dmul_rn(a, b); }
+  __device__ static double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+
+template <typename F>
+__device__ __forceinline__ bool box_geometry_native(const F jac[3][3], bool poisson, TetGeometry& out) {
+  using O = NativeOps<F>;
+  F lu[3][3];
+  int perm[3] = {0, 1, 2};
+  int sign = 1;
+  bool finite = true;
+  #pragma unroll
+  for (int i = 0; i < 3; ++i)
+    #pragma unroll
+    for (int s = 0; s < 3; ++s) lu[i][s] = jac[i][s];
+  #pragma unroll
+  for (int col = 0; col < 3; ++col) {
+    int pivot = col;
+    F best = fabs(lu[col][col]);
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (fabs(lu[r][col]) > best) { best = fabs(lu[r][col]); pivot = r; }
+    F pv = lu[col][col];
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (pivot == r) pv = lu[r][col];
+    if (pv == F(0)) return false;
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r)
+      if (pivot == r) {
+        #pragma unroll
+        for (int c = 0; c < 3; ++c) { const F t = lu[r][c]; lu[r][c] = lu[col][c]; lu[col][c] = t; }
+        const int t = perm[r]; perm[r] = perm[col]; perm[col] = t;
+        sign = -sign;
+      }
+    #pragma unroll
+    for (int r = col + 1; r < 3; ++r) {
+      const F m = O::div(lu[r][col], lu[col][col]);
+      lu[r][col] = m;
+      #pragma unroll
+      for (int c = col + 1; c < 3; ++c) lu[r][c] = O::sub(lu[r][c], O::mul(m, lu[col][c]));
+    }
+  }
+  F det = F(sign);
+  #pragma unroll
+  for (int i = 0; i < 3; ++i) det = O::mul(det, lu[i][i]);
+  finite = finite && isfinite(det);
+  const F adet = fabs(det);
+  out.det = double(det);
+  out.abs_det = double(adet);
+  if (!poisson) {
+    out.g[0] = double(adet);
+    return finite;
+  }
+  F inv[3][3];
+  #pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    F y[3];
+    #pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      F s = perm[r] == k ? F(1) : F(0);
+      #pragma unroll
+      for (int c = 0; c < r; ++c) s = O::sub(s, O::mul(lu[r][c], y[c]));
+      y[r] = s;
+    }
+    #pragma unroll
+    for (int r = 2; r >= 0; --r) {
+      F s = y[r];
+      #pragma unroll
+      for (int c = r + 1; c < 3; ++c) s = O::sub(s, O::mul(lu[r][c], inv[c][k]));
+      inv[r][k] = O::div(s, lu[r][r]);
+    }
+  }
+  int idx = 0;
+  #pragma unroll
+  for (int s = 0; s < 3; ++s)
+    #pragma unroll
+    for (int t = s; t < 3; ++t) {
+      F dot = F(0);
+      #pragma unroll
+      for (int k = 0; k < 3; ++k) dot = O::add(dot, O::mul(inv[s][k], inv[t][k]));
+      const F g = O::mul(adet, dot);
+      finite = finite && isfinite(g);
+      out.g[idx++] = double(g);
+    }
+  return finite;
+}
+
+// Geometry of a box cell at one rule point (geometry.cpp:12-27,190-221) at u_g = UG: J from the
+// 8 vertices and the u_g gradients of the degree-1 box basis at that point (gq[s][k]), then LU,
+// det, inverse and G. Native _rn arithmetic for fp32 / fp64 (bitwise the emulation's values),
+// the flagged emulation for other formats and rare events. False on a zero pivot.
+template <int UG>
+__device__ __forceinline__ bool box_point_geometry(const double vx[8][3], const double gq[3][8],
+                                                   bool poisson, TetGeometry& geo, uint32_t& fl) {
+  bool done = false;
+  if constexpr (UG == kFP32 || UG == kFP64) {
+    using F = typename std::conditional<UG == kFP32, float, double>::type;
+    using O = NativeOps<F>;
+    F jn[3][3];
+    bool fin = true;
+    #pragma unroll
+    for (int i = 0; i < 3; ++i)
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) jn[i][s] = F(0);
+    #pragma unroll
+    for (int k = 0; k < 8; ++k)
+      #pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const F x = F(vx[k][i]);  // one RNE rounding to u_g (exact for u_g = fp64)
+        // tiny (fp32-subnormal) or non-finite inputs take the flagged path for exact flags
+        fin = fin && isfinite(x) && (UG == kFP64 || vx[k][i] == 0.0 || fabs(vx[k][i]) >= 0x1.0p-126);
+        #pragma unroll
+        for (int s = 0; s < 3; ++s) jn[i][s] = O::add(jn[i][s], O::mul(x, F(gq[s][k])));
+      }
+    done = fin && box_geometry_native<F>(jn, poisson, geo);
+  }
+  if (!done) {  // flagged emulation: rare events (zero pivot, non-finite, subnormal inputs)
+    double jac[3][3];
+    #pragma unroll
+    for (int i = 0; i < 3; ++i)
+      #pragma unroll
+      for (int s = 0; s < 3; ++s) jac[i][s] = 0.0;
+    #pragma unroll 1
+    for (int k = 0; k < 8; ++k)
+      #pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double x = droundT<UG>(vx[k][i], fl);
+        #pragma unroll
+        for (int s = 0; s < 3; ++s) jac[i][s] = daddT<UG>(jac[i][s], dmulT<UG>(x, gq[s][k], fl), fl);
+      }
+    return jac_geometry_flagged<UG>(jac, poisson, geo, fl);
+  }
+  return true;
 }
 
 // u_g = fp32: the same op sequence in native fp32 arithmetic. IEEE fp32 +,-,*,/ are the

@@ -138,3 +138,28 @@ def test_box_bounds_bitwise(oracle, hexes, mode, form):
     b, a64 = s.cell_bounds(dev(hx), want_a64=True)
     err = (a - a64).abs().amax(dim=(1, 2)) / a64.abs().amax(dim=(1, 2))
     assert float((err / (S * b[:, 0])).max()) <= 1.0
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_box_action_bitwise(oracle, hexes, mode, form):
+    """Algorithm 2 on hexahedra (geometry at every rule point in the r stage): bitwise the
+    reference's action_kernel (oracle restatement pinned to ref_action_box), p = 1..3."""
+    verts, cells, hx = hexes
+    rng = np.random.default_rng(21 + form)
+    up, ug, uq, us, eng = MODES[mode]
+    cfg = mp.KernelConfig(form=mp.FormKind(form), mode=mp.ModeKind.action, u_p=mp.Fmt(up),
+                          u_g=mp.Fmt(ug), u_q=mp.Fmt(uq), u_s=mp.Fmt(us), engine=mp.EngineKind(eng))
+    for p in (1, 2, 3):
+        s = mp.make_setup(p, cfg, cell_kind=1)
+        n = 9
+        w = rng.uniform(-1, 1, size=(n, s.n_phi))
+        for kind in (COEF_ONE, COEF_NODAL):
+            z = rng.uniform(0.5, 1.5, size=(n, s.n_phi)) if kind == COEF_NODAL else None
+            v = mp.action_kernel(s, dev(hx[:n]), dev(w), coef_kind=kind, coef=None if z is None else dev(z))
+            ref, _ = oracle.action_box(p, form, cfg_tuple(cfg), hx[:n], w, kind, z)
+            got = v.double().cpu().numpy()
+            assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (mode, form, p, kind)
+    vm = s.action(dev(verts), dev(rng.uniform(-1, 1, size=(cells.shape[0], s.n_phi))),
+                  cells=dev(cells, torch.int32))
+    assert torch.isfinite(vm).all()
