@@ -179,11 +179,13 @@ def run_reference(args, rank, world):
     cfg = (MIXED_CFG["u_p"], MIXED_CFG["u_g"], MIXED_CFG["u_q"], MIXED_CFG["u_s"], MIXED_CFG["engine"])
     rates = []
     info = None
+    # each step is a bounded prefix sample sized so the whole K + W run stays near 2.5 minutes
+    per_step = max(0.2, min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=2.0)
+        cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=per_step)
     t_all = time.perf_counter()
     for _ in range(args.steps):
-        r, kind, cores, sample = cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=args.ref_seconds)
+        r, kind, cores, sample = cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=per_step)
         rates.append(r)
         info = (kind, cores, sample)
     wall = time.perf_counter() - t_all
