@@ -30,9 +30,13 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
   uint32_t fl = 0;
   T* W = static_cast<T*>(P.W);
   const int64_t items = P.n_cells * P.nq_pad;
+  extern __shared__ double s_gg[];  // the u_g gradient table, (s * 8 + k) * n_q + q
+  for (int e = threadIdx.x; e < 24 * P.n_q; e += blockDim.x) s_gg[e] = P.ggrad[e];
+  __syncthreads();
   for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items;
        it += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t cell = it / P.nq_pad;
+    // 32-bit division while the item index fits (64-bit division is a long software sequence)
+    const int64_t cell = items < (int64_t(1) << 31) ? int64_t(uint32_t(it) / uint32_t(P.nq_pad)) : it / P.nq_pad;
     const int q = int(it - cell * P.nq_pad);
     T* wrow = W + cell * P.k_pad;
     if (q == 0)
@@ -48,7 +52,7 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
       #pragma unroll
       for (int i = 0; i < 3; ++i) vx[k][i] = P.verts[base + i];
       #pragma unroll
-      for (int s = 0; s < 3; ++s) gq[s][k] = P.ggrad[(size_t(s) * 8 + k) * P.n_q + q];
+      for (int s = 0; s < 3; ++s) gq[s][k] = s_gg[(s * 8 + k) * P.n_q + q];
     }
     TetGeometry geo;
     if (!box_point_geometry<UG>(vx, gq, P.poisson != 0, geo, fl)) {
@@ -77,11 +81,12 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
 
 template <typename T>
 void launch_ug(const GeomBoxParams& P, unsigned grid, cudaStream_t st) {
+  const size_t smem = sizeof(double) * 24 * size_t(P.n_q);  // <= 24 KB for p <= 4
   switch (P.ug) {
-    case kFP64: geom_w_box_kernel<T, kFP64><<<grid, 128, 0, st>>>(P); break;
-    case kFP32: geom_w_box_kernel<T, kFP32><<<grid, 128, 0, st>>>(P); break;
-    case kFP16: geom_w_box_kernel<T, kFP16><<<grid, 128, 0, st>>>(P); break;
-    default: geom_w_box_kernel<T, kBF16><<<grid, 128, 0, st>>>(P); break;
+    case kFP64: geom_w_box_kernel<T, kFP64><<<grid, 128, smem, st>>>(P); break;
+    case kFP32: geom_w_box_kernel<T, kFP32><<<grid, 128, smem, st>>>(P); break;
+    case kFP16: geom_w_box_kernel<T, kFP16><<<grid, 128, smem, st>>>(P); break;
+    default: geom_w_box_kernel<T, kBF16><<<grid, 128, smem, st>>>(P); break;
   }
 }
 
