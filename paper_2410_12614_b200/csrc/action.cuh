@@ -160,10 +160,14 @@ static __device__ __noinline__ bool action_geometry(const double v[4][3], bool p
 //   sWm  [k][C]          TP      round_us(w)
 //   sWH  [s n_q + q][C]  double  what at u_g
 //   sR   [s n_q + q][C]  TQ      r at u_s (exact in the u_q compute type)
-//   sGeo [C][18]         double  G (6: G00 G01 G02 G11 G12 G22 / |det|), 2v0x 2v0y v0z, edges
-constexpr int kGeoWords = 24;  // tets: G (6), 2v0x 2v0y v0z, edges (9); boxes: 8 vertices
+//   sGeo [C][18 | 24]    double  tets: G (6: G00 G01 G02 G11 G12 G22 / |det|), 2v0x 2v0y v0z,
+//                                edges; boxes: the 8 vertices
+// The row width is per cell kind (BOX is a template parameter, so the tet kernel carries
+// none of the per-point box geometry: registers / stack / shared memory as before 8f.3).
+template <bool BOX>
+constexpr int geo_words() { return BOX ? 24 : 18; }
 
-template <int A>
+template <int A, bool BOX>
 __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q, int n_d) {
   using T = typename Arith<A>::T;
   const size_t n1 = size_t(n_d) * n_q;
@@ -171,7 +175,7 @@ __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q
   // before writing its r values), so fp64 compute types need one n1 array per cell
   const size_t r_bytes = sizeof(T) == 8 ? 0 : sizeof(T);
   return size_t(tile) * (size_t(n_phi) * sizeof(T) + n1 * (sizeof(double) + r_bytes) +
-                         kGeoWords * sizeof(double));
+                         geo_words<BOX>() * sizeof(double));
 }
 
 // Box cells: G at rule point q of a cell whose 8 vertices sit in geo (u_g runtime for the
@@ -202,9 +206,10 @@ __device__ __forceinline__ bool box_g_at(const ActionParams& P, const double* ge
 
 // One cell's geometry row at u_g: G (6, upper triangle; mass: |det|), then K1's coefficient
 // inputs (2 v0x, 2 v0y, v0z and the edges with x, y doubled).
+template <bool BOX>
 __device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell, double* geo,
                                              uint32_t& fl) {
-  if (P.box) {  // hexahedra: the vertices; the geometry is evaluated per point in the r stage
+  if constexpr (BOX) {  // hexahedra: the vertices; the geometry is evaluated per point in the r stage
     for (int k = 0; k < 8; ++k) {
       const int64_t base = P.cells ? int64_t(P.cells[cell * 8 + k]) * 3 : cell * 24 + k * 3;
       for (int a = 0; a < 3; ++a) geo[k * 3 + a] = P.verts[base + a];
@@ -247,8 +252,9 @@ __device__ __forceinline__ void load_cb(const T* p, T (&v)[N]) {
   }
 }
 
-template <int A, bool FTZ, int UGK>
+template <int A, bool FTZ, int UGK, bool BOX>
 __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionParams P) {
+  constexpr int kGeoWords = geo_words<BOX>();
   using T = typename Arith<A>::T;
   using Ar = Arith<A>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
     const int nc = int((P.n_cells - c0 < int64_t(C) ? P.n_cells - c0 : int64_t(C)));
     // -- stage: geometry (one thread per cell) and the u_s-rounded w
     for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      if (c < nc) cell_geo_row(P, c0 + c, sGeo + c * kGeoWords, fl);
+      if (c < nc) cell_geo_row<BOX>(P, c0 + c, sGeo + c * kGeoWords, fl);
       else for (int j = 0; j < kGeoWords; ++j) sGeo[c * kGeoWords + j] = 0.0;
     }
     for (int e = threadIdx.x; e < C * nphi; e += blockDim.x) {
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
       for (int t = 0; t < nd; ++t) wt[t] = sWH[size_t(t * nq + q) * C + c];
       double gbox[6];
       const double* gsrc = geo;
-      if (P.box) {  // hexahedra: the geometry at this rule point
+      if constexpr (BOX) {  // hexahedra: the geometry at this rule point
         TetGeometry tg;
         if (c < nc && !box_g_at<UGK>(P, geo, q, tg, fl)) {
           atomicExch(P.error, 3);
