@@ -183,14 +183,8 @@ __host__ __device__ inline size_t action_smem_bytes(int tile, int n_phi, int n_q
 template <int UGK>
 __device__ __forceinline__ bool box_g_at(const ActionParams& P, const double* geo, int q,
                                          TetGeometry& g, uint32_t& fl) {
-  double vx[8][3], gq[3][8];
-  #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    #pragma unroll
-    for (int a = 0; a < 3; ++a) vx[k][a] = geo[k * 3 + a];
-    #pragma unroll
-    for (int s = 0; s < 3; ++s) gq[s][k] = P.ggrad[(size_t(s) * 8 + k) * P.n_q + q];
-  }
+  auto vx = [&](int k, int a) { return geo[k * 3 + a]; };
+  auto gq = [&](int s, int k) { return P.ggrad[(size_t(s) * 8 + k) * P.n_q + q]; };
   const bool poisson = P.n_d == 3;
   if constexpr (UGK == kUg64) return box_point_geometry<kFP64>(vx, gq, poisson, g, fl);
   else if constexpr (UGK == kUg32) return box_point_geometry<kFP32>(vx, gq, poisson, g, fl);

@@ -562,9 +562,13 @@ __device__ __forceinline__ bool box_geometry_native(const F jac[3][3], bool pois
 // 8 vertices and the u_g gradients of the degree-1 box basis at that point (gq[s][k]), then LU,
 // det, inverse and G. Native _rn arithmetic for fp32 / fp64 (bitwise the emulation's values),
 // the flagged emulation for other formats and rare events. False on a zero pivot.
-template <int UG>
-__device__ __forceinline__ bool box_point_geometry(const double vx[8][3], const double gq[3][8],
-                                                   bool poisson, TetGeometry& geo, uint32_t& fl) {
+// vx(k, i) and gq(s, k) read vertex coordinate i of vertex k and gradient component s of basis
+// function k: accessors instead of arrays, so the values are loaded where they are used and the
+// rare fallback reloads them (an [8][3] + [3][8] array kept live for it cost a 528-byte local
+// frame per thread, or 160 registers once its loop was unrolled).
+template <int UG, class VX, class GQ>
+__device__ __forceinline__ bool box_point_geometry(VX vx, GQ gq, bool poisson, TetGeometry& geo,
+                                                   uint32_t& fl) {
   bool done = false;
   if constexpr (UG == kFP32 || UG == kFP64) {
     using F = typename std::conditional<UG == kFP32, float, double>::type;
@@ -579,11 +583,12 @@ __device__ __forceinline__ bool box_point_geometry(const double vx[8][3], const 
     for (int k = 0; k < 8; ++k)
       #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const F x = F(vx[k][i]);  // one RNE rounding to u_g (exact for u_g = fp64)
+        const double xd = vx(k, i);
+        const F x = F(xd);  // one RNE rounding to u_g (exact for u_g = fp64)
         // tiny (fp32-subnormal) or non-finite inputs take the flagged path for exact flags
-        fin = fin && isfinite(x) && (UG == kFP64 || vx[k][i] == 0.0 || fabs(vx[k][i]) >= 0x1.0p-126);
+        fin = fin && isfinite(x) && (UG == kFP64 || xd == 0.0 || fabs(xd) >= 0x1.0p-126);
         #pragma unroll
-        for (int s = 0; s < 3; ++s) jn[i][s] = O::add(jn[i][s], O::mul(x, F(gq[s][k])));
+        for (int s = 0; s < 3; ++s) jn[i][s] = O::add(jn[i][s], O::mul(x, F(gq(s, k))));
       }
     done = fin && box_geometry_native<F>(jn, poisson, geo);
   }
@@ -597,9 +602,9 @@ __device__ __forceinline__ bool box_point_geometry(const double vx[8][3], const 
     for (int k = 0; k < 8; ++k)
       #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const double x = droundT<UG>(vx[k][i], fl);
+        const double x = droundT<UG>(vx(k, i), fl);
         #pragma unroll
-        for (int s = 0; s < 3; ++s) jac[i][s] = daddT<UG>(jac[i][s], dmulT<UG>(x, gq[s][k], fl), fl);
+        for (int s = 0; s < 3; ++s) jac[i][s] = daddT<UG>(jac[i][s], dmulT<UG>(x, gq(s, k), fl), fl);
       }
     return jac_geometry_flagged<UG>(jac, poisson, geo, fl);
   }

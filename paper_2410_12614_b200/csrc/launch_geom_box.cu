@@ -45,15 +45,12 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
       for (int b = 0; b < P.n_blocks; ++b) wrow[b * P.nq_pad + q] = T(0.0f);
       continue;
     }
-    double vx[8][3], gq[3][8];
-    #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t base = P.cells ? int64_t(P.cells[cell * 8 + k]) * 3 : cell * 24 + k * 3;
-      #pragma unroll
-      for (int i = 0; i < 3; ++i) vx[k][i] = P.verts[base + i];
-      #pragma unroll
-      for (int s = 0; s < 3; ++s) gq[s][k] = s_gg[(s * 8 + k) * P.n_q + q];
-    }
+    const int32_t* cv = P.cells ? P.cells + cell * 8 : nullptr;
+    const double* pv = P.verts + cell * 24;
+    auto vx = [&](int k, int i) {
+      return cv ? P.verts[int64_t(cv[k]) * 3 + i] : pv[k * 3 + i];
+    };
+    auto gq = [&](int s, int k) { return s_gg[(s * 8 + k) * P.n_q + q]; };
     TetGeometry geo;
     if (!box_point_geometry<UG>(vx, gq, P.poisson != 0, geo, fl)) {
       atomicExch(P.error, 3);
