@@ -25,13 +25,24 @@ __device__ __forceinline__ T to_w(double v) {
   else return T(float(v));  // v is already a u_s value: the conversion is exact
 }
 
+// u_s implied by the W element type (choose_path: fp16 / bf16 / fp32 W carry exactly that u_s;
+// fp64 W carries any u_s, rounded at run time)
+template <typename T> struct UsOf { static constexpr int v = -1; };
+template <> struct UsOf<__half> { static constexpr int v = kFP16; };
+template <> struct UsOf<__nv_bfloat16> { static constexpr int v = kBF16; };
+template <> struct UsOf<float> { static constexpr int v = kFP32; };
+
 template <typename T, int UG>
 __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) {
   uint32_t fl = 0;
   T* W = static_cast<T*>(P.W);
   const int64_t items = P.n_cells * P.nq_pad;
-  extern __shared__ double s_gg[];  // the u_g gradient table, (s * 8 + k) * n_q + q
-  for (int e = threadIdx.x; e < 24 * P.n_q; e += blockDim.x) s_gg[e] = P.ggrad[e];
+  // the u_g gradient table, (s * 8 + k) * n_q + q; held as float for u_g = fp32 (its values
+  // are fp32 numbers, so the narrowing is exact and the per-point F2F conversions go away)
+  using G = typename std::conditional<UG == kFP32, float, double>::type;
+  extern __shared__ double s_raw[];
+  G* s_gg = reinterpret_cast<G*>(s_raw);
+  for (int e = threadIdx.x; e < 24 * P.n_q; e += blockDim.x) s_gg[e] = G(P.ggrad[e]);
   __syncthreads();
   for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items;
        it += int64_t(gridDim.x) * blockDim.x) {
@@ -70,7 +81,8 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
     for (int b = 0; b < P.n_blocks; ++b) {
       double v = dmulT<UG>(om, geo.g[b], fl);
       if (have_z) v = dmulT<UG>(v, zq, fl);
-      wrow[b * P.nq_pad + q] = to_w<T>(round_us_rt(v, P.us, fl));
+      if constexpr (UsOf<T>::v >= 0) wrow[b * P.nq_pad + q] = to_w<T>(droundT<UsOf<T>::v>(v, fl));
+      else wrow[b * P.nq_pad + q] = to_w<T>(round_us_rt(v, P.us, fl));
     }
   }
   publish_flags(P.flags, fl);
