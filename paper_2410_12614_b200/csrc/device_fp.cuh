@@ -558,6 +558,14 @@ __device__ __forceinline__ bool box_geometry_native(const F jac[3][3], bool pois
   return finite;
 }
 
+// The input screen of the native path: x = round_ug(xd) finite and, for u_g = fp32, xd zero or
+// at least the smallest fp32 normal (tiny inputs take the flagged path for exact flags).
+template <int UG>
+__device__ __forceinline__ bool box_input_ok(double xd) {
+  if constexpr (UG == kFP32) return isfinite(float(xd)) && (xd == 0.0 || fabs(xd) >= 0x1.0p-126);
+  else return isfinite(xd);
+}
+
 // Geometry of a box cell at one rule point (geometry.cpp:12-27,190-221) at u_g = UG: J from the
 // 8 vertices and the u_g gradients of the degree-1 box basis at that point (gq[s][k]), then LU,
 // det, inverse and G. Native _rn arithmetic for fp32 / fp64 (bitwise the emulation's values),
@@ -566,15 +574,19 @@ __device__ __forceinline__ bool box_geometry_native(const F jac[3][3], bool pois
 // function k: accessors instead of arrays, so the values are loaded where they are used and the
 // rare fallback reloads them (an [8][3] + [3][8] array kept live for it cost a 528-byte local
 // frame per thread, or 160 registers once its loop was unrolled).
-template <int UG, class VX, class GQ>
-__device__ __forceinline__ bool box_point_geometry(VX vx, GQ gq, bool poisson, TetGeometry& geo,
-                                                   uint32_t& fl) {
+// Variant with the u_g-rounded coordinates supplied by the caller: xn(k, i) returns
+// F(vx(k, i)) (F = float / double for u_g = fp32 / fp64, else unused) and in_ok says every
+// input passed box_input_ok (finite after rounding, not fp32-subnormal); K1-box uses it to
+// round and screen each vertex once per warp instead of once per point.
+// With SCREEN the inputs are instead read, rounded and screened here (xn, in_ok unused).
+template <int UG, bool SCREEN = false, class XN, class VX, class GQ>
+__device__ __forceinline__ bool box_point_geometry_pre(XN xn, bool in_ok, VX vx, GQ gq, bool poisson,
+                                                       TetGeometry& geo, uint32_t& fl) {
   bool done = false;
   if constexpr (UG == kFP32 || UG == kFP64) {
     using F = typename std::conditional<UG == kFP32, float, double>::type;
     using O = NativeOps<F>;
     F jn[3][3];
-    bool fin = true;
     #pragma unroll
     for (int i = 0; i < 3; ++i)
       #pragma unroll
@@ -583,14 +595,18 @@ __device__ __forceinline__ bool box_point_geometry(VX vx, GQ gq, bool poisson, T
     for (int k = 0; k < 8; ++k)
       #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const double xd = vx(k, i);
-        const F x = F(xd);  // one RNE rounding to u_g (exact for u_g = fp64)
-        // tiny (fp32-subnormal) or non-finite inputs take the flagged path for exact flags
-        fin = fin && isfinite(x) && (UG == kFP64 || xd == 0.0 || fabs(xd) >= 0x1.0p-126);
+        F x;
+        if constexpr (SCREEN) {
+          const double xd = vx(k, i);
+          x = F(xd);  // one RNE rounding to u_g (exact for u_g = fp64)
+          in_ok = in_ok && box_input_ok<UG>(xd);
+        } else {
+          x = xn(k, i);
+        }
         #pragma unroll
         for (int s = 0; s < 3; ++s) jn[i][s] = O::add(jn[i][s], O::mul(x, F(gq(s, k))));
       }
-    done = fin && box_geometry_native<F>(jn, poisson, geo);
+    done = in_ok && box_geometry_native<F>(jn, poisson, geo);
   }
   if (!done) {  // flagged emulation: rare events (zero pivot, non-finite, subnormal inputs)
     double jac[3][3];
@@ -609,6 +625,13 @@ __device__ __forceinline__ bool box_point_geometry(VX vx, GQ gq, bool poisson, T
     return jac_geometry_flagged<UG>(jac, poisson, geo, fl);
   }
   return true;
+}
+
+template <int UG, class VX, class GQ>
+__device__ __forceinline__ bool box_point_geometry(VX vx, GQ gq, bool poisson, TetGeometry& geo,
+                                                   uint32_t& fl) {
+  auto xn = [](int, int) { return 0.0; };  // unused with SCREEN
+  return box_point_geometry_pre<UG, true>(xn, true, vx, gq, poisson, geo, fl);
 }
 
 // u_g = fp32: the same op sequence in native fp32 arithmetic. IEEE fp32 +,-,*,/ are the

@@ -44,26 +44,47 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
   G* s_gg = reinterpret_cast<G*>(s_raw);
   for (int e = threadIdx.x; e < 24 * P.n_q; e += blockDim.x) s_gg[e] = G(P.ggrad[e]);
   __syncthreads();
+  using F = typename std::conditional<UG == kFP32, float, double>::type;
+  const bool warp_cell = UG == kFP32 && (P.nq_pad & 31) == 0;
+  const int lane = threadIdx.x & 31;
   for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items;
        it += int64_t(gridDim.x) * blockDim.x) {
     // 32-bit division while the item index fits (64-bit division is a long software sequence)
     const int64_t cell = items < (int64_t(1) << 31) ? int64_t(uint32_t(it) / uint32_t(P.nq_pad)) : it / P.nq_pad;
     const int q = int(it - cell * P.nq_pad);
     T* wrow = W + cell * P.k_pad;
-    if (q == 0)
-      for (int64_t e = P.k; e < P.k_pad; ++e) wrow[e] = T(0.0f);
-    if (q >= P.n_q) {
-      for (int b = 0; b < P.n_blocks; ++b) wrow[b * P.nq_pad + q] = T(0.0f);
-      continue;
-    }
     const int32_t* cv = P.cells ? P.cells + cell * 8 : nullptr;
     const double* pv = P.verts + cell * 24;
     auto vx = [&](int k, int i) {
       return cv ? P.verts[int64_t(cv[k]) * 3 + i] : pv[k * 3 + i];
     };
-    auto gq = [&](int s, int k) { return s_gg[(s * 8 + k) * P.n_q + q]; };
+    // Warp-cooperative vertices (u_g = fp32, nq_pad a multiple of 32, so the warp's 32 items are
+    // points of one cell and the loop trip count is warp-uniform): lane l < 24 loads, rounds and
+    // screens coordinate l once and the native path takes it by shuffle. Every lane, padding
+    // points included (at the clamped point n_q - 1, results discarded), runs the geometry so
+    // that the shuffles see the full warp.
     TetGeometry geo;
-    if (!box_point_geometry<UG>(vx, gq, P.poisson != 0, geo, fl)) {
+    bool geo_ok;
+    const bool pad = q >= P.n_q;
+    const int qg = pad ? P.n_q - 1 : q;
+    auto gq = [&](int s, int k) { return s_gg[(s * 8 + k) * P.n_q + qg]; };
+    if (warp_cell) {
+      const int l = lane < 24 ? lane : 0;
+      const double xd = vx(l / 3, l % 3);
+      const F xl = F(xd);
+      const bool in_ok = __all_sync(0xffffffffu, box_input_ok<UG>(xd));
+      auto xn = [&](int k, int i) { return __shfl_sync(0xffffffffu, xl, k * 3 + i); };
+      geo_ok = box_point_geometry_pre<UG>(xn, in_ok, vx, gq, P.poisson != 0, geo, fl);
+    } else if (!pad) {
+      geo_ok = box_point_geometry<UG>(vx, gq, P.poisson != 0, geo, fl);
+    }
+    if (q == 0)
+      for (int64_t e = P.k; e < P.k_pad; ++e) wrow[e] = T(0.0f);
+    if (pad) {
+      for (int b = 0; b < P.n_blocks; ++b) wrow[b * P.nq_pad + q] = T(0.0f);
+      continue;
+    }
+    if (!geo_ok) {
       atomicExch(P.error, 3);
       #pragma unroll
       for (int b = 0; b < 6; ++b) geo.g[b] = 0.0;

@@ -163,3 +163,34 @@ def test_box_action_bitwise(oracle, hexes, mode, form):
     vm = s.action(dev(verts), dev(rng.uniform(-1, 1, size=(cells.shape[0], s.n_phi))),
                   cells=dev(cells, torch.int32))
     assert torch.isfinite(vm).all()
+
+
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_box_scaled_weights_rare_inputs_bitwise(oracle, hexes, form):
+    """K1-box's fp32-u_g fast paths (per-point inputs for p = 1, warp-shared vertices for
+    nq_pad % 32 == 0) screen each vertex and fall back to the flagged emulation for
+    fp32-subnormal coordinates and for geometry that overflows fp32: W and the batch's FP flags
+    bitwise the reference's."""
+    _, _, hx = hexes
+    cells = np.array(hx[:6], dtype=np.float64)
+    cells[1, 3, 0] = 1e-40          # fp32-subnormal coordinate
+    cells[2, 5, 2] = -3e-39         # fp32-subnormal, negative
+    cells[3] *= 1e30                # det and G overflow fp32
+    cells[4] *= 1e-30               # G underflows fp32
+    cfg = kconfig("mixed", form)
+    nd = 3 if form == POISSON else 1
+    blocks = PACK if form == POISSON else [(0, 0)]
+    for p in (1, 2, 3):
+        s = mp.make_setup(p, cfg, cell_kind=1)
+        n, nq = cells.shape[0], (p + 1) ** 3
+        w, fl = s.scaled_weights(dev(cells), None, COEF_ONE, None)
+        nqp = s.k // len(blocks)
+        w = np.ascontiguousarray(w.cpu().numpy().reshape(n, len(blocks), nqp)[:, :, :nq]).reshape(n, -1)
+        want_fl = 0
+        for c in range(n):
+            ref, f = oracle.build_C_box(p, form, cfg_tuple(cfg), cells[c], COEF_ONE, None)
+            want_fl |= f
+            ref = ref.reshape(nd, nd, nq)
+            want = np.concatenate([ref[a, b] for a, b in blocks])
+            assert np.array_equal(w[c].view(np.uint64), want.view(np.uint64)), (form, p, c)
+        assert fl == want_fl, (form, p, fl, want_fl)
