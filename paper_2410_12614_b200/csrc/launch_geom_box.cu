@@ -45,10 +45,19 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
   for (int e = threadIdx.x; e < 24 * P.n_q; e += blockDim.x) s_gg[e] = G(P.ggrad[e]);
   __syncthreads();
   using F = typename std::conditional<UG == kFP32, float, double>::type;
-  const bool warp_cell = UG == kFP32 && (P.nq_pad & 31) == 0;
+  // Warp-shared vertices need every lane of a warp on cells that start at a lane multiple of
+  // min(nq_pad, 32): nq_pad a multiple of 32, or 8 / 16 (4 / 2 cells per warp). The item loop
+  // then runs to a multiple of 32 so its trip count is warp-uniform; lanes past the last item
+  // replay the last item's geometry and store nothing.
+  const int grp = P.nq_pad >= 32 ? 32 : P.nq_pad;
+  const bool warp_cell = UG == kFP32 && (P.nq_pad % 32 == 0 || grp == 8 || grp == 16);
   const int lane = threadIdx.x & 31;
-  for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items;
-       it += int64_t(gridDim.x) * blockDim.x) {
+  const int src0 = lane & ~(grp - 1);  // lane of the cell's first item (when warp_cell)
+  const int64_t items_loop = warp_cell ? (items + 31) / 32 * 32 : items;
+  for (int64_t it_raw = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it_raw < items_loop;
+       it_raw += int64_t(gridDim.x) * blockDim.x) {
+    const bool live = it_raw < items;
+    const int64_t it = live ? it_raw : items - 1;
     // 32-bit division while the item index fits (64-bit division is a long software sequence)
     const int64_t cell = items < (int64_t(1) << 31) ? int64_t(uint32_t(it) / uint32_t(P.nq_pad)) : it / P.nq_pad;
     const int q = int(it - cell * P.nq_pad);
@@ -68,16 +77,34 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
     const bool pad = q >= P.n_q;
     const int qg = pad ? P.n_q - 1 : q;
     auto gq = [&](int s, int k) { return s_gg[(s * 8 + k) * P.n_q + qg]; };
-    if (warp_cell) {
+    if (warp_cell && grp == 32) {
+      // one cell per warp: lane l < 24 holds coordinate l
       const int l = lane < 24 ? lane : 0;
       const double xd = vx(l / 3, l % 3);
       const F xl = F(xd);
       const bool in_ok = __all_sync(0xffffffffu, box_input_ok<UG>(xd));
       auto xn = [&](int k, int i) { return __shfl_sync(0xffffffffu, xl, k * 3 + i); };
       geo_ok = box_point_geometry_pre<UG>(xn, in_ok, vx, gq, P.poisson != 0, geo, fl);
+    } else if (warp_cell) {
+      // 2 or 4 cells per warp: lane src0 + k holds vertex k of the lane's cell (three
+      // coordinates); a tiny or non-finite coordinate anywhere in the warp sends the whole warp
+      // to the exact fallback
+      const int kv = (lane - src0) & 7;
+      F xl[3];
+      bool ok = true;
+      #pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double xd = vx(kv, i);
+        xl[i] = F(xd);
+        ok = ok && box_input_ok<UG>(xd);
+      }
+      const bool in_ok = __all_sync(0xffffffffu, ok);
+      auto xn = [&](int k, int i) { return __shfl_sync(0xffffffffu, xl[i], src0 + k); };
+      geo_ok = box_point_geometry_pre<UG>(xn, in_ok, vx, gq, P.poisson != 0, geo, fl);
     } else if (!pad) {
       geo_ok = box_point_geometry<UG>(vx, gq, P.poisson != 0, geo, fl);
     }
+    if (!live) continue;
     if (q == 0)
       for (int64_t e = P.k; e < P.k_pad; ++e) wrow[e] = T(0.0f);
     if (pad) {
