@@ -171,7 +171,7 @@ static_assert(kWAlign % kQPT == 0 && kQPT % 2 == 0, "points per thread must divi
 #define MPFEM_K1_TILE 32
 #endif
 #ifndef MPFEM_K1_MINB
-#define MPFEM_K1_MINB 4
+#define MPFEM_K1_MINB 3  // 3 CTAs/SM (85 registers): K1 75.8 -> 73.7 us at config 1 (r1j A/B)
 #endif
 constexpr int kTileCells = MPFEM_K1_TILE;
 constexpr int kGeomThreads = 256;
