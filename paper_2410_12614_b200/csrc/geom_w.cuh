@@ -162,7 +162,7 @@ struct __align__(16) CellGeo {
 };
 
 #ifndef MPFEM_K1_QPT
-#define MPFEM_K1_QPT 4
+#define MPFEM_K1_QPT 8  // 8 points per item (more independent fp64 chains per thread): with MINB 2, K1 73.7 -> 64.5 us at config 1 (r1j A/B)
 #endif
 constexpr int kWAlign = 8;             // W / T block stride: nq_pad = round_up(n_q, kWAlign)
 constexpr int kQPT = MPFEM_K1_QPT;      // quadrature points per thread (divides kWAlign)
@@ -171,7 +171,7 @@ static_assert(kWAlign % kQPT == 0 && kQPT % 2 == 0, "points per thread must divi
 #define MPFEM_K1_TILE 32
 #endif
 #ifndef MPFEM_K1_MINB
-#define MPFEM_K1_MINB 3  // 3 CTAs/SM (85 registers): K1 75.8 -> 73.7 us at config 1 (r1j A/B)
+#define MPFEM_K1_MINB 2  // 2 CTAs/SM (128 registers, room for the 8-point items; r1j A/B)
 #endif
 constexpr int kTileCells = MPFEM_K1_TILE;
 constexpr int kGeomThreads = 256;
