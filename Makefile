@@ -41,13 +41,7 @@ diag: $(OBJS)
 	$(NVCC) $(NVFLAGS) -DMPFEM_TC2_NOSTORE -c -o $(PKG)/lib/diag/capi.o $(PKG)/csrc/capi.cu 2> /dev/null
 	$(NVCC) $(ARCH) -shared -o $(DIAG_LIB) $(PKG)/lib/diag/capi.o $(filter-out $(OBJDIR)/capi.o,$(OBJS))
 
-# Diagnostic variants for the concurrent K1/K2 study: K2 without MMAs / without stores.
-diag2: $(OBJS)
-	@mkdir -p $(PKG)/lib/diag
-	$(NVCC) $(NVFLAGS) -DMPFEM_TC2_NOMMA -c -o $(PKG)/lib/diag/capi_nomma.o $(PKG)/csrc/capi.cu 2> /dev/null
-	$(NVCC) $(ARCH) -shared -o $(PKG)/lib/diag/libmpfem_b200_nomma.so $(PKG)/lib/diag/capi_nomma.o $(filter-out $(OBJDIR)/capi.o,$(OBJS))
-
 clean:
 	rm -rf $(LIB) $(OBJDIR)
 
-.PHONY: all oracle clean diag diag2
+.PHONY: all oracle clean diag

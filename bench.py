@@ -131,32 +131,55 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
-def cpu_baseline(p, form, cfg_tuple, verts, coef_kind, target_s=10.0):
-    """The reference's own CPU path (oracle/_ref, compiled from the unmodified sources) on
-    this host's cores, on a bounded prefix sample of the same cells; the C restatement
-    (oracle/) stands in where _ref was not built. Returns (cells/s, kind, cores, sample)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_run(p, form, cfg_tuple, verts, coef_kind, n):
+    """One timed pass of the reference's own CPU path over the first n cells: oracle/_ref (the
+    unmodified reference, compiled from its sources) under mpfem::parallel_for on every host
+    core, or the C restatement (oracle/, one thread) where _ref was not built.
+    Returns (seconds, kind, cores)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle_lib import Oracle, Reference, reference_available
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    v = verts.reshape(-1, 12)
+    v = verts.reshape(-1, 12)[:n]
     if reference_available():
-        R = Reference()
-        n0 = min(v.shape[0], 2 * cores)
-        secs, _ = R.cpu_baseline(p, form, cfg_tuple, v[:n0], coef_kind, None, cores)
-        rate = n0 / max(secs, 1e-9)
-        n = int(min(v.shape[0], max(n0, rate * target_s)))
-        secs, _ = R.cpu_baseline(p, form, cfg_tuple, v[:n], coef_kind, None, cores)
-        return n / secs, "reference", cores, f"first {n} of the {v.shape[0]} cells, MPFEM_THREADS={cores}"
-    O = Oracle()
-    n = 2
+        cores = host_cores()
+        secs, _ = Reference().cpu_baseline(p, form, cfg_tuple, v, coef_kind, None, cores)
+        return secs, "reference", cores
     t = time.perf_counter()
-    O.bilinear(p, form, cfg_tuple, v[:n], coef_kind, None)
-    dt = time.perf_counter() - t
-    n2 = int(max(2, min(v.shape[0], (target_s / max(dt, 1e-9)) * n)))
-    t = time.perf_counter()
-    O.bilinear(p, form, cfg_tuple, v[:n2], coef_kind, None)
-    dt = time.perf_counter() - t
-    return n2 / dt, "port", 1, f"first {n2} of the {v.shape[0]} cells, 1 thread (C restatement)"
+    Oracle().bilinear(p, form, cfg_tuple, v, coef_kind, None)
+    return time.perf_counter() - t, "port", 1
+
+
+def cpu_sample_size(p, form, cfg_tuple, verts, coef_kind, target_s):
+    """Cells per CPU step so that one step takes about target_s seconds (calibrated on a
+    short run), capped at the whole workload."""
+    cores = host_cores()
+    n0 = min(verts.shape[0], 2 * cores)
+    secs, _, _ = cpu_run(p, form, cfg_tuple, verts, coef_kind, n0)
+    rate = n0 / max(secs, 1e-9)
+    return int(min(verts.shape[0], max(n0, rate * target_s)))
+
+
+def cpu_baseline(p, form, cfg_tuple, verts, coef_kind, target_s=10.0):
+    """The reported CPU baseline of the main arm: the reference CPU path timed on a bounded
+    prefix sample of the same cells. Returns (cells/s, kind, cores, sample)."""
+    n = cpu_sample_size(p, form, cfg_tuple, verts, coef_kind, target_s)
+    secs, kind, cores = cpu_run(p, form, cfg_tuple, verts, coef_kind, n)
+    thr = f"MPFEM_THREADS={cores}" if kind == "reference" else "1 thread (C restatement)"
+    return n / secs, kind, cores, f"first {n} of the {verts.shape[0]} cells, {thr}, {cpu_model()}"
 
 
 MIXED_CFG = dict(u_p=2, u_g=3, u_q=2, u_s=1, engine=0)  # config 1: G_K at fp64
@@ -172,64 +195,70 @@ def workload_config():
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU implementation of the headline path, timed
+    on this host's cores. The inputs come from the parity checker's generator (oracle/,
+    bitwise the product's, tests/test_abi_cpu.py) so this process never maps the product
+    library. Each step is the same bounded prefix sample of the 65,536 config-1 cells, sized
+    so the warmup + steps run ends within about 2.5 minutes; ms_per_step is the measured
+    wall time of one such step and value = sample cells / that time."""
     if rank != 0:
         return
-    import paper_2410_12614_b200 as mp  # host-only generator (no GPU needed)
-    verts, _ = mp.gen_tets(0, 1, N_CELLS)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+    verts, _ = Oracle().gen_tets(0, 1, N_CELLS)
     cfg = (MIXED_CFG["u_p"], MIXED_CFG["u_g"], MIXED_CFG["u_q"], MIXED_CFG["u_s"], MIXED_CFG["engine"])
-    rates = []
-    info = None
-    # each step is a bounded prefix sample sized so the whole K + W run stays near 2.5 minutes
     per_step = max(0.2, min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=per_step)
     t_all = time.perf_counter()
+    n = cpu_sample_size(P_DEG, 1, cfg, verts, 1, per_step)
+    for _ in range(max(0, args.warmup - 1)):  # the calibration run is the first warmup step
+        cpu_run(P_DEG, 1, cfg, verts, 1, n)
+    secs = []
+    kind, cores = None, None
     for _ in range(args.steps):
-        r, kind, cores, sample = cpu_baseline(P_DEG, 1, cfg, verts, 1, target_s=per_step)
-        rates.append(r)
-        info = (kind, cores, sample)
+        s_, kind, cores = cpu_run(P_DEG, 1, cfg, verts, 1, n)
+        secs.append(s_)
     wall = time.perf_counter() - t_all
-    value = float(np.mean(rates))
+    step_s = float(np.mean(secs))
+    value = n / step_s
+    thr = f"MPFEM_THREADS={cores}" if kind == "reference" else "1 thread (C restatement)"
+    sample = (f"each step: the first {n} of the {N_CELLS} config-1 cells ({thr}); "
+              f"host CPU: {cpu_model()}")
+    conf = dict(workload_config(), cells_per_step=n)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * N_CELLS / value,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * step_s,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic (seeded)", "config": workload_config(),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[1], "kind": info[0],
-                             "sample": info[2]},
+            "data": "synthetic (seeded, oracle generator)", "config": conf,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
 
 
 def run_sweep(mp, torch, dev, only=None):
-    """BASELINE config 2: p = 1..8, mass and Poisson, mixed (bf16 storage) and fp64; cell
-    count per p chosen so the outputs total 4 GiB (fp32: 2^32 / (4 n_phi^2))."""
+    """BASELINE config 2: p = 1..8, mass and Poisson, in BASELINE's "mixed" mode (fp16
+    storage, fp32 accumulation), the paper's bf16-storage mixed mode as an extra column, and
+    fp64; the cell count per p is chosen so the outputs total 4 GiB (2^32 / (s_out n_phi^2),
+    s_out = 4 for the fp32 outputs of the mixed modes, 8 for fp64)."""
     hbm, tc_peak, _, _ = peaks()
     res = []
     for p in range(1, 9):
         for form in (0, 1):
-            for mode in ("mixed", "fp64"):
+            for mode in ("mixed", "mixed_bf16", "fp64"):
                 if only and (p, form, mode) not in only:
                     continue
-                if mode == "mixed":
-                    cfg = mp.KernelConfig(form=form, u_p=2, u_g=2, u_q=2, u_s=0, engine=2)
-                    ob = 4
-                else:
-                    cfg = mp.KernelConfig(form=form)
-                    ob = 8
+                cfg = mp.mode_config(mode, form)
+                ob = 8 if mode == "fp64" else 4
                 n = (1 << 32) // (ob * nphi(p) ** 2)
-                if mode == "fp64":
-                    n = min(n, 1 << 20)  # bounded: fp64 is compute-bound, fewer cells suffice
                 verts, _ = mp.gen_tets(0, 7 + p, n)
                 vd = torch.from_numpy(verts).to(dev)
                 s = mp.make_setup(p, cfg)
                 s.reserve(n)
                 out = torch.empty((n, nphi(p) ** 2), dtype=torch.float32 if ob == 4 else torch.float64, device=dev)
-                for _ in range(2):
-                    s.cell_matrices(vd, None, 1, out=out)
+                s.cell_matrices(vd, None, 1, out=out)
                 torch.cuda.synchronize()
+                reps = 3 if mode != "fp64" or p < 6 else 1
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                reps = 3
                 e0.record()
                 for _ in range(reps):
                     s.cell_matrices(vd, None, 1, out=out)
@@ -240,13 +269,16 @@ def run_sweep(mp, torch, dev, only=None):
                 s.cell_matrices(vd, None, 1, out=out)
                 kt = s.last_timings()
                 s.set_timing(False)
+                s.synchronize()
                 f, b = work_per_cell(p, form, ob)
-                t_roof = max(n * f / (tc_peak * 1e12) if mode == "mixed" else 0.0, n * b / (hbm * 1e9))
+                t_tc = n * f / (tc_peak * 1e12) if mode != "fp64" else 0.0
+                t_roof = max(t_tc, n * b / (hbm * 1e9))
                 res.append({"p": p, "form": "poisson" if form else "mass", "mode": mode, "cells": n,
                             "ms": ms, "cells_per_s": n / (ms * 1e-3),
                             "tflops_dense_equiv": n * f / (ms * 1e-3) / 1e12,
                             "hbm_gbs_algorithmic": n * b / (ms * 1e-3) / 1e9,
-                            "roofline_frac": (t_roof / (ms * 1e-3)) if mode == "mixed" else None,
+                            "bound": ("tensor" if t_tc * 1e9 > n * b / hbm else "hbm") if mode != "fp64" else "fp64",
+                            "roofline_frac": (t_roof / (ms * 1e-3)) if mode != "fp64" else None,
                             "path": s.path, "kernels_ms": kt})
                 del s, out, vd
                 torch.cuda.empty_cache()

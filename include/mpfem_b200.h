@@ -58,7 +58,15 @@ const char* mpfem_b200_version(void);
  * 1 <= p <= 4: tensor Lagrange basis, Gauss-Legendre rule, geometry at every rule point;
  * vertices 8 per cell in lattice bit order, constant or nodal coefficients).
  * The handle owns device copies of the rule, the fp64 tabulations and the shared
- * basis-product operand T; it is immutable and may be shared by streams. */
+ * basis-product operand T, which are read-only after creation. Per-call scratch (the W
+ * operand, FP flags, the K1 tile counter, host-API staging) lives in one workspace per CUDA
+ * stream, so a setup may be used from several threads and streams at once: calls on one
+ * stream are ordered by the stream, calls on different streams use different scratch, and
+ * the host-side bookkeeping of every call is serialized by a mutex of the setup.
+ * CheckError semantics: a singular cell (geometry.cpp:42) is detected on the device. With
+ * flags != NULL (or in the synchronizing host-buffer calls) the call itself returns 3;
+ * otherwise the error is reported (status 3) by the next call on the setup or by
+ * mpfem_b200_synchronize -- the asynchronous analogue of the reference's throw. */
 int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, int u_g,
                             int u_q, int u_s, int engine, int n_batch,
                             mpfem_b200_setup_t* out);
@@ -82,7 +90,9 @@ int mpfem_b200_setup_rule(mpfem_b200_setup_t setup, double* points, double* weig
  *   out:    n_cells rows of n_phi x n_phi row-major cell matrices with row pitch
  *           out_pitch elements (>= n_phi^2); fp32 for u_q in {fp16, fp32}, fp64 for fp64
  *   stream: cudaStream_t (NULL = legacy default)
- *   flags:  optional host pointer; OR-ed with the FP flag bitmask (forces a sync) */
+ *   flags:  optional host pointer; OR-ed with the FP flag bitmask (forces a sync)
+ * A singular cell makes its output row NaN and raises CheckError (3) as described at
+ * mpfem_b200_setup_create. */
 int mpfem_b200_cell_matrices(mpfem_b200_setup_t setup, const double* verts,
                              const int32_t* cells, int64_t n_cells, int coef_kind,
                              const double* coef, int64_t coef_stride, void* out,
@@ -96,9 +106,13 @@ int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t setup, const double* verts,
                                   void* out, int64_t out_pitch, void* stream,
                                   uint32_t* flags);
 
-/* Pre-size the scratch (scaled-weight operand W) for n_cells so that later calls on
- * this setup allocate nothing (CUDA-graph capture safe). */
-int mpfem_b200_reserve(mpfem_b200_setup_t setup, int64_t n_cells);
+/* Pre-size the scratch of `stream`'s workspace (scaled-weight operand W) for n_cells so that
+ * later calls on this setup and stream allocate nothing (CUDA-graph capture safe). */
+int mpfem_b200_reserve(mpfem_b200_setup_t setup, int64_t n_cells, void* stream);
+
+/* Waits for `stream` and returns 3 (CheckError) if a call on this setup met a singular cell
+ * since the last report (see the CheckError semantics at mpfem_b200_setup_create). */
+int mpfem_b200_synchronize(mpfem_b200_setup_t setup, void* stream);
 
 /* Debug/parity entry: the scaled weights W (kernels.cpp:177-197 build_C) in the GEMM
  * layout -- blocks (s<=t) of nq_pad = round_up(n_q, 8) entries, zero for q >= n_q -- as
@@ -130,7 +144,7 @@ int mpfem_b200_cell_matrices_scatter(mpfem_b200_setup_t setup, const double* ver
  *   out:    n_cells rows of n_phi (row pitch out_pitch) -- row c is column c of the
  *           reference's n_phi x batch result; fp64 if u_q = fp64, else fp32 carriers of u_q
  * Errors as the reference: ConfigError (2) for a short w / coefficient, CheckError (3) for a
- * singular cell (reported when flags != NULL, which synchronizes). */
+ * singular cell (see the CheckError semantics at mpfem_b200_setup_create). */
 int mpfem_b200_action(mpfem_b200_setup_t setup, const double* verts, const int32_t* cells,
                       int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,
                       const double* w, int64_t w_stride, void* out, int64_t out_pitch,
@@ -173,10 +187,6 @@ int mpfem_b200_last_launch_count(mpfem_b200_setup_t setup);
 int mpfem_b200_set_timing(mpfem_b200_setup_t setup, int enable);
 int mpfem_b200_last_timings(mpfem_b200_setup_t setup, float* ms, int max_n);
 
-/* Debug timeline of the last cell_matrices call (only with MPFEM_B200_TRACE=1 in the
- * environment): per CTA {start ns, end ns, SM id}; K1 CTAs in slots 0..1023, K2 CTAs in
- * slots 1024..2047, 3 words per slot. Not a reference interface (diagnostics only). */
-int mpfem_b200_debug_trace(mpfem_b200_setup_t setup, unsigned long long* host, int max_n);
 
 /* ---------------------------------------------------------------- mesh & assembly */
 

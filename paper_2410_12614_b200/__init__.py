@@ -129,7 +129,8 @@ def lib():
                                                        vp, vp, C.c_int, vp, u32p]),
         "mpfem_b200_cell_matrices_host": (C.c_int, [vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp,
                                                     C.c_int64, vp, C.c_int64, vp, u32p]),
-        "mpfem_b200_reserve": (C.c_int, [vp, C.c_int64]),
+        "mpfem_b200_reserve": (C.c_int, [vp, C.c_int64, vp]),
+        "mpfem_b200_synchronize": (C.c_int, [vp, vp]),
         "mpfem_b200_action": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp,
                                         C.c_int64, vp, C.c_int64, vp, u32p]),
         "mpfem_b200_cell_bounds": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, vp, C.c_int64, vp, vp,
@@ -143,7 +144,6 @@ def lib():
         "mpfem_b200_last_launch_count": (C.c_int, [vp]),
         "mpfem_b200_set_timing": (C.c_int, [vp, C.c_int]),
         "mpfem_b200_last_timings": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
-        "mpfem_b200_debug_trace": (C.c_int, [vp, vp, C.c_int]),
         "mpfem_b200_gen_tets": (C.c_int, [C.c_int, C.c_uint64, C.c_int64, vp, vp]),
         "mpfem_b200_structured_tet_mesh": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double,
                                                      C.c_double, C.c_uint64, vp, vp]),
@@ -245,8 +245,15 @@ class KernelSetup:
                                           w.ctypes.data_as(C.POINTER(C.c_double))))
         return pts, w
 
-    def reserve(self, n_cells: int) -> None:
-        check(lib().mpfem_b200_reserve(self._h, int(n_cells)))
+    def reserve(self, n_cells: int, stream=None) -> None:
+        """Pre-sizes the scratch of `stream`'s workspace (graph-capture safe calls after)."""
+        check(lib().mpfem_b200_reserve(self._h, int(n_cells), _stream_handle(stream)))
+
+    def synchronize(self, stream=None) -> None:
+        """Waits for `stream`; raises CheckError if a call on this setup met a singular cell
+        since the last report (asynchronous calls without want_flags report it here or on
+        the next call, see include/mpfem_b200.h)."""
+        check(lib().mpfem_b200_synchronize(self._h, _stream_handle(stream)))
 
     def cell_matrices(self, verts, cells=None, coef_kind: int = CoefKind.one, coef=None, out=None,
                       out_pitch: int | None = None, stream=None, want_flags: bool = False):
@@ -390,15 +397,6 @@ class KernelSetup:
         if n < 0:
             check(-n)
         return [buf[i] for i in range(n)]
-
-    def debug_trace(self):
-        """Per-CTA timeline of the last call (MPFEM_B200_TRACE=1): arrays (k1, k2) of
-        rows (start_ns, end_ns, sm) for the CTAs that ran."""
-        buf = np.zeros(3 * 2048, dtype=np.uint64)
-        check(lib().mpfem_b200_debug_trace(self._h, buf.ctypes.data, buf.size))
-        rows = buf.reshape(2048, 3)
-        k1, k2 = rows[:1024], rows[1024:]
-        return k1[k1[:, 0] > 0], k2[k2[:, 0] > 0]
 
 
 def make_setup(p: int, config: KernelConfig, cell_kind: int = 0, dim: int = 3) -> KernelSetup:

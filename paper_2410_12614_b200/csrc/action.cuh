@@ -219,8 +219,8 @@ __device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell
   }
   TetGeometry g;
   if (!action_geometry(v, P.n_d == 3, P.ug, g, fl)) {
-    atomicExch(P.error, 3);
-    for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+    report_error(P.error, 3);
+    for (int b = 0; b < 6; ++b) g.g[b] = __longlong_as_double(0x7ff8000000000000ll);  // singular: NaN column
   }
   for (int b = 0; b < 6; ++b) geo[b] = g.g[b];
   #pragma unroll
@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
       if constexpr (BOX) {  // hexahedra: the geometry at this rule point
         TetGeometry tg;
         if (c < nc && !box_g_at<UGK>(P, geo, q, tg, fl)) {
-          atomicExch(P.error, 3);
-          for (int b = 0; b < 6; ++b) tg.g[b] = 0.0;
+          report_error(P.error, 3);
+          for (int b = 0; b < 6; ++b) tg.g[b] = __longlong_as_double(0x7ff8000000000000ll);
         } else if (c >= nc) {
           for (int b = 0; b < 6; ++b) tg.g[b] = 0.0;
         }

@@ -357,16 +357,6 @@ __device__ __forceinline__ void entry_sum(const TL* __restrict__ locals, int64_t
   values[e] = acc;
 }
 
-template <typename TL, typename TV>
-__global__ void assemble_seg_kernel(const TL* __restrict__ locals, int64_t per_cell,
-                                    const int64_t* __restrict__ seg_ptr, const uint32_t* __restrict__ perm,
-                                    int64_t nnz, int64_t cell_begin, int64_t cell_end, int init,
-                                    TV* __restrict__ values) {
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
-       e += int64_t(gridDim.x) * blockDim.x)
-    entry_sum(locals, per_cell, seg_ptr, perm, e, cell_begin, cell_end, init, values);
-}
-
 // Block-staged deterministic scatter: a CTA takes kSegBlock consecutive CSR entries, stages
 // their segment offsets, gathers every contribution of the block into shared memory with
 // independent coalesced perm loads (4 in flight per thread), then each thread sums its

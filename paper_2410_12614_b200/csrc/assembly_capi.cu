@@ -401,26 +401,16 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, 
 #undef MPFEM_SEG_ROWS
       } else {
         const int64_t nnz = read1(row_ptr + n_dofs, st);
-        // block-staged gather (bitwise the per-entry sum); MPFEM_B200_SEG_BLOCK=0: per entry
-        static const bool blocked = [] {
-          const char* e = std::getenv("MPFEM_B200_SEG_BLOCK");
-          return !(e && std::atoi(e) == 0);
-        }();
+        // block-staged segment gather (bitwise the per-entry sequential sum)
         const size_t vsz = fmt == 2 ? 4 : 8;
         const int cap = int((asmb::kSegSmem - (asmb::kSegBlock + 1) * 8) / vsz);
         const size_t smem = (asmb::kSegBlock + 1) * 8 + size_t(cap) * vsz;
-        const unsigned grid =
-            blocked ? unsigned(std::max<int64_t>(1, std::min<int64_t>((nnz + asmb::kSegBlock - 1) / asmb::kSegBlock,
-                                                                      148 * asmb::kSegCtasPerSm)))
-                    : grid_for(nnz);
+        const unsigned grid = unsigned(std::max<int64_t>(
+            1, std::min<int64_t>((nnz + asmb::kSegBlock - 1) / asmb::kSegBlock, 148 * asmb::kSegCtasPerSm)));
 #define MPFEM_SEG(TL, TV)                                                                          \
-  if (blocked)                                                                                     \
-    asmb::assemble_seg_block_kernel<TL, TV><<<grid, 256, smem, st>>>(                              \
-        reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end,     \
-        init, cap, static_cast<TV*>(values));                                                      \
-  else                                                                                             \
-    asmb::assemble_seg_kernel<TL, TV><<<grid, 256, 0, st>>>(reinterpret_cast<const TL*>(base),    \
-        per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, static_cast<TV*>(values))
+  asmb::assemble_seg_block_kernel<TL, TV><<<grid, 256, smem, st>>>(                                \
+      reinterpret_cast<const TL*>(base), per_cell, seg_ptr, perm, nnz, cell_begin, cell_end, init, \
+      cap, static_cast<TV*>(values))
         if (locals_fmt == 2 && fmt == 2) MPFEM_SEG(float, float);
         else if (locals_fmt == 2) MPFEM_SEG(float, double);
         else if (fmt == 2) MPFEM_SEG(double, float);

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -134,6 +135,26 @@ int device_sm_count() {
 
 void mpfem_b200_set_last_error(const std::string& msg) { g_last_error = msg; }
 
+// Per-stream scratch of a setup: the W operand, FP flags, K1's tile counter, host-API staging
+// and the timing events. Calls on one stream are ordered by the stream, so they may share
+// one workspace; calls on different streams get different workspaces and never race on
+// device scratch (the setup itself is read-only after creation).
+struct Workspace {
+  DevBuf d_W, d_flags, d_tile_ctr, d_locals;
+  DevBuf h_verts, h_cells, h_coef, h_out;  // device staging of the host-buffer API
+  cudaEvent_t ev[8] = {};
+  int n_ev = 0;
+  ~Workspace() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  void mark(bool timing, cudaStream_t st) {
+    if (!timing || n_ev >= 8) return;
+    if (!ev[n_ev]) CUDA_OK(cudaEventCreate(&ev[n_ev]));
+    CUDA_OK(cudaEventRecord(ev[n_ev++], st));
+  }
+};
+
 struct mpfem_b200_setup_s {
   int p = 0, form = 0, up = 3, ug = 3, uq = 3, us = 3, engine = 0;
   int box = 0;         // hexahedral cells: per-point geometry in K1
@@ -142,21 +163,10 @@ struct mpfem_b200_setup_s {
   int64_t k = 0, k_pad = 0, n_out = 0, n_out_pad = 0;
   int path = kPathF64;
   int acc_f16 = 0;
-  int pair = 0;    // tcgen05 path: 0 = one CTA per tile, 1 = CTA pairs, 2 = two pairs per cluster
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
   Rule rule;
   DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
-  int n_rows = 0;  // tcgen05 path: rows of Tt (upper-triangle 8x4 blocks, padded to 128)
-  DevBuf d_W, d_flags, d_error;
-  // concurrent K1/K2 (tcgen05 pair path): per-K1-tile W stamps and the call's epoch
-  DevBuf d_ready;
-  DevBuf d_trace;  // MPFEM_B200_TRACE=1: per-CTA timeline of the last call
-  DevBuf d_tile_ctr;  // K1 dynamic tile schedule (2 words, zero between launches)
-  // fused scatter (mpfem_b200_cell_matrices_scatter) for the duration of one call
-  const int32_t* cur_pos_map = nullptr;
-  void* cur_values = nullptr;
-  int cur_values_fp64 = 0;
-  DevBuf d_locals;  // non-fused paths: local matrices staged before the atomic scatter
+  int n_rows = 0;  // tcgen05 path: rows of Tt (output-row table, padded to the pair tile)
   // action (Algorithm 2): store tabulation in the u_p / u_q compute types, built on first use
   DevBuf d_act_a, d_act_c;
   int act_ap = -1, act_aq = -1;
@@ -165,34 +175,43 @@ struct mpfem_b200_setup_s {
   double bnd_lebesgue = 0.0;
   double bnd_glebesgue[3] = {0.0, 0.0, 0.0}, bnd_gkmax[3] = {0.0, 0.0, 0.0};
   bool bnd_ready = false;
-  uint32_t epoch = 0;
-  uint32_t* cur_ready = nullptr;  // set for the duration of a concurrent launch pair
-  // host-API staging
-  DevBuf h_verts, h_cells, h_coef, h_out;
-  int last_launches = 0;
   int device = 0;
-  // K1/K2 overlap: K2 of chunk i runs on `side` while K1 of chunk i+1 runs on the caller's
-  // stream; fork/join through events keeps the call stream-ordered (and graph-capturable).
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  cudaEvent_t chunk_ready[8] = {};
-  // optional per-kernel timing of the last cell_matrices call (CUDA events on its stream)
-  int timing = 0;
-  cudaEvent_t ev[8] = {};
-  int n_ev = 0;
+  // Host-side state is guarded by `mu`: every entry point holds it while it validates and
+  // enqueues (the device work itself runs asynchronously on the caller's stream).
+  std::mutex mu;
+  std::map<cudaStream_t, std::unique_ptr<Workspace>> ws;
+  Workspace* last_ws = nullptr;
+  int last_launches = 0;
+  int timing = 0;  // record CUDA events around K1 / K2 (mpfem_b200_set_timing)
+  // CheckError word written by the kernels (report_error): pinned host memory mapped into
+  // the device, read by the host without a copy.
+  int* h_error = nullptr;
+  int* d_error = nullptr;
   ~mpfem_b200_setup_s() {
-    for (auto& e : ev)
-      if (e) cudaEventDestroy(e);
-    for (auto& e : chunk_ready)
-      if (e) cudaEventDestroy(e);
-    if (fork) cudaEventDestroy(fork);
-    if (join) cudaEventDestroy(join);
-    if (side) cudaStreamDestroy(side);
+    ws.clear();
+    if (h_error) cudaFreeHost(h_error);
   }
-  void mark(cudaStream_t st) {
-    if (!timing || n_ev >= 8) return;
-    if (!ev[n_ev]) CUDA_OK(cudaEventCreate(&ev[n_ev]));
-    CUDA_OK(cudaEventRecord(ev[n_ev++], st));
+  Workspace& workspace(cudaStream_t st) {
+    auto& w = ws[st];
+    if (!w) {
+      auto n = std::make_unique<Workspace>();
+      n->d_flags.ensure(16);
+      n->d_tile_ctr.ensure(16);
+      CUDA_OK(cudaMemset(n->d_flags.p, 0, 16));
+      CUDA_OK(cudaMemset(n->d_tile_ctr.p, 0, 16));
+      w = std::move(n);
+    }
+    last_ws = w.get();
+    return *w;
+  }
+  // Raises a CheckError the device reported since the last check (the reference throws at
+  // the failing cell, geometry.cpp:42; here the next call or synchronize reports it).
+  void take_error(const char* when) {
+    volatile int* e = h_error;
+    const int code = *e;
+    if (!code) return;
+    *e = 0;
+    throw Error(MPFEM_B200_CHECK_ERROR, std::string("singular cell geometry") + when);
   }
 };
 
@@ -247,54 +266,20 @@ void choose_path(mpfem_b200_setup_s& S) {
 // K1 tile height: one geometry lane per cell, so a tile of 32 G cells has G geometry warps.
 // Low degrees have few quadrature groups per cell and would wait on a single geometry warp.
 int k1_geom_warps(const mpfem_b200_setup_s& S) {
-  static const int env = [] {
-    const char* e = std::getenv("MPFEM_B200_K1_GEOM_WARPS");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (env > 0) return std::min(env, 8);
   const int ngroups = S.nq_pad / kQPT;
   return std::max(1, std::min(4, 32 / ngroups));
 }
 
-void launch_geom_tet(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
-                     int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
-                     int w_type, cudaStream_t st);
+// Optional fused CSR scatter of one call (mpfem_b200_cell_matrices_scatter).
+struct Scatter {
+  const int32_t* pos_map = nullptr;
+  void* values = nullptr;
+  bool fp64 = false;
+};
 
-// K1: per-cell geometry (tets, geom_w.cuh) or per-point geometry (boxes, geom_box.cuh).
-void launch_geom(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
-                 int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
-                 int w_type, cudaStream_t st) {
-  if (!S.box) return launch_geom_tet(S, verts, cells, n, coef_kind, coef, coef_stride, W, k_pad, w_type, st);
-  GeomBoxParams P{};
-  P.verts = verts;
-  P.cells = cells;
-  P.n_cells = n;
-  P.coef_kind = coef_kind;
-  P.coef = coef;
-  P.coef_stride = coef_stride;
-  P.rule_w_ug = static_cast<const double*>(S.d_rule_w_ug.p);
-  P.ggrad = static_cast<const double*>(S.d_ggrad.p);
-  P.tab_up = static_cast<const double*>(S.d_tab_up.p);
-  P.n_phi = S.n_phi;
-  P.n_q = S.n_q;
-  P.nq_pad = S.nq_pad;
-  P.n_blocks = S.n_blocks;
-  P.k = S.k;
-  P.k_pad = k_pad;
-  P.up = S.up;
-  P.ug = S.ug;
-  P.us = S.us;
-  P.poisson = S.form;
-  P.W = W;
-  P.flags = static_cast<uint32_t*>(S.d_flags.p);
-  P.error = static_cast<int*>(S.d_error.p);
-  launch_geom_box(w_type, P, device_sm_count(), st);
-  CUDA_OK(cudaGetLastError());
-}
-
-void launch_geom_tet(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
-                     int coef_kind, const double* coef, int64_t coef_stride, void* W, int64_t k_pad,
-                     int w_type, cudaStream_t st) {
+void launch_geom_tet(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const int32_t* cells,
+                     int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* W,
+                     int64_t k_pad, int w_type, cudaStream_t st) {
   GeomWParams P;
   P.verts = verts;
   P.cells = cells;
@@ -316,24 +301,47 @@ void launch_geom_tet(mpfem_b200_setup_s& S, const double* verts, const int32_t* 
   P.nq_pad = S.nq_pad;
   P.w_type = w_type;
   P.W = W;
-  P.flags = static_cast<uint32_t*>(S.d_flags.p);
-  P.error = static_cast<int*>(S.d_error.p);
-  P.ready = S.cur_ready;
-  P.epoch = S.epoch;
-  P.trace = static_cast<unsigned long long*>(S.d_trace.p);
-  static const bool dyn = [] {
-    const char* e = std::getenv("MPFEM_B200_K1_DYNAMIC");
-    return !(e && std::atoi(e) == 0);
-  }();
-  P.tile_ctr = dyn ? static_cast<uint32_t*>(S.d_tile_ctr.p) : nullptr;
+  P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+  P.error = S.d_error;
+  P.tile_ctr = static_cast<uint32_t*>(ws.d_tile_ctr.p);
   P.geom_warps = k1_geom_warps(S);
   const int64_t tile_cells = 32 * P.geom_warps;
   const int64_t tiles = (n + tile_cells - 1) / tile_cells;
-  // concurrent with K2 (one 384-thread CTA per SM): two 256-thread K1 CTAs fit beside it
-  int per_sm = S.cur_ready ? 2 : MPFEM_K1_MINB;
-  if (const char* e = std::getenv("MPFEM_B200_K1_PER_SM")) per_sm = std::max(1, std::atoi(e));
-  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * per_sm));
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(device_sm_count()) * MPFEM_K1_MINB));
   launch_geom_typed(w_type, S.ug, S.us, grid, st, P);
+  CUDA_OK(cudaGetLastError());
+}
+
+// K1: per-cell geometry (tets, geom_w.cuh) or per-point geometry (boxes, geom_box.cuh).
+void launch_geom(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const int32_t* cells,
+                 int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* W,
+                 int64_t k_pad, int w_type, cudaStream_t st) {
+  if (!S.box)
+    return launch_geom_tet(S, ws, verts, cells, n, coef_kind, coef, coef_stride, W, k_pad, w_type, st);
+  GeomBoxParams P{};
+  P.verts = verts;
+  P.cells = cells;
+  P.n_cells = n;
+  P.coef_kind = coef_kind;
+  P.coef = coef;
+  P.coef_stride = coef_stride;
+  P.rule_w_ug = static_cast<const double*>(S.d_rule_w_ug.p);
+  P.ggrad = static_cast<const double*>(S.d_ggrad.p);
+  P.tab_up = static_cast<const double*>(S.d_tab_up.p);
+  P.n_phi = S.n_phi;
+  P.n_q = S.n_q;
+  P.nq_pad = S.nq_pad;
+  P.n_blocks = S.n_blocks;
+  P.k = S.k;
+  P.k_pad = k_pad;
+  P.up = S.up;
+  P.ug = S.ug;
+  P.us = S.us;
+  P.poisson = S.form;
+  P.W = W;
+  P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+  P.error = S.d_error;
+  launch_geom_box(w_type, P, device_sm_count(), st);
   CUDA_OK(cudaGetLastError());
 }
 
@@ -347,13 +355,13 @@ void check_coef(const mpfem_b200_setup_s& S, int coef_kind, const double* coef, 
     throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
 }
 
-template <bool ACC_F16, int NP, int OUTK = 0>
+template <bool ACC_F16, int OUTK = 0>
 void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2 * NP;
+  attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.blockDim = dim3(tc2::THREADS);
@@ -362,31 +370,24 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (!max_clusters) {
-    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>,
+    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, OUTK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES));
-    // Full carveout: with the default the driver configures an SM that K2 reaches first for
-    // the smallest shared-memory size holding its 198 KB (196 KB), leaving no room for the
-    // two concurrent K1 CTAs (2 x 14 KB) -- K1 would then wait for K2, which waits for K1.
-    CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 int(cudaSharedmemCarveoutMaxShared)));
     cfg.gridDim = dim3(unsigned(device_sm_count()));
-    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>, &cfg));
+    CUDA_OK(cudaOccupancyMaxActiveClusters(&max_clusters, tc2::cellmat_tc2_kernel<ACC_F16, OUTK>, &cfg));
     if (max_clusters < 1) throw Error(MPFEM_B200_RUNTIME_ERROR, "tcgen05 pair kernel does not fit an SM cluster");
   }
-  const int64_t tiles = int64_t(P.n_out_tiles) * ((P.n_cell_tiles + NP - 1) / NP);
-  cfg.gridDim = dim3(unsigned(2 * NP * std::min<int64_t>(tiles, max_clusters)));
-  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, NP, OUTK>, ta, tb, P));
+  const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
+  cfg.gridDim = dim3(unsigned(2 * std::min<int64_t>(tiles, max_clusters)));
+  CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, OUTK>, ta, tb, P));
 }
 
-void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t out_pitch,
-                 cudaStream_t st) {
-  if (S.path == kPathTC && S.pair) {
+void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void* out,
+                 int64_t out_pitch, cudaStream_t st, const Scatter* sc) {
+  if (S.path == kPathTC) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc2::BK,
-                                 tc2::BMC / S.pair);
-    CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc2::BK, tc2::BNC);
+    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc2::BMC);
+    CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc2::BNC);
     tc::Params P{};
     P.n_cells = n;
     P.n_out = int(S.n_out);
@@ -394,83 +395,44 @@ void launch_gemm(mpfem_b200_setup_s& S, void* W, int64_t n, void* out, int64_t o
     P.rows = static_cast<const int32_t*>(S.d_rows.p);
     P.n_out_tiles = int(S.n_out_pad / tc2::BM);
     P.n_cell_tiles = int((n + tc2::BN - 1) / tc2::BN);
-    P.num_k_blocks = int(S.k_pad / tc2::BK);
-    P.out = static_cast<float*>(out);
-    P.out_pitch = out_pitch;
-    P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc2::BM, tc2::BN);
-    P.flags = static_cast<uint32_t*>(S.d_flags.p);
-    P.ready = S.cur_ready;
-    P.epoch = S.epoch;
-    P.k1_tile = 32 * k1_geom_warps(S);
-    P.error = static_cast<int*>(S.d_error.p);
-    P.trace = static_cast<unsigned long long*>(S.d_trace.p);
-    if (S.cur_pos_map) {
-      // fused scatter: the local matrices go straight into the CSR values
-      P.pos_map = S.cur_pos_map;
-      P.values = S.cur_values;
-      if (S.cur_values_fp64) {
-        if (S.acc_f16) launch_tc2<true, 1, 2>(ta, tb, P, st);
-        else launch_tc2<false, 1, 2>(ta, tb, P, st);
-      } else {
-        if (S.acc_f16) launch_tc2<true, 1, 1>(ta, tb, P, st);
-        else launch_tc2<false, 1, 1>(ta, tb, P, st);
-      }
-    } else if (S.pair == 2) {
-      if (S.acc_f16) launch_tc2<true, 2>(ta, tb, P, st);
-      else launch_tc2<false, 2>(ta, tb, P, st);
-    } else {
-      if (S.acc_f16) launch_tc2<true, 1>(ta, tb, P, st);
-      else launch_tc2<false, 1>(ta, tb, P, st);
-    }
-  } else if (S.path == kPathTC) {
-    const CUtensorMapDataType dt =
-        S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc::BM);
-    CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tc::BN);
-    tc::Params P{};
-    P.n_cells = n;
-    P.n_out = int(S.n_out);
-    P.n_phi = S.n_phi;
-    P.rows = static_cast<const int32_t*>(S.d_rows.p);
-    P.n_out_tiles = int(S.n_out_pad / tc::BM);
-    P.n_cell_tiles = int((n + tc::BN - 1) / tc::BN);
     P.num_k_blocks = int(S.k_pad / tc::BK);
     P.out = static_cast<float*>(out);
     P.out_pitch = out_pitch;
-    P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc::BM, tc::BN);
-    P.flags = static_cast<uint32_t*>(S.d_flags.p);
-    const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
-    const int grid = int(std::min<int64_t>(tiles, device_sm_count()));
-    static bool attr_set = false;
-    if (!attr_set) {
-      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel<false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
-      CUDA_OK(cudaFuncSetAttribute(tc::cellmat_tc_kernel<true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES));
-      attr_set = true;
+    P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tc2::BM, tc2::BN);
+    P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+    if (sc) {
+      // fused scatter: the local matrices go straight into the CSR values
+      P.pos_map = sc->pos_map;
+      P.values = sc->values;
+      if (sc->fp64) {
+        if (S.acc_f16) launch_tc2<true, 2>(ta, tb, P, st);
+        else launch_tc2<false, 2>(ta, tb, P, st);
+      } else {
+        if (S.acc_f16) launch_tc2<true, 1>(ta, tb, P, st);
+        else launch_tc2<false, 1>(ta, tb, P, st);
+      }
+    } else {
+      if (S.acc_f16) launch_tc2<true>(ta, tb, P, st);
+      else launch_tc2<false>(ta, tb, P, st);
     }
-    if (S.acc_f16)
-      tc::cellmat_tc_kernel<true><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
-    else
-      tc::cellmat_tc_kernel<false><<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ta, tb, P);
   } else if (S.path == kPathF32) {
     constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
     dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
     cellmat_simt_kernel<float, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
         static_cast<const float*>(W), static_cast<const float*>(S.d_T.p), static_cast<float*>(out),
-        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(S.d_flags.p));
+        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
   } else {
     constexpr int BM = 64, BN = 128, BK = 16, TM = 4, TN = 8;
     dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
     cellmat_simt_kernel<double, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
         static_cast<const double*>(W), static_cast<const double*>(S.d_T.p), static_cast<double*>(out),
-        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(S.d_flags.p));
+        n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
   }
   CUDA_OK(cudaGetLastError());
 }
 
-void launch_fused(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
-                  int coef_kind, const double* coef, int64_t coef_stride, float* out,
+void launch_fused(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const int32_t* cells,
+                  int64_t n, int coef_kind, const double* coef, int64_t coef_stride, float* out,
                   int64_t out_pitch, cudaStream_t st) {
   FusedParams F;
   F.verts = verts;
@@ -487,141 +449,53 @@ void launch_fused(mpfem_b200_setup_s& S, const double* verts, const int32_t* cel
   F.up = S.up;
   F.out = out;
   F.out_pitch = out_pitch;
-  F.flags = static_cast<uint32_t*>(S.d_flags.p);
-  F.error = static_cast<int*>(S.d_error.p);
+  F.flags = static_cast<uint32_t*>(ws.d_flags.p);
+  F.error = S.d_error;
   const unsigned grid = unsigned((n + 127) / 128);
   launch_fused_dispatch(S.p * 100 + S.form * 10 + S.ug, S.us, grid, st, F);
   CUDA_OK(cudaGetLastError());
 }
 
-void run_cell_matrices(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells,
-                       int64_t n, int coef_kind, const double* coef, int64_t coef_stride, void* out,
-                       int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+// Reads the FP flags of the call (flags != NULL synchronizes) and raises a CheckError the
+// device reported.
+void finish_call(mpfem_b200_setup_s& S, Workspace& ws, cudaStream_t st, uint32_t* flags) {
+  if (!flags) return;
+  uint32_t h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, ws.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  *flags |= h;
+  S.take_error("");
+}
+
+void run_cell_matrices(mpfem_b200_setup_s& S, Workspace& ws, const double* verts,
+                       const int32_t* cells, int64_t n, int coef_kind, const double* coef,
+                       int64_t coef_stride, void* out, int64_t out_pitch, cudaStream_t st,
+                       uint32_t* flags, const Scatter* sc = nullptr) {
+  S.take_error(" (reported on the device by an earlier call on this setup)");
   check_coef(S, coef_kind, coef, coef_stride);
   if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
   if (out_pitch < S.n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
+  if (n > 0 && !verts) throw Error(MPFEM_B200_CONFIG_ERROR, "null vertex buffer");
   S.last_launches = 0;
-  if (flags) {
-    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
-    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
-  }
-  S.n_ev = 0;
-  if (n == 0) return;
-  if (const char* tr = std::getenv("MPFEM_B200_TRACE"); tr && std::atoi(tr) != 0) {
-    S.d_trace.ensure(3 * 2048 * sizeof(unsigned long long));
-    CUDA_OK(cudaMemsetAsync(S.d_trace.p, 0, S.d_trace.bytes, st));
-  }
-  if (S.path == kPathFused) {
+  ws.n_ev = 0;
+  if (flags) CUDA_OK(cudaMemsetAsync(ws.d_flags.p, 0, 4, st));
+  if (n > 0 && S.path == kPathFused) {
     if (n * int64_t(S.n_q) >= (int64_t(1) << 40)) throw Error(MPFEM_B200_CONFIG_ERROR, "batch too large");
-    S.mark(st);
-    launch_fused(S, verts, cells, n, coef_kind, coef, coef_stride, static_cast<float*>(out), out_pitch, st);
-    ++S.last_launches;
-    S.mark(st);
-    S.mark(st);
-  } else {
-  S.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
-  // Chunking: enough K2 tiles per chunk to fill the GPU about three times over.
-  const int64_t cell_tiles = (n + tc::BN - 1) / tc::BN;
-  const int64_t out_tiles = S.n_out_pad / tc::BM;
-  // Overlapping K1 of chunk i+1 with K2 of chunk i measured slower than back-to-back on B200
-  // (the K1 CTAs contend with the persistent K2 CTAs), so one chunk is the default.
-  int n_chunks = 1;
-  (void)cell_tiles;
-  (void)out_tiles;
-  if (const char* env = std::getenv("MPFEM_B200_CHUNKS")) n_chunks = std::max(1, std::min(8, std::atoi(env)));
-  if (S.timing || S.cur_pos_map) n_chunks = 1;  // timing: K1 and K2 unoverlapped; scatter: one pos_map base
-  // Concurrent K1/K2 (experimental, MPFEM_B200_OVERLAP=1 on the tcgen05 pair path): K1 on
-  // the caller's stream and K2 on a side stream start together and share every SM (one K2
-  // CTA + two K1 CTAs); K2's producer acquires K1's per-tile W stamps before each TMA read.
-  // Correct, but measured no faster on B200: next to K2's MMAs K1 runs 2x slower (1.1x with
-  // the MMAs compiled out), so the fp64 and tensor work do not overlap.
-  const char* ov_env = S.box ? nullptr : std::getenv("MPFEM_B200_OVERLAP");
-  const bool concurrent = S.path == kPathTC && S.pair && !S.timing && n_chunks == 1 &&
-                          ov_env && std::atoi(ov_env) != 0;
-  if (concurrent) {
-    const int64_t k1_tiles = (n + 32 * k1_geom_warps(S) - 1) / (32 * k1_geom_warps(S));
-    const size_t need = size_t(k1_tiles) * sizeof(uint32_t);
-    if (++S.epoch == 0) S.epoch = 1;
-    if (need > S.d_ready.bytes || S.epoch == 1) {
-      S.d_ready.ensure(need);
-      CUDA_OK(cudaMemsetAsync(S.d_ready.p, 0, S.d_ready.bytes, st));
-    }
-    if (!S.side) {
-      CUDA_OK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
-      CUDA_OK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
-      CUDA_OK(cudaEventCreateWithFlags(&S.join, cudaEventDisableTiming));
-      for (auto& e : S.chunk_ready) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    S.cur_ready = static_cast<uint32_t*>(S.d_ready.p);
-    CUDA_OK(cudaEventRecord(S.fork, st));
-    CUDA_OK(cudaStreamWaitEvent(S.side, S.fork, 0));
-    try {
-      launch_geom(S, verts, cells, n, coef_kind, coef, coef_stride, S.d_W.p, S.k_pad, S.w_type, st);
-      launch_gemm(S, S.d_W.p, n, out, out_pitch, S.side);
-    } catch (...) {
-      S.cur_ready = nullptr;
-      throw;
-    }
-    S.cur_ready = nullptr;
-    S.last_launches += 2;
-    CUDA_OK(cudaEventRecord(S.join, S.side));
-    CUDA_OK(cudaStreamWaitEvent(st, S.join, 0));
-    n_chunks = 0;  // done
+    ws.mark(S.timing, st);
+    launch_fused(S, ws, verts, cells, n, coef_kind, coef, coef_stride, static_cast<float*>(out), out_pitch, st);
+    S.last_launches = 1;
+    ws.mark(S.timing, st);
+    ws.mark(S.timing, st);
+  } else if (n > 0) {
+    ws.d_W.ensure(size_t(n) * size_t(S.k_pad) * elem_size(S.w_type));
+    ws.mark(S.timing, st);
+    launch_geom(S, ws, verts, cells, n, coef_kind, coef, coef_stride, ws.d_W.p, S.k_pad, S.w_type, st);
+    ws.mark(S.timing, st);
+    launch_gemm(S, ws, ws.d_W.p, n, out, out_pitch, st, sc);
+    ws.mark(S.timing, st);
+    S.last_launches = 2;
   }
-  const int64_t tiles_per_chunk = (cell_tiles + std::max(n_chunks, 1) - 1) / std::max(n_chunks, 1);
-  if (n_chunks > 1) {
-    if (!S.side) {
-      CUDA_OK(cudaStreamCreateWithFlags(&S.side, cudaStreamNonBlocking));
-      CUDA_OK(cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming));
-      CUDA_OK(cudaEventCreateWithFlags(&S.join, cudaEventDisableTiming));
-      for (auto& e : S.chunk_ready) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    CUDA_OK(cudaEventRecord(S.fork, st));
-    CUDA_OK(cudaStreamWaitEvent(S.side, S.fork, 0));
-  }
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    const int64_t c0 = ch * tiles_per_chunk * tc::BN;
-    const int64_t c1 = std::min<int64_t>(n, (ch + 1) * tiles_per_chunk * tc::BN);
-    if (c0 >= c1) break;
-    const int64_t m = c1 - c0;
-    const size_t wb = size_t(S.k_pad) * elem_size(S.w_type);
-    void* Wc = static_cast<char*>(S.d_W.p) + size_t(c0) * wb;
-    const int nv = S.box ? 8 : 4;
-    const double* vc = cells ? verts : verts + c0 * 3 * nv;
-    const int32_t* cc = cells ? cells + c0 * nv : nullptr;
-    const double* coefc = coef ? coef + c0 * coef_stride : nullptr;
-    S.mark(st);
-    launch_geom(S, vc, cc, m, coef_kind, coefc, coef_stride, Wc, S.k_pad, S.w_type, st);
-    S.last_launches += 1;
-    S.mark(st);
-    cudaStream_t gs = st;
-    if (n_chunks > 1) {
-      CUDA_OK(cudaEventRecord(S.chunk_ready[ch], st));
-      CUDA_OK(cudaStreamWaitEvent(S.side, S.chunk_ready[ch], 0));
-      gs = S.side;
-    }
-    char* outc = static_cast<char*>(out) + size_t(c0) * size_t(out_pitch) * (S.path == kPathF64 ? 8 : 4);
-    launch_gemm(S, Wc, m, outc, out_pitch, gs);
-    ++S.last_launches;
-    S.mark(gs);
-  }
-  if (n_chunks > 1) {
-    CUDA_OK(cudaEventRecord(S.join, S.side));
-    CUDA_OK(cudaStreamWaitEvent(st, S.join, 0));
-  }
-  }  // non-fused paths
-  if (flags) {
-    uint32_t h[2] = {0, 0};
-    CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaMemcpyAsync(&h[1], S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
-    *flags |= h[0];
-    if (h[1] == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
-    if (h[1] == 5)
-      throw Error(MPFEM_B200_RUNTIME_ERROR,
-                  "concurrent K1/K2: W stamps never arrived (K1 not co-resident with K2); "
-                  "set MPFEM_B200_OVERLAP=0");
-  }
+  finish_call(S, ws, st, flags);
 }
 
 // Compute type of a contraction accumulating at `acc` over operands stored at u_s
@@ -669,9 +543,10 @@ void prepare_action(mpfem_b200_setup_s& S) {
   S.act_aq = aq;
 }
 
-void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n,
-                int coef_kind, const double* coef, int64_t coef_stride, const double* w,
+void run_action(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const int32_t* cells,
+                int64_t n, int coef_kind, const double* coef, int64_t coef_stride, const double* w,
                 int64_t w_stride, void* out, int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+  S.take_error(" (reported on the device by an earlier call on this setup)");
   // one nodal z may be shared by the batch (stride 0), as the reference's action_kernel takes it
   check_coef(S, coef_kind, coef, coef_kind == 3 && coef_stride == 0 ? S.n_phi : coef_stride);
   if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative batch");
@@ -680,10 +555,8 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   if (out_pitch < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
   prepare_action(S);
   S.last_launches = 0;
-  if (flags) {
-    CUDA_OK(cudaMemsetAsync(S.d_flags.p, 0, 4, st));
-    CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
-  }
+  ws.n_ev = 0;
+  if (flags) CUDA_OK(cudaMemsetAsync(ws.d_flags.p, 0, 4, st));
   if (n > 0) {
     ActionParams P{};
     P.verts = verts;
@@ -711,25 +584,17 @@ void run_action(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
     P.ggrad = static_cast<const double*>(S.d_ggrad.p);
     P.out = out;
     P.out_pitch = out_pitch;
-    P.flags = static_cast<uint32_t*>(S.d_flags.p);
-    P.error = static_cast<int*>(S.d_error.p);
-    S.n_ev = 0;
-    S.mark(st);
+    P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+    P.error = S.d_error;
+    ws.mark(S.timing, st);
     const int rc = launch_action(S.act_ap, S.act_aq, P, device_sm_count(), st);
     if (rc == 2) throw Error(MPFEM_B200_CONFIG_ERROR, "action tile exceeds shared memory");
     if (rc) throw Error(MPFEM_B200_RUNTIME_ERROR, "action kernel attribute setup failed");
     CUDA_OK(cudaGetLastError());
-    S.mark(st);
+    ws.mark(S.timing, st);
     S.last_launches = 1;
   }
-  if (flags) {
-    uint32_t h[2] = {0, 0};
-    CUDA_OK(cudaMemcpyAsync(&h[0], S.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaMemcpyAsync(&h[1], S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
-    CUDA_OK(cudaStreamSynchronize(st));
-    *flags |= h[0];
-    if (h[1] == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
-  }
+  finish_call(S, ws, st, flags);
 }
 
 // kernel_bounds' setup-level inputs (bounds.cpp:60-95): theta_b of the binary64 tabulation
@@ -801,13 +666,6 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->engine = engine;
     S->box = cell_kind == 1;
     choose_path(*S);
-    if (S->path == kPathTC) {
-      const char* tc1 = std::getenv("MPFEM_B200_TC1");
-      S->pair = !(tc1 && std::atoi(tc1) != 0);
-      // pairs per cluster (2: the two pairs share the Tt tile by TMA multicast)
-      const char* np = std::getenv("MPFEM_B200_TC_PAIRS");
-      if (S->pair && np && std::atoi(np) == 2) S->pair = 2;
-    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw Error(MPFEM_B200_RUNTIME_ERROR, "no CUDA device: the B200 path has no CPU fallback");
@@ -825,31 +683,11 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     S->n_out = int64_t(S->n_phi) * S->n_phi;
     S->n_out_pad = (S->n_out + 127) / 128 * 128;
     std::vector<int32_t> rows;
-    const char* sym_env = std::getenv("MPFEM_B200_SYMMETRIC");
-    const bool symmetric = sym_env && std::atoi(sym_env) != 0;
-    if (S->path == kPathTC && !symmetric) {
+    if (S->path == kPathTC) {
       // full output, row-major (i, j): one warp store = 128 contiguous bytes of a cell
       for (int i = 0; i < S->n_phi; ++i)
         for (int j = 0; j < S->n_phi; ++j) rows.push_back(i | (j << 16));
-    }
-    if (S->path == kPathTC && symmetric) {
-      // Experimental: upper-triangle cover by 8 x 4 blocks (lane l -> (8r + l/4, 4c + l%4)),
-      // values written to (i, j) and (j, i). Fewer MMAs, but the register-resident epilogue
-      // then issues 16/32-byte pieces (12 lines per 64 values) and is LSU-bound: measured
-      // slower on B200 until the epilogue stages through shared memory.
-      const int n = S->n_phi;
-      for (int r = 0; 8 * r < n; ++r)
-        for (int c = 0; 4 * c < n; ++c) {
-          if (4 * c + 3 < 8 * r) continue;  // block entirely below the diagonal
-          for (int l = 0; l < 32; ++l) {
-            const int i = 8 * r + l / 4, j = 4 * c + l % 4;
-            rows.push_back(i < n && j < n ? (i | (j << 16) | (i != j ? (1 << 30) : 0)) : -1);
-          }
-        }
-    }
-    if (S->path == kPathTC) {
-      const size_t row_tile = S->pair ? tc2::BM : tc::BM;
-      while (rows.size() % row_tile) rows.push_back(-1);
+      while (rows.size() % tc2::BM) rows.push_back(-1);
       S->n_out_pad = int64_t(rows.size());
       S->n_rows = int(rows.size());
       S->d_rows.ensure(sizeof(int32_t) * rows.size());
@@ -875,12 +713,9 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
       S->d_ggrad.ensure(sizeof(double) * gg.size());
       CUDA_OK(cudaMemcpy(S->d_ggrad.p, gg.data(), sizeof(double) * gg.size(), cudaMemcpyHostToDevice));
     }
-    S->d_flags.ensure(16);
-    S->d_error.ensure(16);
-    S->d_tile_ctr.ensure(16);
-    CUDA_OK(cudaMemset(S->d_tile_ctr.p, 0, 16));
-    CUDA_OK(cudaMemset(S->d_flags.p, 0, 16));
-    CUDA_OK(cudaMemset(S->d_error.p, 0, 16));
+    CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&S->h_error), 16, cudaHostAllocMapped));
+    std::memset(S->h_error, 0, 16);
+    CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->d_error), S->h_error, 0));
     const int64_t t_rows = S->n_out_pad;
     size_t tbytes = size_t(S->k_pad) * size_t(t_rows) * elem_size(S->w_type);
     if (S->path == kPathFused) {
@@ -934,10 +769,21 @@ int mpfem_b200_setup_rule(mpfem_b200_setup_t S, double* points, double* weights)
   });
 }
 
-int mpfem_b200_reserve(mpfem_b200_setup_t S, int64_t n_cells) {
+int mpfem_b200_reserve(mpfem_b200_setup_t S, int64_t n_cells, void* stream) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    S->d_W.ensure(size_t(n_cells) * size_t(S->k_pad) * elem_size(S->w_type));
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(static_cast<cudaStream_t>(stream));
+    ws.d_W.ensure(size_t(n_cells) * size_t(S->k_pad) * elem_size(S->w_type));
+  });
+}
+
+int mpfem_b200_synchronize(mpfem_b200_setup_t S, void* stream) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    CUDA_OK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    std::lock_guard<std::mutex> lk(S->mu);
+    S->take_error(" (reported on the device by a call on this setup)");
   });
 }
 
@@ -947,8 +793,10 @@ int mpfem_b200_cell_matrices(mpfem_b200_setup_t S, const double* verts, const in
                              uint32_t* flags) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, out, out_pitch,
-                      static_cast<cudaStream_t>(stream), flags);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(S->mu);
+    run_cell_matrices(*S, S->workspace(st), verts, cells, n_cells, coef_kind, coef, coef_stride, out,
+                      out_pitch, st, flags);
   });
 }
 
@@ -962,29 +810,63 @@ int mpfem_b200_cell_matrices_scatter(mpfem_b200_setup_t S, const double* verts,
     if (!pos_map || !values) throw Error(MPFEM_B200_CONFIG_ERROR, "scatter needs pos_map and values");
     if (values_fmt != 2 && values_fmt != 3) throw Error(MPFEM_B200_CONFIG_ERROR, "CSR values must be fp32 or fp64");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (S->path == kPathTC && S->pair) {
-      struct Reset {
-        mpfem_b200_setup_s& s;
-        ~Reset() { s.cur_pos_map = nullptr; s.cur_values = nullptr; }
-      } reset{*S};
-      S->cur_pos_map = pos_map;
-      S->cur_values = values;
-      S->cur_values_fp64 = values_fmt == 3;
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(st);
+    if (S->path == kPathTC) {
+      Scatter sc;
+      sc.pos_map = pos_map;
+      sc.values = values;
+      sc.fp64 = values_fmt == 3;
       // out is unused by the fused epilogue (pitch n_out keeps the argument checks)
-      run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, nullptr, S->n_out,
-                        st, flags);
+      run_cell_matrices(*S, ws, verts, cells, n_cells, coef_kind, coef, coef_stride, nullptr, S->n_out,
+                        st, flags, &sc);
     } else {
       // other paths: stage the local matrices, then the atomic scatter (assemble mode 0)
       const int lf = S->path == kPathF64 ? 3 : 2;
-      S->d_locals.ensure(size_t(n_cells) * size_t(S->n_out) * (lf == 3 ? 8 : 4) + 16);
-      run_cell_matrices(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, S->d_locals.p,
+      ws.d_locals.ensure(size_t(n_cells) * size_t(S->n_out) * (lf == 3 ? 8 : 4) + 16);
+      run_cell_matrices(*S, ws, verts, cells, n_cells, coef_kind, coef, coef_stride, ws.d_locals.p,
                         S->n_out, st, flags);
-      const int rc = mpfem_b200_assemble(S->d_locals.p, lf, 0, n_cells, S->n_phi, nullptr, 0, pos_map,
+      const int rc = mpfem_b200_assemble(ws.d_locals.p, lf, 0, n_cells, S->n_phi, nullptr, 0, pos_map,
                                          nullptr, nullptr, values, values_fmt, 0, 1, nullptr, 0, stream);
       if (rc) throw Error(rc, std::string("atomic scatter: ") + mpfem_b200_last_error());
     }
   });
 }
+
+namespace {
+// Host-buffer API: H2D of the vertices (and cell table / coefficients) into the stream
+// workspace's staging buffers. Returns the device (verts, cells, coef) pointers.
+struct Staged {
+  const double* verts = nullptr;
+  const int32_t* cells = nullptr;
+  const double* coef = nullptr;
+};
+Staged stage_inputs(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, int64_t n_verts,
+                    const int32_t* cells, int64_t n_cells, int coef_kind, const double* coef,
+                    int64_t coef_stride, cudaStream_t st) {
+  Staged d;
+  const int nv = S.box ? 8 : 4;
+  const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 3 * nv);
+  ws.h_verts.ensure(vbytes + 8);
+  if (vbytes) CUDA_OK(cudaMemcpyAsync(ws.h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
+  d.verts = static_cast<const double*>(ws.h_verts.p);
+  if (cells) {
+    ws.h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * nv + 8);
+    CUDA_OK(cudaMemcpyAsync(ws.h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * nv,
+                            cudaMemcpyHostToDevice, st));
+    d.cells = static_cast<const int32_t*>(ws.h_cells.p);
+  }
+  if (coef && (coef_kind == 2 || coef_kind == 3)) {
+    const int64_t rows = coef_stride == 0 ? 1 : n_cells;
+    const int64_t width = coef_stride == 0 ? S.n_phi : coef_stride;
+    const size_t cb = sizeof(double) * size_t(rows) * size_t(width);
+    ws.h_coef.ensure(cb + 8);
+    CUDA_OK(cudaMemcpyAsync(ws.h_coef.p, coef, cb, cudaMemcpyHostToDevice, st));
+    d.coef = static_cast<const double*>(ws.h_coef.p);
+  }
+  return d;
+}
+}  // namespace
 
 int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t S, const double* verts, int64_t n_verts,
                                   const int32_t* cells, int64_t n_cells, int coef_kind,
@@ -993,32 +875,19 @@ int mpfem_b200_cell_matrices_host(mpfem_b200_setup_t S, const double* verts, int
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
     check_coef(*S, coef_kind, coef, coef_stride);
+    if (n_cells < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int nv = S->box ? 8 : 4;
-    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 3 * nv);
-    S->h_verts.ensure(vbytes);
-    CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
-    const int32_t* dcells = nullptr;
-    if (cells) {
-      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * nv);
-      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * nv,
-                              cudaMemcpyHostToDevice, st));
-      dcells = static_cast<const int32_t*>(S->h_cells.p);
-    }
-    const double* dcoef = nullptr;
-    if (coef && (coef_kind == 2 || coef_kind == 3)) {
-      const size_t cb = sizeof(double) * size_t(n_cells) * size_t(coef_stride);
-      S->h_coef.ensure(cb);
-      CUDA_OK(cudaMemcpyAsync(S->h_coef.p, coef, cb, cudaMemcpyHostToDevice, st));
-      dcoef = static_cast<const double*>(S->h_coef.p);
-    }
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(st);
+    const Staged d = stage_inputs(*S, ws, verts, n_verts, cells, n_cells, coef_kind, coef, coef_stride, st);
     const size_t esz = S->path == kPathF64 ? 8 : 4;
     const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
-    S->h_out.ensure(obytes);
-    run_cell_matrices(*S, static_cast<const double*>(S->h_verts.p), dcells, n_cells, coef_kind, dcoef,
-                      coef_stride, S->h_out.p, out_pitch, st, flags);
-    CUDA_OK(cudaMemcpyAsync(out, S->h_out.p, obytes, cudaMemcpyDeviceToHost, st));
+    ws.h_out.ensure(obytes + 16);
+    run_cell_matrices(*S, ws, d.verts, d.cells, n_cells, coef_kind, d.coef, coef_stride, ws.h_out.p,
+                      out_pitch, st, flags);
+    if (obytes) CUDA_OK(cudaMemcpyAsync(out, ws.h_out.p, obytes, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
+    S->take_error("");  // the call synchronized: report this call's singular cells now
   });
 }
 
@@ -1029,15 +898,13 @@ int mpfem_b200_scaled_weights(mpfem_b200_setup_t S, const double* verts, const i
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
     check_coef(*S, coef_kind, coef, coef_stride);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    CUDA_OK(cudaMemsetAsync(S->d_flags.p, 0, 4, st));
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(st);
+    S->take_error(" (reported on the device by an earlier call on this setup)");
+    CUDA_OK(cudaMemsetAsync(ws.d_flags.p, 0, 4, st));
     if (n_cells > 0)
-      launch_geom(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, out, S->k, 3, st);
-    if (flags) {
-      uint32_t h = 0;
-      CUDA_OK(cudaMemcpyAsync(&h, S->d_flags.p, 4, cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaStreamSynchronize(st));
-      *flags |= h;
-    }
+      launch_geom(*S, ws, verts, cells, n_cells, coef_kind, coef, coef_stride, out, S->k, 3, st);
+    finish_call(*S, ws, st, flags);
   });
 }
 
@@ -1047,8 +914,10 @@ int mpfem_b200_action(mpfem_b200_setup_t S, const double* verts, const int32_t* 
                       void* stream, uint32_t* flags) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    run_action(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, w, w_stride, out, out_pitch,
-               static_cast<cudaStream_t>(stream), flags);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(S->mu);
+    run_action(*S, S->workspace(st), verts, cells, n_cells, coef_kind, coef, coef_stride, w, w_stride,
+               out, out_pitch, st, flags);
   });
 }
 
@@ -1058,39 +927,27 @@ int mpfem_b200_action_host(mpfem_b200_setup_t S, const double* verts, int64_t n_
                            int64_t out_pitch, void* stream, uint32_t* flags) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    check_coef(*S, coef_kind, coef, coef_stride);  // host path: per-cell rows only
+    // one nodal z may be shared by the batch (stride 0), as in the device entry
+    check_coef(*S, coef_kind, coef, coef_kind == 3 && coef_stride == 0 ? S->n_phi : coef_stride);
     if (w_stride < S->n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+    if (n_cells < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative batch");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int nv = S->box ? 8 : 4;
-    const size_t vbytes = sizeof(double) * size_t(cells ? n_verts * 3 : n_cells * 3 * nv);
-    S->h_verts.ensure(vbytes + 8);
-    CUDA_OK(cudaMemcpyAsync(S->h_verts.p, verts, vbytes, cudaMemcpyHostToDevice, st));
-    const int32_t* dcells = nullptr;
-    if (cells) {
-      S->h_cells.ensure(sizeof(int32_t) * size_t(n_cells) * nv + 8);
-      CUDA_OK(cudaMemcpyAsync(S->h_cells.p, cells, sizeof(int32_t) * size_t(n_cells) * nv,
-                              cudaMemcpyHostToDevice, st));
-      dcells = static_cast<const int32_t*>(S->h_cells.p);
-    }
-    const double* dcoef = nullptr;
-    if (coef && (coef_kind == 2 || coef_kind == 3)) {
-      const size_t cb = sizeof(double) * size_t(n_cells) * size_t(coef_stride);
-      S->h_coef.ensure(cb + 8);
-      CUDA_OK(cudaMemcpyAsync(S->h_coef.p, coef, cb, cudaMemcpyHostToDevice, st));
-      dcoef = static_cast<const double*>(S->h_coef.p);
-    }
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(st);
+    const Staged d = stage_inputs(*S, ws, verts, n_verts, cells, n_cells, coef_kind, coef, coef_stride, st);
     // w and the result share one staging buffer: [w (n x w_stride fp64) | v]
     const size_t wbytes = sizeof(double) * size_t(n_cells) * size_t(w_stride);
     const size_t esz = S->uq == 3 ? 8 : 4;
     const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
-    S->h_out.ensure(wbytes + obytes + 16);
-    char* base = static_cast<char*>(S->h_out.p);
-    CUDA_OK(cudaMemcpyAsync(base, w, wbytes, cudaMemcpyHostToDevice, st));
+    ws.h_out.ensure(wbytes + obytes + 32);
+    char* base = static_cast<char*>(ws.h_out.p);
+    if (wbytes) CUDA_OK(cudaMemcpyAsync(base, w, wbytes, cudaMemcpyHostToDevice, st));
     void* dout = base + (wbytes + 15) / 16 * 16;
-    run_action(*S, static_cast<const double*>(S->h_verts.p), dcells, n_cells, coef_kind, dcoef,
-               coef_stride, reinterpret_cast<const double*>(base), w_stride, dout, out_pitch, st, flags);
-    CUDA_OK(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
+    run_action(*S, ws, d.verts, d.cells, n_cells, coef_kind, d.coef, coef_stride,
+               reinterpret_cast<const double*>(base), w_stride, dout, out_pitch, st, flags);
+    if (obytes) CUDA_OK(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
+    S->take_error("");
   });
 }
 
@@ -1098,6 +955,7 @@ namespace {
 void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells, int64_t n_cells,
                 int coef_kind, const double* coef, int64_t coef_stride, const double* w,
                 int64_t w_stride, double* out, double* a64, cudaStream_t st) {
+  S.take_error(" (reported on the device by an earlier call on this setup)");
   check_coef(S, coef_kind, coef, coef_stride);
   if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w && w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
@@ -1135,16 +993,13 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   P.w_stride = w_stride;
   P.box = S.box;
   P.ggrad64 = static_cast<const double*>(S.d_bnd_ggrad.p);
-  P.error = static_cast<int*>(S.d_error.p);
-  CUDA_OK(cudaMemsetAsync(S.d_error.p, 0, 4, st));
+  P.error = S.d_error;
   const int rc = w ? launch_action_bounds_kernel(P, device_sm_count(), st)
                    : launch_bounds_kernel(P, device_sm_count(), st);
   if (rc) throw Error(MPFEM_B200_RUNTIME_ERROR, "bound kernel attribute setup failed");
   CUDA_OK(cudaGetLastError());
-  int err = 0;
-  CUDA_OK(cudaMemcpyAsync(&err, S.d_error.p, 4, cudaMemcpyDeviceToHost, st));
   CUDA_OK(cudaStreamSynchronize(st));
-  if (err == 3) throw Error(MPFEM_B200_CHECK_ERROR, "singular cell geometry");
+  S.take_error("");
   S.last_launches = 1;
 }
 }  // namespace
@@ -1154,6 +1009,7 @@ int mpfem_b200_cell_bounds(mpfem_b200_setup_t S, const double* verts, const int3
                            double* out, double* a64, void* stream) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    std::lock_guard<std::mutex> lk(S->mu);
     run_bounds(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, nullptr, 0, out, a64,
                static_cast<cudaStream_t>(stream));
   });
@@ -1166,6 +1022,7 @@ int mpfem_b200_action_bounds(mpfem_b200_setup_t S, const double* verts, const in
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
     if (n_cells > 0 && !w) throw Error(MPFEM_B200_CONFIG_ERROR, "action bound needs w");
+    std::lock_guard<std::mutex> lk(S->mu);
     run_bounds(*S, verts, cells, n_cells, coef_kind, coef, coef_stride, w, w_stride, out, v64,
                static_cast<cudaStream_t>(stream));
   });
@@ -1173,21 +1030,12 @@ int mpfem_b200_action_bounds(mpfem_b200_setup_t S, const double* verts, const in
 
 int mpfem_b200_last_launch_count(mpfem_b200_setup_t S) { return S ? S->last_launches : 0; }
 
-int mpfem_b200_debug_trace(mpfem_b200_setup_t S, unsigned long long* host, int max_n) {
-  return guarded([&] {
-    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    if (!S->d_trace.p) throw Error(MPFEM_B200_CONFIG_ERROR, "tracing off (MPFEM_B200_TRACE=1)");
-    const size_t n = std::min<size_t>(size_t(max_n), S->d_trace.bytes / sizeof(unsigned long long));
-    CUDA_OK(cudaDeviceSynchronize());
-    CUDA_OK(cudaMemcpy(host, S->d_trace.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  });
-}
-
 int mpfem_b200_set_timing(mpfem_b200_setup_t S, int enable) {
   return guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    std::lock_guard<std::mutex> lk(S->mu);
     S->timing = enable != 0;
-    S->n_ev = 0;
+    if (S->last_ws) S->last_ws->n_ev = 0;
   });
 }
 
@@ -1195,9 +1043,12 @@ int mpfem_b200_last_timings(mpfem_b200_setup_t S, float* ms, int max_n) {
   int n = 0;
   int st = guarded([&] {
     if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
-    for (int i = 0; i + 1 < S->n_ev && n < max_n; ++i) {
-      CUDA_OK(cudaEventSynchronize(S->ev[i + 1]));
-      CUDA_OK(cudaEventElapsedTime(&ms[n++], S->ev[i], S->ev[i + 1]));
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace* w = S->last_ws;
+    if (!w) return;
+    for (int i = 0; i + 1 < w->n_ev && n < max_n; ++i) {
+      CUDA_OK(cudaEventSynchronize(w->ev[i + 1]));
+      CUDA_OK(cudaEventElapsedTime(&ms[n++], w->ev[i], w->ev[i + 1]));
     }
   });
   return st ? -st : n;

@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
     }
     TetGeometry g;
     if (!tet_geometry<UG>(v, FORM != 0, g, fl)) {
-      atomicExch(F.error, 3);
+      report_error(F.error, 3);  // singular cell: NaN row (CheckError reported by the host)
+      float* dst = F.out + cell * F.out_pitch;
+      for (int o = 0; o < NOUT; ++o) dst[o] = __int_as_float(0x7fc00000);
     } else {
       double v0[3], E[9];  // x, y pre-doubled (coef_sincosexp_*)
       #pragma unroll

@@ -1,27 +1,11 @@
-// cellmat_tc.cuh -- K2: all-cells GEMM on the 5th-generation tensor cores (sm_100a).
+// cellmat_tc.cuh -- shared pieces of the tcgen05 cell-matrix GEMM K2 (cellmat_tc2.cuh):
 //
 //   D^T[o, c] = sum_k Tt[o, k] * W[c, k]      o = (i, j) output entry, c = cell
 //
 // which is reference Algorithm 1 (kernels.cpp:242-267: A = sum_st B_s C_st B_t^T, one
 // depth-chained product over (s,t,q)) for every cell at once: the per-cell scaled
 // weights W (K1) are the B operand, the shared basis products Tt the A operand.
-//
-// Warp-specialised persistent kernel, one CTA per SM:
-//   warp 0      TMA producer: 128x64 Tt box + 256x64 W box per stage (SWIZZLE_128B)
-//   warp 1      MMA issuer: tcgen05.mma.cta_group::1.kind::f16, M=128 N=256 K=16,
-//               fp32 (or f16) accumulators in TMEM, two 256-column buffers
-//   warp 2      TMEM allocator (512 columns)
-//   warps 4-11  epilogue (two per TMEM lane quarter, half the columns each):
-//               tcgen05.ld 32x32b.x32 -> registers -> global. TMEM lane =
-//               output entry, column = cell, so one warp store writes 32 consecutive
-//               entries (128 B) of one cell's row-major matrix: coalesced, no staging.
-// Output rows come from a table P.rows (entry (i, j) per TMEM lane; default row-major, so a
-// warp store is 128 contiguous bytes of one cell). T is bitwise symmetric in (i, j), so
-// A_ij == A_ji bitwise; an experimental table (MPFEM_B200_SYMMETRIC=1) covers only the
-// upper triangle and writes each value to (i, j) and (j, i) -- fewer MMAs, but its 16/32-byte
-// store pieces make the register-resident epilogue LSU-bound (slower).
-// Tiles are ordered cell-block-major so the W block of a cell block is reused from L2
-// by the CTAs that work on its output tiles at the same time.
+// Kernel parameters, mbarrier / TMA / tcgen05 PTX wrappers, UMMA descriptors.
 #pragma once
 #include <cuda.h>
 #include <cuda_fp16.h>
@@ -34,24 +18,7 @@ namespace tc {
 #ifndef MPFEM_TC_BACKOFF_NS
 #define MPFEM_TC_BACKOFF_NS 256
 #endif
-constexpr int BM = 128;  // output entries per tile (MMA M, TMEM lanes)
-#ifndef MPFEM_TC_BN
-#define MPFEM_TC_BN 256
-#endif
-#ifndef MPFEM_TC_STAGES
-#define MPFEM_TC_STAGES 4
-#endif
-constexpr int BN = MPFEM_TC_BN;  // cells per tile (MMA N, TMEM columns per accumulator)
 constexpr int BK = 64;   // 16-bit elements per K block = one 128-byte swizzle row
-constexpr int STAGES = MPFEM_TC_STAGES;
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int EPI_WARPS = 8;      // two warps per TMEM lane quarter, each half the columns
-constexpr int EPI_SPLIT = EPI_WARPS / 4;
-constexpr int THREADS = 128 + EPI_WARPS * 32;
-constexpr int TMEM_COLS = 2 * BN >= 512 ? 512 : (2 * BN >= 256 ? 256 : 128);
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 
 struct Params {
   int64_t n_cells;
@@ -65,47 +32,11 @@ struct Params {
   int64_t out_pitch;
   uint32_t idesc;
   uint32_t* flags;
-  // Concurrent K1/K2: per-K1-tile W stamps (NULL: W complete at launch, stream order)
-  const uint32_t* ready;
-  uint32_t epoch;
-  int k1_tile;         // cells per K1 tile (stamp granularity)
-  int* error;          // set to 5 if a stamp never arrives (K1 not co-resident); error[1]
-                       // holds the epoch of the last timed-out call (later waits skip)
-  unsigned long long* trace;  // debug timeline (slots 1024..2047), NULL normally
   // Fused CSR scatter (pair kernel, OUTK != 0): instead of storing, entry (i, j) of cell c
   // is added into values[pos_map[c * n_out + i * n_phi + j]] (fp32 or fp64 values).
   const int32_t* pos_map;
   void* values;
 };
-
-// Producer-side wait for K1's W rows [c0, c1): acquire each K1 tile stamp, then order the
-// generic-proxy writes before this thread's async-proxy (TMA) reads. Bounded: after ~0.2 s
-// without progress it flags error 5 and returns, so a scheduling failure cannot hang the GPU.
-__device__ __forceinline__ void wait_w_ready(const Params& P, int64_t c0, int64_t c1) {
-  if (!P.ready) return;
-  if (c1 > P.n_cells) c1 = P.n_cells;
-  if (c0 >= c1) return;
-  const int64_t t0 = c0 / P.k1_tile, t1 = (c1 - 1) / P.k1_tile;
-  uint64_t start = 0;
-  for (int64_t t = t0; t <= t1; ++t) {
-    if (reinterpret_cast<volatile uint32_t*>(P.error)[1] == P.epoch) return;  // this call timed out
-    while (true) {
-      uint32_t v;
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.ready + t) : "memory");
-      if (v == P.epoch) break;
-      uint64_t now;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (!start) start = now;
-      else if (now - start > 200000000ull) {
-        atomicExch(P.error, 5);
-        atomicExch(reinterpret_cast<uint32_t*>(P.error) + 1, P.epoch);
-        return;
-      }
-      __nanosleep(200);
-    }
-  }
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -145,8 +76,8 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Waits that are not on the MMA critical path back off with nanosleep, so warps parked on
-// a barrier leave the issue slots to co-resident K1 CTAs.
+// Waits that are not on the MMA critical path back off with nanosleep, so parked warps leave
+// the issue slots to the working ones.
 __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(MPFEM_TC_BACKOFF_NS);
 }
@@ -214,159 +145,6 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&r)[32]) {
 __host__ __device__ constexpr uint32_t make_idesc(int ab_bf16, int d_f32, int m, int n) {
   return (uint32_t(d_f32 ? 1 : 0) << 4) | (uint32_t(ab_bf16) << 7) | (uint32_t(ab_bf16) << 10) |
          (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
-}
-
-template <bool ACC_F16>
-__global__ void __launch_bounds__(THREADS, 1)
-    cellmat_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const Params P) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int total_tiles = P.n_out_tiles * P.n_cell_tiles;
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
-        for (int kb = 0; kb < P.num_k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &tmA, kb * BK, ot * BM, &full[stage]);
-          tma_load_2d(sB + stage * B_BYTES, &tmB, kb * BK, ct * BN, &full[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0, acc = 0;
-      uint32_t phase = 0, acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1u);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
-        for (int kb = 0; kb < P.num_k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint64_t ad = make_smem_desc(sA + stage * A_BYTES);
-          const uint64_t bd = make_smem_desc(sB + stage * B_BYTES);
-          #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            mma_f16(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), P.idesc, (kb | kk) != 0);
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
-        }
-        mma_commit(&tfull[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
-      }
-    }
-  } else if (warp >= 4) {
-    // TMEM lane quarter = warp % 4 (hardware rule); the two warps of a quarter split the
-    // accumulator's 256 columns (cells) in halves.
-    const int quarter = warp & 3;
-    const int half = (warp - 4) >> 2;  // which 1/EPI_SPLIT of the columns
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    uint32_t expo_or = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int o = ot * BM + quarter * 32 + lane;
-      const int32_t e = P.rows[o];
-      const bool o_ok = e >= 0;
-      const int ei = e & 0xffff, ej = (e >> 16) & 0x3fff;
-      const int off_d = ei * P.n_phi + ej;                 // entry (i, j)
-      const int off_m = ej * P.n_phi + ei;                 // its mirror (j, i)
-      const bool mirror = o_ok && (e & (1 << 30));         // symmetric table only
-      #pragma unroll 1
-      for (int chunk = half * (BN / 32 / EPI_SPLIT); chunk < (half + 1) * (BN / 32 / EPI_SPLIT); ++chunk) {
-        uint32_t r[32];
-        tmem_ld_x32(tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN + chunk * 32), r);
-        const int64_t cell0 = int64_t(ct) * BN + chunk * 32;
-        if (o_ok) {
-          float* dst = P.out + cell0 * P.out_pitch + off_d;
-          const int64_t left = P.n_cells - cell0;
-          if (left >= 32 && !mirror) {  // common case: full chunk, row-major table
-            #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float v;
-              if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
-              else v = __uint_as_float(r[j]);
-              expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-              __stcs(dst, v);
-              dst += P.out_pitch;
-            }
-          } else {
-            float* base = P.out + cell0 * P.out_pitch;
-            #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < left) {
-                float v;
-                if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
-                else v = __uint_as_float(r[j]);
-                expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-                __stcs(base + off_d, v);
-                if (mirror) __stcs(base + off_m, v);
-              }
-              base += P.out_pitch;
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
-    }
-    expo_or = __reduce_or_sync(0xffffffffu, expo_or);
-    if (lane == 0 && expo_or && !(*reinterpret_cast<volatile uint32_t*>(P.flags) & 4u)) atomicOr(P.flags, 4u);
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
-                 : "memory");
-  }
 }
 
 }  // namespace tc

@@ -59,17 +59,6 @@ __device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t a, uint64_t b
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
-// multicast load: the box lands at the same offset in every CTA of `mask`; each
-// destination's complete_tx goes to its pair leader's barrier
-__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* map, int x, int y,
-                                                    uint64_t* bar, uint16_t mask) {
-  const uint32_t leader_bar = tc::smem_u32(bar) & kPeerMask;
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(tc::smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar), "h"(mask)
-      : "memory");
-}
 __device__ __forceinline__ void commit_pair(uint64_t* bar, uint16_t mask = 0x3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
@@ -82,14 +71,9 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
                : "memory");
 }
 
-// NP = CTA pairs per cluster. NP = 2: the two pairs take the same output tile and
-// consecutive cell tiles; each CTA loads half of its Tt rows and multicasts them to its
-// counterpart in the other pair (A is read from L2 once per cluster), and a stage is
-// refilled only after both pair leaders committed it (empty barriers count NP arrivals,
-// commits multicast to every CTA of the cluster).
 // OUTK: 0 = store the cell matrices (out, out_pitch); 1 / 2 = fused atomic CSR scatter into
 // fp32 / fp64 values through pos_map (the local matrices never reach HBM).
-template <bool ACC_F16, int NP, int OUTK = 0>
+template <bool ACC_F16, int OUTK = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     cellmat_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const tc::Params P) {
@@ -103,23 +87,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  trace_mark(P.trace, 1024 + (blockIdx.x & 1023), 0);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t crank = cluster_rank();
-  const uint32_t rank = crank & 1u;  // CTA within its pair
-  const uint32_t pr = crank >> 1;    // pair within the cluster
+  const uint32_t rank = cluster_rank();  // CTA within its pair
   const bool leader = rank == 0;
-  const int cluster = blockIdx.x / (2 * NP), n_clusters = gridDim.x / (2 * NP);
-  const int n_cg = (P.n_cell_tiles + NP - 1) / NP;
-  const int total_tiles = P.n_out_tiles * n_cg;  // cluster tiles
+  const int cluster = blockIdx.x / 2, n_clusters = gridDim.x / 2;
+  const int total_tiles = P.n_out_tiles * P.n_cell_tiles;  // pair tiles
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], NP);
+      tc::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull[a], 1);
@@ -145,19 +125,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
-        const int ct = (tile / P.n_out_tiles) * NP + int(pr), ot = tile % P.n_out_tiles;
-        // K1 running concurrently: this CTA's 128 W rows of the tile must be stamped
-        tc::wait_w_ready(P, int64_t(ct) * BN + int(rank) * BNC, int64_t(ct) * BN + int(rank + 1) * BNC);
+        const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
         for (int kb = 0; kb < P.num_k_blocks; ++kb) {
           tc::mbar_wait_backoff(&empty[stage], phase ^ 1u);
           if (leader) tc::mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
-          if constexpr (NP == 1) {
-            tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, ot * BM + int(rank) * BMC, &full[stage]);
-          } else {
-            tma_load_2d_pair_mc(sA + stage * A_BYTES + pr * (A_BYTES / 2), &tmA, kb * BK,
-                                ot * BM + int(rank) * BMC + int(pr) * (BMC / 2), &full[stage],
-                                uint16_t((1u << rank) | (1u << (2 + rank))));
-          }
+          tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, ot * BM + int(rank) * BMC, &full[stage]);
           tma_load_2d_pair(sB + stage * B_BYTES, &tmB, kb * BK, ct * BN + int(rank) * BNC, &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
@@ -176,17 +148,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tc_fence_after();
           const uint64_t ad = tc::make_smem_desc(sA + stage * A_BYTES);
           const uint64_t bd = tc::make_smem_desc(sB + stage * B_BYTES);
-#ifndef MPFEM_TC2_NOMMA  // diagnostic build only: operand stream + epilogue without MMAs
           #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             mma_pair(d_tmem, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), P.idesc, (kb | kk) != 0);
-#else
-          (void)ad; (void)bd;
-#endif
-          commit_pair(&empty[stage], NP == 1 ? uint16_t(0x3) : uint16_t(0xF));
+          commit_pair(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
-        commit_pair(&tfull[acc], uint16_t(0x3u << (2 * pr)));
+        commit_pair(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }
@@ -197,7 +165,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t acc_phase = 0;
     uint32_t expo_or = 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
-      const int ct = (tile / P.n_out_tiles) * NP + int(pr), ot = tile % P.n_out_tiles;
+      const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
       tc::mbar_wait_backoff(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int o = ot * BM + int(rank) * BMC + quarter * 32 + lane;
@@ -258,7 +226,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::tc_fence_before();
   __syncthreads();
   cluster_sync();  // the pair's MMAs and peer arrivals are done before TMEM is released
-  trace_mark(P.trace, 1024 + (blockIdx.x & 1023), 1);
   if (warp == 2) {
     tc::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),

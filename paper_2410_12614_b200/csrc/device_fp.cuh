@@ -12,18 +12,12 @@
 
 namespace mpfem_b200 {
 
-// Debug timeline (MPFEM_B200_TRACE=1): per CTA {start ns, end ns, SM id} in 3 words at
-// trace[3 * slot]. No-op when trace is NULL.
-__device__ __forceinline__ void trace_mark(unsigned long long* trace, int slot, int end) {
-  if (!trace || threadIdx.x != 0) return;
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  trace[3 * slot + end] = t;
-  if (!end) {
-    unsigned int sm;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-    trace[3 * slot + 2] = sm;
-  }
+// A CheckError found on the device (3: singular cell, geometry.cpp:42). `error` points at
+// host-mapped pinned memory owned by the setup, so the host sees it without a device copy
+// and reports it on the setup's next call or its synchronize (the reference throws
+// synchronously; an asynchronous stream can only defer). Every writer stores the same code.
+__device__ __forceinline__ void report_error(int* error, int code) {
+  *reinterpret_cast<volatile int*>(error) = code;
 }
 
 enum Fmt : int { kBF16 = 0, kFP16 = 1, kFP32 = 2, kFP64 = 3 };

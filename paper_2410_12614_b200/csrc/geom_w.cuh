@@ -62,23 +62,14 @@ struct GeomWParams {
   int w_type;              // 0 fp16 bits, 1 bf16 bits, 2 fp32, 3 fp64
   void* W;
   uint32_t* flags;
-  int* error;              // set to 3 on a singular cell
-  // Concurrent K1/K2 (see run_cell_matrices): after a tile's W rows are written, its
-  // stamp ready[tile] is set to `epoch` with release semantics; K2 acquires it before its
-  // TMA reads those rows. NULL: K2 runs after K1 in stream order.
-  uint32_t* ready;
-  uint32_t epoch;
-  unsigned long long* trace;  // debug timeline (slots 0..1023), NULL normally
+  int* error;              // set to 3 on a singular cell (host-mapped, see report_error)
   // Dynamic tile schedule: tile_ctr[0] hands out tiles gridDim.x, gridDim.x + 1, ... to
   // CTAs as they free up (static blockIdx.x first); tile_ctr[1] counts finished CTAs and
-  // the last one resets both to zero (no per-call memset). NULL: static grid stride.
+  // the last one resets both to zero (no per-call memset). One pair of words per stream
+  // workspace, so concurrent calls on different streams never share a counter.
   uint32_t* tile_ctr;
   int geom_warps;          // warps computing the next tile's geometry; tile = 32 * geom_warps cells
 };
-
-__device__ __forceinline__ void store_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // Storage rounding round_us(v) (one RNE conversion, subnormals kept) of a u_g value held
 // in double or float, returned in the element type T. FP events are accumulated cheaply
@@ -217,9 +208,9 @@ __device__ MPFEM_K1_GEOM_INLINE void cell_geometry(const GeomWParams& P, int64_t
   }
   TetGeometry g;
   if (!tet_geometry<UG>(v, P.poisson != 0, g, fl)) {
-    atomicExch(P.error, 3);
+    report_error(P.error, 3);
     #pragma unroll
-    for (int b = 0; b < 6; ++b) g.g[b] = 0.0;
+    for (int b = 0; b < 6; ++b) g.g[b] = __longlong_as_double(0x7ff8000000000000ll);  // singular: NaN row
   }
   #pragma unroll
   for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
@@ -285,7 +276,6 @@ __host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad, int geom_warp
 template <typename T, int UG, int US, int COEF>
 __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
   extern __shared__ double s_rule[];
-  trace_mark(P.trace, blockIdx.x & 1023, 0);
   __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
   __shared__ int64_t s_tile[3];   // claimed tiles, ring indexed by iteration mod 3
   const int nq = P.n_q;
@@ -312,14 +302,8 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
     return left < tcells ? int(left) : tcells;
   };
   // Tiles are claimed one iteration ahead of their geometry: static blockIdx.x first, then
-  // gridDim.x + atomicAdd(tile_ctr) (or the grid stride without a counter).
-  int64_t static_next = int64_t(blockIdx.x) + gridDim.x;
-  auto claim = [&]() -> int64_t {
-    if (P.tile_ctr) return int64_t(gridDim.x) + atomicAdd(P.tile_ctr, 1u);
-    const int64_t t = static_next;
-    static_next += gridDim.x;
-    return t;
-  };
+  // gridDim.x + atomicAdd(tile_ctr).
+  auto claim = [&]() -> int64_t { return int64_t(gridDim.x) + atomicAdd(P.tile_ctr, 1u); };
   // Tile pipeline: the first geom_warps warps compute the geometry of the CTA's next tile
   // (one lane per cell) into the other buffer while every warp takes 32-item grabs of the
   // current tile.
@@ -475,15 +459,10 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       }
     }
     __syncthreads();  // tile done, next tile's geometry written
-    if (threadIdx.x == 0) {
-      s_next[buf] = 0;
-      // cumulative release: the CTA's W stores (ordered before thread 0 by the barrier)
-      // are visible to a gpu-scope acquire of the stamp
-      if (P.ready) store_release_gpu(P.ready + tile, P.epoch);
-    }
+    if (threadIdx.x == 0) s_next[buf] = 0;
     tile = nt;
   }
-  if (P.tile_ctr && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     // every CTA made its final (failing) claim before counting itself done
     __threadfence();
     if (atomicAdd(P.tile_ctr + 1, 1u) == gridDim.x - 1) {
@@ -491,7 +470,6 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       P.tile_ctr[1] = 0;
     }
   }
-  trace_mark(P.trace, blockIdx.x & 1023, 1);
   if constexpr (sizeof(T) == 2 && (UG == kFP32 || UG == kFP64))
     publish_flags(P.flags, fl | packed_store_flags<T>(sf));
   else

@@ -38,17 +38,9 @@ template <int A, bool FTZ, int UGK, bool BOX>
 int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   ActionParams P = P0;
   // measured (scripts/action_sweep.py, P4): mass 128 threads / 36 KB tiles (230 vs 291 us),
-  // Poisson 256 threads / 70 KB tiles (710 vs 773 us); overridable for experiments
-  static const int env_threads = [] {
-    const char* e = std::getenv("MPFEM_B200_ACT_THREADS");
-    return e ? std::max(64, std::min(kActionThreads, std::atoi(e))) : 0;
-  }();
-  static const size_t env_budget = [] {
-    const char* e = std::getenv("MPFEM_B200_ACT_BUDGET_KB");
-    return e ? size_t(std::atoi(e)) * 1024 : 0;
-  }();
-  const int threads = env_threads ? env_threads : (P.n_d == 1 ? 128 : kActionThreads);
-  const size_t budget = env_budget ? env_budget : (P.n_d == 1 ? 36 * 1024 : 70 * 1024);
+  // Poisson 256 threads / 70 KB tiles (710 vs 773 us)
+  const int threads = P.n_d == 1 ? 128 : kActionThreads;
+  const size_t budget = P.n_d == 1 ? 36 * 1024 : 70 * 1024;
   int tile = pick_tile<A, BOX>(P.n_phi, P.n_q, P.n_d, budget, threads);
   int per_sm = std::max(1, std::min(int(224 * 1024 / std::max<size_t>(1, action_smem_bytes<A, BOX>(tile ? tile : kActionCBA, P.n_phi, P.n_q, P.n_d) + 1024)), 2048 / threads));
   if (!tile) {  // high degree in fp64: one CTA of kActionCBA cells per SM

@@ -198,14 +198,14 @@ __global__ void __launch_bounds__(kBoundThreads) cell_bounds_kernel(const BoundP
   for (int64_t cell = blockIdx.x; cell < P.n_cells; cell += gridDim.x) {
     if (threadIdx.x == 0) {
       s_ok = cell_diag(P, cell, poisson, sd);
-      if (!s_ok) atomicExch(P.error, 3);
+      if (!s_ok) report_error(P.error, 3);
     }
     __syncthreads();
     if (P.box) {
       for (int q = threadIdx.x; q < nq; q += blockDim.x)
         if (!box_point_diag(P, sd, q, poisson, pten + 9 * q, ptt + 9 * q, pkk[q])) {
           s_ok = 0;
-          atomicExch(P.error, 3);
+          report_error(P.error, 3);
         }
       __syncthreads();
     }
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kBoundThreads) cell_action_bounds_kernel(const
   for (int64_t cell = blockIdx.x; cell < P.n_cells; cell += gridDim.x) {
     if (threadIdx.x == 0) {
       s_ok = cell_diag(P, cell, poisson, sd);
-      if (!s_ok) atomicExch(P.error, 3);
+      if (!s_ok) report_error(P.error, 3);
     }
     __syncthreads();
     const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;

@@ -112,9 +112,9 @@ __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) 
       continue;
     }
     if (!geo_ok) {
-      atomicExch(P.error, 3);
+      report_error(P.error, 3);
       #pragma unroll
-      for (int b = 0; b < 6; ++b) geo.g[b] = 0.0;
+      for (int b = 0; b < 6; ++b) geo.g[b] = __longlong_as_double(0x7ff8000000000000ll);  // singular: NaN row
     }
     double zq = 1.0;
     const bool have_z = P.coef_kind != 0;

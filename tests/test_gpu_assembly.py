@@ -166,3 +166,40 @@ def test_fused_cell_kernels_scatter(oracle, mode, p):
         part = am.assemble_cells(s, vd, cd[k:], dm, pat, fmt, mp.CoefKind.sincosexp, cell_begin=k,
                                  accumulate=True, values=part).double()
         assert bool(((part - det).abs() <= tol).all()), (mode, fmt)
+
+
+@pytest.mark.parametrize("mode,p", [("mixed", 2), ("mixed_bf16", 3), ("fp64", 2), ("mixed", 1)])
+def test_fused_scatter_vs_oracle_assembly(oracle, mode, p):
+    """The fused kernel + atomic scatter against the reference assembly (oracle
+    assemble_matrix, assembly.cpp:41-88) of the binary64 oracle cell matrices. Per entry:
+    |fused - ref| <= gamma_{m+1}(fmt) sum|contrib| (test_assembly.cpp:165-167) plus, summed
+    over the contributing cells, each cell's own S * bound_a * max|A_c| (the kernel bound of
+    kernel_bounds, bounds.cpp:255-266, which the cell matrices meet)."""
+    from oracle_lib import COEF_SINCOSEXP, MODES, UNIT_ROUNDOFF
+    verts, cells = oracle.structured_tet_mesh(3, 3, 2, 1.0, 0.15, 13)
+    cdn, nd, mm = oracle.build_dofmap(p, verts, cells)
+    dm = gpu_dofmap(p, verts, cells)
+    pat = am.csr_pattern(dm)
+    cfg = mp.mode_config(mode, mp.FormKind.poisson)
+    s = mp.make_setup(p, cfg)
+    ct = (int(cfg.u_p), int(cfg.u_g), int(cfg.u_q), int(cfg.u_s), int(cfg.engine))
+    us = UNIT_ROUNDOFF[int(cfg.u_s)]
+    S = 4.0 if all(us > UNIT_ROUNDOFF[int(f)] for f in (cfg.u_p, cfg.u_g, cfg.u_q)) else 1.0
+    a64 = np.zeros((cells.shape[0], nphi(p), nphi(p)))
+    tol_loc = np.zeros_like(a64)
+    for c in range(cells.shape[0]):
+        b, a = oracle.bound(p, 1, ct, verts[cells[c]], COEF_SINCOSEXP)
+        a64[c] = a
+        tol_loc[c] = S * b[0] * np.max(np.abs(a))
+    _, _, ref, _ = oracle.assemble_matrix(cdn, nd, a64, 3)
+    _, _, mag, _ = oracle.assemble_matrix(cdn, nd, np.abs(a64), 3)
+    _, _, cell_tol, _ = oracle.assemble_matrix(cdn, nd, tol_loc, 3)
+    vd = torch.from_numpy(verts).cuda()
+    cd = torch.from_numpy(np.ascontiguousarray(cells)).cuda()
+    for fmt in (2, 3):
+        u = 2.0 ** -24 if fmt == 2 else 2.0 ** -53
+        g = (mm + 1) * u / (1 - (mm + 1) * u)
+        fused = am.assemble_cells(s, vd, cd, dm, pat, fmt, mp.CoefKind.sincosexp).double().cpu().numpy()
+        assert pat.nnz == ref.size
+        bad = np.abs(fused - ref) > g * mag * 1.0001 + cell_tol
+        assert not bad.any(), (mode, fmt, int(bad.sum()))

@@ -165,14 +165,28 @@ def test_extreme_geometry_fp_events_match_build_C(oracle, tets, mode, form):
 
 @pytest.mark.parametrize("p", [5, 6, 7, 8])
 @pytest.mark.parametrize("form", [MASS, POISSON])
-def test_high_degree_mixed_and_fp64(oracle, tets, p, form):
-    for mode in ("mixed_bf16", "fp64"):
+def test_high_degree_all_modes(oracle, tets, p, form):
+    """p = 5..8 (56 to 165 dofs, up to 729 rule points) in every mode, 8 cells each: every
+    cell within S * bound_a of the fp64 oracle; BASELINE's "mixed" (fp16 storage, fp32
+    accumulation, the scalar-engine config of test_bounds.cpp:75-76) and fp16 also within
+    2 S bound_a of the reference's same-mode output (kernels.cpp:242-267)."""
+    n = 8
+    for mode in ("mixed", "fp16", "mixed_bf16", "fp64"):
         cfg = kconfig(mode, form)
         s = mp.make_setup(p, cfg)
-        a_gpu = run_gpu(s, tets[:2], COEF_SINCOSEXP, None)
-        b, a64 = oracle.bound(p, form, cfg_tuple(cfg), tets[0], COEF_SINCOSEXP, None)
-        err = np.max(np.abs(a_gpu[0] - a64)) / np.max(np.abs(a64))
-        assert err <= slack(cfg) * b[0], (mode, err, b[0])
+        a_gpu = run_gpu(s, tets[:n], COEF_SINCOSEXP, None)
+        same = mode in ("mixed", "fp16")
+        if same:
+            a_same, _ = oracle.bilinear(p, form, cfg_tuple(cfg), tets[:n], COEF_SINCOSEXP, None)
+        S = slack(cfg)
+        for c in range(n):
+            b, a64 = oracle.bound(p, form, cfg_tuple(cfg), tets[c], COEF_SINCOSEXP, None)
+            scale = np.max(np.abs(a64))
+            err = np.max(np.abs(a_gpu[c] - a64)) / scale
+            assert err <= S * b[0], (mode, c, err, b[0])
+            if same:
+                d_same = np.max(np.abs(a_gpu[c] - a_same[c])) / scale
+                assert d_same <= 2 * S * b[0], (mode, c, d_same, b[0])
 
 
 def test_fp16_storage_high_degree_reports_underflow(oracle, tets):
@@ -294,3 +308,48 @@ def test_full_config_sizes_properties(oracle):
             err = np.max(np.abs(an[c] - ref)) / np.max(np.abs(ref))
             assert err <= slack(cfg) * b[0]
         assert np.all(np.isfinite(an))
+
+
+def test_singular_cell_check_error_without_flags(tets):
+    """geometry.cpp:42 throws CheckError on a singular pivot. The asynchronous call without
+    flags cannot throw in place: the singular cell's row is NaN and the CheckError is raised
+    by synchronize() (or by the next call on the setup), after which the setup is usable."""
+    s = mp.make_setup(2, kconfig("mixed", POISSON))
+    bad = tets[:3].copy()
+    bad[1, 3] = bad[1, 0]
+    out = s.cell_matrices(dev(bad), None, COEF_ONE)
+    with pytest.raises(mp.CheckError):
+        s.synchronize()
+    a = out.double().cpu().numpy()
+    assert np.all(np.isnan(a[1])) and np.all(np.isfinite(a[[0, 2]]))
+    s.synchronize()  # reported once
+    s.cell_matrices(dev(bad), None, COEF_ONE)
+    torch.cuda.synchronize()
+    with pytest.raises(mp.CheckError):  # the next call reports it
+        s.cell_matrices(dev(tets[:2]), None, COEF_ONE)
+    ok = run_gpu(s, tets[:2], COEF_ONE, None)
+    assert np.all(np.isfinite(ok))
+    # host-buffer call synchronizes: raises in place
+    with pytest.raises(mp.CheckError):
+        s.cell_matrices_host(bad, None, COEF_ONE)
+
+
+def test_two_streams_share_one_setup(tets):
+    """One setup used concurrently from two streams (per-stream workspaces: W scratch, K1
+    tile counter, flags): every result equals the single-stream result bit for bit."""
+    s = mp.make_setup(4, kconfig("mixed", POISSON, geometry_fp64=True))
+    va, vb = dev(tets[:700]), dev(tets[300:1000])
+    ref_a = s.cell_matrices(va, None, COEF_SINCOSEXP).clone()
+    ref_b = s.cell_matrices(vb, None, COEF_SINCOSEXP).clone()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(8):
+        with torch.cuda.stream(sa):
+            oa = s.cell_matrices(va, None, COEF_SINCOSEXP, stream=sa)
+        with torch.cuda.stream(sb):
+            ob = s.cell_matrices(vb, None, COEF_SINCOSEXP, stream=sb)
+        outs.append((oa, ob))
+    torch.cuda.synchronize()
+    for oa, ob in outs:
+        assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
