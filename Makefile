@@ -3,7 +3,7 @@ NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2410_12614_b200
 LIB := $(PKG)/lib/libmpfem_b200.so
 OBJDIR := $(PKG)/lib/obj
-CU_SRCS := capi assembly_capi launch_geom launch_geom_box launch_fused launch_action launch_bounds
+CU_SRCS := capi assembly_capi launch_geom launch_geom_box launch_fused launch_action launch_bounds geom_tensor assembly_host
 CPP_SRCS := host_setup host_mesh
 OBJS := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU_SRCS) $(CPP_SRCS)))
 HDRS := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.hpp) include/mpfem_b200.h

@@ -72,6 +72,45 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
                             mpfem_b200_setup_t* out);
 int mpfem_b200_setup_destroy(mpfem_b200_setup_t setup);
 
+/* make_setup from the caller's own rule and tabulations (kernels.cpp:78-108 having run on the
+ * reference side): the C++ drop-in shim (include/mpfem/batched.hpp) creates its device setup
+ * from the reference KernelSetup this way, so any rule (the make_setup overload with an
+ * explicit QuadratureRule, kernels.hpp:62) and dimension 2 or 3 are accepted.
+ *   points:    n_q x dim rule points; weights: n_q
+ *   tab_store: n_d x n_phi x n_q, KernelSetup::tab_store (evaluated at u_p, stored at u_s;
+ *              n_d = dim for Poisson, 1 for mass)
+ *   tab_up:    n_phi x n_q, KernelSetup::tab_values (basis values at u_p)
+ * p is informational. Such a setup takes geometry tensors (the two calls below), not vertices;
+ * GPU bounds need the vertex setup. */
+int mpfem_b200_setup_create_tab(int cell_kind, int dim, int p, int form, int u_p, int u_g,
+                                int u_q, int u_s, int engine, int n_batch, int n_phi, int n_q,
+                                const double* points, const double* weights,
+                                const double* tab_store, const double* tab_up,
+                                mpfem_b200_setup_t* out);
+
+/* bilinear_kernel(setup, geom, z, flags) (kernels.hpp:85-86) for n_cells cells whose geometry
+ * the caller already evaluated (GeometryData, geometry.hpp:31-41), on HOST buffers:
+ *   G:   n_cells x n_pts x n_d x n_d geometry tensors at u_g (GeometryPoint::tensor, row-major),
+ *        n_pts = 1 (affine cells) or n_q (one entry per rule point)
+ *   z:   NULL (constant one) or nodal coefficients, n_cells rows of z_stride doubles
+ *        (z_stride = 0: one vector shared by every cell)
+ *   out: n_cells x out_pitch, fp32 for u_q in {fp16, fp32}, fp64 for u_q = fp64
+ * W is build_C's C bit for bit (kernels.cpp:177-197); the matrices meet the same tolerances as
+ * mpfem_b200_cell_matrices. Synchronizes. */
+int mpfem_b200_bilinear_from_geometry(mpfem_b200_setup_t setup, const double* G, int n_pts,
+                                      int64_t n_cells, const double* z, int64_t z_stride,
+                                      void* out, int64_t out_pitch, void* stream,
+                                      uint32_t* flags);
+
+/* action_kernel(setup, geoms, w, z, flags) (kernels.hpp:90-92) on HOST buffers with the caller's
+ * geometry tensors (as above, dimension 3): z NULL or one nodal vector (n_phi) shared by the
+ * batch; w n_cells rows of w_stride doubles; out n_cells x out_pitch (row c = the reference's
+ * column c). Bit-identical to the reference in every mode. Synchronizes. */
+int mpfem_b200_action_from_geometry(mpfem_b200_setup_t setup, const double* G, int n_pts,
+                                    int64_t n_cells, const double* z, const double* w,
+                                    int64_t w_stride, void* out, int64_t out_pitch, void* stream,
+                                    uint32_t* flags);
+
 /* Sizes: n_phi, n_q, n_d (1 mass, 3 poisson), K (GEMM depth = blocks x nq_pad), K_pad,
  * path (0 tcgen05, 1 fp32 FFMA, 2 fp64, 3 fused small-degree). */
 int mpfem_b200_setup_info(mpfem_b200_setup_t setup, int* n_phi, int* n_q, int* n_d,
@@ -209,6 +248,14 @@ int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_ve
                       int32_t* cell_dofs, int32_t* n_dofs, int32_t* max_multiplicity,
                       void* stream);
 
+/* The same for either cell kind: cell_kind 0 tets (cells n_cells x 4), 1 hexahedra (cells
+ * n_cells x 8 in lattice-bit order, tensor Lagrange nodes axis 0 fastest). Hexahedral nodes are
+ * keyed by their sub-entity's vertex ids and coordinates in an id-fixed frame, so any
+ * conforming mesh numbers like the reference's geometric identification. */
+int mpfem_b200_dofmap_cells(int cell_kind, int p, const int32_t* cells, int64_t n_cells,
+                            int64_t n_verts, int32_t* cell_dofs, int32_t* n_dofs,
+                            int32_t* max_multiplicity, void* stream);
+
 /* Sparsity pattern = the reference COO key set sorted by (row, col) (assembly.cpp:67-86)
  * as CSR. Two-phase: call with col_idx == NULL to get nnz into *nnz and row_ptr
  * (n_dofs + 1 int64, device) filled; then again with col_idx (nnz int32, device). */
@@ -256,6 +303,33 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
                              int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
                              const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
                              void* values, int fmt, int accumulate, void* stream);
+
+/* ---------------------------------------------------------------- host-buffer assembly
+ * The calls behind the C++ drop-in build_dofmap / assemble_matrix (include/mpfem/batched.hpp):
+ * host arrays in and out, all index and value work on the GPU. */
+
+/* build_dofmap(mesh, basis(cell_kind, dim, p), continuity) (mesh.hpp:61, mesh.cpp:204-298).
+ * continuous: 3D tetrahedral or hexahedral meshes (cells n_cells x 4 or x 8 vertex ids), first-
+ * encounter numbering as mpfem_b200_dofmap_cells; discontinuous: any cell kind, every cell
+ * numbers its own n_loc dofs. cell_dofs: n_cells x n_loc int32 (host). */
+int mpfem_b200_dofmap_host(int cell_kind, int dim, int p, int continuous, const int32_t* cells,
+                           int64_t n_cells, int64_t n_verts, int32_t* cell_dofs, int32_t* n_dofs,
+                           int32_t* max_multiplicity);
+
+/* Assembly plan of a dof map: CSR pattern (the reference COO key set, assembly.cpp:67-86) and
+ * the deterministic scatter plan, built on the GPU. CheckError (3) for a dof out of range
+ * (assembly.cpp:31-37). */
+typedef struct mpfem_b200_asm_plan_s* mpfem_b200_asm_plan_t;
+int mpfem_b200_asm_plan_create(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                               mpfem_b200_asm_plan_t* out, int64_t* nnz);
+/* row_ptr: n_dofs + 1 int64, col_idx: nnz int32 (host; either may be NULL). */
+int mpfem_b200_asm_plan_pattern(mpfem_b200_asm_plan_t plan, int64_t* row_ptr, int32_t* col_idx);
+/* assemble_matrix(locals, dofmap, fmt, flags) (assembly.cpp:41-88) in the deterministic mode:
+ * locals n_cells x n_loc x n_loc binary64 (host), values nnz binary64 carriers of fmt (host),
+ * bitwise the reference's sequential sum for every fmt (0 bf16, 1 fp16, 2 fp32, 3 fp64). */
+int mpfem_b200_asm_plan_assemble(mpfem_b200_asm_plan_t plan, const double* locals, int fmt,
+                                 double* values, uint32_t* flags);
+int mpfem_b200_asm_plan_destroy(mpfem_b200_asm_plan_t plan);
 
 #ifdef __cplusplus
 }

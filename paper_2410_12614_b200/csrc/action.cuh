@@ -60,6 +60,11 @@ struct ActionParams {
   int* error;
   int box;               // hexahedra: geometry at every rule point
   const double* ggrad;   // box: degree-1 gradients at u_g, (s * 8 + k) * n_q + q
+  // Geometry given by the caller (the drop-in C++ API hands over GeometryData,
+  // geometry.hpp:31-41): n_cells x g_pts x n_d x n_d tensors at u_g, g_pts = 1 (affine) or
+  // n_q (one per rule point). NULL: evaluated from the vertices.
+  const double* G;
+  int g_pts;
 };
 
 constexpr int kActionThreads = 256;
@@ -203,6 +208,17 @@ __device__ __forceinline__ bool box_g_at(const ActionParams& P, const double* ge
 template <bool BOX>
 __device__ __forceinline__ void cell_geo_row(const ActionParams& P, int64_t cell, double* geo,
                                              uint32_t& fl) {
+  if (P.G) {  // given tensors: packed upper triangle of the cell's (first) entry
+    const int nd = P.n_d;
+    const double* g = P.G + cell * P.g_pts * nd * nd;
+    for (int b = 0; b < 6; ++b) geo[b] = 0.0;
+    if (nd == 1) geo[0] = g[0];
+    else
+      for (int s = 0, b = 0; s < 3; ++s)
+        for (int t = s; t < 3; ++t, ++b) geo[b] = g[s * 3 + t];
+    for (int j = 6; j < geo_words<BOX>(); ++j) geo[j] = 0.0;
+    return;
+  }
   if constexpr (BOX) {  // hexahedra: the vertices; the geometry is evaluated per point in the r stage
     for (int k = 0; k < 8; ++k) {
       const int64_t base = P.cells ? int64_t(P.cells[cell * 8 + k]) * 3 : cell * 24 + k * 3;
@@ -330,7 +346,14 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
       for (int t = 0; t < nd; ++t) wt[t] = sWH[size_t(t * nq + q) * C + c];
       double gbox[6];
       const double* gsrc = geo;
-      if constexpr (BOX) {  // hexahedra: the geometry at this rule point
+      if (P.G && P.g_pts > 1) {  // given per-point tensors (non-affine cells)
+        const double* g = P.G + ((c0 + (c < nc ? c : 0)) * P.g_pts + q) * nd * nd;
+        if (nd == 1) gbox[0] = g[0];
+        else
+          for (int s = 0, b = 0; s < 3; ++s)
+            for (int t = s; t < 3; ++t, ++b) gbox[b] = g[s * 3 + t];
+        gsrc = gbox;
+      } else if constexpr (BOX) {  // hexahedra: the geometry at this rule point
         TetGeometry tg;
         if (c < nc && !box_g_at<UGK>(P, geo, q, tg, fl)) {
           report_error(P.error, 3);

@@ -91,6 +91,70 @@ __global__ void node_keys_kernel(const int32_t* __restrict__ cells, int64_t n_ce
   }
 }
 
+// Node keys of hexahedral (box) cells: cells n x 8 vertex ids in lattice-bit order (mesh.hpp:
+// 15-24), local node k = lattice point (c0, c1, c2) in [0, p]^3, axis 0 fastest (elements.cpp:
+// 50-87). The node lies on the sub-entity spanned by its non-boundary axes; its key is that
+// entity's vertices and the node's coordinates in a frame fixed by the vertex ids alone, so
+// every cell sharing the entity computes the same key whatever its local orientation:
+//   vertex: (v);  edge: (min, max, t measured from min);  face: (origin = min id, its two
+//   face neighbours ordered by id, coordinates along those);  interior: (cell, k).
+__global__ void node_keys_box_kernel(const int32_t* __restrict__ cells, int64_t n_cells, int p,
+                                     uint64_t* __restrict__ key_hi, uint64_t* __restrict__ key_lo,
+                                     int32_t* __restrict__ pos) {
+  const int n1 = p + 1, n_phi = n1 * n1 * n1;
+  const int64_t total = n_cells * n_phi;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = i / n_phi;
+    const int k = int(i % n_phi);
+    const int co[3] = {k % n1, (k / n1) % n1, k / (n1 * n1)};
+    int fixed_bits = 0, free_ax[3], nf = 0;
+    for (int a = 0; a < 3; ++a) {
+      if (co[a] == p) fixed_bits |= 1 << a;
+      else if (co[a] != 0) free_ax[nf++] = a;
+    }
+    auto vid = [&](int b) { return uint64_t(cells[c * 8 + b]) + 1; };
+    uint64_t hi, lo;
+    if (nf == 3) {
+      hi = (uint64_t(1) << 63) | uint64_t(c);
+      lo = uint64_t(k);
+    } else if (nf == 0) {
+      hi = vid(fixed_bits);
+      lo = 1;
+    } else if (nf == 1) {
+      const int a = free_ax[0];
+      uint64_t va = vid(fixed_bits), vb = vid(fixed_bits | (1 << a));
+      int t = co[a];
+      if (vb < va) {
+        const uint64_t tmp = va; va = vb; vb = tmp;
+        t = p - t;
+      }
+      hi = (va << 21) | vb;
+      lo = 2 | (uint64_t(t) << 8);
+    } else {
+      const int a1 = free_ax[0], a2 = free_ax[1];
+      uint64_t f[2][2];
+      for (int s1 = 0; s1 < 2; ++s1)
+        for (int s2 = 0; s2 < 2; ++s2) f[s1][s2] = vid(fixed_bits | (s1 << a1) | (s2 << a2));
+      int o1 = 0, o2 = 0;
+      for (int s1 = 0; s1 < 2; ++s1)
+        for (int s2 = 0; s2 < 2; ++s2)
+          if (f[s1][s2] < f[o1][o2]) { o1 = s1; o2 = s2; }
+      int t1 = o1 ? p - co[a1] : co[a1], t2 = o2 ? p - co[a2] : co[a2];
+      uint64_t nA = f[1 - o1][o2], nB = f[o1][1 - o2];
+      if (nB < nA) {
+        const uint64_t tmp = nA; nA = nB; nB = tmp;
+        const int tt = t1; t1 = t2; t2 = tt;
+      }
+      hi = (f[o1][o2] << 42) | (nA << 21) | nB;
+      lo = 3 | (uint64_t(t1) << 8) | (uint64_t(t2) << 16);
+    }
+    key_hi[i] = hi;
+    key_lo[i] = lo;
+    pos[i] = int32_t(i);
+  }
+}
+
 // flags[pos] = 1 where the sorted entry starts a new key (first encounter).
 __global__ void first_flags_kernel(const uint64_t* __restrict__ hi, const uint64_t* __restrict__ lo,
                                    const int32_t* __restrict__ pos, int64_t n,

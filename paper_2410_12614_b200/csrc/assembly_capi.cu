@@ -145,31 +145,37 @@ int64_t max_count(const int64_t* inc_ptr, int32_t n_dofs, Scratch& S) {
 
 extern "C" {
 
-int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_verts,
-                      int32_t* cell_dofs, int32_t* n_dofs, int32_t* max_multiplicity,
-                      void* stream) {
+int mpfem_b200_dofmap_cells(int cell_kind, int p, const int32_t* cells, int64_t n_cells,
+                            int64_t n_verts, int32_t* cell_dofs, int32_t* n_dofs,
+                            int32_t* max_multiplicity, void* stream) {
   return aguard([&] {
+    if (cell_kind != 0 && cell_kind != 1) throw AsmError{2, "cell kind must be 0 (tets) or 1 (hexahedra)"};
+    const bool box = cell_kind == 1;
     if (p < 1 || p > 8) throw AsmError{2, "element degree must be in [1, 8]"};
     if (n_cells < 1) throw AsmError{2, "dof map needs at least one cell"};
     if (n_verts >= (int64_t(1) << 21) - 1)
       throw AsmError{2, "vertex ids must fit 21 bits for the packed node keys"};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch S(st);
-    const int n_phi = (p + 1) * (p + 2) * (p + 3) / 6;
+    const int n_phi = box ? (p + 1) * (p + 1) * (p + 1) : (p + 1) * (p + 2) * (p + 3) / 6;
     const int64_t n = n_cells * n_phi;
     if (n >= (int64_t(1) << 31)) throw AsmError{2, "n_cells * n_phi must fit int32"};
-    std::vector<int8_t> al(size_t(n_phi) * 4);
-    for (int k = 0; k < n_phi; ++k) {
-      int a[4];
-      asmb::node_alpha(p, k, a);
-      for (int t = 0; t < 4; ++t) al[size_t(k) * 4 + t] = int8_t(a[t]);
-    }
-    int8_t* d_al = S.get<int8_t>(al.size());
-    ACUDA(cudaMemcpyAsync(d_al, al.data(), al.size(), cudaMemcpyHostToDevice, st));
     uint64_t* hi = S.get<uint64_t>(n);
     uint64_t* lo = S.get<uint64_t>(n);
     int32_t* pos = S.get<int32_t>(n);
-    asmb::node_keys_kernel<<<grid_for(n), 256, 0, st>>>(cells, n_cells, p, n_phi, d_al, hi, lo, pos);
+    if (box) {
+      asmb::node_keys_box_kernel<<<grid_for(n), 256, 0, st>>>(cells, n_cells, p, hi, lo, pos);
+    } else {
+      std::vector<int8_t> al(size_t(n_phi) * 4);
+      for (int k = 0; k < n_phi; ++k) {
+        int a[4];
+        asmb::node_alpha(p, k, a);
+        for (int t = 0; t < 4; ++t) al[size_t(k) * 4 + t] = int8_t(a[t]);
+      }
+      int8_t* d_al = S.get<int8_t>(al.size());
+      ACUDA(cudaMemcpyAsync(d_al, al.data(), al.size(), cudaMemcpyHostToDevice, st));
+      asmb::node_keys_kernel<<<grid_for(n), 256, 0, st>>>(cells, n_cells, p, n_phi, d_al, hi, lo, pos);
+    }
     ACUDA(cudaGetLastError());
     // LSD: stable sort by lo, then by hi -> order (hi, lo, position)
     uint64_t* k1 = S.get<uint64_t>(n);
@@ -216,6 +222,13 @@ int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_ve
   });
 }
 
+int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_verts,
+                      int32_t* cell_dofs, int32_t* n_dofs, int32_t* max_multiplicity,
+                      void* stream) {
+  return mpfem_b200_dofmap_cells(0, p, cells, n_cells, n_verts, cell_dofs, n_dofs, max_multiplicity,
+                                 stream);
+}
+
 int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
                          int64_t* inc_ptr, int64_t* inc, void* stream) {
   return aguard([&] {
@@ -238,7 +251,8 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
     build_incidence(cell_dofs, n, n_dofs, inc_ptr, inc, S);
     const int64_t mmax = max_count(inc_ptr, n_dofs, S);
     if (mmax * n_loc > 8192) throw AsmError{2, "row candidate list exceeds 8192 (multiplicity x n_loc)"};
-    int hcap = 32;
+    // table of hcap slots + a sort list of hcap / 2 >= 32 (the bitonic sort pads to >= 32)
+    int hcap = 64;
     while (hcap < 2 * mmax * n_loc) hcap <<= 1;
     const size_t per_warp = size_t(hcap + hcap / 2) * 4;
     const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (48u << 10) / per_warp)));

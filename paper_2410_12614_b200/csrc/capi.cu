@@ -19,10 +19,13 @@
 #include "action.cuh"
 #include "bounds.cuh"
 #include "cellmat_fused.cuh"
+#include "cellmat_dmma.cuh"
 #include "cellmat_simt.cuh"
 #include "cellmat_tc.cuh"
 #include "cellmat_tc2.cuh"
+#include "cellmat_tcs.cuh"
 #include "geom_box.cuh"
+#include "geom_tensor.cuh"
 #include "geom_w.cuh"
 #include "host_setup.hpp"
 
@@ -164,8 +167,14 @@ struct mpfem_b200_setup_s {
   int path = kPathF64;
   int acc_f16 = 0;
   int w_type = 3;  // element type of W / T: 0 fp16, 1 bf16, 2 fp32, 3 fp64
+  // from_tab: created from the caller's rule and tabulations (mpfem_b200_setup_create_tab,
+  // the C++ drop-in shim); such setups take geometry tensors, not vertices
+  int from_tab = 0, dim = 3;
+  std::vector<double> tab_store_host;  // the store tabulation (action contractions)
   Rule rule;
-  DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_T, d_rows;
+  // d_B: binary64 tabulation (bounds); d_Bs: the store tabulation (evaluated at u_p, stored at
+  // u_s, tab_store of kernels.cpp:86-98) from which the GEMM operand T is built
+  DevBuf d_rule_w, d_rule_w_ug, d_rule_x, d_tab_up, d_B, d_Bs, d_T, d_rows;
   int n_rows = 0;  // tcgen05 path: rows of Tt (output-row table, padded to the pair tile)
   // action (Algorithm 2): store tabulation in the u_p / u_q compute types, built on first use
   DevBuf d_act_a, d_act_c;
@@ -239,7 +248,7 @@ void choose_path(mpfem_b200_setup_s& S) {
   const int us = S.us, uq = S.uq;
   // Tiny GEMM depth (K <= 48) and small matrices: one thread per cell runs the whole
   // path in registers (cellmat_fused.cuh); fp32 accumulation of u_s-rounded operands.
-  if (!S.box && uq == 2 && us <= 2 && (S.ug == 2 || S.ug == 3) && (S.p == 1 || (S.p == 2 && S.form == 0))) {
+  if (!S.box && !S.from_tab && uq == 2 && us <= 2 && (S.ug == 2 || S.ug == 3) && (S.p == 1 || (S.p == 2 && S.form == 0))) {
     S.path = kPathFused;
     S.w_type = us == 2 ? 2 : (us == 1 ? 0 : 1);
     return;
@@ -381,9 +390,48 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, OUTK>, ta, tb, P));
 }
 
+template <bool ACC_F16>
+void launch_tcs(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    CUDA_OK(cudaFuncSetAttribute(tcs::cellmat_tcs_kernel<ACC_F16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tcs::SMEM_BYTES));
+    attr = true;
+  }
+  const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
+  const unsigned grid = unsigned(std::min<int64_t>(tiles, device_sm_count()));
+  tcs::cellmat_tcs_kernel<ACC_F16><<<grid, tcs::THREADS, tcs::SMEM_BYTES, st>>>(ta, tb, P);
+}
+
+// The staged-epilogue kernel (cellmat_tcs.cuh) serves the HBM-bound shapes: short GEMM depth,
+// where the output stream, not the operand stream, bounds K2.
+bool use_tcs(const mpfem_b200_setup_s& S, const void* out) {
+  return S.path == kPathTC && S.k_pad <= 256 && S.n_out_pad % tcs::BO == 0 &&
+         (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+}
+
 void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void* out,
                  int64_t out_pitch, cudaStream_t st, const Scatter* sc) {
-  if (S.path == kPathTC) {
+  if (S.path == kPathTC && !sc && use_tcs(S, out)) {
+    const CUtensorMapDataType dt =
+        S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tcs::BM);
+    CUtensorMap tb = make_map_2d(W, dt, uint64_t(S.k_pad), uint64_t(n), tc::BK, tcs::BN);
+    tc::Params P{};
+    P.n_cells = n;
+    P.n_out = int(S.n_out);
+    P.n_phi = S.n_phi;
+    P.rows = static_cast<const int32_t*>(S.d_rows.p);
+    P.n_out_tiles = int(S.n_out_pad / tcs::BO);
+    P.n_cell_tiles = int((n + tcs::BN - 1) / tcs::BN);
+    P.num_k_blocks = int(S.k_pad / tc::BK);
+    P.out = static_cast<float*>(out);
+    P.out_pitch = out_pitch;
+    P.idesc = tc::make_idesc(S.w_type == 1, !S.acc_f16, tcs::BM, tcs::BN);
+    P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+    if (S.acc_f16) launch_tcs<true>(ta, tb, P, st);
+    else launch_tcs<false>(ta, tb, P, st);
+  } else if (S.path == kPathTC) {
     const CUtensorMapDataType dt =
         S.w_type == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap ta = make_map_2d(S.d_T.p, dt, uint64_t(S.k_pad), uint64_t(S.n_out_pad), tc::BK, tc2::BMC);
@@ -422,9 +470,15 @@ void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void*
         static_cast<const float*>(W), static_cast<const float*>(S.d_T.p), static_cast<float*>(out),
         n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
   } else {
-    constexpr int BM = 64, BN = 128, BK = 16, TM = 4, TN = 8;
-    dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
-    cellmat_simt_kernel<double, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
+    // fp64 accumulation: DMMA (cellmat_dmma.cuh)
+    static bool attr = false;
+    if (!attr) {
+      CUDA_OK(cudaFuncSetAttribute(dm::cellmat_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   dm::SMEM_BYTES));
+      attr = true;
+    }
+    dim3 grid(unsigned(S.n_out_pad / dm::BN), unsigned((n + dm::BM - 1) / dm::BM));
+    dm::cellmat_dmma_kernel<<<grid, dm::THREADS, dm::SMEM_BYTES, st>>>(
         static_cast<const double*>(W), static_cast<const double*>(S.d_T.p), static_cast<double*>(out),
         n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
   }
@@ -472,6 +526,7 @@ void run_cell_matrices(mpfem_b200_setup_s& S, Workspace& ws, const double* verts
                        int64_t coef_stride, void* out, int64_t out_pitch, cudaStream_t st,
                        uint32_t* flags, const Scatter* sc = nullptr) {
   S.take_error(" (reported on the device by an earlier call on this setup)");
+  if (S.from_tab) throw Error(MPFEM_B200_CONFIG_ERROR, "this setup takes geometry tensors (mpfem_b200_bilinear_from_geometry)");
   check_coef(S, coef_kind, coef, coef_stride);
   if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative cell count");
   if (out_pitch < S.n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
@@ -520,9 +575,7 @@ void prepare_action(mpfem_b200_setup_s& S) {
   int ap = action_arith(S.up, S.us), aq = action_arith(S.uq, S.us);
   if (ap != aq) ap = aq = kArGen;
   if (ap == S.act_ap) return;
-  uint32_t fl = 0;
-  const Basis basis = S.box ? box_basis(S.p) : simplex_basis(S.p);
-  const std::vector<double> tab = tabulate(basis, S.rule, S.up, S.us, S.form == 1, fl);
+  const std::vector<double>& tab = S.tab_store_host;  // tab_store (kernels.cpp:86-98)
   const int nphi = S.n_phi, nq = S.n_q, nd = S.n_d, n1 = nd * nq;
   std::vector<double> a(size_t(nphi) * n1), c(size_t(n1) * nphi);
   for (int s = 0; s < nd; ++s)
@@ -545,12 +598,16 @@ void prepare_action(mpfem_b200_setup_s& S) {
 
 void run_action(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const int32_t* cells,
                 int64_t n, int coef_kind, const double* coef, int64_t coef_stride, const double* w,
-                int64_t w_stride, void* out, int64_t out_pitch, cudaStream_t st, uint32_t* flags) {
+                int64_t w_stride, void* out, int64_t out_pitch, cudaStream_t st, uint32_t* flags,
+                const double* G = nullptr, int g_pts = 0) {
   S.take_error(" (reported on the device by an earlier call on this setup)");
+  if (S.from_tab && !G) throw Error(MPFEM_B200_CONFIG_ERROR, "this setup takes geometry tensors (mpfem_b200_action_from_geometry)");
+  if (G && S.dim != 3) throw Error(MPFEM_B200_CONFIG_ERROR, "the action kernel supports dimension 3");
+  if (G && (coef_kind == 1 || coef_kind == 2)) throw Error(MPFEM_B200_CONFIG_ERROR, "geometry tensors take constant or nodal coefficients");
   // one nodal z may be shared by the batch (stride 0), as the reference's action_kernel takes it
   check_coef(S, coef_kind, coef, coef_kind == 3 && coef_stride == 0 ? S.n_phi : coef_stride);
   if (n < 0) throw Error(MPFEM_B200_CONFIG_ERROR, "negative batch");
-  if (n > 0 && (!verts || !w || !out)) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+  if (n > 0 && ((!verts && !G) || !w || !out)) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
   if (out_pitch < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
   prepare_action(S);
@@ -582,6 +639,9 @@ void run_action(mpfem_b200_setup_s& S, Workspace& ws, const double* verts, const
     P.ftz = S.engine == 2;
     P.box = S.box;
     P.ggrad = static_cast<const double*>(S.d_ggrad.p);
+    P.G = G;
+    P.g_pts = g_pts;
+    if (G) P.box = 0;  // geometry given: no per-point evaluation from vertices
     P.out = out;
     P.out_pitch = out_pitch;
     P.flags = static_cast<uint32_t*>(ws.d_flags.p);
@@ -650,6 +710,97 @@ extern "C" {
 const char* mpfem_b200_last_error(void) { return g_last_error.c_str(); }
 const char* mpfem_b200_version(void) { return "mpfem_b200 0.1 sm_100a"; }
 
+}  // extern "C"
+
+namespace {
+
+// Device state of a setup from its host arrays: value tabulation at u_p (tab_up, n_phi x n_q),
+// binary64 tabulation (B64, n_d x n_phi x n_q; may be empty: no GPU bounds), store tabulation
+// (Bs, evaluated at u_p, stored at u_s), and the GEMM operand T built from Bs.
+void finish_setup(mpfem_b200_setup_s& S, const std::vector<double>& tab_up,
+                  const std::vector<double>& B64, const std::vector<double>& Bs) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error(MPFEM_B200_RUNTIME_ERROR, "no CUDA device: the B200 path has no CPU fallback");
+  CUDA_OK(cudaGetDevice(&S.device));
+  S.n_blocks = S.n_d * (S.n_d + 1) / 2;
+  S.nq_pad = (S.n_q + kWAlign - 1) / kWAlign * kWAlign;
+  S.k = int64_t(S.n_blocks) * S.nq_pad;
+  const int64_t kal = S.path == kPathTC ? tc::BK : 16;
+  S.k_pad = (S.k + kal - 1) / kal * kal;
+  S.n_out = int64_t(S.n_phi) * S.n_phi;
+  S.n_out_pad = (S.n_out + 127) / 128 * 128;
+  std::vector<int32_t> rows;
+  if (S.path == kPathTC) {
+    // full output, row-major (i, j): one warp store = 128 contiguous bytes of a cell
+    for (int i = 0; i < S.n_phi; ++i)
+      for (int j = 0; j < S.n_phi; ++j) rows.push_back(i | (j << 16));
+    while (rows.size() % tc2::BM) rows.push_back(-1);
+    S.n_out_pad = int64_t(rows.size());
+    S.n_rows = int(rows.size());
+    S.d_rows.ensure(sizeof(int32_t) * rows.size());
+    CUDA_OK(cudaMemcpy(S.d_rows.p, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice));
+  }
+  uint32_t fl = 0;
+  std::vector<double> w_ug(S.n_q);  // fp_cast(omega_q, fp64, u_g) (kernels.cpp:185)
+  for (int q = 0; q < S.n_q; ++q) w_ug[q] = host_round(S.rule.weights[q], S.ug, fl);
+  auto upload = [](DevBuf& d, const std::vector<double>& v) {
+    d.ensure(sizeof(double) * std::max<size_t>(1, v.size()));
+    if (!v.empty()) CUDA_OK(cudaMemcpy(d.p, v.data(), sizeof(double) * v.size(), cudaMemcpyHostToDevice));
+  };
+  upload(S.d_rule_w, S.rule.weights);
+  upload(S.d_rule_w_ug, w_ug);
+  upload(S.d_rule_x, S.rule.points);
+  upload(S.d_tab_up, tab_up);
+  upload(S.d_B, B64);
+  upload(S.d_Bs, Bs);
+  S.tab_store_host = Bs;
+  CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&S.h_error), 16, cudaHostAllocMapped));
+  std::memset(S.h_error, 0, 16);
+  CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S.d_error), S.h_error, 0));
+  const int64_t t_rows = S.n_out_pad;
+  size_t tbytes = size_t(S.k_pad) * size_t(t_rows) * elem_size(S.w_type);
+  const double* dB = static_cast<const double*>(S.d_Bs.p);
+  if (S.path == kPathFused) {
+    // fp32 T[k][o] with k = block * n_q + q (no padding), values rounded to u_s
+    const int64_t kf = int64_t(S.n_blocks) * S.n_q;
+    S.d_T.ensure(sizeof(float) * size_t(kf) * size_t(S.n_out));
+    const int64_t tot = kf * S.n_out;
+    build_t_kernel<float><<<unsigned((tot + 255) / 256), 256>>>(dB, S.n_phi, S.n_q, S.n_q, S.n_d, S.us, kf, kf, S.n_out, S.n_out, 0, S.d_T.p);
+    CUDA_OK(cudaGetLastError());
+    tbytes = 0;
+  }
+  if (tbytes) S.d_T.ensure(tbytes);
+  const int transposed = S.path == kPathTC;
+  const int64_t total = tbytes ? S.k_pad * t_rows : 0;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 64)));
+  const int32_t* rws = static_cast<const int32_t*>(S.d_rows.p);
+  if (total) switch (S.w_type) {
+    case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S.n_phi, S.n_q, S.nq_pad, S.n_d, S.us, S.k, S.k_pad, S.n_out, t_rows, transposed, S.d_T.p, rws); break;
+    case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S.n_phi, S.n_q, S.nq_pad, S.n_d, S.us, S.k, S.k_pad, S.n_out, t_rows, transposed, S.d_T.p, rws); break;
+    case 2: build_t_kernel<float><<<grid, 256>>>(dB, S.n_phi, S.n_q, S.nq_pad, S.n_d, S.us, S.k, S.k_pad, S.n_out, S.n_out_pad, transposed, S.d_T.p); break;
+    default: build_t_kernel<double><<<grid, 256>>>(dB, S.n_phi, S.n_q, S.nq_pad, S.n_d, S.us, S.k, S.k_pad, S.n_out, S.n_out_pad, transposed, S.d_T.p); break;
+  }
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaDeviceSynchronize());
+}
+
+void init_config(mpfem_b200_setup_s& S, int cell_kind, int p, int form, const int* fmts, int engine) {
+  S.p = p;
+  S.form = form;
+  S.up = fmts[0];
+  S.ug = fmts[1];
+  S.uq = fmts[2];
+  S.us = fmts[3];
+  S.engine = engine;
+  S.box = cell_kind == 1;
+  choose_path(S);
+}
+
+}  // namespace
+
+extern "C" {
+
 int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, int u_g, int u_q,
                             int u_s, int engine, int n_batch, mpfem_b200_setup_t* out) {
   return guarded([&] {
@@ -657,89 +808,57 @@ int mpfem_b200_setup_create(int cell_kind, int dim, int p, int form, int u_p, in
     int fmts[4] = {u_p, u_g, u_q, u_s};
     validate(cell_kind, dim, p, form, fmts, engine, n_batch);
     auto S = std::make_unique<mpfem_b200_setup_s>();
-    S->p = p;
-    S->form = form;
-    S->up = u_p;
-    S->ug = u_g;
-    S->uq = u_q;
-    S->us = u_s;
-    S->engine = engine;
-    S->box = cell_kind == 1;
-    choose_path(*S);
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw Error(MPFEM_B200_RUNTIME_ERROR, "no CUDA device: the B200 path has no CPU fallback");
-    CUDA_OK(cudaGetDevice(&S->device));
+    init_config(*S, cell_kind, p, form, fmts, engine);
     S->rule = S->box ? box_rule(p) : simplex_rule(p);
     Basis basis = S->box ? box_basis(p) : simplex_basis(p);
     S->n_phi = basis.n_phi;
     S->n_q = S->rule.n_q;
     S->n_d = form ? 3 : 1;
-    S->n_blocks = form ? 6 : 1;
-    S->nq_pad = (S->n_q + kWAlign - 1) / kWAlign * kWAlign;
-    S->k = int64_t(S->n_blocks) * S->nq_pad;
-    const int64_t kal = S->path == kPathTC ? tc::BK : 16;
-    S->k_pad = (S->k + kal - 1) / kal * kal;
-    S->n_out = int64_t(S->n_phi) * S->n_phi;
-    S->n_out_pad = (S->n_out + 127) / 128 * 128;
-    std::vector<int32_t> rows;
-    if (S->path == kPathTC) {
-      // full output, row-major (i, j): one warp store = 128 contiguous bytes of a cell
-      for (int i = 0; i < S->n_phi; ++i)
-        for (int j = 0; j < S->n_phi; ++j) rows.push_back(i | (j << 16));
-      while (rows.size() % tc2::BM) rows.push_back(-1);
-      S->n_out_pad = int64_t(rows.size());
-      S->n_rows = int(rows.size());
-      S->d_rows.ensure(sizeof(int32_t) * rows.size());
-      CUDA_OK(cudaMemcpy(S->d_rows.p, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice));
-    }
     uint32_t fl = 0;
     std::vector<double> tab_up = tabulate(basis, S->rule, u_p, u_p, false, fl);
     std::vector<double> B = tabulate(basis, S->rule, 3, 3, form == 1, fl);
-    S->d_rule_w.ensure(sizeof(double) * S->n_q);
-    std::vector<double> w_ug(S->n_q);  // fp_cast(omega_q, fp64, u_g) (kernels.cpp:185)
-    for (int q = 0; q < S->n_q; ++q) w_ug[q] = host_round(S->rule.weights[q], u_g, fl);
-    S->d_rule_w_ug.ensure(sizeof(double) * S->n_q);
-    S->d_rule_x.ensure(sizeof(double) * 3 * S->n_q);
-    S->d_tab_up.ensure(sizeof(double) * tab_up.size());
-    S->d_B.ensure(sizeof(double) * B.size());
-    CUDA_OK(cudaMemcpy(S->d_rule_w.p, S->rule.weights.data(), sizeof(double) * S->n_q, cudaMemcpyHostToDevice));
-    CUDA_OK(cudaMemcpy(S->d_rule_w_ug.p, w_ug.data(), sizeof(double) * S->n_q, cudaMemcpyHostToDevice));
-    CUDA_OK(cudaMemcpy(S->d_rule_x.p, S->rule.points.data(), sizeof(double) * 3 * S->n_q, cudaMemcpyHostToDevice));
-    CUDA_OK(cudaMemcpy(S->d_tab_up.p, tab_up.data(), sizeof(double) * tab_up.size(), cudaMemcpyHostToDevice));
-    CUDA_OK(cudaMemcpy(S->d_B.p, B.data(), sizeof(double) * B.size(), cudaMemcpyHostToDevice));
+    // T is built from the reference's own operand values: the tabulation evaluated at u_p
+    // and stored at u_s (kernels.cpp:86-98). A format that cannot evaluate the basis (fp16 at
+    // p >= 7 raises invalid, as in the reference) therefore yields the reference's NaN
+    // matrices instead of silently better ones.
+    std::vector<double> Bs = tabulate(basis, S->rule, u_p, u_s, form == 1, fl);
     if (S->box) {  // jacobian() at every rule point: degree-1 box gradients at u_g
       const std::vector<double> gg = tabulate(box_basis(1), S->rule, u_g, u_g, true, fl);
       S->d_ggrad.ensure(sizeof(double) * gg.size());
       CUDA_OK(cudaMemcpy(S->d_ggrad.p, gg.data(), sizeof(double) * gg.size(), cudaMemcpyHostToDevice));
     }
-    CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&S->h_error), 16, cudaHostAllocMapped));
-    std::memset(S->h_error, 0, 16);
-    CUDA_OK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->d_error), S->h_error, 0));
-    const int64_t t_rows = S->n_out_pad;
-    size_t tbytes = size_t(S->k_pad) * size_t(t_rows) * elem_size(S->w_type);
-    if (S->path == kPathFused) {
-      // fp32 T[k][o] with k = block * n_q + q (no padding), values rounded to u_s
-      const int64_t kf = int64_t(S->n_blocks) * S->n_q;
-      S->d_T.ensure(sizeof(float) * size_t(kf) * size_t(S->n_out));
-      const int64_t tot = kf * S->n_out;
-      build_t_kernel<float><<<unsigned((tot + 255) / 256), 256>>>(static_cast<const double*>(S->d_B.p), S->n_phi, S->n_q, S->n_q, form, u_s, kf, kf, S->n_out, S->n_out, 0, S->d_T.p);
-      CUDA_OK(cudaGetLastError());
-      tbytes = 0;
-    }
-    if (tbytes) S->d_T.ensure(tbytes);
-    const int transposed = S->path == kPathTC;
-    const int64_t total = tbytes ? S->k_pad * t_rows : 0;
-    const unsigned grid = unsigned(std::min<int64_t>((total + 255) / 256, 148 * 64));
-    const double* dB = static_cast<const double*>(S->d_B.p);
-    if (total) switch (S->w_type) {
-      case 0: build_t_kernel<__half><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, t_rows, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
-      case 1: build_t_kernel<__nv_bfloat16><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, t_rows, transposed, S->d_T.p, static_cast<const int32_t*>(S->d_rows.p)); break;
-      case 2: build_t_kernel<float><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-      default: build_t_kernel<double><<<grid, 256>>>(dB, S->n_phi, S->n_q, S->nq_pad, form, u_s, S->k, S->k_pad, S->n_out, S->n_out_pad, transposed, S->d_T.p); break;
-    }
-    CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaDeviceSynchronize());
+    finish_setup(*S, tab_up, B, Bs);
+    *out = S.release();
+  });
+}
+
+int mpfem_b200_setup_create_tab(int cell_kind, int dim, int p, int form, int u_p, int u_g,
+                                int u_q, int u_s, int engine, int n_batch, int n_phi, int n_q,
+                                const double* points, const double* weights,
+                                const double* tab_store, const double* tab_up,
+                                mpfem_b200_setup_t* out) {
+  return guarded([&] {
+    if (!out) throw Error(MPFEM_B200_CONFIG_ERROR, "null output handle");
+    int fmts[4] = {u_p, u_g, u_q, u_s};
+    if (dim != 2 && dim != 3) throw Error(MPFEM_B200_CONFIG_ERROR, "dimension must be 2 or 3");
+    validate(cell_kind, 3, std::max(1, std::min(p, 4)), form, fmts, engine, n_batch);
+    if (n_phi < 1 || n_q < 1 || !points || !weights || !tab_store || !tab_up)
+      throw Error(MPFEM_B200_CONFIG_ERROR, "setup from tabulation needs the rule and both tabulations");
+    auto S = std::make_unique<mpfem_b200_setup_s>();
+    S->from_tab = 1;
+    S->dim = dim;
+    init_config(*S, cell_kind, p, form, fmts, engine);
+    S->n_phi = n_phi;
+    S->n_q = n_q;
+    S->n_d = form ? dim : 1;
+    S->rule.n_q = n_q;
+    S->rule.weights.assign(weights, weights + n_q);
+    S->rule.points.assign(size_t(3) * n_q, 0.0);
+    for (int q = 0; q < n_q; ++q)
+      for (int a = 0; a < dim; ++a) S->rule.points[size_t(3) * q + a] = points[size_t(dim) * q + a];
+    std::vector<double> tu(tab_up, tab_up + size_t(n_phi) * n_q);
+    std::vector<double> bs(tab_store, tab_store + size_t(S->n_d) * n_phi * n_q);
+    finish_setup(*S, tu, {}, bs);
     *out = S.release();
   });
 }
@@ -960,6 +1079,7 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   if (n_cells < 0 || (n_cells > 0 && (!verts || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
   if (w && w_stride < S.n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
   if (S.box && w) throw Error(MPFEM_B200_CONFIG_ERROR, "the action bound supports tetrahedra");
+  if (S.from_tab) throw Error(MPFEM_B200_CONFIG_ERROR, "GPU bounds need a setup made from (cell, p, config)");
   prepare_bounds(S);
   if (n_cells == 0) return;
   BoundParams P{};
@@ -1003,6 +1123,123 @@ void run_bounds(mpfem_b200_setup_s& S, const double* verts, const int32_t* cells
   S.last_launches = 1;
 }
 }  // namespace
+
+namespace {
+// Stages geometry tensors (and an optional nodal coefficient) of a host-buffer tensor call in
+// the stream workspace: [G | z] in h_verts / h_coef.
+void stage_tensor(mpfem_b200_setup_s& S, Workspace& ws, const double* G, int n_pts, int64_t n_cells,
+                  const double* z, int64_t z_stride, cudaStream_t st, const double** dG,
+                  const double** dz) {
+  if (n_pts != 1 && n_pts != S.n_q)
+    throw Error(MPFEM_B200_CONFIG_ERROR, "geometry needs one entry per cell (affine) or per rule point");
+  const int nd = S.form ? S.dim : 1;
+  const size_t gb = sizeof(double) * size_t(n_cells) * size_t(n_pts) * size_t(nd * nd);
+  ws.h_verts.ensure(gb + 8);
+  if (gb) CUDA_OK(cudaMemcpyAsync(ws.h_verts.p, G, gb, cudaMemcpyHostToDevice, st));
+  *dG = static_cast<const double*>(ws.h_verts.p);
+  *dz = nullptr;
+  if (z) {
+    const size_t zb = sizeof(double) * size_t(z_stride == 0 ? 1 : n_cells) * size_t(S.n_phi);
+    ws.h_coef.ensure(zb + 8);
+    if (z_stride == 0 || z_stride == S.n_phi) {
+      CUDA_OK(cudaMemcpyAsync(ws.h_coef.p, z, zb, cudaMemcpyHostToDevice, st));
+    } else {
+      CUDA_OK(cudaMemcpy2DAsync(ws.h_coef.p, sizeof(double) * S.n_phi, z, sizeof(double) * z_stride,
+                                sizeof(double) * S.n_phi, size_t(n_cells), cudaMemcpyHostToDevice, st));
+    }
+    *dz = static_cast<const double*>(ws.h_coef.p);
+  }
+}
+}  // namespace
+
+int mpfem_b200_bilinear_from_geometry(mpfem_b200_setup_t S, const double* G, int n_pts,
+                                      int64_t n_cells, const double* z, int64_t z_stride,
+                                      void* out, int64_t out_pitch, void* stream, uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (n_cells < 0 || (n_cells > 0 && (!G || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+    if (out_pitch < S->n_out) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch smaller than n_phi^2");
+    if (z_stride != 0 && z_stride < S->n_phi)
+      throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient z needs one entry per basis function");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(S->mu);
+    S->take_error(" (reported on the device by an earlier call on this setup)");
+    Workspace& ws = S->workspace(st);
+    S->last_launches = 0;
+    ws.n_ev = 0;
+    CUDA_OK(cudaMemsetAsync(ws.d_flags.p, 0, 4, st));
+    if (n_cells > 0) {
+      const double *dG, *dz;
+      stage_tensor(*S, ws, G, n_pts, n_cells, z, z_stride, st, &dG, &dz);
+      ws.d_W.ensure(size_t(n_cells) * size_t(S->k_pad) * elem_size(S->w_type));
+      const size_t esz = S->path == kPathF64 ? 8 : 4;
+      const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
+      ws.h_out.ensure(obytes + 16);
+      WTensorParams P{};
+      P.G = dG;
+      P.n_pts = n_pts;
+      P.n_cells = n_cells;
+      P.z = dz;
+      P.z_stride = z_stride == 0 ? 0 : S->n_phi;
+      P.rule_w_ug = static_cast<const double*>(S->d_rule_w_ug.p);
+      P.tab_up = static_cast<const double*>(S->d_tab_up.p);
+      P.n_phi = S->n_phi;
+      P.n_q = S->n_q;
+      P.nq_pad = S->nq_pad;
+      P.nd = S->form ? S->dim : 1;
+      P.n_blocks = S->n_blocks;
+      P.up = S->up;
+      P.ug = S->ug;
+      P.us = S->us;
+      P.k_pad = S->k_pad;
+      P.W = ws.d_W.p;
+      P.flags = static_cast<uint32_t*>(ws.d_flags.p);
+      ws.mark(S->timing, st);
+      launch_w_from_tensor(S->w_type, P, device_sm_count(), st);
+      CUDA_OK(cudaGetLastError());
+      ws.mark(S->timing, st);
+      if (S->path == kPathFused) throw Error(MPFEM_B200_CONFIG_ERROR, "fused path takes vertices");
+      launch_gemm(*S, ws, ws.d_W.p, n_cells, ws.h_out.p, out_pitch, st, nullptr);
+      ws.mark(S->timing, st);
+      S->last_launches = 2;
+      CUDA_OK(cudaMemcpyAsync(out, ws.h_out.p, obytes, cudaMemcpyDeviceToHost, st));
+    }
+    uint32_t h = 0;
+    CUDA_OK(cudaMemcpyAsync(&h, ws.d_flags.p, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (flags) *flags |= h;
+  });
+}
+
+int mpfem_b200_action_from_geometry(mpfem_b200_setup_t S, const double* G, int n_pts,
+                                    int64_t n_cells, const double* z, const double* w,
+                                    int64_t w_stride, void* out, int64_t out_pitch, void* stream,
+                                    uint32_t* flags) {
+  return guarded([&] {
+    if (!S) throw Error(MPFEM_B200_CONFIG_ERROR, "null setup");
+    if (n_cells < 0 || (n_cells > 0 && (!G || !w || !out))) throw Error(MPFEM_B200_CONFIG_ERROR, "null buffer");
+    if (w_stride < S->n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "coefficient w needs one entry per basis function");
+    if (out_pitch < S->n_phi) throw Error(MPFEM_B200_CONFIG_ERROR, "output pitch below n_phi");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> lk(S->mu);
+    Workspace& ws = S->workspace(st);
+    const double *dG = nullptr, *dz = nullptr;
+    if (n_cells > 0) stage_tensor(*S, ws, G, n_pts, n_cells, z, 0, st, &dG, &dz);
+    const size_t wbytes = sizeof(double) * size_t(n_cells) * size_t(w_stride);
+    const size_t esz = S->uq == 3 ? 8 : 4;
+    const size_t obytes = esz * size_t(n_cells) * size_t(out_pitch);
+    ws.h_out.ensure(wbytes + obytes + 32);
+    char* base = static_cast<char*>(ws.h_out.p);
+    if (wbytes) CUDA_OK(cudaMemcpyAsync(base, w, wbytes, cudaMemcpyHostToDevice, st));
+    void* dout = base + (wbytes + 15) / 16 * 16;
+    uint32_t fl = 0;
+    run_action(*S, ws, nullptr, nullptr, n_cells, dz ? 3 : 0, dz, 0, reinterpret_cast<const double*>(base),
+               w_stride, dout, out_pitch, st, &fl, dG, n_pts);
+    if (obytes) CUDA_OK(cudaMemcpyAsync(out, dout, obytes, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    if (flags) *flags |= fl;
+  });
+}
 
 int mpfem_b200_cell_bounds(mpfem_b200_setup_t S, const double* verts, const int32_t* cells,
                            int64_t n_cells, int coef_kind, const double* coef, int64_t coef_stride,

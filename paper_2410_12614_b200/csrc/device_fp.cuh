@@ -849,26 +849,36 @@ __device__ __forceinline__ float sinpi_poly_f(float r) {
   for (int k = 5; k >= 0; --k) p = fmaf(p, s, kSinPiF[k]);
   return r * p;
 }
-__device__ __forceinline__ float flip_if_odd_f(float v, float n) {
-  const int odd = static_cast<int>(n) & 1;
-  return __int_as_float(__float_as_int(v) ^ (odd << 31));
+// Round-to-nearest-even of |a| < 2^22 by the 1.5 * 2^23 magic add: the FMA pipe instead of
+// FRND / F2I on the conversion pipe (which K1's D2F conversions already load). The integer
+// is read from the low mantissa bits of the biased sum.
+__device__ __forceinline__ float magic_round_f(float a, int& ni) {
+  const float big = __fadd_rn(a, 12582912.0f);
+  ni = __float_as_int(big) - 0x4B400000;
+  return __fsub_rn(big, 12582912.0f);
+}
+__device__ __forceinline__ float flip_if_odd_i(float v, int ni) {
+  return __int_as_float(__float_as_int(v) ^ ((ni & 1) << 31));
 }
 __device__ __forceinline__ float fast_sinpi_f(float a) {
-  const float n = rintf(a);
-  return flip_if_odd_f(sinpi_poly_f(a - n), n);
+  int ni;
+  const float n = magic_round_f(a, ni);
+  return flip_if_odd_i(sinpi_poly_f(a - n), ni);
 }
 __device__ __forceinline__ float fast_cospi_f(float a) {
-  const float n = rintf(a);
-  return flip_if_odd_f(sinpi_poly_f(0.5f - fabsf(a - n)), n);
+  int ni;
+  const float n = magic_round_f(a, ni);
+  return flip_if_odd_i(sinpi_poly_f(0.5f - fabsf(a - n)), ni);
 }
 __device__ __forceinline__ float fast_exp_f(float z) {
-  const float n = rintf(z * 1.4426950408889634f);
+  int ni;
+  const float n = magic_round_f(z * 1.4426950408889634f, ni);
   float r = fmaf(-n, 0.693145751953125f, z);
   r = fmaf(-n, 1.428606765330187e-06f, r);
   float p = kExpF[8];
   #pragma unroll
   for (int k = 7; k >= 0; --k) p = fmaf(p, r, kExpF[k]);
-  return p * __int_as_float((static_cast<int>(n) + 127) << 23);
+  return p * __int_as_float((ni + 127) << 23);
 }
 
 // The analytic coefficient from a cell's origin and edge vectors with the x and y components

@@ -150,6 +150,8 @@ struct __align__(16) CellGeo {
   double g[6];  // G_00 G_01 G_02 G_11 G_12 G_22 (poisson) or |det| (mass)
   double v0[3];  // (2 v0x, 2 v0y, v0z)
   double e[9];   // e[s*3 + i] = (v_{s+1}[i] - v0[i]), x and y components doubled
+  float gf[6];   // g as fp32 (exact for u_g = fp32: no per-entry conversion in the expansion)
+  float pad[2];
 };
 
 #ifndef MPFEM_K1_QPT
@@ -213,7 +215,10 @@ __device__ MPFEM_K1_GEOM_INLINE void cell_geometry(const GeomWParams& P, int64_t
     for (int b = 0; b < 6; ++b) g.g[b] = __longlong_as_double(0x7ff8000000000000ll);  // singular: NaN row
   }
   #pragma unroll
-  for (int b = 0; b < 6; ++b) o.g[b] = g.g[b];
+  for (int b = 0; b < 6; ++b) {
+    o.g[b] = g.g[b];
+    o.gf[b] = float(g.g[b]);
+  }
   // origin and edges with x, y pre-doubled (the coefficient's sinpi(2x), cospi(2y) arguments)
   #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -270,7 +275,8 @@ __device__ __forceinline__ uint32_t packed_store_flags(const StoreFlags& sf) {
 // dynamic shared memory of geom_w_kernel: weights and the three point coordinates, each
 // nq_pad doubles in [j][group] order, then the two geometry buffers of 32 * geom_warps cells
 __host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad, int geom_warps = 1) {
-  return size_t(4) * nq_pad * sizeof(double) + size_t(2) * 32 * geom_warps * sizeof(CellGeo);
+  return size_t(4) * nq_pad * sizeof(double) + size_t(2) * 32 * geom_warps * sizeof(CellGeo) +
+         size_t(nq_pad) * sizeof(float);
 }
 
 template <typename T, int UG, int US, int COEF>
@@ -286,10 +292,12 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
   const int nb = P.poisson ? 6 : 1;
   double* sW = s_rule;
   double* sX = s_rule + nqp;  // sX[a * nqp + perm(q)]
+  float* sWf = reinterpret_cast<float*>(s_geo0 + 2 * tcells);  // the weights as fp32 (u_g = fp32)
   for (int q = threadIdx.x; q < nqp; q += blockDim.x) {
     const int pq = (q % kQPT) * ngroups + q / kQPT;
     const bool ok = q < nq;
     sW[pq] = ok ? P.rule_w[q] : 0.0;
+    sWf[pq] = ok ? float(P.rule_w[q]) : 0.0f;
     #pragma unroll
     for (int a = 0; a < 3; ++a) sX[a * nqp + pq] = ok ? P.rule_x[3 * q + a] : 0.0;
   }
@@ -338,15 +346,18 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
       const CellGeo& cg = geo_t[cl];
       const double* coef = P.coef ? P.coef + cell * P.coef_stride : nullptr;
       double zq[kQPT], om[kQPT];
+      float zqf[kQPT], omf[kQPT];  // u_g = fp32: the same values in fp32 (exact)
       #pragma unroll
       for (int j = 0; j < kQPT; ++j) {
         const int pq = j * ngroups + grp;
-        om[j] = sW[pq];
+        if constexpr (UG == kFP32) omf[j] = sWf[pq];
+        else om[j] = sW[pq];
         zq[j] = 1.0;
+        zqf[j] = 1.0f;
         if constexpr (COEF != 0) {
           const double xi[3] = {sX[pq], sX[nqp + pq], sX[2 * nqp + pq]};
           if constexpr (COEF == 1 && UG == kFP32) {
-            zq[j] = double(coef_sincosexp_f(cg.v0, cg.e, xi));
+            zqf[j] = coef_sincosexp_f(cg.v0, cg.e, xi);
           } else if constexpr (COEF == 1) {
             zq[j] = droundT<UG>(coef_sincosexp_e(cg.v0, cg.e, xi), fl);
           } else if constexpr (COEF == 2) {
@@ -363,6 +374,10 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
         }
       }
       constexpr bool have_z = COEF != 0;
+      if constexpr (UG == kFP32 && COEF != 1) {
+        #pragma unroll
+        for (int j = 0; j < kQPT; ++j) zqf[j] = float(zq[j]);
+      }
       T* wrow = static_cast<T*>(P.W) + cell * P.k_pad + q0;
       // C_stq = round_us(round_ug(round_ug(omega G_st) zhat_q))  (kernels.cpp:189-192).
       // Points q >= n_q (only in a cell's last group) are exact zeros whatever G is.
@@ -387,7 +402,10 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
         uint32_t zqz[KW];
         #pragma unroll
         for (int k = 0; k < KW; ++k)
-          zqz[k] = (zq[2 * k] == 0.0 ? 0x0000ffffu : 0u) | (zq[2 * k + 1] == 0.0 ? 0xffff0000u : 0u);
+          if constexpr (UG == kFP32)
+            zqz[k] = (zqf[2 * k] == 0.0f ? 0x0000ffffu : 0u) | (zqf[2 * k + 1] == 0.0f ? 0xffff0000u : 0u);
+          else
+            zqz[k] = (zq[2 * k] == 0.0 ? 0x0000ffffu : 0u) | (zq[2 * k + 1] == 0.0 ? 0xffff0000u : 0u);
         #pragma unroll
         for (int b = 0; b < 6; ++b) {
           if (b < nb) {
@@ -395,8 +413,20 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
             uint32_t wd[KW];
             #pragma unroll
             for (int k = 0; k < KW; ++k) {
-              const uint32_t lo = storage_bits16<T>(w_value<UG, have_z>(om[2 * k], gb, zq[2 * k]));
-              const uint32_t hi = storage_bits16<T>(w_value<UG, have_z>(om[2 * k + 1], gb, zq[2 * k + 1]));
+              uint32_t lo, hi;
+              if constexpr (UG == kFP32) {
+                const float gf = cg.gf[b];
+                float v0 = __fmul_rn(omf[2 * k], gf), v1 = __fmul_rn(omf[2 * k + 1], gf);
+                if (have_z) {
+                  v0 = __fmul_rn(v0, zqf[2 * k]);
+                  v1 = __fmul_rn(v1, zqf[2 * k + 1]);
+                }
+                lo = storage_bits16<T>(v0);
+                hi = storage_bits16<T>(v1);
+              } else {
+                lo = storage_bits16<T>(w_value<UG, have_z>(om[2 * k], gb, zq[2 * k]));
+                hi = storage_bits16<T>(w_value<UG, have_z>(om[2 * k + 1], gb, zq[2 * k + 1]));
+              }
               wd[k] = (lo | (hi << 16)) & keep[k];
             }
             #pragma unroll
@@ -432,8 +462,8 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
           #pragma unroll
           for (int j = 0; j < kQPT; ++j) {
             if constexpr (UG == kFP32) {
-              float val = __fmul_rn(float(om[j]), float(gb));  // fp32 values: exact-then-round
-              if (have_z) val = __fmul_rn(val, float(zq[j]));
+              float val = __fmul_rn(omf[j], cg.gf[b]);  // fp32 values: exact-then-round
+              if (have_z) val = __fmul_rn(val, zqf[j]);
               if (pad[j]) val = 0.0f;
               pk.v[j] = to_storage<T, US>(val, sf);
             } else if constexpr (UG == kFP64) {
@@ -476,13 +506,26 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
     publish_flags(P.flags, fl | store_flags_bits(sf));
 }
 
-// Shared basis-product operand T from the fp64 tabulation B (n_d x n_phi x n_q):
+// Shared basis-product operand T from the store tabulation B (n_d x n_phi x n_q, u_s values):
 //   T[(b,q), (i,j)] = round_us(B_s[i,q] B_t[j,q] (+ B_t[i,q] B_s[j,q] if s<t)).
 // transposed != 0 stores Tt[o][k] (K contiguous; the tcgen05 A operand), else T[k][o].
 // rows: optional output-row table (tcgen05 path): row o computes entry (i, j) =
 // (rows[o] & 0xffff, rows[o] >> 16), or nothing when rows[o] < 0; NULL means o = i*n_phi + j.
+// (s, t) of packed block b: the row-major upper triangle of an n_d x n_d tensor
+// (n_d = 3: (0,0) (0,1) (0,2) (1,1) (1,2) (2,2), the order K1 writes W in)
+__host__ __device__ inline void block_pair(int b, int nd, int& s, int& t) {
+  s = 0;
+  int row = nd;
+  while (b >= row) {
+    b -= row;
+    ++s;
+    --row;
+  }
+  t = s + b;
+}
+
 template <typename T>
-__global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, int poisson, int us,
+__global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, int nd, int us,
                                int64_t k_len, int64_t k_pad, int64_t n_out, int64_t n_out_pad,
                                int transposed, void* out, const int32_t* rows = nullptr) {
   const int64_t total = k_pad * n_out_pad;
@@ -503,11 +546,7 @@ __global__ void build_t_kernel(const double* B, int n_phi, int n_q, int nq_pad, 
     }
     if (k < k_len && valid && q < n_q) {
       int s = 0, t = 0;
-      if (poisson) {
-        const int ss[6] = {0, 0, 0, 1, 1, 2}, tt[6] = {0, 1, 2, 1, 2, 2};
-        s = ss[b];
-        t = tt[b];
-      }
+      block_pair(b, nd, s, t);
       const double bsi = B[(int64_t(s) * n_phi + i) * n_q + q];
       const double btj = B[(int64_t(t) * n_phi + j) * n_q + q];
       val = __dmul_rn(bsi, btj);
