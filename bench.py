@@ -480,8 +480,9 @@ def max_over_ranks(torch, value, dev):
 
 def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
     """BASELINE config 4: 96^3 hexes x 6 tets, Poisson with c(x), mixed (bf16 storage)
-    cell kernels, deterministic CSR assembly in fp32 and fp64; z-slabs over the ranks with
-    the interface partial-sum exchange. Times are CUDA-event times, max over ranks."""
+    cell kernels, deterministic CSR assembly in fp32 and fp64. One GPU: the global pattern and
+    plan; N GPUs: the partitioned z-slab assembly (per-rank numbering, pattern and plan of the
+    slab + one halo layer, interface partial sums sent up). CUDA-event times, max over ranks."""
     from paper_2410_12614_b200 import assembly as am
     from paper_2410_12614_b200 import distributed as D
     hbm = peaks()[0]
@@ -491,9 +492,6 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
     cpl = 6 * n * n
     cb, ce = D.slab_cell_range(rank, world, n, cpl)
     out = []
-
-    class Backend:
-        assemble_matrix = staticmethod(am.assemble_matrix)
 
     def timed(fn, reps=3):
         fn()
@@ -512,39 +510,51 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
         return ms, r
 
     for p in degrees:
-        t_dof, dm = timed(lambda: am.build_dofmap(p, cdev, verts.shape[0]), 1)
-        t_pat, pat = timed(lambda: am.csr_pattern(dm), 1)
-        plan = D.plan_slabs(dm, pat, rank, world, cb, ce)
         s = mp.make_setup(p, mp.mode_config("mixed_bf16", mp.FormKind.poisson))
         s.reserve(ce - cb)
         local = torch.empty((ce - cb, nphi(p), nphi(p)), dtype=torch.float32, device=dev)
         t_cell, _ = timed(lambda: s.cell_matrices(vd, cdev[cb:ce], mp.CoefKind.sincosexp, out=local.view(ce - cb, -1)))
+        if world > 1:
+            # partitioned: per-rank numbering of slab + halo layer, all-gather of the new-dof
+            # counts, local-row / global-column pattern and plan, exchange plan (distributed.py)
+            be = am.CudaPartitionBackend()
+            t_part, part = timed(lambda: D.build_partition(be, p, cdev, verts.shape[0], rank, world, n, cpl), 1)
+            res = {"p": p, "n_dofs": part.n_dofs, "nnz_rank": part.pat.nnz, "cells_per_rank": ce - cb,
+                   "halo_cells": cb - part.halo_begin, "partition_setup_ms": t_part, "cell_kernels_ms": t_cell,
+                   "interface_values_sent": int(part.send_pos.numel())}
+            for fmt in (2, 3):
+                vals = torch.empty(part.pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
+                t_asm, _ = timed(lambda: D.assemble_partition(be, part, local, fmt, values=vals))
+                res[f"assemble_{'fp32' if fmt == 2 else 'fp64'}_ms"] = t_asm
+                del vals
+            res["kernels_plus_assembly_fp32_ms"] = t_cell + res["assemble_fp32_ms"]
+            out.append(res)
+            del local, part, s
+            torch.cuda.empty_cache()
+            continue
+        t_dof, dm = timed(lambda: am.build_dofmap(p, cdev, verts.shape[0]), 1)
+        t_pat, pat = timed(lambda: am.csr_pattern(dm), 1)
         res = {"p": p, "n_dofs": dm.n_dofs, "nnz": pat.nnz, "cells_per_rank": ce - cb,
                "dofmap_ms": t_dof, "csr_pattern_ms": t_pat, "cell_kernels_ms": t_cell}
         for fmt in (2, 3):
             sv = 4 if fmt == 2 else 8
             vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
-            if world > 1:
-                t_asm, _ = timed(lambda: D.assemble_slab(Backend, local, dm, pat, plan, fmt, values=vals))
-            else:
-                t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
+            t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
             del vals
-            nb = (ce - cb) * (nphi(p) ** 2 * 4 + 4 * nphi(p)) + pat.nnz / world * (sv + 4) + 8 * (dm.n_dofs + 1) / world
+            nb = (ce - cb) * (nphi(p) ** 2 * 4 + 4 * nphi(p)) + pat.nnz * (sv + 4) + 8 * (dm.n_dofs + 1)
             key = "fp32" if fmt == 2 else "fp64"
             res[f"assemble_{key}_ms"] = t_asm
             res[f"assemble_{key}_hbm_frac"] = nb / (t_asm * 1e-3) / 1e9 / hbm
-        if world == 1:
-            vals = torch.empty(pat.nnz, dtype=torch.float32, device=dev)
-            t_at, _ = timed(lambda: am.assemble_matrix(local, dm, pat, 2, am.ATOMIC, values=vals))
-            res["assemble_atomic_fp32_ms"] = t_at
+        vals = torch.empty(pat.nnz, dtype=torch.float32, device=dev)
+        t_at, _ = timed(lambda: am.assemble_matrix(local, dm, pat, 2, am.ATOMIC, values=vals))
+        res["assemble_atomic_fp32_ms"] = t_at
         res["kernels_plus_assembly_fp32_ms"] = t_cell + res["assemble_fp32_ms"]
-        if world == 1:
-            # cell kernels fused with the atomic scatter (K2 adds from TMEM, no locals in HBM)
-            vals = torch.zeros(pat.nnz, dtype=torch.float32, device=dev)
-            t_fused, _ = timed(lambda: am.assemble_cells(s, vd, cdev, dm, pat, 2, mp.CoefKind.sincosexp,
-                                                         accumulate=True, values=vals))
-            res["fused_kernels_atomic_scatter_fp32_ms"] = t_fused
-            del vals
+        # cell kernels fused with the atomic scatter (K2 adds from TMEM, no locals in HBM)
+        vals.zero_()
+        t_fused, _ = timed(lambda: am.assemble_cells(s, vd, cdev, dm, pat, 2, mp.CoefKind.sincosexp,
+                                                     accumulate=True, values=vals))
+        res["fused_kernels_atomic_scatter_fp32_ms"] = t_fused
+        del vals
         out.append(res)
         del local, pat, dm, s
         torch.cuda.empty_cache()
@@ -729,7 +739,7 @@ def main():
     }
     if not args.no_assembly:
         line["assembly"] = {"workload": "config4: 96^3 x 6 tets, poisson P2/P3, mixed-bf16 kernels, "
-                                        "deterministic CSR, z-slabs over ranks",
+                                        "deterministic CSR, partitioned z-slabs over ranks",
                             "results": run_assembly(mp, torch, dev, rank, world)}
     if not args.no_modes and rank == 0:
         line["modes"] = run_modes(mp, torch, dev, flush)

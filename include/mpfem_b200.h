@@ -263,6 +263,27 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
                            int32_t n_dofs, int64_t* row_ptr, int32_t* col_idx, int64_t* nnz,
                            void* stream);
 
+/* Partitioned (multi-GPU) variants, SURVEY 8e / paper_2410_12614_b200/distributed.py: a rank
+ * numbers its cells plus one halo layer locally (rows) while columns carry the global ids.
+ * csr_pattern_cols / scatter_plan_cols: as csr_pattern / scatter_plan, with the row of local
+ * entry (c, i) taken from cell_dofs and the column of (c, j) from col_dofs (NULL: cell_dofs). */
+int mpfem_b200_csr_pattern_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                int n_loc, int32_t n_dofs, int64_t* row_ptr, int32_t* col_idx,
+                                int64_t* nnz, void* stream);
+int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                 int n_loc, int32_t n_dofs, const int64_t* row_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, int64_t* seg_ptr,
+                                 uint32_t* perm, void* stream);
+/* table[key_dofs[i]] = val_dofs[i] for i < n (layer-local id -> global id). */
+int mpfem_b200_dofmap_table(const int32_t* key_dofs, const int32_t* val_dofs, int64_t n, int32_t* table,
+                            void* stream);
+/* global[i] = local[i] < n_table ? table[local[i]] : offset + local[i] - n_table. */
+int mpfem_b200_dofmap_globalize(const int32_t* local_dofs, int64_t n, const int32_t* table,
+                                int32_t n_table, int32_t offset, int32_t* global_dofs, void* stream);
+/* pos[i] = CSR position of (rows[i], cols[i]) in (row_ptr, col_idx), -1 when absent. */
+int mpfem_b200_csr_find(const int64_t* row_ptr, const int32_t* col_idx, const int32_t* rows,
+                        const int32_t* cols, int64_t n, int64_t* pos, void* stream);
+
 /* Incidence (dof -> (cell, local) pairs in ascending cell order) used by the
  * deterministic assembly; inc_ptr: n_dofs + 1 int64, inc: n_cells x n_loc int64
  * (packed cell * n_loc + local). */

@@ -157,6 +157,13 @@ def lib():
                                           vp, C.c_int64, vp]),
         "mpfem_b200_assemble_pull": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp,
                                                C.c_int32, vp, vp, vp, vp, C.c_int, C.c_int, vp]),
+        "mpfem_b200_csr_pattern_cols": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int32, vp, vp, i64p, vp]),
+        "mpfem_b200_scatter_plan_cols": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp,
+                                                   vp, vp, vp]),
+        "mpfem_b200_dofmap_table": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
+        "mpfem_b200_dofmap_globalize": (C.c_int, [vp, C.c_int64, vp, C.c_int32, C.c_int32, vp, vp]),
+        "mpfem_b200_csr_find": (C.c_int, [vp, vp, vp, vp, C.c_int64, vp, vp]),
+        "mpfem_b200_dofmap_cells": (C.c_int, [C.c_int, C.c_int, vp, C.c_int64, C.c_int64, vp, i32p, i32p, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name, None)

@@ -168,3 +168,72 @@ def assemble_cells(setup, verts, cells, dm: DofMap, pat: CsrPattern, fmt: int = 
                                                  _stream_handle(stream),
                                                  C.byref(fl) if want_flags else None))
     return (values, fl.value) if want_flags else values
+
+
+class CudaPartitionBackend:
+    """The device operations of the partitioned multi-GPU assembly (distributed.py) on the
+    C-ABI: first-encounter dof maps of cell ranges, the layer table / globalisation of the
+    numbering, local-row / global-column CSR patterns with their scatter plan, CSR position
+    lookup, and the rows-restricted deterministic scatter."""
+
+    def dofmap(self, p: int, cells, n_verts: int):
+        dm = build_dofmap(p, cells, n_verts)
+        return dm.cell_dofs, dm.n_dofs
+
+    def table(self, key, val, n_table: int):
+        import torch
+        t = torch.full((max(n_table, 1),), -1, dtype=torch.int32, device=key.device)
+        check(lib().mpfem_b200_dofmap_table(_ptr(key), _ptr(val), int(key.numel()), _ptr(t), _stream_handle(None)))
+        return t[:n_table]
+
+    def globalize(self, local, table, n_table: int, offset: int):
+        import torch
+        out = torch.empty_like(local)
+        tb = table if table is not None and table.numel() else torch.zeros(1, dtype=torch.int32, device=local.device)
+        check(lib().mpfem_b200_dofmap_globalize(_ptr(local), int(local.numel()), _ptr(tb), int(n_table),
+                                                int(offset), _ptr(out), _stream_handle(None)))
+        return out
+
+    def pattern(self, row_dofs, col_dofs, n_rows: int):
+        import torch
+        dev = row_dofs.device
+        n, n_loc = int(row_dofs.shape[0]), int(row_dofs.shape[1])
+        row_ptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+        nnz = C.c_int64(0)
+        sh = _stream_handle(None)
+        check(lib().mpfem_b200_csr_pattern_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
+                                                _ptr(row_ptr), None, C.byref(nnz), sh))
+        col_idx = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+        check(lib().mpfem_b200_csr_pattern_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
+                                                _ptr(row_ptr), _ptr(col_idx), C.byref(nnz), sh))
+        inc_ptr = torch.empty(n_rows + 1, dtype=torch.int64, device=dev)
+        inc = torch.empty(n * n_loc, dtype=torch.int64, device=dev)
+        check(lib().mpfem_b200_incidence(_ptr(row_dofs), n, n_loc, n_rows, _ptr(inc_ptr), _ptr(inc), sh))
+        pat = CsrPattern(n_rows, row_ptr, col_idx, inc_ptr, inc)
+        nk = n * n_loc * n_loc
+        pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
+        pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int64, device=dev)
+        pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
+        check(lib().mpfem_b200_scatter_plan_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
+                                                 _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
+                                                 _ptr(pat.seg_ptr), _ptr(pat.perm), sh))
+        pat.n_local = n_loc
+        return pat
+
+    def find(self, pat, rows, cols):
+        import torch
+        pos = torch.empty(int(rows.numel()), dtype=torch.int64, device=rows.device)
+        check(lib().mpfem_b200_csr_find(_ptr(pat.row_ptr), _ptr(pat.col_idx), _ptr(rows), _ptr(cols),
+                                        int(rows.numel()), _ptr(pos), _stream_handle(None)))
+        return pos
+
+    def assemble_rows(self, local, pat, fmt, cell_begin, cell_end, rows, accumulate, values):
+        if rows is None or rows.numel() == 0:
+            return values
+        lf = FP32 if local.dtype.itemsize == 4 else FP64
+        check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), pat.n_local,
+                                        _ptr(pat.row_ptr), pat.n_rows, _ptr(pat.pos_map),
+                                        _ptr(pat.seg_ptr), _ptr(pat.perm), _ptr(values), int(fmt),
+                                        DETERMINISTIC, int(accumulate), _ptr(rows), int(rows.numel()),
+                                        _stream_handle(None)))
+        return values

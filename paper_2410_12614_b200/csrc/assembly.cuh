@@ -213,6 +213,42 @@ __global__ void dof_count_kernel(const int32_t* __restrict__ cell_dofs, int64_t 
     atomicAdd(reinterpret_cast<unsigned long long*>(&counts[cell_dofs[i]]), 1ull);
 }
 
+// ---------------------------------------------------------------- partitioned numbering
+// (distributed.py) A rank numbers the nodes of its cells plus one halo layer
+// first-encounter order; the nodes of a single cell layer are numbered the same way by both
+// ranks that hold it, so a table layer-local id -> global id moves the numbering across.
+// table[key[i]] = val[i] (every writer of one key writes the same value).
+__global__ void dof_table_kernel(const int32_t* __restrict__ key, const int32_t* __restrict__ val,
+                                 int64_t n, int32_t* __restrict__ table) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    table[key[i]] = val[i];
+}
+// global = local < n_table ? table[local] (halo nodes, numbered by the lower rank)
+//                          : offset + local - n_table (the rank's own new nodes)
+__global__ void dof_globalize_kernel(const int32_t* __restrict__ local, int64_t n,
+                                     const int32_t* __restrict__ table, int32_t n_table,
+                                     int32_t offset, int32_t* __restrict__ global) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t d = local[i];
+    global[i] = d < n_table ? table[d] : offset + (d - n_table);
+  }
+}
+// CSR position of (rows[i], cols[i]) by binary search in the row's sorted columns (-1: absent).
+__global__ void csr_find_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                int64_t n, int64_t* __restrict__ pos) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = row_ptr[rows[i]], hi = row_ptr[rows[i] + 1];
+    const int32_t c = cols[i];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col_idx[mid] < c) lo = mid + 1;
+      else hi = mid;
+    }
+    pos[i] = (lo < row_ptr[rows[i] + 1] && col_idx[lo] == c) ? lo : -1;
+  }
+}
+
 // ---------------------------------------------------------------- CSR pattern
 // One warp per row r. The row's candidate columns are the dofs of its incident cells
 // (inc lists, ascending cell); duplicates are removed in a shared-memory open-addressing

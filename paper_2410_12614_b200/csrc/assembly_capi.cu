@@ -229,6 +229,52 @@ int mpfem_b200_dofmap(int p, const int32_t* cells, int64_t n_cells, int64_t n_ve
                                  stream);
 }
 
+int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                           int64_t* row_ptr, int32_t* col_idx, int64_t* nnz, void* stream) {
+  return mpfem_b200_csr_pattern_cols(cell_dofs, nullptr, n_cells, n_loc, n_dofs, row_ptr, col_idx, nnz,
+                                     stream);
+}
+
+int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
+                            const int64_t* row_ptr, const int32_t* col_idx, int32_t* pos_map,
+                            int64_t* seg_ptr, uint32_t* perm, void* stream) {
+  return mpfem_b200_scatter_plan_cols(cell_dofs, nullptr, n_cells, n_loc, n_dofs, row_ptr, col_idx,
+                                      pos_map, seg_ptr, perm, stream);
+}
+
+int mpfem_b200_dofmap_table(const int32_t* key_dofs, const int32_t* val_dofs, int64_t n, int32_t* table,
+                            void* stream) {
+  return aguard([&] {
+    if (n < 0) throw AsmError{2, "negative length"};
+    if (n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    asmb::dof_table_kernel<<<grid_for(n), 256, 0, st>>>(key_dofs, val_dofs, n, table);
+    ACUDA(cudaGetLastError());
+  });
+}
+
+int mpfem_b200_dofmap_globalize(const int32_t* local_dofs, int64_t n, const int32_t* table,
+                                int32_t n_table, int32_t offset, int32_t* global_dofs, void* stream) {
+  return aguard([&] {
+    if (n < 0 || n_table < 0) throw AsmError{2, "negative length"};
+    if (n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    asmb::dof_globalize_kernel<<<grid_for(n), 256, 0, st>>>(local_dofs, n, table, n_table, offset, global_dofs);
+    ACUDA(cudaGetLastError());
+  });
+}
+
+int mpfem_b200_csr_find(const int64_t* row_ptr, const int32_t* col_idx, const int32_t* rows,
+                        const int32_t* cols, int64_t n, int64_t* pos, void* stream) {
+  return aguard([&] {
+    if (n < 0) throw AsmError{2, "negative length"};
+    if (n == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    asmb::csr_find_kernel<<<grid_for(n), 256, 0, st>>>(row_ptr, col_idx, rows, cols, n, pos);
+    ACUDA(cudaGetLastError());
+  });
+}
+
 int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
                          int64_t* inc_ptr, int64_t* inc, void* stream) {
   return aguard([&] {
@@ -239,9 +285,11 @@ int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc, i
   });
 }
 
-int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
-                           int64_t* row_ptr, int32_t* col_idx, int64_t* nnz, void* stream) {
+int mpfem_b200_csr_pattern_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                int n_loc, int32_t n_dofs, int64_t* row_ptr, int32_t* col_idx,
+                                int64_t* nnz, void* stream) {
   return aguard([&] {
+    if (!col_dofs) col_dofs = cell_dofs;
     if (n_loc < 1 || n_dofs < 1) throw AsmError{2, "dof map has no complete cells"};
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch S(st);
@@ -262,7 +310,7 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
     const unsigned grid = unsigned(std::min<int64_t>((n_dofs + warps - 1) / warps, 148 * 32));
     int64_t* row_nnz = S.get<int64_t>(size_t(n_dofs) + 1);
     ACUDA(cudaMemsetAsync(row_nnz + n_dofs, 0, sizeof(int64_t), st));
-    asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs, hcap,
+    asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(col_dofs, n_loc, inc_ptr, inc, n_dofs, hcap,
                                                           0, row_nnz, nullptr, nullptr);
     ACUDA(cudaGetLastError());
     size_t tb = 0;
@@ -273,17 +321,19 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
     if (total >= (int64_t(1) << 31)) throw AsmError{2, "nnz must fit int32 positions (split the mesh)"};
     if (nnz) *nnz = total;
     if (col_idx) {
-      asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, n_dofs,
+      asmb::csr_rows_kernel<<<grid, warps * 32, smem, st>>>(col_dofs, n_loc, inc_ptr, inc, n_dofs,
                                                             hcap, 1, nullptr, row_ptr, col_idx);
       ACUDA(cudaGetLastError());
     }
   });
 }
 
-int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
-                            const int64_t* row_ptr, const int32_t* col_idx, int32_t* pos_map,
-                            int64_t* seg_ptr, uint32_t* perm, void* stream) {
+int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                 int n_loc, int32_t n_dofs, const int64_t* row_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, int64_t* seg_ptr,
+                                 uint32_t* perm, void* stream) {
   return aguard([&] {
+    if (!col_dofs) col_dofs = cell_dofs;
     if (n_loc < 1 || n_dofs < 1 || !pos_map) throw AsmError{2, "scatter plan needs a dof map and pos_map"};
     const int64_t nk = n_cells * n_loc * n_loc;
     if (nk > int64_t(UINT32_MAX)) throw AsmError{2, "n_cells * n_loc^2 must fit 32 bits"};
@@ -311,7 +361,7 @@ int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc
     };
     {
       auto [grid, warps, smem] = launch_dims(size_t(rcap) * 8, reinterpret_cast<const void*>(asmb::plan_pos_kernel));
-      asmb::plan_pos_kernel<<<grid, warps * 32, smem, st>>>(cell_dofs, n_loc, inc_ptr, inc, row_ptr, col_idx,
+      asmb::plan_pos_kernel<<<grid, warps * 32, smem, st>>>(col_dofs, n_loc, inc_ptr, inc, row_ptr, col_idx,
                                                             n_dofs, rcap, pos_map, counts);
       ACUDA(cudaGetLastError());
     }
