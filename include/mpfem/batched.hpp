@@ -29,7 +29,7 @@ std::vector<Mat> bilinear_kernel(const KernelSetup& setup, const std::vector<Geo
                                  const std::vector<Coefficients>& z, FpFlags& flags);
 
 // Releases the device setups the shim created (cached per configuration, rule and
-// tabulation); optional, they are also released at exit.
+// tabulation). Optional: without it they live until the process exits.
 void release_device_setups();
 
 }  // namespace mpfem

@@ -3,7 +3,7 @@
 // against the reference library or against the B200 drop-in shim. Supports the macros those
 // tests use: TEST_CASE, CHECK, CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, CHECK_NOTHROW,
 // doctest::Approx(..).epsilon(..). Prints one line per test case and a summary; exit status
-// 0 iff every check passed. Filter with argv[1] (substring of the case name).
+// 0 iff every check passed. Arguments select the cases whose name contains any of them.
 #pragma once
 #include <cmath>
 #include <cstdio>
@@ -59,10 +59,11 @@ inline void fail(const char* file, int line, const char* what) {
 }  // namespace detail
 
 inline int run(int argc, char** argv) {
-  const char* filter = argc > 1 ? argv[1] : nullptr;
   int n_cases = 0, n_failed = 0;
   for (auto& c : detail::registry()) {
-    if (filter && !std::strstr(c.name, filter)) continue;
+    bool selected = argc <= 1;  // no filter: every case; else cases matching any argument
+    for (int a = 1; a < argc && !selected; ++a) selected = std::strstr(c.name, argv[a]) != nullptr;
+    if (!selected) continue;
     ++n_cases;
     detail::case_failures() = 0;
     const long f0 = detail::failures();

@@ -54,16 +54,16 @@ uint64_t fnv(uint64_t h, const void* p, size_t n) {
 
 using SetupKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int, int, uint64_t>;
 
+// Device setups live until release_device_setups() or process exit. The cache is never
+// destroyed by a static destructor: at exit the CUDA runtime may already be torn down, and
+// releasing device memory then corrupts its state; the driver reclaims everything anyway.
 struct Cache {
   std::mutex mu;
   std::map<SetupKey, mpfem_b200_setup_t> setups;
-  ~Cache() {
-    for (auto& kv : setups) mpfem_b200_setup_destroy(kv.second);
-  }
 };
 Cache& cache() {
-  static Cache c;
-  return c;
+  static Cache* c = new Cache();
+  return *c;
 }
 
 // The device setup of a reference KernelSetup: same config, rule and operand tabulations.

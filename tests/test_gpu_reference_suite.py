@@ -41,6 +41,7 @@ def run_suite():
 def test_reference_unit_tests_against_b200_shim():
     r, cases = run_suite()
     print(r.stdout)
+    assert "test cases: 29" in r.stdout and r.returncode in (0, 1), (r.returncode, r.stdout[-2000:])
     assert len(cases) == 29, r.stdout[-2000:]
     failed = {n for n, st in cases.items() if st == "FAIL"}
     unexpected = failed - set(UNSUPPORTED)
