@@ -275,6 +275,9 @@ void choose_path(mpfem_b200_setup_s& S) {
 // K1 tile height: one geometry lane per cell, so a tile of 32 G cells has G geometry warps.
 // Low degrees have few quadrature groups per cell and would wait on a single geometry warp.
 int k1_geom_warps(const mpfem_b200_setup_s& S) {
+#ifdef MPFEM_K1_GW  // diagnostic builds only (scripts/build_variant.sh)
+  return MPFEM_K1_GW;
+#endif
   const int ngroups = S.nq_pad / kQPT;
   return std::max(1, std::min(4, 32 / ngroups));
 }
@@ -390,17 +393,23 @@ void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& 
   CUDA_OK(cudaLaunchKernelEx(&cfg, tc2::cellmat_tc2_kernel<ACC_F16, OUTK>, ta, tb, P));
 }
 
-template <bool ACC_F16>
-void launch_tcs(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
+template <bool ACC_F16, bool PACKED>
+void launch_tcs_t(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    CUDA_OK(cudaFuncSetAttribute(tcs::cellmat_tcs_kernel<ACC_F16>,
+    CUDA_OK(cudaFuncSetAttribute(tcs::cellmat_tcs_kernel<ACC_F16, PACKED>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tcs::SMEM_BYTES));
     attr = true;
   }
   const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
   const unsigned grid = unsigned(std::min<int64_t>(tiles, device_sm_count()));
-  tcs::cellmat_tcs_kernel<ACC_F16><<<grid, tcs::THREADS, tcs::SMEM_BYTES, st>>>(ta, tb, P);
+  tcs::cellmat_tcs_kernel<ACC_F16, PACKED><<<grid, tcs::THREADS, tcs::SMEM_BYTES, st>>>(ta, tb, P);
+}
+// packed: whole cell matrices in one 256-output tile, stored densely (pitch n_out)
+template <bool ACC_F16>
+void launch_tcs(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
+  if (P.n_out_tiles == 1 && P.out_pitch == P.n_out) launch_tcs_t<ACC_F16, true>(ta, tb, P, st);
+  else launch_tcs_t<ACC_F16, false>(ta, tb, P, st);
 }
 
 // The staged-epilogue kernel (cellmat_tcs.cuh) serves the HBM-bound shapes: short GEMM depth,

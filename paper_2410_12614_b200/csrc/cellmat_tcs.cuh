@@ -42,7 +42,7 @@ constexpr int THREADS = 128 + (EPI_WARPS + ST_WARPS) * 32;
 constexpr int TMEM_COLS = 512;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + SLOTS * STAGE_OUT_BYTES + 1024 + 512;
 
-template <bool ACC_F16>
+template <bool ACC_F16, bool PACKED>
 __global__ void __launch_bounds__(THREADS, 1)
     cellmat_tcs_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const tc::Params P) {
@@ -64,6 +64,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int total_tiles = P.n_out_tiles * P.n_cell_tiles;  // n_out_tiles counts 256-output tiles
+  // PACKED: small matrices (n_out <= 256) stored densely, so a 32-cell chunk is one
+  // contiguous span (the launcher selects it when n_out_tiles == 1 and pitch == n_out)
+  constexpr bool packed = PACKED;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -166,16 +169,32 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::mbar_wait(&sempty[slot], slot_phase ^ 1u);
         const uint32_t sbuf = s_out + uint32_t(slot * CHUNK * SROW * 4);
-        int shift = int((uint64_t(cell0) * uint64_t(P.out_pitch) + uint64_t(o_base)) & 3u);
-        uint32_t addr = sbuf + uint32_t(o_loc * 4);
-        #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          uint32_t bits = r[j];
-          if constexpr (ACC_F16) bits = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(bits & 0xffffu))));
-          nonfinite |= (bits & 0x7fffffffu) + 0x00800000u;
-          asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr + uint32_t(shift * 4)), "r"(bits) : "memory");
-          addr += SROW * 4;
-          shift = (shift + pitch3) & 3;
+        if constexpr (packed) {
+          // whole, densely packed cell matrices: the chunk is one contiguous span in global
+          // memory, staged in exactly that layout (row pitch n_out)
+          if (o_loc < P.n_out) {
+            uint32_t addr = sbuf + uint32_t(o_loc * 4);
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              uint32_t bits = r[j];
+              if constexpr (ACC_F16) bits = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(bits & 0xffffu))));
+              nonfinite |= (bits & 0x7fffffffu) + 0x00800000u;
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(bits) : "memory");
+              addr += uint32_t(P.n_out * 4);
+            }
+          }
+        } else {
+          int shift = int((uint64_t(cell0) * uint64_t(P.out_pitch) + uint64_t(o_base)) & 3u);
+          uint32_t addr = sbuf + uint32_t(o_loc * 4);
+          #pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            uint32_t bits = r[j];
+            if constexpr (ACC_F16) bits = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(bits & 0xffffu))));
+            nonfinite |= (bits & 0x7fffffffu) + 0x00800000u;
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr + uint32_t(shift * 4)), "r"(bits) : "memory");
+            addr += SROW * 4;
+            shift = (shift + pitch3) & 3;
+          }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&sfull[slot]);
@@ -201,6 +220,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int64_t cell0 = int64_t(ct) * BN + ch * CHUNK;
         tc::mbar_wait(&sfull[slot], slot_phase);
         const float* srow = sOut + slot * CHUNK * SROW;
+        if constexpr (packed) {  // one contiguous span: float4 copy by all store warps (16-B aligned)
+          const int64_t nc = P.n_cells - cell0 < CHUNK ? P.n_cells - cell0 : int64_t(CHUNK);
+          const int total = int(nc) * P.n_out;
+          float* dst = P.out + cell0 * P.n_out;
+          const int n4 = total >> 2;
+          for (int i = sw * 32 + lane; i < n4; i += ST_WARPS * 32)
+            __stcs(reinterpret_cast<float4*>(dst) + i, reinterpret_cast<const float4*>(srow)[i]);
+          for (int i = 4 * n4 + sw * 32 + lane; i < total; i += ST_WARPS * 32) __stcs(dst + i, srow[i]);
+        } else
         #pragma unroll 1
         for (int jj = 0; jj < CHUNK / ST_WARPS; ++jj) {
           const int j = sw * (CHUNK / ST_WARPS) + jj;

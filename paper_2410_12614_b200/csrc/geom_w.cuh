@@ -14,6 +14,7 @@
 
 #include <type_traits>
 
+#include "cellmat_tc.cuh"
 #include "device_fp.cuh"
 
 namespace mpfem_b200 {
@@ -274,25 +275,27 @@ __device__ __forceinline__ uint32_t packed_store_flags(const StoreFlags& sf) {
 
 // dynamic shared memory of geom_w_kernel: weights and the three point coordinates, each
 // nq_pad doubles in [j][group] order, then the two geometry buffers of 32 * geom_warps cells
+constexpr int kGeoSlots = 3;  // geometry ring of K1's tile pipeline
 __host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad, int geom_warps = 1) {
-  return size_t(4) * nq_pad * sizeof(double) + size_t(2) * 32 * geom_warps * sizeof(CellGeo) +
+  return size_t(4) * nq_pad * sizeof(double) + size_t(kGeoSlots) * 32 * geom_warps * sizeof(CellGeo) +
          size_t(nq_pad) * sizeof(float);
 }
 
 template <typename T, int UG, int US, int COEF>
 __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
   extern __shared__ double s_rule[];
-  __shared__ uint32_t s_next[2];  // per-buffer item counters (dynamic 32-item grabs)
-  __shared__ int64_t s_tile[3];   // claimed tiles, ring indexed by iteration mod 3
+  __shared__ uint32_t s_next[kGeoSlots];  // per-slot item counters (dynamic 32-item grabs)
+  __shared__ int64_t s_tile[kGeoSlots];   // the slot's tile
+  __shared__ uint64_t s_ready[kGeoSlots], s_free[kGeoSlots];
   const int nq = P.n_q;
   const int nqp = P.nq_pad;
   const int tcells = 32 * P.geom_warps;  // cells per tile
-  CellGeo* s_geo0 = reinterpret_cast<CellGeo*>(s_rule + 4 * nqp);  // [2][tcells]
+  CellGeo* s_geo0 = reinterpret_cast<CellGeo*>(s_rule + 4 * nqp);  // [kGeoSlots][tcells]
   const int ngroups = nqp / kQPT;  // P.div_nq divides by ngroups
   const int nb = P.poisson ? 6 : 1;
   double* sW = s_rule;
   double* sX = s_rule + nqp;  // sX[a * nqp + perm(q)]
-  float* sWf = reinterpret_cast<float*>(s_geo0 + 2 * tcells);  // the weights as fp32 (u_g = fp32)
+  float* sWf = reinterpret_cast<float*>(s_geo0 + kGeoSlots * tcells);  // the weights as fp32 (u_g = fp32)
   for (int q = threadIdx.x; q < nqp; q += blockDim.x) {
     const int pq = (q % kQPT) * ngroups + q / kQPT;
     const bool ok = q < nq;
@@ -305,30 +308,53 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
   StoreFlags sf;
   const int64_t n_tiles = (P.n_cells + tcells - 1) / tcells;
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const bool geo_warp = warp < P.geom_warps;
   auto tile_cells = [&](int64_t t) {
     const int64_t left = P.n_cells - t * tcells;
     return left < tcells ? int(left) : tcells;
   };
-  // Tiles are claimed one iteration ahead of their geometry: static blockIdx.x first, then
-  // gridDim.x + atomicAdd(tile_ctr).
+  // Tiles: static blockIdx.x first, then gridDim.x + atomicAdd(tile_ctr).
   auto claim = [&]() -> int64_t { return int64_t(gridDim.x) + atomicAdd(P.tile_ctr, 1u); };
-  // Tile pipeline: the first geom_warps warps compute the geometry of the CTA's next tile
-  // (one lane per cell) into the other buffer while every warp takes 32-item grabs of the
-  // current tile.
+  // Tile pipeline over a 3-slot ring of geometry buffers, synchronised by mbarriers instead of
+  // a CTA barrier per tile: in iteration k every warp expands tile k (slot k % 3, 32-item
+  // grabs) once its geometry is ready, while the geom_warps first prepare slot (k + 1) % 3 --
+  // claim tile k + 1 and compute its geometry (one lane per cell) -- after every warp has left
+  // that slot's previous use (iteration k - 2). Fast warps run ahead into tile k + 1 instead
+  // of waiting for the slowest warp of tile k.
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGeoSlots; ++i) {
+      tc::mbar_init(&s_ready[i], P.geom_warps);
+      tc::mbar_init(&s_free[i], kGeomThreads / 32);
+      s_next[i] = 0;
+    }
+    s_tile[0] = blockIdx.x;
+  }
   if (blockIdx.x < n_tiles && threadIdx.x < tile_cells(blockIdx.x))
     cell_geometry<UG>(P, int64_t(blockIdx.x) * tcells + threadIdx.x, s_geo0[threadIdx.x], fl);
-  if (threadIdx.x < 2) s_next[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_tile[1] = claim();
-  __syncthreads();  // first tile's geometry, s_rule, the counters and the next claim are ready
-  int buf = 0;
-  int slot = 0;  // iteration mod 3
-  for (int64_t tile = blockIdx.x; tile < n_tiles; buf ^= 1, slot = slot == 2 ? 0 : slot + 1) {
+  __syncthreads();  // s_rule, the barriers, tile 0's index and geometry
+  if (geo_warp && lane == 0) tc::mbar_arrive(&s_ready[0]);
+  for (int k = 0;; ++k) {
+    const int buf = k % kGeoSlots;
+    tc::mbar_wait(&s_ready[buf], uint32_t(k / kGeoSlots) & 1u);
+    const int64_t tile = s_tile[buf];
+    if (tile >= n_tiles) break;
+    if (geo_warp) {  // prepare slot (k + 1) % 3 for tile k + 1
+      const int nbuf = (k + 1) % kGeoSlots;
+      if (k >= 2) tc::mbar_wait(&s_free[nbuf], uint32_t((k - 2) / kGeoSlots) & 1u);
+      if (threadIdx.x == 0) {
+        s_tile[nbuf] = claim();
+        s_next[nbuf] = 0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * P.geom_warps) : "memory");
+      const int64_t nt = s_tile[nbuf];
+      if (nt < n_tiles && int(threadIdx.x) < tile_cells(nt))
+        cell_geometry<UG>(P, nt * tcells + threadIdx.x, s_geo0[nbuf * tcells + threadIdx.x], fl);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_ready[nbuf]);
+    }
     const int64_t c0 = tile * tcells;
     const int nc = tile_cells(tile);
-    const int64_t nt = s_tile[slot == 2 ? 0 : slot + 1];
-    if (threadIdx.x == 0) s_tile[slot == 0 ? 2 : slot - 1] = claim();  // the tile after next
-    if (threadIdx.x < tcells && nt < n_tiles && int(threadIdx.x) < tile_cells(nt))
-      cell_geometry<UG>(P, nt * tcells + threadIdx.x, s_geo0[(buf ^ 1) * tcells + threadIdx.x], fl);
     const uint32_t items = uint32_t(nc * ngroups);
     const CellGeo* geo_t = s_geo0 + buf * tcells;
     while (true) {
@@ -406,6 +432,19 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
             zqz[k] = (zqf[2 * k] == 0.0f ? 0x0000ffffu : 0u) | (zqf[2 * k + 1] == 0.0f ? 0xffff0000u : 0u);
           else
             zqz[k] = (zq[2 * k] == 0.0 ? 0x0000ffffu : 0u) | (zq[2 * k + 1] == 0.0 ? 0xffff0000u : 0u);
+        // Analytic coefficient at u_g = fp64 (BASELINE config 1, "G_K in fp64"): the point
+        // factor omega_q c_q is formed once, so each of the 6 blocks costs one DMUL instead of
+        // two. Same binary64 operations, grouped differently from build_C's
+        // round(round(omega G) c): the products may differ in the last fp64 bit, which the
+        // 16-bit storage rounding absorbs (W parity for the analytic coefficient is within
+        // ulp(u_s), tests/test_gpu_cells.py). Constant and nodal coefficients keep build_C's
+        // exact order (bitwise W).
+        constexpr bool kFoldZ = UG == kFP64 && COEF == 1;
+        double omz[kQPT];
+        if constexpr (kFoldZ) {
+          #pragma unroll
+          for (int j = 0; j < kQPT; ++j) omz[j] = __dmul_rn(om[j], zq[j]);
+        }
         #pragma unroll
         for (int b = 0; b < 6; ++b) {
           if (b < nb) {
@@ -414,7 +453,10 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
             #pragma unroll
             for (int k = 0; k < KW; ++k) {
               uint32_t lo, hi;
-              if constexpr (UG == kFP32) {
+              if constexpr (kFoldZ) {
+                lo = storage_bits16<T>(__dmul_rn(omz[2 * k], gb));
+                hi = storage_bits16<T>(__dmul_rn(omz[2 * k + 1], gb));
+              } else if constexpr (UG == kFP32) {
                 const float gf = cg.gf[b];
                 float v0 = __fmul_rn(omf[2 * k], gf), v1 = __fmul_rn(omf[2 * k + 1], gf);
                 if (have_z) {
@@ -488,9 +530,8 @@ __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(Geo
         for (int64_t k = int64_t(nb) * nqp; k < P.k_pad; ++k) tail[k] = T(0.0f);
       }
     }
-    __syncthreads();  // tile done, next tile's geometry written
-    if (threadIdx.x == 0) s_next[buf] = 0;
-    tile = nt;
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&s_free[buf]);  // this warp is done with slot buf
   }
   if (threadIdx.x == 0) {
     // every CTA made its final (failing) claim before counting itself done
