@@ -474,7 +474,7 @@ void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void*
     }
   } else if (S.path == kPathF32) {
     constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
-    dim3 grid(unsigned(S.n_out_pad / BN), unsigned((n + BM - 1) / BM));
+    dim3 grid(unsigned((n + BM - 1) / BM), unsigned(S.n_out_pad / BN));
     cellmat_simt_kernel<float, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
         static_cast<const float*>(W), static_cast<const float*>(S.d_T.p), static_cast<float*>(out),
         n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
@@ -486,7 +486,7 @@ void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void*
                                    dm::SMEM_BYTES));
       attr = true;
     }
-    dim3 grid(unsigned(S.n_out_pad / dm::BN), unsigned((n + dm::BM - 1) / dm::BM));
+    dim3 grid(unsigned((n + dm::BM - 1) / dm::BM), unsigned(S.n_out_pad / dm::BN));
     dm::cellmat_dmma_kernel<<<grid, dm::THREADS, dm::SMEM_BYTES, st>>>(
         static_cast<const double*>(W), static_cast<const double*>(S.d_T.p), static_cast<double*>(out),
         n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));

@@ -45,8 +45,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;  // warp tile (64 cells, 32 outputs)
-  const int64_t c_base = int64_t(blockIdx.y) * BM;
-  const int64_t o_base = int64_t(blockIdx.x) * BN;
+  const int64_t c_base = int64_t(blockIdx.x) * BM;  // cell tiles on x (2^31 - 1 blocks)
+  const int64_t o_base = int64_t(blockIdx.y) * BN;
   // global -> register staging: A row (tid / 2) columns (tid % 2) * 8 .. + 8; B row tid / 16
   // columns (tid % 16) * 8 .. + 8
   const int ar = tid >> 1, ac = (tid & 1) * 8;

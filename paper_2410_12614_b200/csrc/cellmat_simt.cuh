@@ -20,8 +20,8 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   __shared__ T Bs[BK][BN];
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
-  const int64_t c0 = int64_t(blockIdx.y) * BM;
-  const int64_t o0 = int64_t(blockIdx.x) * BN;
+  const int64_t c0 = int64_t(blockIdx.x) * BM;  // cell tiles on x (2^31 - 1 blocks)
+  const int64_t o0 = int64_t(blockIdx.y) * BN;
   T acc[TM][TN];
   #pragma unroll
   for (int i = 0; i < TM; ++i)

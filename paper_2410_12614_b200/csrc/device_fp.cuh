@@ -772,10 +772,19 @@ __constant__ double kSinPiC[9] = {3.141592653589793, -5.167712780049969, 2.55016
                                   0.0004662998161898394, -2.1903497074626018e-05, 7.697826768224191e-07};
 __device__ __forceinline__ double sinpi_poly(double r) {  // sin(pi r), |r| <= 0.5
   const double s = r * r;
+#ifdef MPFEM_ESTRIN  // diagnostic builds only: Estrin scheme (depth 4 instead of 8)
+  const double s2 = s * s, s4 = s2 * s2;
+  const double a0 = fma(kSinPiC[1], s, kSinPiC[0]), a1 = fma(kSinPiC[3], s, kSinPiC[2]);
+  const double a2 = fma(kSinPiC[5], s, kSinPiC[4]), a3 = fma(kSinPiC[7], s, kSinPiC[6]);
+  const double b0 = fma(a1, s2, a0), b1 = fma(a3, s2, a2);
+  const double p = fma(fma(kSinPiC[8], s4, b1), s4, b0);
+  return r * p;
+#else
   double p = kSinPiC[8];
   #pragma unroll
   for (int k = 7; k >= 0; --k) p = fma(p, s, kSinPiC[k]);
   return r * p;
+#endif
 }
 // Rounding to an integer without the fp64 conversion pipe (FRND / F2I run at a fraction
 // of DFMA throughput): t = a + 1.5*2^52 rounds a to the nearest integer (ties to even) in
