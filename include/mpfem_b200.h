@@ -272,7 +272,7 @@ int mpfem_b200_csr_pattern_cols(const int32_t* cell_dofs, const int32_t* col_dof
                                 int64_t* nnz, void* stream);
 int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
                                  int n_loc, int32_t n_dofs, const int64_t* row_ptr,
-                                 const int32_t* col_idx, int32_t* pos_map, int64_t* seg_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
                                  uint32_t* perm, void* stream);
 /* table[key_dofs[i]] = val_dofs[i] for i < n (layer-local id -> global id). */
 int mpfem_b200_dofmap_table(const int32_t* key_dofs, const int32_t* val_dofs, int64_t n, int32_t* table,
@@ -292,12 +292,12 @@ int mpfem_b200_incidence(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
 
 /* Scatter plan for a mesh (computed once, like the pattern):
  *   pos_map (n_cells x n_loc x n_loc int32): CSR position of every local entry;
- *   seg_ptr (nnz + 1 int64) and perm (n_cells x n_loc^2 uint32): local-entry indices sorted
+ *   seg_ptr (nnz + 1 uint32) and perm (n_cells x n_loc^2 uint32): local-entry indices sorted
  *   stably by position -- each CSR entry's contributions in the reference's order
  *   (cell asc, i asc, j asc; assembly.cpp:50-67). seg_ptr/perm may be NULL (atomic only). */
 int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
                             int32_t n_dofs, const int64_t* row_ptr, const int32_t* col_idx,
-                            int32_t* pos_map, int64_t* seg_ptr, uint32_t* perm, void* stream);
+                            int32_t* pos_map, uint32_t* seg_ptr, uint32_t* perm, void* stream);
 
 /* Replaces assemble_matrix (assembly.cpp:41-88): scatter-add of local matrices into
  * CSR values. mode 0 = atomic (red.global at pos_map, order-free), 1 = deterministic
@@ -311,7 +311,7 @@ int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc
  *               prefix partial sums received from the rank owning lower cells). */
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
                         int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
-                        const int32_t* pos_map, const int64_t* seg_ptr, const uint32_t* perm,
+                        const int32_t* pos_map, const uint32_t* seg_ptr, const uint32_t* perm,
                         void* values, int fmt, int mode, int accumulate, const int32_t* rows,
                         int64_t n_rows, void* stream);
 

@@ -36,7 +36,7 @@ class CsrPattern:
     inc_ptr: "object"  # int64 (n_rows + 1): dof -> incident (cell, local) pairs
     inc: "object"      # int64 (n_cells * n_local), cell * n_local + local, ascending
     pos_map: "object" = None  # int32 (n_cells * n_local^2): CSR position of each local entry
-    seg_ptr: "object" = None  # int64 (nnz + 1): contribution segments per CSR entry
+    seg_ptr: "object" = None  # int32 view of uint32 (nnz + 1): contribution segments per CSR entry
     perm: "object" = None     # int32 view of uint32 (n_cells * n_local^2): reference order
 
     @property
@@ -88,7 +88,7 @@ def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: 
         nk = dm.n_cells * dm.n_local * dm.n_local
         pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
         if deterministic_plan:
-            pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int64, device=dev)
+            pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int32, device=dev)
             pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
         check(lib().mpfem_b200_scatter_plan(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
                                             _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
@@ -212,7 +212,7 @@ class CudaPartitionBackend:
         pat = CsrPattern(n_rows, row_ptr, col_idx, inc_ptr, inc)
         nk = n * n_loc * n_loc
         pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
-        pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int64, device=dev)
+        pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int32, device=dev)
         pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
         check(lib().mpfem_b200_scatter_plan_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
                                                  _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),

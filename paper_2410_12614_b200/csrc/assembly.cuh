@@ -16,13 +16,16 @@
 //
 // Scatter plan (precomputed once per mesh, like the pattern): pos_map gives the CSR
 // position of every local entry; perm lists the local entries sorted stably by that
-// position, so within an entry's segment they appear in the reference's order (cell asc,
+// position (seg_ptr: nnz + 1 offsets into perm, uint32 -- n_cells n_loc^2 < 2^32 is required
+// anyway), so within an entry's segment they appear in the reference's order (cell asc,
 // i asc, j asc). Deterministic mode sums each segment sequentially at the value format --
 // the reference's sum bit for bit; atomic mode issues one red.global.add per local entry.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
+
+#include "l2_hints.cuh"
 
 namespace mpfem_b200 {
 namespace asmb {
@@ -367,7 +370,7 @@ __global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
                                 const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
                                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                 int32_t n_rows, int rcap, int32_t* __restrict__ pos_map,
-                                int64_t* __restrict__ counts) {
+                                uint32_t* __restrict__ counts) {
   extern __shared__ int32_t sbuf[];
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -393,7 +396,7 @@ __global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
       __syncwarp();
     }
     if (counts)
-      for (int i = lane; i < u; i += 32) counts[o + i] = cnt[i];
+      for (int i = lane; i < u; i += 32) counts[o + i] = uint32_t(cnt[i]);
     __syncwarp();
   }
 }
@@ -403,12 +406,12 @@ __global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
 // cursors that start at seg_ptr. Same walk as plan_pos_kernel; positions from pos_map.
 __global__ void plan_perm_kernel(int n_loc, const int64_t* __restrict__ inc_ptr,
                                  const int64_t* __restrict__ inc, const int64_t* __restrict__ row_ptr,
-                                 const int32_t* __restrict__ pos_map, const int64_t* __restrict__ seg_ptr,
+                                 const int32_t* __restrict__ pos_map, const uint32_t* __restrict__ seg_ptr,
                                  int32_t n_rows, int rcap, uint32_t* __restrict__ perm) {
-  extern __shared__ int64_t cursor_buf[];
+  extern __shared__ uint32_t cursor_buf[];
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t* cur = cursor_buf + int64_t(w) * rcap;
+  uint32_t* cur = cursor_buf + int64_t(w) * rcap;
   for (int64_t r = int64_t(blockIdx.x) * warps + w; r < n_rows; r += int64_t(gridDim.x) * warps) {
     const int64_t o = row_ptr[r];
     const int u = int(row_ptr[r + 1] - o);
@@ -442,13 +445,13 @@ __device__ __forceinline__ TV cast_value(TL x) {
 // contribution taken exactly (start from -0.0); else continue from values[e].
 template <typename TL, typename TV>
 __device__ __forceinline__ void entry_sum(const TL* __restrict__ locals, int64_t per_cell,
-                                          const int64_t* __restrict__ seg_ptr,
+                                          const uint32_t* __restrict__ seg_ptr,
                                           const uint32_t* __restrict__ perm, int64_t e,
                                           int64_t cell_begin, int64_t cell_end, int init,
                                           TV* __restrict__ values) {
   TV acc = init ? TV(-0.0) : values[e];
-  const int64_t b = seg_ptr[e], en = seg_ptr[e + 1];
-  for (int64_t t = b; t < en; ++t) {
+  const uint32_t b = seg_ptr[e], en = seg_ptr[e + 1];
+  for (uint32_t t = b; t < en; ++t) {
     const int64_t k = perm[t];
     const int64_t cell = k / per_cell;
     if (cell < cell_begin || cell >= cell_end) continue;
@@ -476,14 +479,15 @@ __device__ __forceinline__ void entry_sum(const TL* __restrict__ locals, int64_t
 constexpr int kSegBlock = MPFEM_SEG_BLOCK;
 constexpr int kSegSmem = MPFEM_SEG_SMEM_KB * 1024;  // dynamic shared memory per CTA
 constexpr int kSegCtasPerSm = MPFEM_SEG_CTAS;
+constexpr int kSegHeadBytes = ((kSegBlock + 1) * 4 + 15) / 16 * 16;  // staged segment offsets
 template <typename TL, typename TV>
 __global__ void __launch_bounds__(256) assemble_seg_block_kernel(
-    const TL* __restrict__ locals, int64_t per_cell, const int64_t* __restrict__ seg_ptr,
+    const TL* __restrict__ locals, int64_t per_cell, const uint32_t* __restrict__ seg_ptr,
     const uint32_t* __restrict__ perm, int64_t nnz, int64_t cell_begin, int64_t cell_end, int init,
     int cap, TV* __restrict__ values) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int64_t* s_seg = reinterpret_cast<int64_t*>(smem_raw);
-  TV* s_val = reinterpret_cast<TV*>(s_seg + kSegBlock + 1);
+  uint32_t* s_seg = reinterpret_cast<uint32_t*>(smem_raw);
+  TV* s_val = reinterpret_cast<TV*>(smem_raw + kSegHeadBytes);
   const int64_t kb = cell_begin * per_cell, ke = cell_end * per_cell;
   const int64_t n_blocks = (nnz + kSegBlock - 1) / kSegBlock;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
@@ -492,7 +496,7 @@ __global__ void __launch_bounds__(256) assemble_seg_block_kernel(
     for (int i = threadIdx.x; i <= n; i += blockDim.x) s_seg[i] = seg_ptr[e0 + i];
     __syncthreads();
     const int64_t t0 = s_seg[0];
-    const int64_t tn = s_seg[n] - t0;
+    const int64_t tn = int64_t(s_seg[n]) - t0;
     if (tn <= cap) {
       const int T = int(tn);
       for (int t = threadIdx.x; t < T; t += 4 * blockDim.x) {
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(256) assemble_seg_block_kernel(
       __syncthreads();
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
         TV acc = init ? TV(-0.0) : values[e0 + i];
-        const int b = int(s_seg[i] - t0), en = int(s_seg[i + 1] - t0);
+        const int b = int(int64_t(s_seg[i]) - t0), en = int(int64_t(s_seg[i + 1]) - t0);
         for (int t = b; t < en; ++t) acc = acc + s_val[t];
         values[e0 + i] = acc;
       }
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(256) assemble_pull_kernel(
 template <typename TL, typename TV>
 __global__ void assemble_seg_rows_kernel(const TL* __restrict__ locals, int64_t per_cell,
                                          const int64_t* __restrict__ row_ptr,
-                                         const int64_t* __restrict__ seg_ptr,
+                                         const uint32_t* __restrict__ seg_ptr,
                                          const uint32_t* __restrict__ perm,
                                          const int32_t* __restrict__ rows, int64_t n_rows,
                                          int64_t cell_begin, int64_t cell_end, int init,
@@ -665,13 +669,19 @@ __global__ void assemble_seg_rows_kernel(const TL* __restrict__ locals, int64_t 
   }
 }
 
-// Atomic scatter: thread per local entry, red.global.add at its precomputed position.
+// Atomic scatter: thread per local entry, red.global.add at its precomputed position. The
+// local matrices and the plan are read once (streaming loads, evict-first) and the reductions
+// carry an evict-last hint, so that the L2 keeps the CSR value lines the neighbouring cells
+// return to (config 4 P3: 11.5 -> 7.5 ms, P2 2.23 -> 1.66 ms; profiles/r2_asm_order_experiment.txt).
+// A Morton traversal of the cells on top of that gained <= 3 % at P3 and lost at P2 (same
+// file): the kernel is bound by the streams it must read (locals, plan) at ~4.4 TB/s.
 template <typename TL, typename TV>
 __global__ void assemble_atomic_kernel(const TL* __restrict__ locals, const int32_t* __restrict__ pos_map,
                                        int64_t k_begin, int64_t k_end, TV* __restrict__ values) {
+  const uint64_t keep = policy_evict_last();
   for (int64_t k = k_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < k_end;
        k += int64_t(gridDim.x) * blockDim.x)
-    atomicAdd(&values[pos_map[k]], cast_value<TL, TV>(locals[k]));
+    red_add_keep(&values[__ldcs(pos_map + k)], cast_value<TL, TV>(__ldcs(locals + k)), keep);
 }
 
 }  // namespace asmb

@@ -237,7 +237,7 @@ int mpfem_b200_csr_pattern(const int32_t* cell_dofs, int64_t n_cells, int n_loc,
 
 int mpfem_b200_scatter_plan(const int32_t* cell_dofs, int64_t n_cells, int n_loc, int32_t n_dofs,
                             const int64_t* row_ptr, const int32_t* col_idx, int32_t* pos_map,
-                            int64_t* seg_ptr, uint32_t* perm, void* stream) {
+                            uint32_t* seg_ptr, uint32_t* perm, void* stream) {
   return mpfem_b200_scatter_plan_cols(cell_dofs, nullptr, n_cells, n_loc, n_dofs, row_ptr, col_idx,
                                       pos_map, seg_ptr, perm, stream);
 }
@@ -330,7 +330,7 @@ int mpfem_b200_csr_pattern_cols(const int32_t* cell_dofs, const int32_t* col_dof
 
 int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
                                  int n_loc, int32_t n_dofs, const int64_t* row_ptr,
-                                 const int32_t* col_idx, int32_t* pos_map, int64_t* seg_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
                                  uint32_t* perm, void* stream) {
   return aguard([&] {
     if (!col_dofs) col_dofs = cell_dofs;
@@ -349,8 +349,8 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
     const int64_t umax = max_count(row_ptr, n_dofs, S);
     while (rcap < umax) rcap <<= 1;
     const int64_t nnz = read1(row_ptr + n_dofs, st);
-    int64_t* counts = nullptr;
-    if (seg_ptr) counts = S.get<int64_t>(size_t(nnz) + 1);
+    uint32_t* counts = nullptr;
+    if (seg_ptr) counts = S.get<uint32_t>(size_t(nnz) + 1);
     auto launch_dims = [&](size_t per_warp, const void* fn) {
       const int warps = int(std::max<size_t>(1, std::min<size_t>(8, (48u << 10) / per_warp)));
       const size_t smem = size_t(warps) * per_warp;
@@ -366,13 +366,13 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
       ACUDA(cudaGetLastError());
     }
     if (!seg_ptr) return;
-    ACUDA(cudaMemsetAsync(counts + nnz, 0, sizeof(int64_t), st));
+    ACUDA(cudaMemsetAsync(counts + nnz, 0, sizeof(uint32_t), st));
     size_t tb = 0;
     ACUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, counts, seg_ptr, nnz + 1, st));
     void* tmp = S.get<char>(tb);
     ACUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, counts, seg_ptr, nnz + 1, st));
     {
-      auto [grid, warps, smem] = launch_dims(size_t(rcap) * 8, reinterpret_cast<const void*>(asmb::plan_perm_kernel));
+      auto [grid, warps, smem] = launch_dims(size_t(rcap) * 4, reinterpret_cast<const void*>(asmb::plan_perm_kernel));
       asmb::plan_perm_kernel<<<grid, warps * 32, smem, st>>>(n_loc, inc_ptr, inc, row_ptr, pos_map, seg_ptr,
                                                              n_dofs, rcap, perm);
       ACUDA(cudaGetLastError());
@@ -422,7 +422,7 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
 
 int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, int64_t cell_end,
                         int n_loc, const int64_t* row_ptr, int32_t n_dofs, const int32_t* pos_map,
-                        const int64_t* seg_ptr, const uint32_t* perm, void* values, int fmt,
+                        const uint32_t* seg_ptr, const uint32_t* perm, void* values, int fmt,
                         int mode, int accumulate, const int32_t* rows, int64_t n_rows,
                         void* stream) {
   return aguard([&] {
@@ -467,8 +467,8 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin, 
         const int64_t nnz = read1(row_ptr + n_dofs, st);
         // block-staged segment gather (bitwise the per-entry sequential sum)
         const size_t vsz = fmt == 2 ? 4 : 8;
-        const int cap = int((asmb::kSegSmem - (asmb::kSegBlock + 1) * 8) / vsz);
-        const size_t smem = (asmb::kSegBlock + 1) * 8 + size_t(cap) * vsz;
+        const int cap = int((asmb::kSegSmem - asmb::kSegHeadBytes) / vsz);
+        const size_t smem = asmb::kSegHeadBytes + size_t(cap) * vsz;
         const unsigned grid = unsigned(std::max<int64_t>(
             1, std::min<int64_t>((nnz + asmb::kSegBlock - 1) / asmb::kSegBlock, 148 * asmb::kSegCtasPerSm)));
 #define MPFEM_SEG(TL, TV)                                                                          \

@@ -87,12 +87,12 @@ __global__ void iota_dofs_kernel(int32_t* cd, int64_t n) {
 // fmt, then each entry's contributions summed in the reference's order (seg_ptr / perm: cell
 // asc, i asc, j asc) with one rounding to fmt per addition. Binary64 carriers; the binary64
 // sum of two 16-bit values is exact, so dround gives the reference's fp_add bit for bit.
-__global__ void assemble_fmt_kernel(const double* __restrict__ locals, const int64_t* __restrict__ seg_ptr,
+__global__ void assemble_fmt_kernel(const double* __restrict__ locals, const uint32_t* __restrict__ seg_ptr,
                                     const uint32_t* __restrict__ perm, int64_t nnz, int fmt,
                                     double* __restrict__ values, uint32_t* flags) {
   uint32_t fl = 0;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t b = seg_ptr[e], en = seg_ptr[e + 1];
+    const uint32_t b = seg_ptr[e], en = seg_ptr[e + 1];
     double acc = dround(locals[perm[b]], fmt, fl);
     for (int64_t t = b + 1; t < en; ++t) acc = dadd(acc, dround(locals[perm[t]], fmt, fl), fmt, fl);
     values[e] = acc;
@@ -162,10 +162,10 @@ int mpfem_b200_asm_plan_create(const int32_t* cell_dofs, int64_t n_cells, int n_
                                    &P->nnz, nullptr));
       const int64_t nk = n * n_loc;
       HCUDA(cudaMalloc(&P->d_pos_map, sizeof(int32_t) * std::max<int64_t>(nk, 1)));
-      HCUDA(cudaMalloc(&P->d_seg_ptr, sizeof(int64_t) * (size_t(P->nnz) + 1)));
+      HCUDA(cudaMalloc(&P->d_seg_ptr, sizeof(uint32_t) * (size_t(P->nnz) + 1)));
       HCUDA(cudaMalloc(&P->d_perm, sizeof(uint32_t) * std::max<int64_t>(nk, 1)));
       HCALL(mpfem_b200_scatter_plan(cd, n_cells, n_loc, n_dofs, rp, static_cast<const int32_t*>(P->d_col_idx),
-                                    static_cast<int32_t*>(P->d_pos_map), static_cast<int64_t*>(P->d_seg_ptr),
+                                    static_cast<int32_t*>(P->d_pos_map), static_cast<uint32_t*>(P->d_seg_ptr),
                                     static_cast<uint32_t*>(P->d_perm), nullptr));
       HCUDA(cudaDeviceSynchronize());
     } catch (...) {
@@ -199,7 +199,7 @@ int mpfem_b200_asm_plan_assemble(mpfem_b200_asm_plan_t P, const double* locals, 
     const int64_t* rp = static_cast<const int64_t*>(P->d_row_ptr);
     if (fmt >= 2) {
       HCALL(mpfem_b200_assemble(dl.p, 3, 0, P->n_cells, P->n_loc, rp, P->n_dofs,
-                                static_cast<const int32_t*>(P->d_pos_map), static_cast<const int64_t*>(P->d_seg_ptr),
+                                static_cast<const int32_t*>(P->d_pos_map), static_cast<const uint32_t*>(P->d_seg_ptr),
                                 static_cast<const uint32_t*>(P->d_perm), dv.p, fmt, 1, 0, nullptr, 0, nullptr));
       if (fmt == 2) {  // fp32 values -> binary64 carriers (exact)
         DevMem dw(sizeof(double) * size_t(P->nnz));
@@ -211,7 +211,7 @@ int mpfem_b200_asm_plan_assemble(mpfem_b200_asm_plan_t P, const double* locals, 
       }
     } else {
       assemble_fmt_kernel<<<grid_of(P->nnz), 256>>>(static_cast<const double*>(dl.p),
-                                                    static_cast<const int64_t*>(P->d_seg_ptr),
+                                                    static_cast<const uint32_t*>(P->d_seg_ptr),
                                                     static_cast<const uint32_t*>(P->d_perm), P->nnz, fmt,
                                                     static_cast<double*>(dv.p), static_cast<uint32_t*>(df.p));
       HCUDA(cudaGetLastError());

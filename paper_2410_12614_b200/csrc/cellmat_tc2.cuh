@@ -12,6 +12,7 @@
 //     TMEM and arrive on the leader's tmem-empty barrier.
 #pragma once
 #include "cellmat_tc.cuh"
+#include "l2_hints.cuh"
 
 namespace mpfem_b200 {
 namespace tc2 {
@@ -50,6 +51,22 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       " [%0], [%1, {%2, %3}], [%4];" ::"r"(tc::smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
       : "memory");
+}
+// same, with an L2 eviction-priority hint (createpolicy): streamed operands marked evict-first
+// leave the L2 to the lines that are reused
+__device__ __forceinline__ void tma_load_2d_pair_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                      uint64_t* bar, uint64_t policy) {
+  const uint32_t leader_bar = tc::smem_u32(bar) & kPeerMask;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void mma_pair(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                          uint32_t accumulate) {
@@ -124,13 +141,19 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      [[maybe_unused]] const uint64_t w_policy = OUTK != 0 ? policy_evict_first() : 0;
       for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
         const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
         for (int kb = 0; kb < P.num_k_blocks; ++kb) {
           tc::mbar_wait_backoff(&empty[stage], phase ^ 1u);
           if (leader) tc::mbar_expect_tx(&full[stage], 2 * STAGE_BYTES);
           tma_load_2d_pair(sA + stage * A_BYTES, &tmA, kb * BK, ot * BM + int(rank) * BMC, &full[stage]);
-          tma_load_2d_pair(sB + stage * B_BYTES, &tmB, kb * BK, ct * BN + int(rank) * BNC, &full[stage]);
+          // fused scatter: W is read once per output tile and must not push the CSR value
+          // lines (the reductions' working set) out of the L2
+          if constexpr (OUTK != 0)
+            tma_load_2d_pair_hint(sB + stage * B_BYTES, &tmB, kb * BK, ct * BN + int(rank) * BNC, &full[stage], w_policy);
+          else
+            tma_load_2d_pair(sB + stage * B_BYTES, &tmB, kb * BK, ct * BN + int(rank) * BNC, &full[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
       }
@@ -164,6 +187,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t expo_or = 0;
+    [[maybe_unused]] const uint64_t keep = OUTK != 0 ? asmb::policy_evict_last() : 0;
     for (int tile = cluster; tile < total_tiles; tile += n_clusters) {
       const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
       tc::mbar_wait_backoff(&tfull[acc], acc_phase);
@@ -192,8 +216,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if constexpr (ACC_F16) v = __half2float(__ushort_as_half(static_cast<unsigned short>(r[j] & 0xffffu)));
                 else v = __uint_as_float(r[j]);
                 expo_or |= (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
-                if constexpr (OUTK == 1) atomicAdd(static_cast<float*>(P.values) + pos[j], v);
-                else atomicAdd(static_cast<double*>(P.values) + pos[j], double(v));
+                if constexpr (OUTK == 1) asmb::red_add_keep(static_cast<float*>(P.values) + pos[j], v, keep);
+                else asmb::red_add_keep(static_cast<double*>(P.values) + pos[j], double(v), keep);
               }
             }
           }
