@@ -480,8 +480,8 @@ def max_over_ranks(torch, value, dev):
 
 def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
     """BASELINE config 4: 96^3 hexes x 6 tets, Poisson with c(x), mixed (bf16 storage)
-    cell kernels, deterministic CSR assembly in fp32 and fp64. One GPU: the global pattern and
-    plan; N GPUs: the partitioned z-slab assembly (per-rank numbering, pattern and plan of the
+    cell kernels, deterministic CSR assembly (row pull) in fp32 and fp64. One GPU: the global pattern and
+    pos_map; N GPUs: the partitioned z-slab assembly (per-rank numbering, pattern and plan of the
     slab + one halo layer, interface partial sums sent up). CUDA-event times, max over ranks."""
     from paper_2410_12614_b200 import assembly as am
     from paper_2410_12614_b200 import distributed as D
@@ -536,12 +536,14 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
         t_pat, pat = timed(lambda: am.csr_pattern(dm), 1)
         res = {"p": p, "n_dofs": dm.n_dofs, "nnz": pat.nnz, "cells_per_rank": ce - cb,
                "dofmap_ms": t_dof, "csr_pattern_ms": t_pat, "cell_kernels_ms": t_cell}
+        # deterministic (default): row pull over the incidence lists + pos_map. Algorithmic bytes:
+        # local matrices + pos_map once, the incidence list, CSR values written once, row/inc pointers
         for fmt in (2, 3):
             sv = 4 if fmt == 2 else 8
             vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
             t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
             del vals
-            nb = (ce - cb) * (nphi(p) ** 2 * 4 + 4 * nphi(p)) + pat.nnz * (sv + 4) + 8 * (dm.n_dofs + 1)
+            nb = (ce - cb) * (nphi(p) ** 2 * 8 + 8 * nphi(p)) + pat.nnz * sv + 16 * (dm.n_dofs + 1)
             key = "fp32" if fmt == 2 else "fp64"
             res[f"assemble_{key}_ms"] = t_asm
             res[f"assemble_{key}_hbm_frac"] = nb / (t_asm * 1e-3) / 1e9 / hbm
@@ -554,6 +556,14 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
         t_fused, _ = timed(lambda: am.assemble_cells(s, vd, cdev, dm, pat, 2, mp.CoefKind.sincosexp,
                                                      accumulate=True, values=vals))
         res["fused_kernels_atomic_scatter_fp32_ms"] = t_fused
+        del vals, pat
+        torch.cuda.empty_cache()
+        # the seg_ptr/perm segment-gather kernel (patterns built with deterministic_plan=True)
+        t_pat2, pat = timed(lambda: am.csr_pattern(dm, deterministic_plan=True), 1)
+        vals = torch.empty(pat.nnz, dtype=torch.float32, device=dev)
+        t_plan, _ = timed(lambda: am.assemble_matrix(local, dm, pat, 2, am.DETERMINISTIC, values=vals))
+        res["csr_pattern_with_segment_plan_ms"] = t_pat2
+        res["assemble_segment_gather_fp32_ms"] = t_plan
         del vals
         out.append(res)
         del local, pat, dm, s

@@ -315,15 +315,18 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
                         void* values, int fmt, int mode, int accumulate, const int32_t* rows,
                         int64_t n_rows, void* stream);
 
-/* Deterministic assemble_matrix without the seg_ptr/perm plan (for patterns built without
- * it: 18 GB less at config-4 P3; about 2x slower than mode 1 with the plan): rows pull their incident (cell, local row) pairs from the
- * incidence lists (mpfem_b200_incidence, ascending cell order) and the CSR positions from
- * pos_map; values are bitwise those of mode 1 of mpfem_b200_assemble (the reference's
- * ascending-cell sequential sum, assembly.cpp:50-67). Arguments as mpfem_b200_assemble. */
+/* Deterministic assemble_matrix by row pull (no seg_ptr/perm plan needed): one warp per CSR row
+ * replays the row's incident (cell, local row) pairs -- from the incidence lists
+ * (mpfem_b200_incidence, ascending cell order) -- adding each pair's contiguous n_loc local
+ * entries at their CSR positions (pos_map); values are bitwise those of mode 1 of
+ * mpfem_b200_assemble (the reference's ascending-cell sequential sum, assembly.cpp:50-67).
+ * rows/n_rows restrict the pass to those rows (NULL: every row); other arguments as
+ * mpfem_b200_assemble. */
 int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
                              int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
                              const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
-                             void* values, int fmt, int accumulate, void* stream);
+                             void* values, int fmt, int accumulate, const int32_t* rows,
+                             int64_t n_rows, void* stream);
 
 /* ---------------------------------------------------------------- host-buffer assembly
  * The calls behind the C++ drop-in build_dofmap / assemble_matrix (include/mpfem/batched.hpp):

@@ -69,9 +69,11 @@ def incidence(dm: DofMap, stream=None):
     return inc_ptr, inc
 
 
-def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: bool = True) -> CsrPattern:
+def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: bool = False) -> CsrPattern:
     """The reference COO key set (assembly.cpp:67-86) as CSR, plus the incidence lists and
-    (plan=True) the scatter plan used by assemble_matrix."""
+    (plan=True) the scatter plan used by assemble_matrix: pos_map, and with
+    deterministic_plan=True also seg_ptr/perm for the segment-gather kernel (the default
+    deterministic path, row pull, does not need them)."""
     import torch
     dev = dm.cell_dofs.device
     row_ptr = torch.empty(dm.n_dofs + 1, dtype=torch.int64, device=dev)
@@ -105,10 +107,10 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
     `local` holds the local matrices of cells [cell_begin, cell_end), (n, n_loc, n_loc)
     fp32 or fp64. Deterministic mode reproduces the reference's ascending-cell sequential
     sum bitwise; atomic mode is order-free (within gamma_{m+1} of the exact sum).
-    Deterministic mode gathers each entry's segment through the seg_ptr/perm plan (block-
-    staged in shared memory). Patterns built with deterministic_plan=False (no seg_ptr/perm:
-    18 GB less at config-4 P3) use the row-pull kernel instead (pull=True forces it), which
-    replays the incidence lists in ascending cell order -- the same bits, about 2x slower."""
+    Deterministic mode runs the row-pull kernel (incidence lists + pos_map: rows replay their
+    incident local rows in ascending cell order from shared memory). Patterns built with
+    deterministic_plan=True carry seg_ptr/perm (13 GB at config-4 P3) and use the block-staged
+    segment gather instead unless pull=True -- the same bits, about 1.5x slower at config 4."""
     import torch
     if cell_end is None:
         cell_end = cell_begin + int(local.shape[0])
@@ -126,13 +128,13 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
         raise ConfigError("assemble_matrix needs a pattern built with plan=True")
     if pull is None:
         pull = pat.seg_ptr is None
-    if mode == DETERMINISTIC and rows is None and pull:
+    if mode == DETERMINISTIC and pull:
         # row-pull: incidence lists + pos_map, no seg_ptr/perm plan needed
         check(lib().mpfem_b200_assemble_pull(_ptr(local), lf, int(cell_begin), int(cell_end),
                                              dm.n_local, _ptr(pat.row_ptr), dm.n_dofs,
                                              _ptr(pat.inc_ptr), _ptr(pat.inc), _ptr(pat.pos_map),
-                                             _ptr(values), int(fmt), int(accumulate),
-                                             _stream_handle(stream)))
+                                             _ptr(values), int(fmt), int(accumulate), _ptr(rows),
+                                             n_rows, _stream_handle(stream)))
         return values
     check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), dm.n_local,
                                     _ptr(pat.row_ptr), dm.n_dofs, _ptr(pat.pos_map),
@@ -212,11 +214,9 @@ class CudaPartitionBackend:
         pat = CsrPattern(n_rows, row_ptr, col_idx, inc_ptr, inc)
         nk = n * n_loc * n_loc
         pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
-        pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int32, device=dev)
-        pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
         check(lib().mpfem_b200_scatter_plan_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
                                                  _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
-                                                 _ptr(pat.seg_ptr), _ptr(pat.perm), sh))
+                                                 None, None, sh))
         pat.n_local = n_loc
         return pat
 
@@ -231,9 +231,9 @@ class CudaPartitionBackend:
         if rows is None or rows.numel() == 0:
             return values
         lf = FP32 if local.dtype.itemsize == 4 else FP64
-        check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), pat.n_local,
-                                        _ptr(pat.row_ptr), pat.n_rows, _ptr(pat.pos_map),
-                                        _ptr(pat.seg_ptr), _ptr(pat.perm), _ptr(values), int(fmt),
-                                        DETERMINISTIC, int(accumulate), _ptr(rows), int(rows.numel()),
-                                        _stream_handle(None)))
+        check(lib().mpfem_b200_assemble_pull(_ptr(local), lf, int(cell_begin), int(cell_end), pat.n_local,
+                                             _ptr(pat.row_ptr), pat.n_rows, _ptr(pat.inc_ptr),
+                                             _ptr(pat.inc), _ptr(pat.pos_map), _ptr(values), int(fmt),
+                                             int(accumulate), _ptr(rows), int(rows.numel()),
+                                             _stream_handle(None)))
         return values

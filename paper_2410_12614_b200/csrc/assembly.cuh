@@ -531,127 +531,202 @@ __global__ void __launch_bounds__(256) assemble_seg_block_kernel(
   }
 }
 
-// Row-pull deterministic scatter (no seg_ptr/perm plan): a CTA takes kPullRows rows; for
-// each row its incident (cell, local row i) pairs come from the incidence list in ascending
-// cell order (inc is sorted by (dof, position)). All local entries of those pairs -- the
-// contiguous n_loc-wide rows of the local matrices -- and their CSR positions (pos_map) are
-// gathered into shared memory with independent coalesced loads; then one warp per row
-// replays the pairs in ascending cell order, lanes adding the pair's n_loc entries into
-// distinct accumulators. Each CSR entry therefore receives its contributions in ascending
-// cell order starting from -0.0: bitwise the reference's sequential sum (assembly.cpp:50-67)
-// and entry_sum. Batches beyond the shared-memory caps run the same replay on global memory.
-constexpr int kPullRows = 16;
-struct PullCaps {
-  int entries, pairs, inc;
-};
-template <typename TV>
-__host__ __device__ constexpr PullCaps pull_caps() {
-  return PullCaps{2048, 4096, 256};
+// Row-pull deterministic scatter (no seg_ptr/perm plan). A warp owns a batch of consecutive CSR
+// rows whose entries fit its shared-memory accumulators. The batch's incident (cell, local row i)
+// pairs are the contiguous run inc[inc_ptr[r0] .. inc_ptr[r1]) -- sorted by (dof, cell * n_loc + i),
+// i.e. ascending cell order within every row. A pair's n_loc local entries are the contiguous row i
+// of the cell's matrix and their CSR positions the matching n_loc words of pos_map, so both streams
+// are read in contiguous runs (the seg_ptr/perm gather and the atomic scatter touch every
+// contribution as a separate 4-byte sector access). Chunks of whole pairs are copied to a
+// shared-memory ring with cp.async (kPullStages chunks in flight per warp, no registers held) and
+// replayed pair by pair into the accumulators: every CSR entry receives its contributions in
+// ascending cell order starting from -0.0 -- bitwise the reference's sequential sum
+// (assembly.cpp:50-67) and entry_sum. A single row beyond the caps runs the same ordered replay on
+// global memory. rows != NULL restricts the pass to those rows (runs of consecutive rows in the
+// list form batches; multi-GPU slabs); pairs of cells outside [cell_begin, cell_end) are skipped.
+constexpr int kPullWarps = 4;     // warps per CTA, each autonomous
+#ifndef MPFEM_PULL_STAGES
+#define MPFEM_PULL_STAGES 3
+#define MPFEM_PULL_ACC 512
+#define MPFEM_PULL_INC 128
+#endif
+#ifndef MPFEM_PULL_MINB
+#define MPFEM_PULL_MINB 1
+#endif
+constexpr int kPullStages = MPFEM_PULL_STAGES;  // cp.async ring depth per warp
+constexpr int kPullAccCap = MPFEM_PULL_ACC;     // accumulators (CSR entries) per batch
+constexpr int kPullIncCap = MPFEM_PULL_INC;     // pairs per batch
+template <typename TL, typename TV, int CH>
+__host__ __device__ constexpr size_t pull_warp_bytes() {
+  return sizeof(TV) * kPullAccCap + sizeof(int64_t) * kPullIncCap +
+         size_t(kPullStages) * CH * (sizeof(TL) + sizeof(int32_t));
 }
-template <typename TV>
-__host__ __device__ constexpr size_t pull_smem_bytes() {
-  constexpr PullCaps c = pull_caps<TV>();
-  return sizeof(TV) * (c.entries + c.pairs) + sizeof(int32_t) * c.pairs + sizeof(int64_t) * c.inc +
-         2 * sizeof(int64_t) * (kPullRows + 1);
+template <int BYTES>
+__device__ __forceinline__ void cp_async_bytes(void* smem_dst, const void* gsrc) {
+  const uint32_t d = uint32_t(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(BYTES) : "memory");
 }
-template <typename TL, typename TV>
-__global__ void __launch_bounds__(256) assemble_pull_kernel(
-    const TL* __restrict__ locals, int64_t per_cell, int n_loc, const int64_t* __restrict__ row_ptr,
+// VEC consecutive elements of T (VEC * sizeof(T) in {4, 8, 16, 32} bytes, both sides aligned to
+// min(16, that))
+template <typename T, int VEC>
+__device__ __forceinline__ void cp_async_vec(T* smem_dst, const T* gsrc) {
+  constexpr int bytes = int(sizeof(T)) * VEC;
+  if constexpr (bytes <= 16) {
+    cp_async_bytes<bytes>(smem_dst, gsrc);
+  } else {
+    #pragma unroll
+    for (int h = 0; h < bytes / 16; ++h)
+      cp_async_bytes<16>(reinterpret_cast<char*>(smem_dst) + 16 * h,
+                         reinterpret_cast<const char*>(gsrc) + 16 * h);
+  }
+}
+// VEC: elements per copy (n_loc % VEC == 0 and the arrays aligned accordingly; chosen by the host)
+template <typename TL, typename TV, int CH, int VEC>
+__global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pull_kernel(
+    const TL* __restrict__ locals, int n_loc, const int64_t* __restrict__ row_ptr,
     const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
-    const int32_t* __restrict__ pos_map, int32_t n_rows, int64_t cell_begin, int64_t cell_end,
-    int init, TV* __restrict__ values) {
-  constexpr PullCaps cap = pull_caps<TV>();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TV* s_acc = reinterpret_cast<TV*>(smem_raw);
-  TV* s_x = s_acc + cap.entries;
-  int64_t* s_inc = reinterpret_cast<int64_t*>(s_x + cap.pairs);
-  int64_t* s_rp = s_inc + cap.inc;
-  int64_t* s_ip = s_rp + (kPullRows + 1);
-  int32_t* s_p = reinterpret_cast<int32_t*>(s_ip + (kPullRows + 1));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  const int64_t n_batches = (int64_t(n_rows) + kPullRows - 1) / kPullRows;
-  const uint32_t nl = uint32_t(n_loc);
-  for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
-    const int64_t r0 = b * kPullRows;
-    const int nr = int(int64_t(n_rows) - r0 < kPullRows ? int64_t(n_rows) - r0 : int64_t(kPullRows));
-    if (threadIdx.x <= nr) {
-      s_rp[threadIdx.x] = row_ptr[r0 + threadIdx.x];
-      s_ip[threadIdx.x] = inc_ptr[r0 + threadIdx.x];
-    }
-    __syncthreads();
-    const int64_t e0 = s_rp[0], i0 = s_ip[0];
-    const int64_t ne = s_rp[nr] - e0, ni = s_ip[nr] - i0, np = ni * n_loc;
-    if (ne <= cap.entries && ni <= cap.inc && np <= cap.pairs) {
-      for (int e = threadIdx.x; e < int(ne); e += blockDim.x) s_acc[e] = init ? TV(-0.0) : values[e0 + e];
-      for (int t = threadIdx.x; t < int(ni); t += blockDim.x) s_inc[t] = inc[i0 + t];
-      __syncthreads();
-      for (int q = threadIdx.x; q < int(np); q += 4 * blockDim.x) {
-        int64_t k[4];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = q + u * int(blockDim.x);
-          k[u] = -1;
-          if (qq < int(np)) {
-            const uint32_t t = uint32_t(qq) / nl, j = uint32_t(qq) - t * nl;
-            const int64_t ki = s_inc[t];
-            const int64_t cell = ki / n_loc;
-            if (cell >= cell_begin && cell < cell_end) k[u] = cell * per_cell + (ki - cell * n_loc) * n_loc + j;
-          }
-        }
-        TV x[4];
-        int32_t pp[4];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          x[u] = k[u] >= 0 ? cast_value<TL, TV>(locals[k[u]]) : TV(-0.0);
-          pp[u] = k[u] >= 0 ? int32_t(int64_t(pos_map[k[u]]) - e0) : -1;
-        }
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = q + u * int(blockDim.x);
-          if (qq < int(np)) {
-            s_x[qq] = x[u];
-            s_p[qq] = pp[u];
-          }
-        }
-      }
-      __syncthreads();
-      for (int rr = warp; rr < nr; rr += nwarps) {
-        const int t1 = int(s_ip[rr + 1] - i0);
-        for (int t = int(s_ip[rr] - i0); t < t1; ++t) {
-          for (int j = lane; j < n_loc; j += 32) {
-            const int q = t * n_loc + j, pq = s_p[q];
-            if (pq >= 0) s_acc[pq] = s_acc[pq] + s_x[q];
-          }
-          __syncwarp();
-        }
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < int(ne); e += blockDim.x) values[e0 + e] = s_acc[e];
-    } else {
-      // oversized batch: the same ordered replay, one warp per row, on global memory
-      for (int rr = warp; rr < nr; rr += nwarps) {
-        const int64_t ra = s_rp[rr], rb = s_rp[rr + 1];
+    const int32_t* __restrict__ pos_map, const int32_t* __restrict__ rows, int64_t n_rows,
+    int64_t cell_begin, int64_t cell_end, int init, TV* __restrict__ values) {
+  extern __shared__ __align__(16) unsigned char pull_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* base = pull_smem + size_t(warp) * pull_warp_bytes<TL, TV, CH>();
+  int64_t* s_inc = reinterpret_cast<int64_t*>(base);  // first entry id of the pair, -1: skipped
+  TV* s_acc = reinterpret_cast<TV*>(s_inc + kPullIncCap);
+  TL* s_x = reinterpret_cast<TL*>(s_acc + kPullAccCap);
+  int32_t* s_p = reinterpret_cast<int32_t*>(s_x + kPullStages * CH);
+  const int64_t kb = cell_begin * n_loc, ke = cell_end * n_loc;  // pair ids of the cell range
+  const int pairs_per_chunk = CH / n_loc;                          // >= 1 (host checks n_loc <= CH)
+  const int upp = n_loc / VEC;                                     // copy units per pair
+  const int dq = 32 / upp, dr = 32 - dq * upp;
+  const int lane_t = lane / upp, lane_j = lane - lane_t * upp;
+  const int64_t n_blocks = (n_rows + 31) >> 5;
+  const int64_t wstride = int64_t(gridDim.x) * kPullWarps;
+  for (int64_t blk = int64_t(blockIdx.x) * kPullWarps + warp; blk < n_blocks; blk += wstride) {
+    // lane l holds row l of the 32-row block
+    const int64_t ri = (blk << 5) + lane;
+    const bool have = ri < n_rows;
+    const int64_t r = have ? (rows ? int64_t(rows[ri]) : ri) : 0;
+    const int64_t my_e0 = have ? row_ptr[r] : 0, my_e1 = have ? row_ptr[r + 1] : 0;
+    const int64_t my_b0 = have ? inc_ptr[r] : 0, my_b1 = have ? inc_ptr[r + 1] : 0;
+    const int n_have = __popc(__ballot_sync(0xffffffffu, have));
+    int start = 0;
+    while (start < n_have) {
+      const int64_t e0 = __shfl_sync(0xffffffffu, my_e0, start);
+      const int64_t b0 = __shfl_sync(0xffffffffu, my_b0, start);
+      // rows start .. start + nr - 1: a run of consecutive rows (always, without a row list)
+      // that fits the caps
+      const int64_t r_start = __shfl_sync(0xffffffffu, r, start);
+      const bool fits = lane >= start && lane < n_have && r == r_start + (lane - start) &&
+                        my_e1 - e0 <= kPullAccCap && my_b1 - b0 <= kPullIncCap;
+      const unsigned run = ~(__ballot_sync(0xffffffffu, fits) >> start);
+      const int nr = run ? __ffs(run) - 1 : 32 - start;
+      if (nr == 0) {
+        // one long row: the same ordered replay on global memory
+        const int64_t e1 = __shfl_sync(0xffffffffu, my_e1, start);
+        const int64_t b1 = __shfl_sync(0xffffffffu, my_b1, start);
         if (init)
-          for (int64_t e = ra + lane; e < rb; e += 32) values[e] = TV(-0.0);
+          for (int64_t e = e0 + lane; e < e1; e += 32) values[e] = TV(-0.0);
         __syncwarp();
-        for (int64_t t = s_ip[rr]; t < s_ip[rr + 1]; ++t) {
-          const int64_t ki = inc[t], cell = ki / n_loc;
-          if (cell >= cell_begin && cell < cell_end) {
-            const int64_t kbase = cell * per_cell + (ki - cell * n_loc) * n_loc;
+        for (int64_t t = b0; t < b1; ++t) {
+          const int64_t ki = inc[t];
+          if (ki >= kb && ki < ke) {
             for (int j = lane; j < n_loc; j += 32) {
-              const int64_t pos = pos_map[kbase + j];
-              values[pos] = values[pos] + cast_value<TL, TV>(locals[kbase + j]);
+              const int64_t k = ki * n_loc + j;
+              const int64_t pos = pos_map[k];
+              values[pos] = values[pos] + cast_value<TL, TV>(locals[k]);
             }
           }
           __syncwarp();
         }
+        start += 1;
+        continue;
       }
+      const int last = start + nr - 1;
+      const int ne = int(__shfl_sync(0xffffffffu, my_e1, last) - e0);
+      const int ni = int(__shfl_sync(0xffffffffu, my_b1, last) - b0);
+      const int e0i = int(e0);  // pos_map is int32, so every position fits
+      for (int t = lane; t < ni; t += 32) {
+        const int64_t ki = __ldcs(inc + b0 + t);
+        s_inc[t] = (ki >= kb && ki < ke) ? ki * n_loc : int64_t(-1);
+      }
+      for (int i = lane; i < ne; i += 32) s_acc[i] = init ? TV(-0.0) : values[e0 + i];
+      __syncwarp();
+      const int n_chunks = (ni + pairs_per_chunk - 1) / pairs_per_chunk;
+      auto issue = [&](int c) {
+        if (c < n_chunks) {
+          const int t0 = c * pairs_per_chunk;
+          const int nu = min(ni - t0, pairs_per_chunk) * upp;
+          TL* sx = s_x + (c % kPullStages) * CH;
+          int32_t* sp = s_p + (c % kPullStages) * CH;
+          int t = lane_t, j = lane_j;
+          for (int u = lane; u < nu; u += 32) {
+            const int64_t k0 = s_inc[t0 + t];
+            if (k0 >= 0) {
+              cp_async_vec<TL, VEC>(sx + u * VEC, locals + k0 + j * VEC);
+              cp_async_vec<int32_t, VEC>(sp + u * VEC, pos_map + k0 + j * VEC);
+            } else {
+              // a skipped pair adds -0.0 to the batch's first entry: no change in any bit
+              #pragma unroll
+              for (int v = 0; v < VEC; ++v) {
+                sx[u * VEC + v] = TL(-0.0);
+                sp[u * VEC + v] = e0i;
+              }
+            }
+            t += dq;
+            j += dr;
+            if (j >= upp) {
+              j -= upp;
+              ++t;
+            }
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      #pragma unroll
+      for (int c = 0; c < kPullStages - 1; ++c) issue(c);
+      for (int c = 0; c < n_chunks; ++c) {
+        issue(c + kPullStages - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kPullStages - 1) : "memory");
+        __syncwarp();
+        const int npairs = min(ni - c * pairs_per_chunk, pairs_per_chunk);
+        const TL* sx = s_x + (c % kPullStages) * CH;
+        const int32_t* sp = s_p + (c % kPullStages) * CH;
+        if (n_loc <= 32) {
+          // one lane per local column; the next pair's operands are fetched ahead of the
+          // dependent accumulator update
+          const bool on = lane < n_loc;
+          int a = on ? sp[lane] - e0i : 0;
+          TV x = on ? cast_value<TL, TV>(sx[lane]) : TV(0);
+          for (int t = 0; t < npairs; ++t) {
+            sx += n_loc;
+            sp += n_loc;
+            const bool more = on && t + 1 < npairs;
+            const int a_next = more ? sp[lane] - e0i : 0;
+            const TV x_next = more ? cast_value<TL, TV>(sx[lane]) : TV(0);
+            if (on) s_acc[a] = s_acc[a] + x;
+            __syncwarp();  // pairs are applied one after the other (ascending cell order per row)
+            a = a_next;
+            x = x_next;
+          }
+        } else {
+          for (int t = 0; t < npairs; ++t) {
+            for (int j = lane; j < n_loc; j += 32) {
+              const int a = sp[j] - e0i;
+              s_acc[a] = s_acc[a] + cast_value<TL, TV>(sx[j]);
+            }
+            sx += n_loc;
+            sp += n_loc;
+            __syncwarp();
+          }
+        }
+      }
+      for (int i = lane; i < ne; i += 32) values[e0 + i] = s_acc[i];
+      __syncwarp();
+      start += nr;
     }
-    __syncthreads();
   }
 }
 
-// Same for a list of rows: one warp per row, lanes over the row's entries.
 template <typename TL, typename TV>
 __global__ void assemble_seg_rows_kernel(const TL* __restrict__ locals, int64_t per_cell,
                                          const int64_t* __restrict__ row_ptr,

@@ -383,7 +383,8 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
 int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
                              int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
                              const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
-                             void* values, int fmt, int accumulate, void* stream) {
+                             void* values, int fmt, int accumulate, const int32_t* rows,
+                             int64_t n_rows, void* stream) {
   return aguard([&] {
     if (locals_fmt != 2 && locals_fmt != 3) throw AsmError{2, "local matrices must be fp32 or fp64"};
     if (fmt != 2 && fmt != 3) throw AsmError{2, "CSR values must be fp32 or fp64"};
@@ -396,25 +397,59 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
     const size_t esz = locals_fmt == 2 ? 4 : 8;
     const char* base = static_cast<const char*>(locals) - size_t(cell_begin) * size_t(per_cell) * esz;
     const int init = accumulate ? 0 : 1;
-    const int64_t batches = (int64_t(n_dofs) + asmb::kPullRows - 1) / asmb::kPullRows;
-#define MPFEM_PULL(TL, TV)                                                                         \
+    const int64_t nr = rows ? n_rows : int64_t(n_dofs);
+    if (nr == 0) return;
+    if (n_loc > 256) throw AsmError{2, "row-pull assembly supports n_loc <= 256"};
+    const int64_t blocks32 = (nr + 31) / 32;  // a warp takes 32-row blocks
+    // elements per cp.async: 4 / 2 / 1 by n_loc and the arrays' alignment
+    auto aligned = [](const void* q, size_t a) { return reinterpret_cast<uintptr_t>(q) % a == 0; };
+    int vec = 1;
+    if (n_loc % 4 == 0 && aligned(base, 16) && aligned(pos_map, 16)) vec = 4;
+    else if (n_loc % 2 == 0 && aligned(base, std::min<size_t>(16, 2 * esz)) && aligned(pos_map, 8)) vec = 2;
+// Shared-memory carveout of the pull kernel: 75 % leaves the L1 large enough to keep the partly
+// used sectors of neighbouring local rows until the next CSR row asks for them (measured at config 4,
+// P3 fp32: carveout 100 % 9.3 ms, 75 % 6.0 ms, 50 % 6.5 ms, 25 % 12.1 ms).
+#ifndef MPFEM_PULL_CARVEOUT
+#define MPFEM_PULL_CARVEOUT 75
+#endif
+#define MPFEM_PULL_CARVE(...) ACUDA(cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributePreferredSharedMemoryCarveout, MPFEM_PULL_CARVEOUT));
+#define MPFEM_PULL_V(TL, TV, CH, VEC)                                                              \
   {                                                                                                \
-    constexpr size_t smem = asmb::pull_smem_bytes<TV>();                                           \
+    constexpr size_t smem = asmb::kPullWarps * asmb::pull_warp_bytes<TL, TV, CH>();                \
     static bool attr = false;                                                                      \
+    static int per_sm = 1;                                                                         \
     if (!attr) {                                                                                   \
-      ACUDA(cudaFuncSetAttribute(asmb::assemble_pull_kernel<TL, TV>,                               \
+      ACUDA(cudaFuncSetAttribute(asmb::assemble_pull_kernel<TL, TV, CH, VEC>,                      \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));         \
+      MPFEM_PULL_CARVE(asmb::assemble_pull_kernel<TL, TV, CH, VEC>)                                \
+      ACUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                         \
+          &per_sm, asmb::assemble_pull_kernel<TL, TV, CH, VEC>, asmb::kPullWarps * 32, smem));     \
       attr = true;                                                                                 \
     }                                                                                              \
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(batches, 148 * 8)));    \
-    asmb::assemble_pull_kernel<TL, TV><<<grid, 256, smem, st>>>(                                   \
-        reinterpret_cast<const TL*>(base), per_cell, n_loc, row_ptr, inc_ptr, inc, pos_map,        \
-        n_dofs, cell_begin, cell_end, init, static_cast<TV*>(values));                             \
+    const unsigned grid = unsigned(std::max<int64_t>(                                              \
+        1, std::min<int64_t>((blocks32 + asmb::kPullWarps - 1) / asmb::kPullWarps,                 \
+                             int64_t(148) * std::max(per_sm, 1))));                                \
+    asmb::assemble_pull_kernel<TL, TV, CH, VEC><<<grid, asmb::kPullWarps * 32, smem, st>>>(        \
+        reinterpret_cast<const TL*>(base), n_loc, row_ptr, inc_ptr, inc, pos_map, rows, nr,        \
+        cell_begin, cell_end, init, static_cast<TV*>(values));                                     \
+  }
+#define MPFEM_PULL_J(TL, TV, CH)                                                                   \
+  {                                                                                                \
+    if (vec == 4) MPFEM_PULL_V(TL, TV, CH, 4)                                                      \
+    else if (vec == 2) MPFEM_PULL_V(TL, TV, CH, 2)                                                 \
+    else MPFEM_PULL_V(TL, TV, CH, 1)                                                               \
+  }
+#define MPFEM_PULL(TL, TV)                                                                         \
+  {                                                                                                \
+    if (n_loc <= 64) MPFEM_PULL_J(TL, TV, 128)                                                     \
+    else MPFEM_PULL_J(TL, TV, 256)                                                                 \
   }
     if (locals_fmt == 2 && fmt == 2) MPFEM_PULL(float, float)
     else if (locals_fmt == 2) MPFEM_PULL(float, double)
     else if (fmt == 2) MPFEM_PULL(double, float)
     else MPFEM_PULL(double, double)
+#undef MPFEM_PULL_V
+#undef MPFEM_PULL_J
 #undef MPFEM_PULL
     ACUDA(cudaGetLastError());
   });

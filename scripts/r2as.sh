@@ -1,0 +1,12 @@
+#!/bin/bash
+set -u
+OUT=gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_assembly.py tests/test_gpu_distributed.py tests/test_gpu_reference_suite.py -m gpu -x -q > $OUT/pytest_asm.log 2>&1; echo "pytest rc=$?"; tail -4 $OUT/pytest_asm.log
+timeout 1200 python bench.py --steps 20 --no-cpu-baseline --no-modes --no-action --no-hex > $OUT/bench_asm.json 2> $OUT/bench_asm.err; echo "bench rc=$?"; tail -2 $OUT/bench_asm.err
+python - <<'PY'
+import json
+d = json.loads(open('gpurun_out/bench_asm.json').read().strip().splitlines()[-1])
+for r in d['assembly']['results']:
+    print({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()})
+PY
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:assemble_pull -c 1 -s 1 -o $OUT/pull_p3 -f python scripts/pull_prof.py 3 > $OUT/pull_ncu.log 2>&1; echo "ncu rc=$?"; tail -1 $OUT/pull_ncu.log

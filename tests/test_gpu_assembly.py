@@ -38,14 +38,17 @@ def test_dofmap_known_answers(oracle):
         assert gpu_dofmap(p, verts, cells).n_dofs == (p * n + 1) ** 3
 
 
-@pytest.mark.parametrize("p,dims", [(1, (4, 3, 3)), (2, (4, 3, 3)), (3, (4, 3, 3)), (6, (2, 2, 1))])
+@pytest.mark.parametrize("p,dims", [(1, (4, 3, 3)), (2, (4, 3, 3)), (3, (4, 3, 3)), (4, (2, 2, 2)),
+                                    (6, (2, 2, 1)), (8, (1, 1, 1))])
 def test_csr_pattern_and_values_bitwise(oracle, p, dims):
-    # p = 6 (n_loc = 84): row batches exceed the row-pull kernel's shared-memory caps, so its
-    # global-memory replay is exercised too
+    # the row-pull kernel's variants: 16 / 8 / 4-byte copies (n_loc = 4, 20, 84 / 10 / 35, 165), 128- and
+    # 256-entry chunks (n_loc <= 64 / above); p >= 6 rows exceed the shared-memory caps, so the
+    # global-memory replay is exercised too. The pattern carries seg_ptr/perm so that the default
+    # call takes the segment-gather kernel and pull=True the row-pull kernel.
     verts, cells = oracle.structured_tet_mesh(*dims, 1.0, 0.15, 11)
     cd, nd, _ = oracle.build_dofmap(p, verts, cells)
     dm = gpu_dofmap(p, verts, cells)
-    pat = am.csr_pattern(dm)
+    pat = am.csr_pattern(dm, deterministic_plan=True)
     rng = np.random.default_rng(p)
     loc32 = rng.uniform(-1, 1, size=(cells.shape[0], nphi(p), nphi(p))).astype(np.float32)
     for fmt in (2, 3):
@@ -72,8 +75,39 @@ def test_csr_pattern_and_values_bitwise(oracle, p, dims):
     # fp64 locals into fp32 values (cast at fmt, assembly.cpp:57)
     loc64 = rng.uniform(-1, 1, size=(cells.shape[0], nphi(p), nphi(p)))
     rows, cols, vals, _ = oracle.assemble_matrix(cd, nd, loc64, 2)
-    v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat, 2, am.DETERMINISTIC)
+    for pull in (False, True):
+        v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat, 2, am.DETERMINISTIC, pull=pull)
+        assert np.array_equal(v.double().cpu().numpy().view(np.uint64), vals.view(np.uint64)), pull
+    # a pattern without seg_ptr/perm (the default) takes the row-pull kernel
+    pat0 = am.csr_pattern(dm)
+    assert pat0.seg_ptr is None
+    v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat0, 2)
     assert np.array_equal(v.double().cpu().numpy().view(np.uint64), vals.view(np.uint64))
+
+
+def test_row_pull_row_lists_bitwise(oracle):
+    """Rows-restricted row pull (the multi-GPU slab pass): a list with runs of consecutive rows,
+    isolated rows and a reversed tail writes exactly those rows, bitwise the full assembly."""
+    p = 3
+    verts, cells = oracle.structured_tet_mesh(4, 3, 3, 1.0, 0.15, 7)
+    dm = gpu_dofmap(p, verts, cells)
+    pat = am.csr_pattern(dm)
+    rng = np.random.default_rng(3)
+    loc = torch.from_numpy(rng.uniform(-1, 1, size=(cells.shape[0], 20, 20)).astype(np.float32)).cuda()
+    full = am.assemble_matrix(loc, dm, pat, 2)
+    nd = dm.n_dofs
+    pick = np.concatenate([np.arange(5, 75), np.arange(100, 400, 7), np.arange(nd - 40, nd)[::-1]]).astype(np.int32)
+    rows = torch.from_numpy(pick).cuda()
+    vals = torch.full((pat.nnz,), 123.0, dtype=torch.float32, device="cuda")
+    am.assemble_matrix(loc, dm, pat, 2, rows=rows, values=vals)
+    torch.cuda.synchronize()
+    rp = pat.row_ptr.cpu().numpy()
+    mask = np.zeros(pat.nnz, dtype=bool)
+    for r in pick:
+        mask[rp[r]:rp[r + 1]] = True
+    got, ref = vals.cpu().numpy(), full.cpu().numpy()
+    assert np.array_equal(got[mask].view(np.uint32), ref[mask].view(np.uint32))
+    assert np.all(got[~mask] == 123.0)
 
 
 def test_partial_cell_ranges_compose_bitwise(oracle):
@@ -82,7 +116,7 @@ def test_partial_cell_ranges_compose_bitwise(oracle):
     p = 2
     verts, cells = oracle.structured_tet_mesh(3, 3, 4, 1.0, 0.15, 5)
     dm = gpu_dofmap(p, verts, cells)
-    pat = am.csr_pattern(dm)
+    pat = am.csr_pattern(dm, deterministic_plan=True)
     rng = np.random.default_rng(9)
     loc = torch.from_numpy(rng.uniform(-1, 1, size=(cells.shape[0], 10, 10)).astype(np.float32)).cuda()
     full = am.assemble_matrix(loc, dm, pat, 2)
