@@ -536,14 +536,16 @@ def run_assembly(mp, torch, dev, rank, world, degrees=(2, 3), n=96):
         t_pat, pat = timed(lambda: am.csr_pattern(dm), 1)
         res = {"p": p, "n_dofs": dm.n_dofs, "nnz": pat.nnz, "cells_per_rank": ce - cb,
                "dofmap_ms": t_dof, "csr_pattern_ms": t_pat, "cell_kernels_ms": t_cell}
-        # deterministic (default): row pull over the incidence lists + pos_map. Algorithmic bytes:
-        # local matrices + pos_map once, the incidence list, CSR values written once, row/inc pointers
+        # deterministic (default): row pull over the incidence lists + pull_pos. Algorithmic bytes:
+        # local matrices (4 B) + positions (2 B pull_pos, 4 B pos_map) once per local entry, the
+        # incidence list (8 B per pair), CSR values written once, row/inc pointers
         for fmt in (2, 3):
             sv = 4 if fmt == 2 else 8
             vals = torch.empty(pat.nnz, dtype=torch.float32 if fmt == 2 else torch.float64, device=dev)
             t_asm, _ = timed(lambda: am.assemble_matrix(local, dm, pat, fmt, am.DETERMINISTIC, values=vals))
             del vals
-            nb = (ce - cb) * (nphi(p) ** 2 * 8 + 8 * nphi(p)) + pat.nnz * sv + 16 * (dm.n_dofs + 1)
+            nb = (ce - cb) * (nphi(p) ** 2 * (4 + (2 if pat.pull_pos is not None else 4)) + 8 * nphi(p)) \
+                + pat.nnz * sv + 16 * (dm.n_dofs + 1)
             key = "fp32" if fmt == 2 else "fp64"
             res[f"assemble_{key}_ms"] = t_asm
             res[f"assemble_{key}_hbm_frac"] = nb / (t_asm * 1e-3) / 1e9 / hbm

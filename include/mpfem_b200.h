@@ -274,6 +274,16 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
                                  int n_loc, int32_t n_dofs, const int64_t* row_ptr,
                                  const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
                                  uint32_t* perm, void* stream);
+/* scatter_plan_cols with the row-pull kernel's position stream: pull_pos[t * n_loc + j] is the
+ * CSR position of local entry j of incidence-list slot t, as a uint16 offset from the first entry
+ * of the row's 32-row block (rows 32 b .. 32 b + 31; status 2 when a row has more than 2,048
+ * entries: use pos_map then). n_cells * n_loc^2 + 8 entries, 16-byte aligned -- the kernel copies
+ * whole 16-byte units. pos_map may be NULL when only pull_pos is wanted (then seg_ptr and perm
+ * too). */
+int mpfem_b200_scatter_plan_pull(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                 int n_loc, int32_t n_dofs, const int64_t* row_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
+                                 uint32_t* perm, uint16_t* pull_pos, void* stream);
 /* table[key_dofs[i]] = val_dofs[i] for i < n (layer-local id -> global id). */
 int mpfem_b200_dofmap_table(const int32_t* key_dofs, const int32_t* val_dofs, int64_t n, int32_t* table,
                             void* stream);
@@ -321,12 +331,14 @@ int mpfem_b200_assemble(const void* locals, int locals_fmt, int64_t cell_begin,
  * entries at their CSR positions (pos_map); values are bitwise those of mode 1 of
  * mpfem_b200_assemble (the reference's ascending-cell sequential sum, assembly.cpp:50-67).
  * rows/n_rows restrict the pass to those rows (NULL: every row); other arguments as
- * mpfem_b200_assemble. */
+ * mpfem_b200_assemble. pull_pos (optional, from mpfem_b200_scatter_plan_pull) replaces pos_map
+ * (which may then be NULL): the same positions as uint16 offsets into 32-row blocks, stored in
+ * the order this kernel reads them, i.e. one sequential stream of half the bytes. */
 int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
                              int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
                              const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
-                             void* values, int fmt, int accumulate, const int32_t* rows,
-                             int64_t n_rows, void* stream);
+                             const uint16_t* pull_pos, void* values, int fmt, int accumulate,
+                             const int32_t* rows, int64_t n_rows, void* stream);
 
 /* ---------------------------------------------------------------- host-buffer assembly
  * The calls behind the C++ drop-in build_dofmap / assemble_matrix (include/mpfem/batched.hpp):

@@ -156,8 +156,10 @@ def lib():
                                           C.c_int32, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                           vp, C.c_int64, vp]),
         "mpfem_b200_assemble_pull": (C.c_int, [vp, C.c_int, C.c_int64, C.c_int64, C.c_int, vp,
-                                               C.c_int32, vp, vp, vp, vp, C.c_int, C.c_int, vp,
+                                               C.c_int32, vp, vp, vp, vp, vp, C.c_int, C.c_int, vp,
                                                C.c_int64, vp]),
+        "mpfem_b200_scatter_plan_pull": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp,
+                                                   vp, vp, vp, vp]),
         "mpfem_b200_csr_pattern_cols": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int32, vp, vp, i64p, vp]),
         "mpfem_b200_scatter_plan_cols": (C.c_int, [vp, vp, C.c_int64, C.c_int, C.c_int32, vp, vp, vp,
                                                    vp, vp, vp]),

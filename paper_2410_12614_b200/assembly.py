@@ -38,6 +38,7 @@ class CsrPattern:
     pos_map: "object" = None  # int32 (n_cells * n_local^2): CSR position of each local entry
     seg_ptr: "object" = None  # int32 view of uint32 (nnz + 1): contribution segments per CSR entry
     perm: "object" = None     # int32 view of uint32 (n_cells * n_local^2): reference order
+    pull_pos: "object" = None  # uint16 (n_cells * n_local^2 + 8): positions in row-pull order
 
     @property
     def nnz(self) -> int:
@@ -69,11 +70,14 @@ def incidence(dm: DofMap, stream=None):
     return inc_ptr, inc
 
 
-def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: bool = False) -> CsrPattern:
+def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: bool = False,
+                pull_plan: bool = True, pos_map: bool = True) -> CsrPattern:
     """The reference COO key set (assembly.cpp:67-86) as CSR, plus the incidence lists and
     (plan=True) the scatter plan used by assemble_matrix: pos_map, and with
     deterministic_plan=True also seg_ptr/perm for the segment-gather kernel (the default
-    deterministic path, row pull, does not need them)."""
+    deterministic path, row pull, does not need them). pull_plan adds pull_pos, the row-pull
+    kernel's own uint16 position stream (half of pos_map's bytes, read sequentially);
+    pos_map=False leaves out the int32 pos_map that the atomic and fused scatters use."""
     import torch
     dev = dm.cell_dofs.device
     row_ptr = torch.empty(dm.n_dofs + 1, dtype=torch.int64, device=dev)
@@ -88,13 +92,29 @@ def csr_pattern(dm: DofMap, stream=None, plan: bool = True, deterministic_plan: 
     pat = CsrPattern(dm.n_dofs, row_ptr, col_idx, inc_ptr, inc)
     if plan:
         nk = dm.n_cells * dm.n_local * dm.n_local
-        pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
+        if pos_map or deterministic_plan or not pull_plan:
+            pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
         if deterministic_plan:
             pat.seg_ptr = torch.empty(nnz.value + 1, dtype=torch.int32, device=dev)
             pat.perm = torch.empty(nk, dtype=torch.int32, device=dev)
-        check(lib().mpfem_b200_scatter_plan(_ptr(dm.cell_dofs), dm.n_cells, dm.n_local, dm.n_dofs,
-                                            _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
-                                            _ptr(pat.seg_ptr), _ptr(pat.perm), sh))
+        if pull_plan:
+            pat.pull_pos = torch.empty(nk + 8, dtype=torch.uint16, device=dev)
+
+        def build():
+            check(lib().mpfem_b200_scatter_plan_pull(_ptr(dm.cell_dofs), None, dm.n_cells, dm.n_local,
+                                                     dm.n_dofs, _ptr(row_ptr), _ptr(col_idx),
+                                                     _ptr(pat.pos_map), _ptr(pat.seg_ptr),
+                                                     _ptr(pat.perm), _ptr(pat.pull_pos), sh))
+        try:
+            build()
+        except ConfigError:
+            # rows beyond pull_pos's uint16 range (high p): the row-pull kernel reads pos_map
+            if pat.pull_pos is None:
+                raise
+            pat.pull_pos = None
+            if pat.pos_map is None:
+                pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
+            build()
     return pat
 
 
@@ -124,17 +144,20 @@ def assemble_matrix(local, dm: DofMap, pat: CsrPattern, fmt: int = FP64,
         values = torch.empty(pat.nnz, dtype=torch.float32 if fmt == FP32 else torch.float64,
                              device=local.device)
     n_rows = 0 if rows is None else int(rows.numel())
-    if pat.pos_map is None:
+    if pat.pos_map is None and pat.pull_pos is None:
         raise ConfigError("assemble_matrix needs a pattern built with plan=True")
     if pull is None:
         pull = pat.seg_ptr is None
+    if pat.pos_map is None and not (mode == DETERMINISTIC and pull):
+        raise ConfigError("this assembly mode needs a pattern built with pos_map=True")
     if mode == DETERMINISTIC and pull:
         # row-pull: incidence lists + pos_map, no seg_ptr/perm plan needed
         check(lib().mpfem_b200_assemble_pull(_ptr(local), lf, int(cell_begin), int(cell_end),
                                              dm.n_local, _ptr(pat.row_ptr), dm.n_dofs,
                                              _ptr(pat.inc_ptr), _ptr(pat.inc), _ptr(pat.pos_map),
-                                             _ptr(values), int(fmt), int(accumulate), _ptr(rows),
-                                             n_rows, _stream_handle(stream)))
+                                             _ptr(pat.pull_pos), _ptr(values), int(fmt),
+                                             int(accumulate), _ptr(rows), n_rows,
+                                             _stream_handle(stream)))
         return values
     check(lib().mpfem_b200_assemble(_ptr(local), lf, int(cell_begin), int(cell_end), dm.n_local,
                                     _ptr(pat.row_ptr), dm.n_dofs, _ptr(pat.pos_map),
@@ -214,9 +237,16 @@ class CudaPartitionBackend:
         pat = CsrPattern(n_rows, row_ptr, col_idx, inc_ptr, inc)
         nk = n * n_loc * n_loc
         pat.pos_map = torch.empty(nk, dtype=torch.int32, device=dev)
-        check(lib().mpfem_b200_scatter_plan_cols(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
-                                                 _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
-                                                 None, None, sh))
+        pat.pull_pos = torch.empty(nk + 8, dtype=torch.uint16, device=dev)
+        try:
+            check(lib().mpfem_b200_scatter_plan_pull(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
+                                                     _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
+                                                     None, None, _ptr(pat.pull_pos), sh))
+        except ConfigError:  # rows beyond pull_pos's uint16 range: pos_map only
+            pat.pull_pos = None
+            check(lib().mpfem_b200_scatter_plan_pull(_ptr(row_dofs), _ptr(col_dofs), n, n_loc, n_rows,
+                                                     _ptr(row_ptr), _ptr(col_idx), _ptr(pat.pos_map),
+                                                     None, None, None, sh))
         pat.n_local = n_loc
         return pat
 
@@ -233,7 +263,8 @@ class CudaPartitionBackend:
         lf = FP32 if local.dtype.itemsize == 4 else FP64
         check(lib().mpfem_b200_assemble_pull(_ptr(local), lf, int(cell_begin), int(cell_end), pat.n_local,
                                              _ptr(pat.row_ptr), pat.n_rows, _ptr(pat.inc_ptr),
-                                             _ptr(pat.inc), _ptr(pat.pos_map), _ptr(values), int(fmt),
-                                             int(accumulate), _ptr(rows), int(rows.numel()),
+                                             _ptr(pat.inc), _ptr(pat.pos_map), _ptr(pat.pull_pos),
+                                             _ptr(values), int(fmt), int(accumulate), _ptr(rows),
+                                             int(rows.numel()),
                                              _stream_handle(None)))
         return values

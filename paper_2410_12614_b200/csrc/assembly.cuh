@@ -355,7 +355,10 @@ __global__ void csr_rows_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
 // Per row (one warp): the row's sorted columns in shared memory; every incident local row
 // (cell, i) maps its n_loc entries by binary search -> pos_map, and (counts != NULL) the
 // number of contributions per CSR position (distinct positions within one cell; the warp
-// walks the incident cells in order, so plain shared-memory increments suffice).
+// walks the incident cells in order, so plain shared-memory increments suffice). pull_pos
+// (optional) receives the same positions as uint16 offsets from the first entry of the row's
+// 32-row block (rows 32 b .. 32 b + 31), laid out in the order the row-pull kernel consumes
+// them: entry (t, j) of incidence-list slot t.
 __device__ __forceinline__ int lower_bound_i32(const int32_t* L, int n, int32_t v) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -370,7 +373,7 @@ __global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
                                 const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
                                 const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                 int32_t n_rows, int rcap, int32_t* __restrict__ pos_map,
-                                uint32_t* __restrict__ counts) {
+                                uint32_t* __restrict__ counts, uint16_t* __restrict__ pull_pos) {
   extern __shared__ int32_t sbuf[];
   const int warps = blockDim.x >> 5;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -385,12 +388,16 @@ __global__ void plan_pos_kernel(const int32_t* __restrict__ cell_dofs, int n_loc
     }
     __syncwarp();
     const int64_t b = inc_ptr[r], m = inc_ptr[r + 1] - b;
+    const int blk_off = pull_pos ? int(o - row_ptr[r & ~int64_t(31)]) : 0;
     for (int64_t k = 0; k < m; ++k) {
       const int64_t pk = inc[b + k];
       const int64_t cell = pk / n_loc;
       for (int j = lane; j < n_loc; j += 32) {
         const int idx = lower_bound_i32(L, u, cell_dofs[cell * n_loc + j]);
-        pos_map[pk * n_loc + j] = int32_t(o + idx);
+        if (pos_map) pos_map[pk * n_loc + j] = int32_t(o + idx);
+        // pull order: the pair's slot in the incidence list; position relative to the first
+        // entry of the row's 32-row block
+        if (pull_pos) pull_pos[(b + k) * n_loc + j] = uint16_t(blk_off + idx);
         if (counts) cnt[idx] += 1;
       }
       __syncwarp();
@@ -551,15 +558,22 @@ constexpr int kPullWarps = 4;     // warps per CTA, each autonomous
 #define MPFEM_PULL_INC 128
 #endif
 #ifndef MPFEM_PULL_MINB
-#define MPFEM_PULL_MINB 1
+#define MPFEM_PULL_MINB 7
 #endif
 constexpr int kPullStages = MPFEM_PULL_STAGES;  // cp.async ring depth per warp
 constexpr int kPullAccCap = MPFEM_PULL_ACC;     // accumulators (CSR entries) per batch
 constexpr int kPullIncCap = MPFEM_PULL_INC;     // pairs per batch
-template <typename TL, typename TV, int CH>
+// bytes of one stage's position slots: int32 CSR positions (pos_map) or uint16 row-relative
+// positions (pull_pos; 8 entries of slack: the stream is copied from the 16-byte boundary below)
+template <int CH, bool P16>
+__host__ __device__ constexpr size_t pull_pos_stage_bytes() {
+  return P16 ? size_t(CH + 8) * 2 : size_t(CH) * 4;
+}
+template <typename TL, typename TV, int CH, bool P16>
 __host__ __device__ constexpr size_t pull_warp_bytes() {
-  return sizeof(TV) * kPullAccCap + sizeof(int64_t) * kPullIncCap +
-         size_t(kPullStages) * CH * (sizeof(TL) + sizeof(int32_t));
+  // + 128 bytes: the replay's operand prefetch runs up to 31 entries past the last staged pair
+  return sizeof(TV) * (kPullAccCap + 32) + sizeof(int64_t) * kPullIncCap +
+         size_t(kPullStages) * (CH * sizeof(TL) + pull_pos_stage_bytes<CH, P16>()) + 128;
 }
 template <int BYTES>
 __device__ __forceinline__ void cp_async_bytes(void* smem_dst, const void* gsrc) {
@@ -581,19 +595,24 @@ __device__ __forceinline__ void cp_async_vec(T* smem_dst, const T* gsrc) {
   }
 }
 // VEC: elements per copy (n_loc % VEC == 0 and the arrays aligned accordingly; chosen by the host)
-template <typename TL, typename TV, int CH, int VEC>
+// P16: positions come from pull_pos (uint16 offsets into the row's 32-row block, in incidence-
+// list order: one sequential stream, half the bytes of pos_map and no partly used sectors)
+// instead of pos_map; batches then stay inside one 32-row block.
+template <typename TL, typename TV, int CH, int VEC, bool P16>
 __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pull_kernel(
     const TL* __restrict__ locals, int n_loc, const int64_t* __restrict__ row_ptr,
     const int64_t* __restrict__ inc_ptr, const int64_t* __restrict__ inc,
-    const int32_t* __restrict__ pos_map, const int32_t* __restrict__ rows, int64_t n_rows,
+    const int32_t* __restrict__ pos_map, const uint16_t* __restrict__ pull_pos,
+    const int32_t* __restrict__ rows, int64_t n_rows,
     int64_t cell_begin, int64_t cell_end, int init, TV* __restrict__ values) {
   extern __shared__ __align__(16) unsigned char pull_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* base = pull_smem + size_t(warp) * pull_warp_bytes<TL, TV, CH>();
+  unsigned char* base = pull_smem + size_t(warp) * pull_warp_bytes<TL, TV, CH, P16>();
   int64_t* s_inc = reinterpret_cast<int64_t*>(base);  // first entry id of the pair, -1: skipped
   TV* s_acc = reinterpret_cast<TV*>(s_inc + kPullIncCap);
-  TL* s_x = reinterpret_cast<TL*>(s_acc + kPullAccCap);
-  int32_t* s_p = reinterpret_cast<int32_t*>(s_x + kPullStages * CH);
+  TL* s_x = reinterpret_cast<TL*>(s_acc + kPullAccCap + 32);  // + one scratch slot per lane
+  unsigned char* s_p = reinterpret_cast<unsigned char*>(s_x + kPullStages * CH);
+  constexpr size_t kPosStage = pull_pos_stage_bytes<CH, P16>();
   const int64_t kb = cell_begin * n_loc, ke = cell_end * n_loc;  // pair ids of the cell range
   const int pairs_per_chunk = CH / n_loc;                          // >= 1 (host checks n_loc <= CH)
   const int upp = n_loc / VEC;                                     // copy units per pair
@@ -608,6 +627,9 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
     const int64_t r = have ? (rows ? int64_t(rows[ri]) : ri) : 0;
     const int64_t my_e0 = have ? row_ptr[r] : 0, my_e1 = have ? row_ptr[r + 1] : 0;
     const int64_t my_b0 = have ? inc_ptr[r] : 0, my_b1 = have ? inc_ptr[r + 1] : 0;
+    // P16: first entry of the row's 32-row block (lane 0's row without a row list)
+    int64_t my_blk0 = 0;
+    if constexpr (P16) my_blk0 = rows ? (have ? row_ptr[r & ~int64_t(31)] : 0) : __shfl_sync(0xffffffffu, my_e0, 0);
     const int n_have = __popc(__ballot_sync(0xffffffffu, have));
     int start = 0;
     while (start < n_have) {
@@ -617,13 +639,15 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
       // that fits the caps
       const int64_t r_start = __shfl_sync(0xffffffffu, r, start);
       const bool fits = lane >= start && lane < n_have && r == r_start + (lane - start) &&
-                        my_e1 - e0 <= kPullAccCap && my_b1 - b0 <= kPullIncCap;
+                        my_e1 - e0 <= kPullAccCap && my_b1 - b0 <= kPullIncCap &&
+                        (!P16 || (r >> 5) == (r_start >> 5));
       const unsigned run = ~(__ballot_sync(0xffffffffu, fits) >> start);
       const int nr = run ? __ffs(run) - 1 : 32 - start;
       if (nr == 0) {
         // one long row: the same ordered replay on global memory
         const int64_t e1 = __shfl_sync(0xffffffffu, my_e1, start);
         const int64_t b1 = __shfl_sync(0xffffffffu, my_b1, start);
+        const int64_t blk0 = __shfl_sync(0xffffffffu, my_blk0, start);
         if (init)
           for (int64_t e = e0 + lane; e < e1; e += 32) values[e] = TV(-0.0);
         __syncwarp();
@@ -632,7 +656,7 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
           if (ki >= kb && ki < ke) {
             for (int j = lane; j < n_loc; j += 32) {
               const int64_t k = ki * n_loc + j;
-              const int64_t pos = pos_map[k];
+              const int64_t pos = P16 ? blk0 + pull_pos[t * n_loc + j] : int64_t(pos_map[k]);
               values[pos] = values[pos] + cast_value<TL, TV>(locals[k]);
             }
           }
@@ -651,25 +675,39 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
       }
       for (int i = lane; i < ne; i += 32) s_acc[i] = init ? TV(-0.0) : values[e0 + i];
       __syncwarp();
+      // P16: accumulator slot = staged block offset - (batch start - block start)
+      const int cbase = P16 ? int(e0 - __shfl_sync(0xffffffffu, my_blk0, start)) : e0i;
+      const uintptr_t pbytes0 = P16 ? reinterpret_cast<uintptr_t>(pull_pos + b0 * n_loc) : 0;
       const int n_chunks = (ni + pairs_per_chunk - 1) / pairs_per_chunk;
       auto issue = [&](int c) {
         if (c < n_chunks) {
           const int t0 = c * pairs_per_chunk;
           const int nu = min(ni - t0, pairs_per_chunk) * upp;
           TL* sx = s_x + (c % kPullStages) * CH;
-          int32_t* sp = s_p + (c % kPullStages) * CH;
+          int32_t* sp = reinterpret_cast<int32_t*>(s_p + (c % kPullStages) * kPosStage);
+          if constexpr (P16) {
+            // the chunk's positions are one contiguous run of pull_pos: 16-byte copies from the
+            // boundary below (the staged run keeps the stream's misalignment)
+            const uintptr_t src = pbytes0 + uint32_t(2 * t0 * n_loc);
+            const uintptr_t a0 = src & ~uintptr_t(15);
+            const int units = (int(src & 15) + nu * VEC * 2 + 15) >> 4;
+            for (int u = lane; u < units; u += 32)
+              cp_async_bytes<16>(reinterpret_cast<unsigned char*>(sp) + 16 * u,
+                                 reinterpret_cast<const unsigned char*>(a0) + 16 * u);
+          }
           int t = lane_t, j = lane_j;
           for (int u = lane; u < nu; u += 32) {
             const int64_t k0 = s_inc[t0 + t];
             if (k0 >= 0) {
               cp_async_vec<TL, VEC>(sx + u * VEC, locals + k0 + j * VEC);
-              cp_async_vec<int32_t, VEC>(sp + u * VEC, pos_map + k0 + j * VEC);
+              if constexpr (!P16) cp_async_vec<int32_t, VEC>(sp + u * VEC, pos_map + k0 + j * VEC);
             } else {
-              // a skipped pair adds -0.0 to the batch's first entry: no change in any bit
+              // a skipped pair adds -0.0 (to the batch's first entry without pull_pos): no
+              // change in any bit
               #pragma unroll
               for (int v = 0; v < VEC; ++v) {
                 sx[u * VEC + v] = TL(-0.0);
-                sp[u * VEC + v] = e0i;
+                if constexpr (!P16) sp[u * VEC + v] = e0i;
               }
             }
             t += dq;
@@ -690,20 +728,30 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
         __syncwarp();
         const int npairs = min(ni - c * pairs_per_chunk, pairs_per_chunk);
         const TL* sx = s_x + (c % kPullStages) * CH;
-        const int32_t* sp = s_p + (c % kPullStages) * CH;
+        const unsigned char* spb = s_p + (c % kPullStages) * kPosStage;
+        const int32_t* sp = reinterpret_cast<const int32_t*>(spb);
+        // P16: staged uint16 run, shifted by the stream's offset from its 16-byte boundary
+        const uint16_t* sq = reinterpret_cast<const uint16_t*>(spb);
+        if constexpr (P16) sq += int((pbytes0 + uint32_t(2 * c * pairs_per_chunk * n_loc)) & 15) >> 1;
+        auto slot = [&](int idx) -> int {
+          if constexpr (P16) return int(sq[idx]) - cbase;
+          else return sp[idx] - cbase;
+        };
         if (n_loc <= 32) {
-          // one lane per local column; the next pair's operands are fetched ahead of the
-          // dependent accumulator update
+          // one lane per local column, branch-free: lanes past n_loc update a scratch slot of
+          // their own; the next pair's operands are fetched ahead of the dependent accumulator
+          // update (the read after the chunk's last pair stays inside the warp's buffers and is
+          // not used)
           const bool on = lane < n_loc;
-          int a = on ? sp[lane] - e0i : 0;
-          TV x = on ? cast_value<TL, TV>(sx[lane]) : TV(0);
+          const int scratch = kPullAccCap + lane;
+          int a = on ? slot(lane) : scratch;
+          TV x = cast_value<TL, TV>(sx[lane]);
+          int idx = lane;
           for (int t = 0; t < npairs; ++t) {
-            sx += n_loc;
-            sp += n_loc;
-            const bool more = on && t + 1 < npairs;
-            const int a_next = more ? sp[lane] - e0i : 0;
-            const TV x_next = more ? cast_value<TL, TV>(sx[lane]) : TV(0);
-            if (on) s_acc[a] = s_acc[a] + x;
+            idx += n_loc;
+            const int a_next = on ? slot(idx) : scratch;
+            const TV x_next = cast_value<TL, TV>(sx[idx]);
+            s_acc[a] = s_acc[a] + x;
             __syncwarp();  // pairs are applied one after the other (ascending cell order per row)
             a = a_next;
             x = x_next;
@@ -711,11 +759,9 @@ __global__ void __launch_bounds__(kPullWarps * 32, MPFEM_PULL_MINB) assemble_pul
         } else {
           for (int t = 0; t < npairs; ++t) {
             for (int j = lane; j < n_loc; j += 32) {
-              const int a = sp[j] - e0i;
-              s_acc[a] = s_acc[a] + cast_value<TL, TV>(sx[j]);
+              const int a = slot(t * n_loc + j);
+              s_acc[a] = s_acc[a] + cast_value<TL, TV>(sx[t * n_loc + j]);
             }
-            sx += n_loc;
-            sp += n_loc;
             __syncwarp();
           }
         }

@@ -332,9 +332,19 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
                                  int n_loc, int32_t n_dofs, const int64_t* row_ptr,
                                  const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
                                  uint32_t* perm, void* stream) {
+  return mpfem_b200_scatter_plan_pull(cell_dofs, col_dofs, n_cells, n_loc, n_dofs, row_ptr, col_idx,
+                                      pos_map, seg_ptr, perm, nullptr, stream);
+}
+
+int mpfem_b200_scatter_plan_pull(const int32_t* cell_dofs, const int32_t* col_dofs, int64_t n_cells,
+                                 int n_loc, int32_t n_dofs, const int64_t* row_ptr,
+                                 const int32_t* col_idx, int32_t* pos_map, uint32_t* seg_ptr,
+                                 uint32_t* perm, uint16_t* pull_pos, void* stream) {
   return aguard([&] {
     if (!col_dofs) col_dofs = cell_dofs;
-    if (n_loc < 1 || n_dofs < 1 || !pos_map) throw AsmError{2, "scatter plan needs a dof map and pos_map"};
+    if (n_loc < 1 || n_dofs < 1 || (!pos_map && !pull_pos))
+      throw AsmError{2, "scatter plan needs a dof map and pos_map or pull_pos"};
+    if (seg_ptr && !pos_map) throw AsmError{2, "the seg_ptr/perm plan needs pos_map"};
     const int64_t nk = n_cells * n_loc * n_loc;
     if (nk > int64_t(UINT32_MAX)) throw AsmError{2, "n_cells * n_loc^2 must fit 32 bits"};
     if ((seg_ptr == nullptr) != (perm == nullptr))
@@ -348,6 +358,8 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
     int rcap = 32;
     const int64_t umax = max_count(row_ptr, n_dofs, S);
     while (rcap < umax) rcap <<= 1;
+    // pull_pos holds uint16 offsets into 32-row blocks
+    if (pull_pos && umax * 32 > 65536) throw AsmError{2, "pull_pos needs rows of at most 2048 entries"};
     const int64_t nnz = read1(row_ptr + n_dofs, st);
     uint32_t* counts = nullptr;
     if (seg_ptr) counts = S.get<uint32_t>(size_t(nnz) + 1);
@@ -362,7 +374,7 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
     {
       auto [grid, warps, smem] = launch_dims(size_t(rcap) * 8, reinterpret_cast<const void*>(asmb::plan_pos_kernel));
       asmb::plan_pos_kernel<<<grid, warps * 32, smem, st>>>(col_dofs, n_loc, inc_ptr, inc, row_ptr, col_idx,
-                                                            n_dofs, rcap, pos_map, counts);
+                                                            n_dofs, rcap, pos_map, counts, pull_pos);
       ACUDA(cudaGetLastError());
     }
     if (!seg_ptr) return;
@@ -383,14 +395,16 @@ int mpfem_b200_scatter_plan_cols(const int32_t* cell_dofs, const int32_t* col_do
 int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_begin,
                              int64_t cell_end, int n_loc, const int64_t* row_ptr, int32_t n_dofs,
                              const int64_t* inc_ptr, const int64_t* inc, const int32_t* pos_map,
-                             void* values, int fmt, int accumulate, const int32_t* rows,
-                             int64_t n_rows, void* stream) {
+                             const uint16_t* pull_pos, void* values, int fmt, int accumulate,
+                             const int32_t* rows, int64_t n_rows, void* stream) {
   return aguard([&] {
     if (locals_fmt != 2 && locals_fmt != 3) throw AsmError{2, "local matrices must be fp32 or fp64"};
     if (fmt != 2 && fmt != 3) throw AsmError{2, "CSR values must be fp32 or fp64"};
     if (cell_end < cell_begin || n_loc < 1) throw AsmError{2, "bad cell range"};
-    if (!row_ptr || !inc_ptr || !inc || !pos_map)
-      throw AsmError{2, "row-pull assembly needs row_ptr, the incidence lists and pos_map"};
+    if (!row_ptr || !inc_ptr || !inc || (!pos_map && !pull_pos))
+      throw AsmError{2, "row-pull assembly needs row_ptr, the incidence lists and pos_map or pull_pos"};
+    if (pull_pos && reinterpret_cast<uintptr_t>(pull_pos) % 16 != 0)
+      throw AsmError{2, "pull_pos must be 16-byte aligned"};
     if (n_dofs == 0) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t per_cell = int64_t(n_loc) * n_loc;
@@ -404,8 +418,9 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
     // elements per cp.async: 4 / 2 / 1 by n_loc and the arrays' alignment
     auto aligned = [](const void* q, size_t a) { return reinterpret_cast<uintptr_t>(q) % a == 0; };
     int vec = 1;
-    if (n_loc % 4 == 0 && aligned(base, 16) && aligned(pos_map, 16)) vec = 4;
-    else if (n_loc % 2 == 0 && aligned(base, std::min<size_t>(16, 2 * esz)) && aligned(pos_map, 8)) vec = 2;
+    const bool p16 = pull_pos != nullptr;
+    if (n_loc % 4 == 0 && aligned(base, 16) && (p16 || aligned(pos_map, 16))) vec = 4;
+    else if (n_loc % 2 == 0 && aligned(base, std::min<size_t>(16, 2 * esz)) && (p16 || aligned(pos_map, 8))) vec = 2;
 // Shared-memory carveout of the pull kernel: 75 % leaves the L1 large enough to keep the partly
 // used sectors of neighbouring local rows until the next CSR row asks for them (measured at config 4,
 // P3 fp32: carveout 100 % 9.3 ms, 75 % 6.0 ms, 50 % 6.5 ms, 25 % 12.1 ms).
@@ -413,25 +428,30 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
 #define MPFEM_PULL_CARVEOUT 75
 #endif
 #define MPFEM_PULL_CARVE(...) ACUDA(cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributePreferredSharedMemoryCarveout, MPFEM_PULL_CARVEOUT));
-#define MPFEM_PULL_V(TL, TV, CH, VEC)                                                              \
+#define MPFEM_PULL_P(TL, TV, CH, VEC, P16)                                                         \
   {                                                                                                \
-    constexpr size_t smem = asmb::kPullWarps * asmb::pull_warp_bytes<TL, TV, CH>();                \
+    constexpr size_t smem = asmb::kPullWarps * asmb::pull_warp_bytes<TL, TV, CH, P16>();           \
     static bool attr = false;                                                                      \
     static int per_sm = 1;                                                                         \
     if (!attr) {                                                                                   \
-      ACUDA(cudaFuncSetAttribute(asmb::assemble_pull_kernel<TL, TV, CH, VEC>,                      \
+      ACUDA(cudaFuncSetAttribute(asmb::assemble_pull_kernel<TL, TV, CH, VEC, P16>,                 \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));         \
-      MPFEM_PULL_CARVE(asmb::assemble_pull_kernel<TL, TV, CH, VEC>)                                \
+      MPFEM_PULL_CARVE(asmb::assemble_pull_kernel<TL, TV, CH, VEC, P16>)                           \
       ACUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                         \
-          &per_sm, asmb::assemble_pull_kernel<TL, TV, CH, VEC>, asmb::kPullWarps * 32, smem));     \
+          &per_sm, asmb::assemble_pull_kernel<TL, TV, CH, VEC, P16>, asmb::kPullWarps * 32, smem)); \
       attr = true;                                                                                 \
     }                                                                                              \
     const unsigned grid = unsigned(std::max<int64_t>(                                              \
         1, std::min<int64_t>((blocks32 + asmb::kPullWarps - 1) / asmb::kPullWarps,                 \
                              int64_t(148) * std::max(per_sm, 1))));                                \
-    asmb::assemble_pull_kernel<TL, TV, CH, VEC><<<grid, asmb::kPullWarps * 32, smem, st>>>(        \
-        reinterpret_cast<const TL*>(base), n_loc, row_ptr, inc_ptr, inc, pos_map, rows, nr,        \
-        cell_begin, cell_end, init, static_cast<TV*>(values));                                     \
+    asmb::assemble_pull_kernel<TL, TV, CH, VEC, P16><<<grid, asmb::kPullWarps * 32, smem, st>>>(   \
+        reinterpret_cast<const TL*>(base), n_loc, row_ptr, inc_ptr, inc, pos_map, pull_pos, rows,  \
+        nr, cell_begin, cell_end, init, static_cast<TV*>(values));                                 \
+  }
+#define MPFEM_PULL_V(TL, TV, CH, VEC)                                                              \
+  {                                                                                                \
+    if (p16) MPFEM_PULL_P(TL, TV, CH, VEC, true)                                                   \
+    else MPFEM_PULL_P(TL, TV, CH, VEC, false)                                                      \
   }
 #define MPFEM_PULL_J(TL, TV, CH)                                                                   \
   {                                                                                                \
@@ -449,6 +469,7 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
     else if (fmt == 2) MPFEM_PULL(double, float)
     else MPFEM_PULL(double, double)
 #undef MPFEM_PULL_V
+#undef MPFEM_PULL_P
 #undef MPFEM_PULL_J
 #undef MPFEM_PULL
     ACUDA(cudaGetLastError());

@@ -19,7 +19,7 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 for p in ps:
     dm = am.build_dofmap(p, cd, verts.shape[0])
-    pat = am.csr_pattern(dm, deterministic_plan=True)
+    pat = am.csr_pattern(dm)
     s = mp.make_setup(p, mp.mode_config("mixed_bf16", mp.FormKind.poisson))
     local = s.cell_matrices(vd, cd, mp.CoefKind.sincosexp)
     res = {"p": p, "lib": os.environ.get("MPFEM_B200_LIB", "default").split("/")[-1]}

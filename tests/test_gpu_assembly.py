@@ -78,11 +78,17 @@ def test_csr_pattern_and_values_bitwise(oracle, p, dims):
     for pull in (False, True):
         v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat, 2, am.DETERMINISTIC, pull=pull)
         assert np.array_equal(v.double().cpu().numpy().view(np.uint64), vals.view(np.uint64)), pull
-    # a pattern without seg_ptr/perm (the default) takes the row-pull kernel
-    pat0 = am.csr_pattern(dm)
-    assert pat0.seg_ptr is None
-    v = am.assemble_matrix(torch.from_numpy(loc64).cuda(), dm, pat0, 2)
-    assert np.array_equal(v.double().cpu().numpy().view(np.uint64), vals.view(np.uint64))
+    # patterns without seg_ptr/perm (the default) take the row-pull kernel: with its own uint16
+    # position stream (pull_pos, with and without the int32 pos_map beside it) or with pos_map only
+    for kw in ({}, {"pos_map": False}, {"pull_plan": False}):
+        pat0 = am.csr_pattern(dm, **kw)
+        assert pat0.seg_ptr is None
+        assert (pat0.pull_pos is None) == (kw.get("pull_plan") is False)
+        assert (pat0.pos_map is None) == (kw.get("pos_map") is False)
+        for loc in (loc64, loc32):
+            ref = oracle.assemble_matrix(cd, nd, loc.astype(np.float64), 2)[2]
+            v = am.assemble_matrix(torch.from_numpy(loc).cuda(), dm, pat0, 2)
+            assert np.array_equal(v.double().cpu().numpy().view(np.uint64), ref.view(np.uint64)), kw
 
 
 def test_row_pull_row_lists_bitwise(oracle):
