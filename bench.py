@@ -43,20 +43,34 @@ def peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def profiled_traffic(kernel_prefix="cellmat_tc2_kernel"):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from
-    the committed `ncu --set full` capture summary (profiles/r*_ncu_summary.json), or None."""
+def profiled_traffic(kernel_prefix="cellmat_tc2_kernel<0, 0>", fallback_prefix="cellmat_tc2_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel from the
+    latest committed `ncu --set full` capture summary (profiles/r*_ncu_summary.json `ncu_full`,
+    profiles/r*_zoo_summary.json `poisson_k2`: the headline workload), or None."""
     import glob
+
+    def to_bytes(v):
+        if isinstance(v, (int, float)):
+            return float(v) * 1e6  # older summaries: bare Mbyte numbers
+        num, _, unit = str(v).partition(" ")
+        return float(num) * {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1e6)
+
     best = None
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json"))):
+    paths = glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")) + \
+        glob.glob(os.path.join(ROOT, "profiles", "r*_zoo_summary.json"))
+    def round_key(path):  # r1k < r2a < r2x < r2ba: shorter round tags are older
+        tag = os.path.basename(path).split("_")[0]
+        return (len(tag), tag, os.path.basename(path))
+
+    for path in sorted(paths, key=round_key):
         try:
             with open(path) as f:
                 d = json.load(f)
-            for k in d.get("ncu_full", []):
-                if kernel_prefix in k.get("kernel", ""):
-                    rd = float(k["dram__bytes_read.sum"]) * 1e6  # ncu reports Mbyte
-                    wr = float(k["dram__bytes_write.sum"]) * 1e6
-                    best = {"bytes": rd + wr, "source": os.path.relpath(path, ROOT)}
+            for k in list(d.get("ncu_full", [])) + list(d.get("poisson_k2", [])):
+                name = k.get("kernel", "")
+                if kernel_prefix in name or (fallback_prefix in name and "<" not in name):
+                    best = {"bytes": to_bytes(k["dram__bytes_read.sum"]) + to_bytes(k["dram__bytes_write.sum"]),
+                            "source": os.path.relpath(path, ROOT)}
         except Exception:
             continue
     return best
