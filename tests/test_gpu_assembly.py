@@ -179,6 +179,55 @@ def test_config4_full_size_p2_properties():
     assert torch.equal(torch.sort(key).values, torch.sort(keyt).values)
 
 
+@pytest.mark.slow
+def test_config4_full_size_p2_bitwise_pin(oracle):
+    """BASELINE config 4 at its full size (96^3 x 6 = 5,308,416 tets, P2, Poisson, mixed-bf16
+    cell kernels): the GPU dof map equals the reference restatement's (mesh.cpp:204-298) entry
+    for entry, and the deterministic CSR assembly (fp32 and fp64 values) equals the reference
+    assembly (assembly.cpp:41-88) bit for bit on windows of rows at the start, in the middle and
+    at the end of the matrix. A window's rows are complete in the sub-assembly of exactly the
+    cells incident to it, taken in ascending order, so the oracle sums each entry's contributions
+    in the same order as the full assembly would; rows outside the window are ignored. Whole-
+    matrix properties on top: the sum of all entries equals the sum of all local entries, and
+    the Poisson rows sum to ~0."""
+    n, p = 96, 2
+    verts, cells = oracle.structured_tet_mesh(n, n, n, 1.0, 0.15, 1)
+    cd, nd, mm = oracle.build_dofmap(p, verts, cells)
+    vd = torch.from_numpy(verts).cuda()
+    cdev = torch.from_numpy(cells).cuda()
+    dm = am.build_dofmap(p, cdev, verts.shape[0])
+    assert dm.n_dofs == nd == 7189057 and dm.max_multiplicity == mm
+    assert torch.equal(dm.cell_dofs.cpu(), torch.from_numpy(cd))
+    s = mp.make_setup(p, mp.mode_config("mixed_bf16", mp.FormKind.poisson))
+    loc = s.cell_matrices(vd, cdev, mp.CoefKind.sincosexp).view(-1, 10, 10)
+    pat = am.csr_pattern(dm)
+    rp = pat.row_ptr.cpu().numpy()
+    col = pat.col_idx.cpu().numpy()
+    w = 20000
+    for fmt in (2, 3):
+        vals = am.assemble_matrix(loc, dm, pat, fmt)
+        torch.cuda.synchronize()
+        v = vals.double().cpu().numpy()
+        for r0 in (0, nd // 2 - w // 2, nd - w):
+            r1 = r0 + w
+            touched = np.nonzero(((cd >= r0) & (cd < r1)).any(axis=1))[0]  # ascending cells
+            lsub = loc[torch.from_numpy(touched).cuda()].double().cpu().numpy()
+            rows, cols, rv, _ = oracle.assemble_matrix(cd[touched], nd, lsub, fmt)
+            keep = (rows >= r0) & (rows < r1)
+            a, b = rp[r0], rp[r1]
+            assert keep.sum() == b - a
+            assert np.array_equal(cols[keep], col[a:b])
+            assert np.array_equal(rows[keep], np.repeat(np.arange(r0, r1), np.diff(rp[r0:r1 + 1])))
+            assert np.array_equal(rv[keep].view(np.uint64), v[a:b].view(np.uint64)), (fmt, r0)
+        if fmt == 3:
+            total, ltotal = float(vals.sum()), float(loc.double().sum())
+            scale = float(loc.double().abs().sum())
+            assert abs(total - ltotal) <= 1e-9 * scale
+            rs = torch.segment_reduce(vals, "sum", lengths=pat.row_ptr[1:] - pat.row_ptr[:-1])
+            assert float(rs.abs().max()) <= 1e-2 * float(vals.abs().max())
+        del vals
+
+
 @pytest.mark.parametrize("mode,p", [("mixed", 2), ("mixed_bf16", 3), ("fp64", 2), ("mixed", 1)])
 def test_fused_cell_kernels_scatter(oracle, mode, p):
     """assemble_cells (cell kernels fused with the atomic scatter; on the tcgen05 path K2 adds
