@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int pitch3 = int(P.out_pitch & 3);
     int acc = 0, slot = 0;
     uint32_t acc_phase = 0, slot_phase = 0;
-    uint32_t nonfinite = 0;  // bit 31 set by any value with an all-ones exponent
+    uint32_t magmax = 0;  // max of (bits << 1): a value with an all-ones exponent gives >= 0xff000000
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const int ct = tile / P.n_out_tiles, ot = tile % P.n_out_tiles;
       const int o_base = ot * BO;
@@ -178,22 +178,25 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int j = 0; j < 32; ++j) {
               uint32_t bits = r[j];
               if constexpr (ACC_F16) bits = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(bits & 0xffffu))));
-              nonfinite |= (bits & 0x7fffffffu) + 0x00800000u;
+              magmax = max(magmax, bits << 1);
               asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(bits) : "memory");
               addr += uint32_t(P.n_out * 4);
             }
           }
         } else {
-          int shift = int((uint64_t(cell0) * uint64_t(P.out_pitch) + uint64_t(o_base)) & 3u);
-          uint32_t addr = sbuf + uint32_t(o_loc * 4);
+          // the shift of row j depends on j mod 4 only (4 pitches are a multiple of 16 bytes):
+          // four base addresses, the row offset is an immediate of the unrolled store
+          const int shift0 = int((uint64_t(cell0) * uint64_t(P.out_pitch) + uint64_t(o_base)) & 3u);
+          uint32_t* base4[4];  // derived from the shared array: the stores compile to STS
+          #pragma unroll
+          for (int k = 0; k < 4; ++k)
+            base4[k] = reinterpret_cast<uint32_t*>(sOut) + slot * CHUNK * SROW + o_loc + ((shift0 + k * pitch3) & 3);
           #pragma unroll
           for (int j = 0; j < 32; ++j) {
             uint32_t bits = r[j];
             if constexpr (ACC_F16) bits = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(bits & 0xffffu))));
-            nonfinite |= (bits & 0x7fffffffu) + 0x00800000u;
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr + uint32_t(shift * 4)), "r"(bits) : "memory");
-            addr += SROW * 4;
-            shift = (shift + pitch3) & 3;
+            magmax = max(magmax, bits << 1);  // sign dropped: non-finite iff >= 0xff000000
+            base4[j & 3][j * SROW] = bits;
           }
         }
         __syncwarp();
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
-    const uint32_t bad = __reduce_or_sync(0xffffffffu, nonfinite) & 0x80000000u;
+    const uint32_t bad = __reduce_max_sync(0xffffffffu, magmax) >= 0xff000000u;
     if (lane == 0 && bad && !(*reinterpret_cast<volatile uint32_t*>(P.flags) & 4u)) atomicOr(P.flags, 4u);
   } else if (warp >= 4 + EPI_WARPS) {
     // store warps: staging slot -> global, each warp CHUNK / ST_WARPS cells per chunk: scalar
