@@ -451,7 +451,7 @@ int mpfem_b200_assemble_pull(const void* locals, int locals_fmt, int64_t cell_be
 #define MPFEM_PULL_V(TL, TV, CH, VEC)                                                              \
   {                                                                                                \
     if (p16) MPFEM_PULL_P(TL, TV, CH, VEC, true)                                                   \
-    else MPFEM_PULL_P(TL, TV, CH, VEC, false)                                                      \
+    else MPFEM_PULL_P(TL, TV, CH, 1, false) /* pos_map fallback: 4-byte copies only */             \
   }
 #define MPFEM_PULL_J(TL, TV, CH)                                                                   \
   {                                                                                                \
