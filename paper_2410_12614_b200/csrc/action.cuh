@@ -120,6 +120,22 @@ struct Arith<kArGen> {
   }
 };
 
+// One multiply-add of a contraction. FMA (fp32 accumulation over fp16-stored operands only): the
+// product of two fp16 values has at most 22 significant bits and an exponent within fp32's
+// normal range, so it is exact in fp32 and round(a * b + acc) = round(round(a * b) + acc): one
+// FFMA gives the bits of the reference's rounded product followed by its rounded sum.
+template <int A, bool FMA>
+__device__ __forceinline__ typename Arith<A>::T madd(typename Arith<A>::T acc, typename Arith<A>::T a,
+                                                     typename Arith<A>::T b, int f, bool ftz, uint32_t& fl) {
+  if constexpr (A == kArF32 && FMA) {
+    float r = __fmaf_rn(a, b, acc);
+    if (ftz && fabsf(r) < 0x1.0p-126f) r = copysignf(0.0f, r);
+    return r;
+  } else {
+    return Arith<A>::add(acc, Arith<A>::mul(a, b, f, fl), f, ftz, fl);
+  }
+}
+
 // The integrand stage at u_g: hardware ops when u_g is fp64 or fp32 (every operand -- G,
 // what, omega, zhat -- is already a u_g value, so the fp32 op is the reference's rounded
 // binary64 op), the flagged emulation otherwise.
@@ -262,7 +278,7 @@ __device__ __forceinline__ void load_cb(const T* p, T (&v)[N]) {
   }
 }
 
-template <int A, bool FTZ, int UGK, bool BOX>
+template <int A, bool FTZ, int UGK, bool BOX, bool FMA = false>
 __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionParams P) {
   constexpr int kGeoWords = geo_words<BOX>();
   using T = typename Arith<A>::T;
@@ -312,7 +328,7 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
         load_cb(wp, wv);
         #pragma unroll
         for (int j = 0; j < kActionCBA; ++j)
-          acc[j] = Ar::add(acc[j], Ar::mul(wv[j], b, P.up, fl), P.up, FTZ, fl);
+          acc[j] = madd<A, FMA>(acc[j], wv[j], b, P.up, FTZ, fl);
       }
       #pragma unroll
       for (int j = 0; j < kActionCBA; ++j)
@@ -398,7 +414,7 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
         load_cb(rp, rv);
         #pragma unroll
         for (int j = 0; j < kActionCB; ++j)
-          acc[j] = Ar::add(acc[j], Ar::mul(b, rv[j], P.uq, fl), P.uq, FTZ, fl);
+          acc[j] = madd<A, FMA>(acc[j], b, rv[j], P.uq, FTZ, fl);
       }
       #pragma unroll
       for (int j = 0; j < kActionCB; ++j) {

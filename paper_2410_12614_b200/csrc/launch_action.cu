@@ -34,7 +34,7 @@ int pick_tile(int n_phi, int n_q, int n_d, size_t budget, int threads) {
   return best;
 }
 
-template <int A, bool FTZ, int UGK, bool BOX>
+template <int A, bool FTZ, int UGK, bool BOX, bool FMA = false>
 int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   ActionParams P = P0;
   // measured (scripts/action_sweep.py, P4): mass 128 threads / 36 KB tiles (230 vs 291 us),
@@ -52,14 +52,14 @@ int launch_one(const ActionParams& P0, int sm_count, cudaStream_t st) {
   P.tile = tile;
   static size_t smem_set = 0;
   if (smem > smem_set) {
-    if (cudaFuncSetAttribute(action_kernel<A, FTZ, UGK, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(action_kernel<A, FTZ, UGK, BOX, FMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(std::max<size_t>(smem, 48 * 1024))) != cudaSuccess)
       return 4;
     smem_set = smem;
   }
   const int64_t tiles = (P.n_cells + tile - 1) / tile;
   const unsigned grid = unsigned(std::min<int64_t>(tiles, int64_t(sm_count) * per_sm));
-  action_kernel<A, FTZ, UGK, BOX><<<grid, threads, smem, st>>>(P);
+  action_kernel<A, FTZ, UGK, BOX, FMA><<<grid, threads, smem, st>>>(P);
   return 0;
 }
 }  // namespace
@@ -70,6 +70,11 @@ int launch_kind(int ap, int aq, const ActionParams& P, int sm_count, cudaStream_
   const bool ftz = P.ftz != 0;
   if (a == kArF64 && P.ug == kFP64) return launch_one<kArF64, false, kUg64, BOX>(P, sm_count, st);
   if (a == kArF16 && P.ug == kFP32) return launch_one<kArF16, false, kUg32, BOX>(P, sm_count, st);
+  // fp32 accumulation over fp16-stored operands: products are exact, one FFMA per term (action.cuh madd)
+  if (a == kArF32 && P.us == kFP16 && P.ug == kFP32)
+    return ftz ? launch_one<kArF32, true, kUg32, BOX, true>(P, sm_count, st) : launch_one<kArF32, false, kUg32, BOX, true>(P, sm_count, st);
+  if (a == kArF32 && P.us == kFP16 && P.ug == kFP64)
+    return ftz ? launch_one<kArF32, true, kUg64, BOX, true>(P, sm_count, st) : launch_one<kArF32, false, kUg64, BOX, true>(P, sm_count, st);
   if (a == kArF32 && P.ug == kFP32)
     return ftz ? launch_one<kArF32, true, kUg32, BOX>(P, sm_count, st) : launch_one<kArF32, false, kUg32, BOX>(P, sm_count, st);
   if (a == kArF32 && P.ug == kFP64)
