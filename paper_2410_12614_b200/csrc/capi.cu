@@ -473,9 +473,8 @@ void launch_gemm(mpfem_b200_setup_s& S, Workspace& ws, void* W, int64_t n, void*
       else launch_tc2<false>(ta, tb, P, st);
     }
   } else if (S.path == kPathF32) {
-    constexpr int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
-    dim3 grid(unsigned((n + BM - 1) / BM), unsigned(S.n_out_pad / BN));
-    cellmat_simt_kernel<float, BM, BN, BK, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, st>>>(
+    dim3 grid(unsigned((n + sg::BM - 1) / sg::BM), unsigned(S.n_out_pad / sg::BN));
+    sg::cellmat_ffma_kernel<<<grid, sg::THREADS, 0, st>>>(
         static_cast<const float*>(W), static_cast<const float*>(S.d_T.p), static_cast<float*>(out),
         n, int(S.n_out), S.n_out_pad, S.k_pad, out_pitch, static_cast<uint32_t*>(ws.d_flags.p));
   } else {
