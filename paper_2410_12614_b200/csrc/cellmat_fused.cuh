@@ -11,6 +11,9 @@
 // T (the shared basis products, rounded to u_s) lives in shared memory and is read as a
 // broadcast (every thread reads the same T[k, o]). HBM traffic is 96 B in + 4 n_phi^2 B
 // out per cell: the path's algorithmic bytes.
+// Only the upper triangle (i <= j) is accumulated: T[k, (i, j)] and T[k, (j, i)] are the same
+// bits (B_s[i] B_t[j] + B_t[i] B_s[j] is symmetric in (i, j)) and both entries would run the same
+// fmaf sequence, so A[j, i] is A[i, j] bit for bit; the mirror happens at the store.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -52,9 +55,23 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
   constexpr int NB = FORM ? 6 : 1;
   constexpr int K = NB * NQ;
   constexpr int NOUT = NPHI * NPHI;
-  __shared__ __align__(16) float sT[K * NOUT];
+  constexpr int NU = NPHI * (NPHI + 1) / 2;  // upper triangle, u(i, j) = i NPHI - i (i - 1) / 2 + j - i
+  constexpr int NUP = (NU + 3) / 4 * 4;      // padded to whole float4
+  __shared__ __align__(16) float sT[K * NUP];
   __shared__ double sW[NQ], sX[NQ * 3];
-  for (int i = threadIdx.x; i < K * NOUT; i += blockDim.x) sT[i] = F.T[i];
+  for (int idx = threadIdx.x; idx < K * NUP; idx += blockDim.x) {
+    const int k = idx / NUP, u = idx - k * NUP;
+    float t = 0.0f;
+    if (u < NU) {
+      int i = 0, rem = u;
+      while (rem >= NPHI - i) {
+        rem -= NPHI - i;
+        ++i;
+      }
+      t = F.T[k * NOUT + i * NPHI + i + rem];
+    }
+    sT[idx] = t;
+  }
   for (int i = threadIdx.x; i < NQ; i += blockDim.x) sW[i] = F.rule_w_ug[i];
   for (int i = threadIdx.x; i < NQ * 3; i += blockDim.x) sX[i] = F.rule_x[i];
   __syncthreads();
@@ -99,9 +116,9 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
         for (int s = 0; s < 3; ++s) E[s * 3 + a] = sc * __dsub_rn(v[s + 1][a], v[0][a]);
       }
       const double* zc = F.coef ? F.coef + cell * F.coef_stride : nullptr;
-      float acc[NOUT];
+      float acc[NUP];
       #pragma unroll
-      for (int o = 0; o < NOUT; ++o) acc[o] = 0.0f;
+      for (int o = 0; o < NUP; ++o) acc[o] = 0.0f;
       // depth loop q-outer: W_(b,q) is generated and consumed immediately
       #pragma unroll 1
       for (int q = 0; q < NQ; ++q) {
@@ -130,9 +147,9 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
             if constexpr (COEF != 0) val = droundT<UG>(__dmul_rn(val, zq), fl);
           }
           const float wk = round_storage_f<US>(val, sf);
-          const float4* trow = reinterpret_cast<const float4*>(sT + (b * NQ + q) * NOUT);
+          const float4* trow = reinterpret_cast<const float4*>(sT + (b * NQ + q) * NUP);
           #pragma unroll
-          for (int o4 = 0; o4 < NOUT / 4; ++o4) {
+          for (int o4 = 0; o4 < NUP / 4; ++o4) {
             const float4 t = trow[o4];
             acc[4 * o4 + 0] = fmaf(wk, t.x, acc[4 * o4 + 0]);
             acc[4 * o4 + 1] = fmaf(wk, t.y, acc[4 * o4 + 1]);
@@ -143,17 +160,24 @@ __global__ void __launch_bounds__(128) cellmat_fused_kernel(FusedParams F) {
       }
       uint32_t bad = 0;
       #pragma unroll
-      for (int o = 0; o < NOUT; ++o) bad |= (__float_as_uint(acc[o]) & 0x7f800000u) == 0x7f800000u;
+      for (int o = 0; o < NU; ++o) bad |= (__float_as_uint(acc[o]) & 0x7f800000u) == 0x7f800000u;
       if (bad) fl |= kInvalid;
+      // entry o = i NPHI + j of the row-major matrix from the upper triangle (indices are
+      // compile-time after unrolling: registers stay statically addressed)
+      auto full = [&](int o) -> float {
+        const int i = o / NPHI, j = o - i * NPHI;
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        return acc[lo * NPHI - lo * (lo - 1) / 2 + hi - lo];
+      };
       float* dst = F.out + cell * F.out_pitch;
       if ((F.out_pitch & 3) == 0) {
         #pragma unroll
         for (int o4 = 0; o4 < NOUT / 4; ++o4)
           __stcs(reinterpret_cast<float4*>(dst) + o4,
-                 make_float4(acc[4 * o4], acc[4 * o4 + 1], acc[4 * o4 + 2], acc[4 * o4 + 3]));
+                 make_float4(full(4 * o4), full(4 * o4 + 1), full(4 * o4 + 2), full(4 * o4 + 3)));
       } else {
         #pragma unroll
-        for (int o = 0; o < NOUT; ++o) __stcs(dst + o, acc[o]);
+        for (int o = 0; o < NOUT; ++o) __stcs(dst + o, full(o));
       }
     }
   }
