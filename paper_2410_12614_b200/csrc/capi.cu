@@ -371,16 +371,20 @@ template <bool ACC_F16, int OUTK = 0>
 void launch_tc2(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params& P, cudaStream_t st) {
   static int max_clusters = 0;
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // K2's prologue (barriers, TMEM allocation, cluster sync) overlaps K1's tail; the kernel
+  // waits (griddepcontrol.wait) before it touches W
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.blockDim = dim3(tc2::THREADS);
   cfg.dynamicSmemBytes = tc2::SMEM_BYTES;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (!max_clusters) {
     CUDA_OK(cudaFuncSetAttribute(tc2::cellmat_tc2_kernel<ACC_F16, OUTK>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES));
@@ -403,7 +407,17 @@ void launch_tcs_t(const CUtensorMap& ta, const CUtensorMap& tb, const tc::Params
   }
   const int64_t tiles = int64_t(P.n_out_tiles) * P.n_cell_tiles;
   const unsigned grid = unsigned(std::min<int64_t>(tiles, device_sm_count()));
-  tcs::cellmat_tcs_kernel<ACC_F16, PACKED><<<grid, tcs::THREADS, tcs::SMEM_BYTES, st>>>(ta, tb, P);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see launch_tc2
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tcs::THREADS);
+  cfg.dynamicSmemBytes = tcs::SMEM_BYTES;
+  cfg.stream = st;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, tcs::cellmat_tcs_kernel<ACC_F16, PACKED>, ta, tb, P));
 }
 // packed: whole cell matrices in one 256-output tile, stored densely (pitch n_out)
 template <bool ACC_F16>

@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // Launched with programmatic stream serialisation behind K1: everything above overlaps
+  // K1's tail; W, the flags word and the output are touched only after K1 has completed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {

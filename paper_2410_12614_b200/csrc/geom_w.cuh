@@ -283,6 +283,10 @@ __host__ __device__ constexpr size_t geom_w_smem_bytes(int nq_pad, int geom_warp
 
 template <typename T, int UG, int US, int COEF>
 __global__ void __launch_bounds__(kGeomThreads, MPFEM_K1_MINB) geom_w_kernel(GeomWParams P) {
+  // Programmatic dependent launch: K2 (launched with programmatic stream serialisation) may
+  // become resident on SMs this grid has left and run its prologue; it reads W only after
+  // its griddepcontrol.wait, i.e. after this whole grid has completed and flushed.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ double s_rule[];
   __shared__ uint32_t s_next[kGeoSlots];  // per-slot item counters (dynamic 32-item grabs)
   __shared__ int64_t s_tile[kGeoSlots];   // the slot's tile

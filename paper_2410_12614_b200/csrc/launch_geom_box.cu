@@ -34,6 +34,7 @@ template <> struct UsOf<float> { static constexpr int v = kFP32; };
 
 template <typename T, int UG>
 __global__ void __launch_bounds__(128) geom_w_box_kernel(const GeomBoxParams P) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see geom_w_kernel
   uint32_t fl = 0;
   T* W = static_cast<T*>(P.W);
   const int64_t items = P.n_cells * P.nq_pad;
