@@ -278,6 +278,114 @@ __device__ __forceinline__ void load_cb(const T* p, T (&v)[N]) {
   }
 }
 
+// The two contractions as CB-cell x NB-column register tiles: one shared-memory vector of the
+// cells and NB tabulation words feed CB * NB multiply-adds (each output still sums its terms in
+// ascending order, so the bits are those of the one-column form). Measured at config 0 / 1
+// (65,536 P4 tets, mixed): NB = 2 gains 6 % for Poisson (n1 = 375 columns) and loses 8 % for
+// mass (n1 = 125: too few items per tile), NB = 4 loses everywhere (profiles/r2br_action_nb_ab.txt).
+template <int A, bool FTZ, bool FMA, int NB>
+__device__ __forceinline__ void what_stage(const ActionParams& P, const typename Arith<A>::T* sWm,
+                                           double* sWH, const typename Arith<A>::T* tabA, int C,
+                                           uint32_t& fl) {
+  using T = typename Arith<A>::T;
+  constexpr int kActionNB = NB;
+  const int nphi = P.n_phi, n1 = P.n_d * P.n_q;
+  // a thread keeps a CBA-cell x kActionNB-column register tile: one shared-memory vector of
+  // the cells and kActionNB tabulation words feed CBA * kActionNB multiply-adds (each output
+  // still sums k ascending, so the bits are unchanged)
+  const int groups_a = C / kActionCBA;
+  const int n1b = (n1 + kActionNB - 1) / kActionNB;
+  for (int item = threadIdx.x; item < groups_a * n1b; item += blockDim.x) {
+    const int cg = item / n1b, n = (item - cg * n1b) * kActionNB;
+    T acc[kActionNB][kActionCBA];
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u)
+      #pragma unroll
+      for (int j = 0; j < kActionCBA; ++j) acc[u][j] = T(0);
+    // columns past n1 repeat the last one (computed, not stored)
+    int col[kActionNB];
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u) col[u] = min(n + u, n1 - 1);
+    const T* bp = tabA;
+    const T* wp = sWm + cg * kActionCBA;
+    #pragma unroll 2
+    for (int k = 0; k < nphi; ++k, bp += n1, wp += C) {
+      T b[kActionNB];
+      #pragma unroll
+      for (int u = 0; u < kActionNB; ++u) b[u] = __ldg(bp + col[u]);
+      T wv[kActionCBA];
+      load_cb(wp, wv);
+      #pragma unroll
+      for (int u = 0; u < kActionNB; ++u)
+        #pragma unroll
+        for (int j = 0; j < kActionCBA; ++j)
+          acc[u][j] = madd<A, FMA>(acc[u][j], wv[j], b[u], P.up, FTZ, fl);
+    }
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u)
+      if (n + u < n1) {
+        #pragma unroll
+        for (int j = 0; j < kActionCBA; ++j)
+          sWH[size_t(n + u) * C + cg * kActionCBA + j] = dround_fast(double(acc[u][j]), P.ug, fl);
+      }
+  }
+}
+
+template <int A, bool FTZ, bool FMA, int NB>
+__device__ __forceinline__ void v_stage(const ActionParams& P, const typename Arith<A>::T* sR,
+                                        const typename Arith<A>::T* tabC, int C, int64_t c0, int nc,
+                                        uint32_t& fl) {
+  using T = typename Arith<A>::T;
+  constexpr int kActionNB = NB;
+  const int nphi = P.n_phi, n1 = P.n_d * P.n_q;
+  const int groups = C / kActionCB;
+  const int nphib = (nphi + kActionNB - 1) / kActionNB;
+  for (int item = threadIdx.x; item < groups * nphib; item += blockDim.x) {
+    const int cg = item / nphib, i = (item - cg * nphib) * kActionNB;
+    T acc[kActionNB][kActionCB];
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u)
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) acc[u][j] = T(0);
+    int col[kActionNB];
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u) col[u] = min(i + u, nphi - 1);
+    const T* bp = tabC;
+    const T* rp = sR + cg * kActionCB;
+    #pragma unroll 4
+    for (int kk = 0; kk < n1; ++kk, bp += nphi, rp += C) {
+      T b[kActionNB];
+      #pragma unroll
+      for (int u = 0; u < kActionNB; ++u) b[u] = __ldg(bp + col[u]);
+      T rv[kActionCB];
+      load_cb(rp, rv);
+      #pragma unroll
+      for (int u = 0; u < kActionNB; ++u)
+        #pragma unroll
+        for (int j = 0; j < kActionCB; ++j)
+          acc[u][j] = madd<A, FMA>(acc[u][j], b[u], rv[j], P.uq, FTZ, fl);
+    }
+    #pragma unroll
+    for (int u = 0; u < kActionNB; ++u) {
+      if (i + u >= nphi) continue;
+      #pragma unroll
+      for (int j = 0; j < kActionCB; ++j) {
+        const int c = cg * kActionCB + j;
+        if (c < nc) {
+          double v = double(acc[u][j]);
+          if (!isfinite(v)) fl |= isnan(v) ? kInvalid : kOverflow;
+          // NaN leaves as the reference's canonical quiet NaN (softfloat.hpp round_to)
+          if (isnan(v)) v = canonical_nan_d();
+          if (P.uq == kFP64)
+            static_cast<double*>(P.out)[(c0 + c) * P.out_pitch + i + u] = v;
+          else
+            static_cast<float*>(P.out)[(c0 + c) * P.out_pitch + i + u] = float(v);
+        }
+      }
+    }
+  }
+}
+
 template <int A, bool FTZ, int UGK, bool BOX, bool FMA = false>
 __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionParams P) {
   constexpr int kGeoWords = geo_words<BOX>();
@@ -313,27 +421,8 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
     __syncthreads();
 
     // -- what (eval_w_at_ug): column n = s n_q + q, CBA cells per thread, k ascending at u_p
-    const int groups_a = C / kActionCBA;
-    for (int item = threadIdx.x; item < groups_a * n1; item += blockDim.x) {
-      const int cg = item / n1, n = item - cg * n1;
-      T acc[kActionCBA];
-      #pragma unroll
-      for (int j = 0; j < kActionCBA; ++j) acc[j] = T(0);
-      const T* bp = tabA + n;
-      const T* wp = sWm + cg * kActionCBA;
-      #pragma unroll 2
-      for (int k = 0; k < nphi; ++k, bp += n1, wp += C) {
-        const T b = __ldg(bp);
-        T wv[kActionCBA];
-        load_cb(wp, wv);
-        #pragma unroll
-        for (int j = 0; j < kActionCBA; ++j)
-          acc[j] = madd<A, FMA>(acc[j], wv[j], b, P.up, FTZ, fl);
-      }
-      #pragma unroll
-      for (int j = 0; j < kActionCBA; ++j)
-        sWH[size_t(n) * C + cg * kActionCBA + j] = dround_fast(double(acc[j]), P.ug, fl);
-    }
+    if (poisson) what_stage<A, FTZ, FMA, 2>(P, sWm, sWH, tabA, C, fl);
+    else what_stage<A, FTZ, FMA, 1>(P, sWm, sWH, tabA, C, fl);
     __syncthreads();
 
     // -- integrand r at u_g, stored at u_s: one thread per (q, cell), cell fastest
@@ -400,37 +489,8 @@ __global__ void __launch_bounds__(kActionThreads) action_kernel(const ActionPara
     __syncthreads();
 
     // -- v = b_cat_action r at u_q: output i, CB cells per thread, (s, q) ascending
-    for (int item = threadIdx.x; item < groups * nphi; item += blockDim.x) {
-      const int cg = item / nphi, i = item - cg * nphi;
-      T acc[kActionCB];
-      #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) acc[j] = T(0);
-      const T* bp = tabC + i;
-      const T* rp = sR + cg * kActionCB;
-      #pragma unroll 4
-      for (int kk = 0; kk < n1; ++kk, bp += nphi, rp += C) {
-        const T b = __ldg(bp);
-        T rv[kActionCB];
-        load_cb(rp, rv);
-        #pragma unroll
-        for (int j = 0; j < kActionCB; ++j)
-          acc[j] = madd<A, FMA>(acc[j], b, rv[j], P.uq, FTZ, fl);
-      }
-      #pragma unroll
-      for (int j = 0; j < kActionCB; ++j) {
-        const int c = cg * kActionCB + j;
-        if (c < nc) {
-          double v = double(acc[j]);
-          if (!isfinite(v)) fl |= isnan(v) ? kInvalid : kOverflow;
-          // NaN leaves as the reference's canonical quiet NaN (softfloat.hpp round_to)
-          if (isnan(v)) v = canonical_nan_d();
-          if (P.uq == kFP64)
-            static_cast<double*>(P.out)[(c0 + c) * P.out_pitch + i] = v;
-          else
-            static_cast<float*>(P.out)[(c0 + c) * P.out_pitch + i] = float(v);
-        }
-      }
-    }
+    if (poisson) v_stage<A, FTZ, FMA, 2>(P, sR, tabC, C, c0, nc, fl);
+    else v_stage<A, FTZ, FMA, 1>(P, sR, tabC, C, c0, nc, fl);
     __syncthreads();
   }
   publish_flags(P.flags, fl);
