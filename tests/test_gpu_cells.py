@@ -361,3 +361,28 @@ def test_two_streams_share_one_setup(tets):
     torch.cuda.synchronize()
     for oa, ob in outs:
         assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
+
+
+@pytest.mark.parametrize("form", [MASS, POISSON])
+def test_cuda_graph_replay_bitwise(tets, form):
+    """K1 -> K2 captured in a CUDA graph after reserve() (mpfem_b200_reserve: no allocation in
+    later calls) and replayed: the programmatic dependent launch edge between the two kernels
+    (K2's griddepcontrol.wait) must survive capture; every replay equals the eager result bit
+    for bit. Mass takes the staged K2-s kernel, Poisson the CTA-pair kernel."""
+    s = mp.make_setup(4, kconfig("mixed", form, geometry_fp64=(form == POISSON)))
+    v = dev(tets[:900])
+    ref = s.cell_matrices(v, None, COEF_SINCOSEXP).clone()
+    st = torch.cuda.Stream()
+    out = torch.empty_like(ref)
+    with torch.cuda.stream(st):
+        s.reserve(v.shape[0], stream=st)
+        s.cell_matrices(v, None, COEF_SINCOSEXP, out=out, stream=st)  # warm: attributes, modules
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        s.cell_matrices(v, None, COEF_SINCOSEXP, out=out, stream=st)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
